@@ -1,0 +1,456 @@
+#!/usr/bin/env python
+"""bench.py — hybrid-batch paged attention of Niyama (arXiv 2503.22562) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl niyama|reference] [--config l8b|l70b]
+
+A STEP is one pass of the whole hot path over one
+batch, for one layer: a1 min slack + max feasible chunk (host), a2 plan (host
+bookkeeping + one H2D), a3 KV append (kernel), a4-a6 the fused hybrid
+attention launch (kernel), a7 head all-gather (NCCL, N>1), a8 predictor eval
+(host).  The same batch is replayed every step (sequences are truncated back
+after planning, host-only).  Default workload = BASELINE config 2:
+Llama-3-8B attention shapes (32 q / 8 kv heads, d 128, bf16, block 16), a
+512-token prefill chunk at offset 1536 plus 64 decodes with ctx ~ U{1..4096}
+(PCG64 seed 0, sum ctx 133,674).  value = tokens of the batch (T = 576) per
+second of device time, max over ranks (strong scaling: heads are sharded over
+N GPUs, the batch is fixed).
+
+Timing: CUDA events on the launching stream, W untimed warm-up steps, a
+barrier + synchronize on both sides of exactly K timed steps.  L2: inputs
+larger than L2 (556 MB of KV read per step vs 126 MB of L2).  The
+`roofline` object uses the attention launch's own per-launch event times.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hybrid-batch attn tokens/s & roofline % (Llama-3-8B shapes, chunk 512+64 dec)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="niyama", choices=["niyama", "reference"])
+    ap.add_argument("--config", default="l8b", choices=["l8b", "l70b"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--settle-s", type=float, default=1.0, help="untimed GPU work before warm-up (clock settle)")
+    return ap.parse_args()
+
+
+def workload(name):
+    import workloads as W
+    if name == "l8b":
+        return W.config2_l8b()
+    return W.config4_l70b()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def algorithmic(wl, hq, hkv):
+    """B_KV = [sum(o+c) + sum ctx] * Hkv * d * 2 * elt; F = 4 d Hq [sum(c o + c(c+1)/2) + sum ctx]."""
+    s, d = wl.shape, wl.final.desc
+    tok = sum(o + c for o, c in zip(d.prefill_offset, d.prefill_len)) + sum(d.decode_ctx)
+    pairs = sum(c * o + c * (c + 1) // 2 for o, c in zip(d.prefill_offset, d.prefill_len)) + sum(d.decode_ctx)
+    B = tok * hkv * s.head_dim * 2 * s.elt_bytes
+    F = 4.0 * s.head_dim * hq * pairs
+    return B, F
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 100 ms while running."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.lines = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ts, line in self.lines:
+            if not (t0 <= ts <= t1):
+                continue
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n:
+        raise SystemExit(f"--gpus {n} but WORLD_SIZE={world}")
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if os.environ.get("NIYAMA_BENCH_GLOO") is None else "gloo")
+        pg = dist
+    return rank, world, local, pg
+
+
+def cpu_baseline(wl, budget_s=20.0):
+    """The fp64 oracle as it stands, on this host's cores, over a bounded row sample."""
+    import numpy as np
+    from oracle import attention as OA
+    from oracle.kvcache import KVPool
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        threads = 1
+    s = wl.shape
+    pool = KVPool(1, s.num_kv_heads, s.head_dim, s.block_size, wl.num_blocks, s.dtype)
+    plan = None
+    for st in wl.steps:
+        plan = pool.plan(st.desc)
+        pool.append(0, plan, st.k, st.v)
+    T = len(plan.rows)
+    D = wl.final.desc.num_decode
+    prefill_rows = list(range(0, T - D, max(1, (T - D) // 32)))
+    rows = prefill_rows + list(range(T - D, T))
+    t0 = time.perf_counter()
+    done = 0
+    for r in rows:
+        OA.hybrid_attention(pool, 0, plan, wl.final.q, s.num_q_heads, rows=[r])
+        done += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+            "host_cpus": os.cpu_count(),
+            "sample": f"{done} of {T} batch rows ({len(prefill_rows)} evenly spaced prefill rows + all {D} decode "
+                      f"rows, all {s.num_q_heads} heads), fp64 numpy, {dt:.1f} s"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle (this tier's reference arm), rank 0 only."""
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle import attention as OA
+    from oracle.kvcache import KVPool
+    wl = workload(args.config)
+    s = wl.shape
+    pool = KVPool(1, s.num_kv_heads, s.head_dim, s.block_size, wl.num_blocks, s.dtype)
+    plan = None
+    for st in wl.steps:
+        plan = pool.plan(st.desc)
+        pool.append(0, plan, st.k, st.v)
+    T = len(plan.rows)
+    D = wl.final.desc.num_decode
+    g = np.random.default_rng(0)
+    per_step = 8
+    cand = list(range(T))
+
+    def one():
+        rows = sorted(g.choice(cand, size=per_step, replace=False).tolist())
+        OA.hybrid_attention(pool, 0, plan, wl.final.q, s.num_q_heads, rows=rows)
+        return len(rows)
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    n = sum(one() for _ in range(args.steps))
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        threads = 1
+    v = n / dt
+    out = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": wl.name, "step": f"fp64 oracle on {per_step} random rows of the batch"},
+           "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle",
+                            "sample": f"{per_step} random batch rows per step of {T}"},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    rank, world, local, dist = dist_setup(args.gpus)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2503_22562_b200 as ny
+    import workloads as W
+    from oracle import predictor as _unused  # noqa: F401  (not used on the product path)
+    del _unused
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    wl = workload(args.config)
+    s = wl.shape
+    hq, hkv = s.num_q_heads // world, s.num_kv_heads // world
+    q0, k0 = rank * hq, rank * hkv
+    kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
+                    dtype=s.dtype, world_size=world, rank=rank, device=local)
+    if world > 1:
+        uid = ny.get_unique_id() if rank == 0 else bytes(128)
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        kv.comm_init(obj[0])
+
+    def dev_bf16(a, lo, hi):
+        return torch.from_numpy(np.ascontiguousarray(a[:, lo:hi]).view(np.int16)).to(dev).view(torch.bfloat16)
+
+    # prefix fill (untimed): sequences pre-filled by the library's own append
+    for st in wl.steps[:-1]:
+        p = kv.plan(st.desc)
+        kv.append(p, 0, dev_bf16(st.k, k0, k0 + hkv), dev_bf16(st.v, k0, k0 + hkv))
+        torch.cuda.synchronize()
+        p.close()
+    fin = wl.final
+    desc = fin.desc
+    T = desc.num_rows
+    q = dev_bf16(fin.q, q0, q0 + hq)
+    k_new = dev_bf16(fin.k, k0, k0 + hkv)
+    v_new = dev_bf16(fin.v, k0, k0 + hkv)
+    o_full = torch.empty((s.num_q_heads, T, s.head_dim), dtype=torch.bfloat16, device=dev)
+    lse_full = torch.empty((s.num_q_heads, T), dtype=torch.float32, device=dev)
+    o = o_full[q0:q0 + hq]
+    lse = lse_full[q0:q0 + hq]
+    stream = torch.cuda.current_stream()
+    rewind = [(sq, o_) for sq, o_ in zip(desc.prefill_seq, desc.prefill_offset)] + \
+             [(sq, c - 1) for sq, c in zip(desc.decode_seq, desc.decode_ctx)]
+
+    # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
+    fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
+    cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
+    theta = [4e-6, 0.0, 0.0, 0.0, 0.0, 1.2]
+    if os.path.exists(fit_path):
+        fj = json.load(open(fit_path))
+        theta = fj.get("theta", theta) if fj.get("world", 1) == world and fj.get("config") == args.config else theta
+    pred = ny.Predictor.from_params(cfg, theta)
+    # a1 inputs: decodes carry Table 3 tiers, interactive ones are mid-stream
+    tiers = desc.tiers()
+    qos = []
+    for j, c in enumerate(desc.decode_ctx):
+        tier = tiers[desc.num_prefill + j] % 3
+        if tier == 0:
+            qos.append(ny._binding.DecodeQoSC(1, 40, 1, 0, 0.0, 6.0, 0.05, 0.0))
+        else:
+            qos.append(ny._binding.DecodeQoSC(0, 1, 400, 0, 0.0, 0.0, 0.0, 600.0 if tier == 1 else 1800.0))
+    a1 = {}
+
+    def a1_step():
+        import ctypes as C
+        arr = (ny._binding.DecodeQoSC * max(1, len(qos)))(*qos)
+        sl = C.c_double()
+        ny._binding.lib.niyama_min_slack(arr, len(qos), 7.9, C.byref(sl))
+        c, inf = pred.max_feasible_chunk(desc.decode_ctx, desc.prefill_offset[0] if desc.num_prefill else 0,
+                                         desc.prefill_len[0] if desc.num_prefill else 0, sl.value, 2048)
+        a1["slack_s"], a1["chunk"], a1["infeasible"] = sl.value, c, inf
+
+    ev = []
+
+    def step(record=None):
+        a1_step()                                       # a1 (host)
+        plan = kv.plan(desc, stream)                    # a2
+        kv.append(plan, 0, k_new, v_new, stream)        # a3
+        if record is not None:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        kv.attention(plan, 0, q, o, lse, 0.0, stream)   # a4-a6
+        if record is not None:
+            b.record(stream)
+            record.append((a, b))
+        if world > 1:
+            kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
+        pred.predict(desc)                              # a8
+        for sq, n in rewind:
+            kv.truncate(sq, n)
+        plan.close()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    t_settle = time.time()
+    while time.time() - t_settle < args.settle_s:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(ev)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_wall1 = time.time()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    attn_ms = [a.elapsed_time(b) for a, b in ev]
+    attn_avg_ms = sum(attn_ms) / len(attn_ms)
+    if dist:
+        t = torch.tensor([ms, attn_avg_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, attn_avg_ms = float(t[0]), float(t[1])
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
+    h_q = q.cpu().pin_memory()
+    h_k = k_new.cpu().pin_memory()
+    h_v = v_new.cpu().pin_memory()
+    h_o = torch.empty_like(o_full, device="cpu").pin_memory()
+    d_q, d_k, d_v = torch.empty_like(q), torch.empty_like(k_new), torch.empty_like(v_new)
+
+    def e2e_step():
+        d_q.copy_(h_q, non_blocking=True)
+        d_k.copy_(h_k, non_blocking=True)
+        d_v.copy_(h_v, non_blocking=True)
+        a1_step()
+        plan = kv.plan(desc, stream)
+        kv.append(plan, 0, d_k, d_v, stream)
+        kv.attention(plan, 0, d_q, o, lse, 0.0, stream)
+        if world > 1:
+            kv.allgather_heads(plan, o_full, lse_full, stream)
+        pred.predict(desc)
+        for sq, n in rewind:
+            kv.truncate(sq, n)
+        plan.close()
+        h_o.copy_(o_full, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t[0])
+    clocks.stop()
+    h2d = (h_q.numel() + h_k.numel() + h_v.numel()) * 2
+    d2h = h_o.numel() * 2
+
+    B_kv, F = algorithmic(wl, hq, hkv)
+    hbm_peak, tf_peak, peak_src = peaks()
+    attn_s = attn_avg_ms * 1e-3
+    achieved = B_kv / attn_s / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        pj = json.load(open(prof))
+        traffic = pj.get(f"{args.config}-g{world}", {}).get("dram_bytes_per_launch")
+    value = T * args.steps / (ms * 1e-3)
+    out = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic: seeded PCG64, Q/K/V ~ N(0,1) rounded to bf16; decode ctx ~ U{1..4096} (seed 0)",
+        "config": {"workload": wl.name, "Hq": s.num_q_heads, "Hkv": s.num_kv_heads, "head_dim": s.head_dim,
+                   "block_size": s.block_size, "chunk": sum(desc.prefill_len),
+                   "chunk_offset": desc.prefill_offset[0] if desc.num_prefill else 0,
+                   "num_decode": desc.num_decode, "sum_ctx": int(sum(desc.decode_ctx)), "T": T,
+                   "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
+                   "l2": f"inputs larger than L2 ({B_kv / 1e6:.0f} MB KV read per step per GPU vs 126 MB L2)",
+                   "step": "a1 slack+chunk, a2 plan, a3 append, a4-a6 fused attention" +
+                           (", a7 NCCL all-gather" if world > 1 else "") + ", a8 predict; 1 layer"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "hybrid_attn_bf16_kernel", "algorithmic_bytes_per_launch": B_kv,
+                     "launch_us": attn_avg_ms * 1e3, "peak_source": peak_src,
+                     "tensor_frac": F / attn_s / (tf_peak * 1e12),
+                     "t_roof_us": max(F / (tf_peak * 1e12), B_kv / (hbm_peak * 1e9)) * 1e6},
+        "attn_tokens_per_s": T / attn_s,
+        "e2e": {"value": T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clocks.summary(t_settle, t_wall1),
+        "a1": a1,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,249 @@
+/*
+ * niyama.h — C ABI of the B200-native hybrid-batch paged-attention path of
+ * Niyama (arXiv 2503.22562).  Library: paper_2503_22562_b200/libniyama.so
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n,
+ * §8 = SURVEY.md §8 (the hot-path scope table), Rn = DESIGN.md reading n.
+ *
+ * What the path computes.  Each serving iteration Niyama builds ONE hybrid
+ * batch: the decode step of every running request plus a prefill chunk
+ * (§3.1 steps ④-⑥: "A lightweight predictor is then used to estimate
+ * the latency of the batch ... A mixed batch of prefill and decode tokens is
+ * constructed ... dispatched to the execution engine on the GPU").  Attention
+ * of that batch over a block-table KV cache (vLLM PagedAttention, P:319
+ * §3.6) is the data-parallel hot path.  For batch row r (visible keys n_r)
+ * and query head h (kv head h / (Hq/Hkv), R7):
+ *     O[h][r] = softmax(scale * q_{r,h} K^T) V,  LSE[h][r] = ln sum exp(...)
+ * with causal visibility (prefill row at position p sees keys [0, p]; a
+ * decode row sees its whole context, R4).  §8(a) rows a1-a8 map to:
+ *   a1 niyama_min_slack + niyama_max_feasible_chunk      (host, fp64)
+ *   a2 niyama_plan_create                                (host planner)
+ *   a3 niyama_kv_append                                  (scatter kernel)
+ *   a4-a6 niyama_hybrid_attention                        (ONE fused launch)
+ *   a7 niyama_comm_init + niyama_allgather_heads         (NCCL over NVLink)
+ *   a8 niyama_predictor_fit + niyama_predict_iter_time   (host, fp64)
+ *
+ * Conventions (all calls):
+ *  - Every call returns niyama_status unless noted; on error the message is
+ *    available from niyama_last_error() (thread-local, valid until the next
+ *    call on the same thread).  Validation happens before any side effect or
+ *    launch; the API never aborts and takes no locks.  One niyama_kv per
+ *    host thread / stream (single-threaded per replica).
+ *  - "device" pointers are CUDA global-memory pointers on cfg.device;
+ *    "host" pointers are ordinary host memory.  All device work is enqueued
+ *    on the caller's stream and is asynchronous; a plan must outlive every
+ *    launch that uses it (destroy is stream-ordered).
+ *  - Tensors are dense row-major, no padding.  bf16 values are raw IEEE
+ *    bfloat16; f32 values are IEEE binary32.
+ *  - There is no CPU fallback: with cfg.device = NIYAMA_DEVICE_NONE the
+ *    library keeps only host bookkeeping (planner tests) and every call that
+ *    would touch the GPU returns NIYAMA_EUNSUPPORTED.
+ */
+#ifndef NIYAMA_H_
+#define NIYAMA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* niyama_stream; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+  NIYAMA_OK = 0,
+  NIYAMA_EINVAL = 1,       /* malformed argument or descriptor (names the field) */
+  NIYAMA_ENOBLOCKS = 2,    /* KV pool exhausted; nothing was reserved (all-or-nothing) */
+  NIYAMA_ENOSEQ = 3,       /* decode / release / gather of an unknown sequence */
+  NIYAMA_ESTATE = 4,       /* cached length != prefill offset, or != decode ctx-1 (R4) */
+  NIYAMA_ECUDA = 5,        /* CUDA runtime/launch failure (message has cudaGetErrorString) */
+  NIYAMA_ENCCL = 6,        /* NCCL failure */
+  NIYAMA_EUNSUPPORTED = 7  /* shape/dtype not built, or no device (NIYAMA_DEVICE_NONE) */
+} niyama_status;
+
+const char* niyama_last_error(void);
+const char* niyama_version(void);
+
+#define NIYAMA_DEVICE_NONE (-1)
+
+typedef enum { NIYAMA_BF16 = 0, NIYAMA_F32 = 1 } niyama_dtype;
+
+/* KV-cache configuration.  Heads are GLOBAL counts; with world_size G the
+ * library on `rank` owns kv heads [rank*Hkv/G, (rank+1)*Hkv/G) and query
+ * heads [rank*Hq/G, (rank+1)*Hq/G) (GQA groups stay whole, §8e
+ * tensor parallelism).  Supported: head_dim*elt a multiple of 128 bytes
+ * (bf16: 64, 128; f32: 32, 64), Hq/Hkv a power of two <= 128, block_size in
+ * {16, 32, 64, 128} (R9: default 16). */
+typedef struct {
+  int32_t num_layers;
+  int32_t num_q_heads;
+  int32_t num_kv_heads;
+  int32_t head_dim;
+  int32_t block_size;
+  int32_t num_blocks;   /* pool capacity in blocks (each block holds block_size tokens of every local kv head) */
+  niyama_dtype dtype;   /* stored type of K/V/Q/O */
+  int32_t world_size;   /* >= 1 */
+  int32_t rank;         /* 0 <= rank < world_size */
+  int32_t device;       /* CUDA ordinal, or NIYAMA_DEVICE_NONE (host bookkeeping only) */
+} niyama_kv_config;
+
+typedef struct niyama_kv niyama_kv;
+typedef struct niyama_plan niyama_plan;
+
+/* Create the pool.  The library allocates and OWNS num_layers*2*num_blocks*
+ * (Hkv/G)*block_size*head_dim elements of device memory (zero-filled) plus
+ * the block tables.  Errors: EINVAL (shape), EUNSUPPORTED, ECUDA (OOM). */
+niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv** out);
+void niyama_kv_destroy(niyama_kv* kv); /* synchronises the device; NULL is a no-op */
+
+/* Request finished (P:205 ⑦, §8 a13 feedback): free its blocks (they become
+ * the smallest-free-id candidates again, R9).  ENOSEQ if unknown. */
+niyama_status niyama_kv_release(niyama_kv* kv, int64_t seq_id);
+/* Roll a sequence back to its first new_len tokens (new_len <= cached
+ * length): blocks beyond ceil(new_len/B) return to the free set (R9).  Host
+ * bookkeeping only; KV bytes are not touched (stream order keeps in-flight
+ * launches valid: a later plan that re-reserves a block is ordered after
+ * them on the same stream).  Used for iteration replay and rollback. */
+niyama_status niyama_kv_truncate(niyama_kv* kv, int64_t seq_id, int32_t new_len);
+/* Host read of a sequence's block table: n = number of blocks; copies
+ * min(n, cap) ids to out (host).  ENOSEQ if unknown. */
+niyama_status niyama_kv_block_table(const niyama_kv* kv, int64_t seq_id, int32_t* out, int32_t cap, int32_t* n);
+niyama_status niyama_kv_seq_len(const niyama_kv* kv, int64_t seq_id, int32_t* len);
+niyama_status niyama_kv_num_free(const niyama_kv* kv, int32_t* n);
+/* Test read-back: logical K and V of positions [0, len) of seq in layer, as
+ * dense [len][Hkv_loc][head_dim] in the stored dtype, to DEVICE buffers
+ * k_out, v_out.  EINVAL if len > cached length. */
+niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t seq_id, int32_t len, void* k_out,
+                               void* v_out, niyama_stream stream);
+
+/* One iteration's hybrid batch (P:205 ⑤; D2 in SURVEY §2.3).  HOST pointers,
+ * copied during niyama_plan_create (caller may free afterwards).
+ * Rows of the batch: prefill slice i contributes prefill_len[i] rows at
+ * positions prefill_offset[i] .. +len-1 (in slice order), then one row per
+ * decode j at position decode_ctx[j]-1 (R6).  A slice of an unknown seq
+ * with offset 0 creates the sequence (len 0 is allowed and just registers
+ * it).  decode_ctx counts the keys visible after appending the new token
+ * (R4).  A seq id may appear at most once per batch.  tier[i] (i over
+ * slices then decodes; may be NULL) is the request's QoS tier, 0 = strictest
+ * (Table 3); it only orders work inside the launch and never changes
+ * any result bit (R13). */
+typedef struct {
+  int32_t num_prefill;
+  const int64_t* prefill_seq;
+  const int32_t* prefill_offset;
+  const int32_t* prefill_len;
+  int32_t num_decode;
+  const int64_t* decode_seq;
+  const int32_t* decode_ctx;
+  const uint8_t* tier;
+} niyama_batch_desc;
+
+/* a2 — plan an iteration: validate (EINVAL/ENOSEQ/ESTATE), reserve blocks
+ * (smallest free ids, descriptor order, all-or-nothing → ENOBLOCKS, R9),
+ * advance the cached lengths, and build the device work list (prefill tiles
+ * and split-KV decode units, longest first) with ONE async H2D on `stream`.
+ * The plan is reused by every layer's append/attention of the iteration. */
+niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_desc* desc, niyama_stream stream,
+                                 niyama_plan** out);
+void niyama_plan_destroy(niyama_plan* plan); /* stream-ordered free on the plan's stream */
+
+typedef struct {
+  int32_t num_rows;           /* T = sum prefill_len + num_decode */
+  int32_t num_prefill_rows;
+  int32_t num_decode;
+  int32_t num_prefill_tiles;  /* 128-row (packed GQA) x 128-key tcgen05 tiles */
+  int32_t num_decode_units;   /* (decode row, kv head, key split) items */
+  int32_t split_len;          /* decode split length in tokens (batch-level choice) */
+  int32_t rows_per_tile;      /* 128 / (Hq/Hkv) chunk rows per prefill tile */
+  int32_t reserved;
+  int64_t sum_ctx;            /* sum of decode ctx */
+} niyama_plan_info;
+niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_plan_info* out);
+/* Host copy of the slot map: row r's new K/V goes to (block_out[r], slot_out[r]). */
+niyama_status niyama_plan_slots(const niyama_plan* plan, int32_t* block_out, int32_t* slot_out, int32_t cap);
+
+/* a3 — scatter the batch's new K/V rows into the pool (bit copy, no dtype
+ * conversion): pool[table[s][p/B]][h][p%B] = K_new[row][h].  k_new, v_new:
+ * DEVICE [T][Hkv_loc][head_dim]. */
+niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
+                               const void* v_new, niyama_stream stream);
+
+/* a4-a6 — ONE launch: causal prefill-chunk tiles (tcgen05/TMEM, bf16) and
+ * split-KV decode units (HBM-bound, mma.sync) with the log-sum-exp merge of
+ * a row's splits done in-launch by its last split (merge order = split
+ * order, so results are bitwise deterministic).
+ *   q   DEVICE [T][Hq_loc][head_dim]   (post-RoPE, R8)
+ *   o   DEVICE [Hq_loc][T][head_dim]   (head-major so the all-gather needs no transpose)
+ *   lse DEVICE [Hq_loc][T] f32 natural-log LSE (R11), or NULL
+ *   softmax_scale <= 0 selects 1/sqrt(head_dim).
+ * Append must have been enqueued before for the same layer and plan.
+ * T = 0 is a no-op. */
+niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q,
+                                      void* o, float* lse, float softmax_scale, niyama_stream stream);
+
+/* a7 — head sharding across the GPUs of one node (§8e).  comm_init creates
+ * the library's own NCCL communicator from a 128-byte ncclUniqueId produced
+ * by rank 0 and broadcast by the caller (world/rank from the config).
+ * allgather_heads gathers every rank's [Hq/G][T][d] slice into o_full
+ * [Hq][T][d] IN PLACE (this rank's slice must already sit at
+ * o_full + rank*(Hq/G)*T*d) and likewise lse_full [Hq][T] if non-NULL. */
+niyama_status niyama_comm_init(niyama_kv* kv, const void* nccl_unique_id);
+niyama_status niyama_get_unique_id(void* out128); /* ncclGetUniqueId, for rank 0 */
+niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, void* o_full, float* lse_full,
+                                     niyama_stream stream);
+
+/* a8 — iteration-time predictor (P:205 ④; R16).  Features of a batch
+ * on this rank's shape: phi = [1, c, D, B_KV, F, max(F/F_PEAK, B_KV/B_PEAK)]
+ * with c = prefill rows, D = decodes, B_KV = [sum(o+c) + sum ctx]*Hkv*d*2*elt
+ * bytes, F = 4*d*Hq*[sum(c*o + c(c+1)/2) + sum ctx] flops, F_PEAK/B_PEAK the
+ * nominal B200 peaks below.  t_hat = theta . phi, theta >= 0 fitted by
+ * non-negative least squares on relative residuals of measured samples. */
+#define NIYAMA_F_PEAK_BF16 2.25e15
+#define NIYAMA_F_PEAK_F32 1.125e15
+#define NIYAMA_B_PEAK 8.0e12
+#define NIYAMA_NUM_FEATURES 6
+
+typedef struct {
+  int32_t chunk_len;    /* prefill rows of the (single) slice, 0 if none */
+  int32_t chunk_offset;
+  int32_t num_decode;
+  int64_t sum_ctx;      /* sum of decode ctx */
+  double seconds;       /* measured launch time (> 0) */
+} niyama_sample;
+typedef struct niyama_predictor niyama_predictor;
+
+niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
+                                   niyama_predictor** out);
+niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta6,
+                                           niyama_predictor** out); /* theta >= 0 required */
+niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta6_out);
+/* Seconds for the batch (slices and decodes of desc; tiers ignored); < 0 on invalid input. */
+double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc);
+/* a1 — largest C in [0, min(max_chunk, prefill_remaining)] such that the batch
+ * {C prefill rows at chunk_offset} + desc's decodes predicts <= slack_s (a
+ * latency equal to the slack is feasible, R18; 1e-12 relative guard).  If
+ * even C = 0 is infeasible: chunk_out = 0 and infeasible_out = 1 (a flag,
+ * not an error).  desc's prefill slices are ignored. */
+niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_batch_desc* decodes_only,
+                                        int32_t chunk_offset, int32_t prefill_remaining, double slack_s,
+                                        int32_t max_chunk, int32_t* chunk_out, int32_t* infeasible_out);
+void niyama_predictor_destroy(niyama_predictor* p);
+
+/* a1 — slack of the running decodes (§3.3; Eq. 1-3).
+ * Interactive decode: D_n - now with D_n = t_arrival + TTFT + (n-1)*TBT (Eq. 2)
+ * and n = next_token.  Non-interactive: (D_total - now)/max(1, est_remaining)
+ * with D_total = t_arrival + TTLT (Eq. 3; pacing bound R17).  Result: the
+ * minimum over decodes, +INFINITY for n = 0. */
+typedef struct {
+  int32_t interactive;   /* 1 = TTFT/TBT class, 0 = TTLT class */
+  int32_t next_token;    /* 1-based token position n produced by this iteration */
+  int32_t est_remaining; /* non-interactive: estimated tokens still to decode */
+  int32_t reserved;
+  double t_arrival, slo_ttft, slo_tbt, slo_ttlt; /* seconds */
+} niyama_decode_qos;
+niyama_status niyama_min_slack(const niyama_decode_qos* decodes, int32_t n, double now, double* slack_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NIYAMA_H_ */

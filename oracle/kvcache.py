@@ -131,6 +131,18 @@ class KVPool:
             bisect.insort(self.free, b)
         del self.length[seq]
 
+    def truncate(self, seq: int, new_len: int) -> None:
+        """Keep the first new_len tokens; blocks past ceil(new_len/B) are freed (R9)."""
+        if seq not in self.length:
+            raise OracleError(ENOSEQ, f"truncate of unknown seq {seq}")
+        if new_len < 0 or new_len > self.length[seq]:
+            raise OracleError(EINVAL, "truncate: new_len outside [0, len]")
+        keep = -(-new_len // self.B)
+        for b in self.table[seq][keep:]:
+            bisect.insort(self.free, b)
+        self.table[seq] = self.table[seq][:keep]
+        self.length[seq] = new_len
+
     # -- a3 append ----------------------------------------------------------
     def append(self, layer: int, plan: Plan, k_new: np.ndarray, v_new: np.ndarray) -> None:
         """pool[table[s][p//B]][h][p%B][:] = K_new[row][h][:] (bit copy), same for V."""

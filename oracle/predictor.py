@@ -64,6 +64,7 @@ class Sample:
 
 def features(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int]) -> np.ndarray:
     """phi for one batch; slices = [(offset, len)], decode_ctx = [ctx]."""
+    slices = [(o, n) for o, n in slices if n > 0]   # a zero-length slice is no slice
     c = sum(n for _, n in slices)
     D = len(decode_ctx)
     sum_ctx = sum(decode_ctx)

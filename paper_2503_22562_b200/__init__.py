@@ -1,0 +1,12 @@
+"""B200-native hybrid-batch paged attention for Niyama (arXiv 2503.22562).
+
+The hot path lives in libniyama.so (C ABI: include/niyama.h;
+CUDA kernels for sm_100a in csrc/).  This package is a thin ctypes binding
+with the same names; PyTorch is used by callers only for device memory,
+streams and process groups.
+"""
+from ._binding import (BF16, DEVICE_NONE, F32, KVCache, NiyamaError, Plan, PlanInfo, Predictor, get_unique_id,
+                       lib, min_slack)
+
+__all__ = ["BF16", "DEVICE_NONE", "F32", "KVCache", "NiyamaError", "Plan", "PlanInfo", "Predictor",
+           "get_unique_id", "lib", "min_slack"]

@@ -1,0 +1,339 @@
+"""ctypes binding of libniyama.so (include/niyama.h).  Argument marshalling only:
+every step of the hot path runs in the library's CUDA kernels; there is no CPU
+fallback, and importing this module fails loudly when the library is missing."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libniyama.so")
+
+OK, EINVAL, ENOBLOCKS, ENOSEQ, ESTATE, ECUDA, ENCCL, EUNSUPPORTED = range(8)
+STATUS_NAMES = ["OK", "EINVAL", "ENOBLOCKS", "ENOSEQ", "ESTATE", "ECUDA", "ENCCL", "EUNSUPPORTED"]
+BF16, F32 = 0, 1
+DEVICE_NONE = -1
+NUM_FEATURES = 6
+
+
+class NiyamaError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {message}")
+        self.status = status
+        self.code = status
+
+
+class KVConfig(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_q_heads", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32), ("block_size", C.c_int32), ("num_blocks", C.c_int32),
+                ("dtype", C.c_int), ("world_size", C.c_int32), ("rank", C.c_int32), ("device", C.c_int32)]
+
+
+class BatchDescC(C.Structure):
+    _fields_ = [("num_prefill", C.c_int32), ("prefill_seq", C.POINTER(C.c_int64)),
+                ("prefill_offset", C.POINTER(C.c_int32)), ("prefill_len", C.POINTER(C.c_int32)),
+                ("num_decode", C.c_int32), ("decode_seq", C.POINTER(C.c_int64)),
+                ("decode_ctx", C.POINTER(C.c_int32)), ("tier", C.POINTER(C.c_uint8))]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("num_rows", C.c_int32), ("num_prefill_rows", C.c_int32), ("num_decode", C.c_int32),
+                ("num_prefill_tiles", C.c_int32), ("num_decode_units", C.c_int32), ("split_len", C.c_int32),
+                ("rows_per_tile", C.c_int32), ("reserved", C.c_int32), ("sum_ctx", C.c_int64)]
+
+
+class SampleC(C.Structure):
+    _fields_ = [("chunk_len", C.c_int32), ("chunk_offset", C.c_int32), ("num_decode", C.c_int32),
+                ("sum_ctx", C.c_int64), ("seconds", C.c_double)]
+
+
+class DecodeQoSC(C.Structure):
+    _fields_ = [("interactive", C.c_int32), ("next_token", C.c_int32), ("est_remaining", C.c_int32),
+                ("reserved", C.c_int32), ("t_arrival", C.c_double), ("slo_ttft", C.c_double),
+                ("slo_tbt", C.c_double), ("slo_ttlt", C.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python paper_2503_22562_b200/build.py` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_int
+    sigs = {
+        "niyama_last_error": ([], C.c_char_p),
+        "niyama_version": ([], C.c_char_p),
+        "niyama_kv_create": ([C.POINTER(KVConfig), C.POINTER(vp)], st),
+        "niyama_kv_destroy": ([vp], None),
+        "niyama_kv_release": ([vp, i64], st),
+        "niyama_kv_truncate": ([vp, i64, i32], st),
+        "niyama_kv_block_table": ([vp, i64, C.POINTER(i32), i32, C.POINTER(i32)], st),
+        "niyama_kv_seq_len": ([vp, i64, C.POINTER(i32)], st),
+        "niyama_kv_num_free": ([vp, C.POINTER(i32)], st),
+        "niyama_kv_gather": ([vp, i32, i64, i32, vp, vp, vp], st),
+        "niyama_plan_create": ([vp, C.POINTER(BatchDescC), vp, C.POINTER(vp)], st),
+        "niyama_plan_destroy": ([vp], None),
+        "niyama_plan_get_info": ([vp, C.POINTER(PlanInfo)], st),
+        "niyama_plan_slots": ([vp, C.POINTER(i32), C.POINTER(i32), i32], st),
+        "niyama_kv_append": ([vp, vp, i32, vp, vp, vp], st),
+        "niyama_hybrid_attention": ([vp, vp, i32, vp, vp, vp, C.c_float, vp], st),
+        "niyama_comm_init": ([vp, vp], st),
+        "niyama_get_unique_id": ([vp], st),
+        "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
+        "niyama_predictor_fit": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(vp)], st),
+        "niyama_predictor_from_params": ([C.POINTER(KVConfig), C.POINTER(C.c_double), C.POINTER(vp)], st),
+        "niyama_predictor_params": ([vp, C.POINTER(C.c_double)], st),
+        "niyama_predict_iter_time": ([vp, C.POINTER(BatchDescC)], C.c_double),
+        "niyama_max_feasible_chunk": ([vp, C.POINTER(BatchDescC), i32, i32, C.c_double, i32, C.POINTER(i32),
+                                       C.POINTER(i32)], st),
+        "niyama_predictor_destroy": ([vp], None),
+        "niyama_min_slack": ([C.POINTER(DecodeQoSC), i32, C.c_double, C.POINTER(C.c_double)], st),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = res
+    return lib
+
+
+lib = _load()
+
+
+def _check(status: int):
+    if status != OK:
+        raise NiyamaError(status, lib.niyama_last_error().decode())
+
+
+def _ptr(x) -> Optional[int]:
+    """Device/host pointer of a torch tensor (must be contiguous) or a raw int."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        if hasattr(x, "is_contiguous") and not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return x.data_ptr()
+    raise TypeError(f"expected a tensor or an int pointer, got {type(x)}")
+
+
+def _stream(s) -> Optional[int]:
+    if s is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover - torch is part of the image
+            pass
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+class _Desc:
+    """Keeps the numpy buffers of a batch descriptor alive while the C struct is used."""
+
+    def __init__(self, desc):
+        ps = getattr(desc, "prefill_seq", []) or []
+        ds = getattr(desc, "decode_seq", []) or []
+        self.ps = np.ascontiguousarray(ps, dtype=np.int64)
+        self.po = np.ascontiguousarray(getattr(desc, "prefill_offset", []) or [], dtype=np.int32)
+        self.pl = np.ascontiguousarray(getattr(desc, "prefill_len", []) or [], dtype=np.int32)
+        self.ds = np.ascontiguousarray(ds, dtype=np.int64)
+        self.dc = np.ascontiguousarray(getattr(desc, "decode_ctx", []) or [], dtype=np.int32)
+        tier = getattr(desc, "tier", None)
+        self.tier = None if tier is None else np.ascontiguousarray(tier, dtype=np.uint8)
+        if len(self.po) != len(self.ps) or len(self.pl) != len(self.ps) or len(self.dc) != len(self.ds):
+            raise ValueError("descriptor arrays disagree in length")
+        if self.tier is not None and len(self.tier) != len(self.ps) + len(self.ds):
+            raise ValueError("tier array length")
+
+        def p(a, t):
+            return a.ctypes.data_as(C.POINTER(t)) if a is not None and len(a) else None
+
+        self.c = BatchDescC(len(self.ps), p(self.ps, C.c_int64), p(self.po, C.c_int32), p(self.pl, C.c_int32),
+                            len(self.ds), p(self.ds, C.c_int64), p(self.dc, C.c_int32), p(self.tier, C.c_uint8))
+
+
+def _cfg(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_blocks, dtype, world_size, rank, device):
+    dt = {"bf16": BF16, "f32": F32, BF16: BF16, F32: F32}[dtype]
+    return KVConfig(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_blocks, dt, world_size, rank,
+                    DEVICE_NONE if device is None else device)
+
+
+class Plan:
+    def __init__(self, kv: "KVCache", handle: int):
+        self.kv = kv
+        self.handle = handle
+
+    def info(self) -> PlanInfo:
+        out = PlanInfo()
+        _check(lib.niyama_plan_get_info(self.handle, C.byref(out)))
+        return out
+
+    def slots(self):
+        n = self.info().num_rows
+        blk = np.zeros(max(n, 1), np.int32)
+        slot = np.zeros(max(n, 1), np.int32)
+        _check(lib.niyama_plan_slots(self.handle, blk.ctypes.data_as(C.POINTER(C.c_int32)),
+                                     slot.ctypes.data_as(C.POINTER(C.c_int32)), n))
+        return list(zip(blk[:n].tolist(), slot[:n].tolist()))
+
+    def close(self):
+        if self.handle:
+            lib.niyama_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class KVCache:
+    """Library-owned paged KV pool (niyama_kv)."""
+
+    def __init__(self, num_layers: int, num_q_heads: int, num_kv_heads: int, head_dim: int, num_blocks: int,
+                 block_size: int = 16, dtype: str = "bf16", world_size: int = 1, rank: int = 0,
+                 device: Optional[int] = 0):
+        self.cfg = _cfg(num_layers, num_q_heads, num_kv_heads, head_dim, block_size, num_blocks, dtype, world_size,
+                        rank, device)
+        h = C.c_void_p()
+        _check(lib.niyama_kv_create(C.byref(self.cfg), C.byref(h)))
+        self.handle = h.value
+        self.dtype = dtype
+
+    # -- bookkeeping
+    def plan(self, desc, stream=None) -> Plan:
+        d = _Desc(desc)
+        h = C.c_void_p()
+        _check(lib.niyama_plan_create(self.handle, C.byref(d.c), _stream(stream), C.byref(h)))
+        return Plan(self, h.value)
+
+    def release(self, seq: int):
+        _check(lib.niyama_kv_release(self.handle, int(seq)))
+
+    def truncate(self, seq: int, new_len: int):
+        _check(lib.niyama_kv_truncate(self.handle, int(seq), int(new_len)))
+
+    def block_table(self, seq: int):
+        n = C.c_int32()
+        _check(lib.niyama_kv_block_table(self.handle, int(seq), None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.int32)
+        _check(lib.niyama_kv_block_table(self.handle, int(seq), out.ctypes.data_as(C.POINTER(C.c_int32)), n.value,
+                                         C.byref(n)))
+        return out[: n.value].tolist()
+
+    def seq_len(self, seq: int) -> int:
+        n = C.c_int32()
+        _check(lib.niyama_kv_seq_len(self.handle, int(seq), C.byref(n)))
+        return n.value
+
+    def num_free(self) -> int:
+        n = C.c_int32()
+        _check(lib.niyama_kv_num_free(self.handle, C.byref(n)))
+        return n.value
+
+    # -- device work
+    def append(self, plan: Plan, layer: int, k_new, v_new, stream=None):
+        _check(lib.niyama_kv_append(self.handle, plan.handle, layer, _ptr(k_new), _ptr(v_new), _stream(stream)))
+
+    def attention(self, plan: Plan, layer: int, q, o, lse=None, scale: float = 0.0, stream=None):
+        _check(lib.niyama_hybrid_attention(self.handle, plan.handle, layer, _ptr(q), _ptr(o), _ptr(lse),
+                                           float(scale), _stream(stream)))
+
+    def gather(self, layer: int, seq: int, n: int, k_out, v_out, stream=None):
+        _check(lib.niyama_kv_gather(self.handle, layer, int(seq), n, _ptr(k_out), _ptr(v_out), _stream(stream)))
+
+    def comm_init(self, unique_id: bytes):
+        buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(lib.niyama_comm_init(self.handle, buf))
+
+    def allgather_heads(self, plan: Plan, o_full, lse_full=None, stream=None):
+        _check(lib.niyama_allgather_heads(self.handle, plan.handle, _ptr(o_full), _ptr(lse_full), _stream(stream)))
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.niyama_kv_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.niyama_get_unique_id(buf))
+    return buf.raw
+
+
+class Predictor:
+    """Iteration-time predictor (niyama_predictor), features per include/niyama.h (a8)."""
+
+    def __init__(self, handle: int):
+        self.handle = handle
+
+    @staticmethod
+    def shape_cfg(num_q_heads, num_kv_heads, head_dim, dtype="bf16", world_size=1):
+        return _cfg(1, num_q_heads, num_kv_heads, head_dim, 16, 1, dtype, world_size, 0, None)
+
+    @classmethod
+    def fit(cls, cfg: KVConfig, samples: Sequence) -> "Predictor":
+        arr = (SampleC * len(samples))(*[SampleC(s.chunk_len, s.chunk_offset, s.num_decode, s.sum_ctx, s.seconds)
+                                         for s in samples])
+        h = C.c_void_p()
+        _check(lib.niyama_predictor_fit(C.byref(cfg), arr, len(samples), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def from_params(cls, cfg: KVConfig, theta) -> "Predictor":
+        th = (C.c_double * NUM_FEATURES)(*[float(x) for x in theta])
+        h = C.c_void_p()
+        _check(lib.niyama_predictor_from_params(C.byref(cfg), th, C.byref(h)))
+        return cls(h.value)
+
+    def params(self) -> np.ndarray:
+        th = (C.c_double * NUM_FEATURES)()
+        _check(lib.niyama_predictor_params(self.handle, th))
+        return np.array(list(th))
+
+    def predict(self, desc) -> float:
+        d = _Desc(desc)
+        return lib.niyama_predict_iter_time(self.handle, C.byref(d.c))
+
+    def max_feasible_chunk(self, decode_ctx, chunk_offset, prefill_remaining, slack, max_chunk):
+        class _D:
+            pass
+        dd = _D()
+        dd.decode_seq = list(range(len(decode_ctx)))
+        dd.decode_ctx = list(decode_ctx)
+        d = _Desc(dd)
+        c, inf = C.c_int32(), C.c_int32()
+        _check(lib.niyama_max_feasible_chunk(self.handle, C.byref(d.c), chunk_offset, prefill_remaining,
+                                             float(slack), max_chunk, C.byref(c), C.byref(inf)))
+        return c.value, bool(inf.value)
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib.niyama_predictor_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+
+def min_slack(decodes, now: float) -> float:
+    """decodes: objects with interactive, t_arrival, slo_ttft, slo_tbt, slo_ttlt, next_token, est_remaining."""
+    arr = (DecodeQoSC * max(1, len(decodes)))(*[
+        DecodeQoSC(int(bool(q.interactive)), int(q.next_token), int(q.est_remaining), 0, float(q.t_arrival),
+                   float(q.slo_ttft), float(q.slo_tbt), float(q.slo_ttlt)) for q in decodes])
+    out = C.c_double()
+    _check(lib.niyama_min_slack(arr, len(decodes), float(now), C.byref(out)))
+    return out.value

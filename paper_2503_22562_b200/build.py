@@ -1,0 +1,67 @@
+"""Build libniyama.so in-tree for sm_100a (nvcc cross-compiles; no GPU needed).
+
+    python paper_2503_22562_b200/build.py [--force]     (or __graft_entry__.build())
+
+kernels.cu is compiled by nvcc with -gencode arch=compute_100a,code=sm_100a
+-lineinfo; runtime.cpp by the host compiler; the shared library links the
+static CUDA runtime and the NCCL that torch loads (site-packages/nvidia/nccl,
+2.28.x) so a process never holds two NCCLs.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+import sysconfig
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+INCLUDE = os.path.join(ROOT, "include")
+BUILD = os.path.join(HERE, "_build")
+LIB = os.path.join(HERE, "libniyama.so")
+CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+NVCC = os.path.join(CUDA, "bin", "nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    purelib = sysconfig.get_paths()["purelib"]
+    base = os.path.join(purelib, "nvidia", "nccl")
+    return os.path.join(base, "include"), os.path.join(base, "lib")
+
+
+def _run(cmd):
+    print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    nccl_inc, nccl_lib = nccl_dirs()
+    headers = [os.path.join(CSRC, f) for f in ("internal.h", "ptx.cuh")] + [os.path.join(INCLUDE, "niyama.h")]
+    k_src = os.path.join(CSRC, "kernels.cu")
+    r_src = os.path.join(CSRC, "runtime.cpp")
+    k_obj = os.path.join(BUILD, "kernels.o")
+    r_obj = os.path.join(BUILD, "runtime.o")
+    common = ["-O3", "-std=c++17", "-I", INCLUDE, "-I", CSRC]
+    if force or _stale(k_obj, [k_src] + headers):
+        _run([NVCC, *ARCH, *common, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC", "-c", k_src, "-o", k_obj])
+    if force or _stale(r_obj, [r_src] + headers):
+        _run([os.environ.get("CXX", "g++"), *common, "-I", os.path.join(CUDA, "include"), "-I", nccl_inc, "-fPIC",
+              "-Wall", "-Wextra", "-Wno-unused-parameter", "-c", r_src, "-o", r_obj])
+    if force or _stale(LIB, [k_obj, r_obj]):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, k_obj, r_obj, "-L", nccl_lib,
+              "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "--no-undefined"])
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv)

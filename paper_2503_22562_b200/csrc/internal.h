@@ -1,0 +1,92 @@
+// Internal structures shared by the host runtime (runtime.cpp) and the
+// sm_100a kernels (kernels.cu).  Not part of the public C ABI (include/niyama.h).
+#pragma once
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace niyama {
+
+// KV pool physical layout:
+//   pool[layer][K=0|V=1][block][kv_head][panel][slot][128 B]
+// A (block, kv head) chunk is block_size * head_dim * elt bytes, contiguous.
+// Each token row (head_dim * elt bytes) is cut into 128-byte panels; inside a
+// panel the 16-byte chunk c of the row at slot s is stored at chunk position
+// c ^ (s & 7) — the tcgen05 / TMA SWIZZLE_128B pattern.  A bulk copy of any
+// 8-row-aligned run of a panel into 1024-byte aligned shared memory is
+// therefore already a canonical UMMA SW128 operand (K-major for K, MN-major
+// for V) and is bank-conflict free for ldmatrix.
+
+// Prefill tile: 128 MMA rows = g query heads x R chunk rows (R = 128/g) of one
+// kv head, over keys [0, nkeys).  (a4)
+struct PrefillTile {
+  int32_t tbl;    // offset of the sequence's block table in the tables array
+  int32_t o;      // slice offset (positions of rows are o + t0 + i)
+  int32_t c;      // slice length
+  int32_t t0;     // first slice row of this tile
+  int32_t row0;   // batch row of slice row 0
+  int32_t kvh;    // local kv head
+  int32_t nkeys;  // o + min(t0 + R, c): keys visible to the tile's last row
+  int32_t nblk;   // blocks of the table covering nkeys
+};
+
+// Decode unit: one decode row, one kv head, keys [k0, k1).  (a5)
+struct DecodeUnit {
+  int32_t tbl;
+  int32_t ctx;
+  int32_t row;     // batch row
+  int32_t kvh;
+  int32_t k0, k1;  // k0 multiple of 16
+  int32_t split;   // split index within the (row, kv head) pair
+  int32_t nsplit;
+  int32_t pbase;   // partial index of split 0 of this pair
+  int32_t pair;    // decode index * Hkv_loc + kvh (merge counter)
+  int32_t pad0, pad1;
+};
+
+// Per-row info for the generic (f32) path.
+struct RowInfo {
+  int32_t tbl;
+  int32_t n;  // visible keys
+};
+
+struct AttnParams {
+  const uint8_t* pool_k;  // layer base of K
+  const uint8_t* pool_v;  // layer base of V
+  const void* q;
+  void* o;
+  float* lse;
+  const int32_t* tables;
+  const PrefillTile* tiles;
+  const DecodeUnit* units;
+  const RowInfo* rows;
+  float* part_o;    // [n_partials][g][d]
+  float* part_ml;   // [n_partials][g][2]
+  int32_t* counters;  // [num_decode * Hkv] merge counters (self-resetting)
+  int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter (self-resetting)
+  int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
+  int32_t T, Hq, Hkv, d, B, g, R;
+  int32_t n_tiles, n_units;
+  float scale_log2;     // softmax scale * log2(e)
+};
+
+struct AppendParams {
+  uint8_t* pool_k;
+  uint8_t* pool_v;
+  const uint8_t* k_new;
+  const uint8_t* v_new;
+  const int32_t* slot_map;  // [T] block * B + slot
+  int64_t chunk_bytes;
+  int32_t T, Hkv, row_bytes, B;
+};
+
+// Launchers (kernels.cu).  Return cudaSuccess or the launch error.
+cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
+cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const int32_t* table, int32_t len,
+                          int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, uint8_t* k_out,
+                          uint8_t* v_out, cudaStream_t s);
+cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s);
+cudaError_t launch_attention_generic_f32(const AttnParams& p, cudaStream_t s);
+int attention_bf16_smem_bytes();
+
+}  // namespace niyama

@@ -1,0 +1,938 @@
+// Host runtime of the Niyama hybrid-batch paged-attention library: KV pool and
+// block allocator, per-iteration planner (a2), launch wrappers (a3-a6), NCCL
+// head all-gather (a7), iteration-time predictor (a8) and slack (a1).
+// C ABI: include/niyama.h.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <set>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "internal.h"
+#include "niyama.h"
+
+using namespace niyama;
+
+namespace {
+
+thread_local std::string g_err;
+
+niyama_status fail(niyama_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define NY_CUDA(x)                                                                         \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) return fail(NIYAMA_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define NY_NCCL(x)                                                                          \
+  do {                                                                                      \
+    ncclResult_t r_ = (x);                                                                  \
+    if (r_ != ncclSuccess) return fail(NIYAMA_ENCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Seq {
+  std::vector<int32_t> blocks;
+  int32_t len = 0;
+};
+
+}  // namespace
+
+struct niyama_kv {
+  niyama_kv_config cfg{};
+  int hq = 0, hkv = 0, d = 0, B = 0, elt = 0, g = 0, row_bytes = 0;
+  int64_t chunk_bytes = 0;  // one (block, kv head) chunk
+  int64_t half_bytes = 0;   // K (or V) of one layer
+  bool has_device = false;
+  int num_sms = 148;
+  uint8_t* pool = nullptr;
+  std::set<int32_t> free_;
+  std::unordered_map<int64_t, Seq> seqs;
+  ncclComm_t comm = nullptr;
+  void* staging = nullptr;
+  size_t staging_cap = 0;
+  cudaEvent_t staging_ev = nullptr;
+  bool staging_pending = false;
+};
+
+struct niyama_plan {
+  niyama_kv* kv = nullptr;
+  cudaStream_t stream = nullptr;
+  int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0, n_partials = 0;
+  int64_t sum_ctx = 0;
+  std::vector<int32_t> slot_map;
+  std::vector<int32_t> tables;
+  std::vector<PrefillTile> tiles;
+  std::vector<DecodeUnit> units;
+  std::vector<RowInfo> rows;
+  uint8_t* dbuf = nullptr;
+  int32_t* d_slot = nullptr;
+  int32_t* d_tables = nullptr;
+  PrefillTile* d_tiles = nullptr;
+  DecodeUnit* d_units = nullptr;
+  RowInfo* d_rows = nullptr;
+  float* d_part_o = nullptr;
+  float* d_part_ml = nullptr;
+  int32_t* d_counters = nullptr;
+  int32_t* d_work = nullptr;
+};
+
+struct niyama_predictor {
+  int hq = 0, hkv = 0, d = 0, elt = 0;
+  double fpeak = NIYAMA_F_PEAK_BF16;
+  double theta[NIYAMA_NUM_FEATURES] = {0, 0, 0, 0, 0, 0};
+};
+
+extern "C" const char* niyama_last_error(void) { return g_err.c_str(); }
+extern "C" const char* niyama_version(void) { return "niyama-b200 0.1 (sm_100a)"; }
+
+// ================================================================ KV pool
+extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv** out) {
+  if (!cfg || !out) return fail(NIYAMA_EINVAL, "cfg/out is NULL");
+  *out = nullptr;
+  const niyama_kv_config& c = *cfg;
+  if (c.num_layers < 1) return fail(NIYAMA_EINVAL, "num_layers < 1");
+  if (c.num_q_heads < 1 || c.num_kv_heads < 1 || c.num_q_heads % c.num_kv_heads)
+    return fail(NIYAMA_EINVAL, "num_q_heads must be a positive multiple of num_kv_heads");
+  const int g = c.num_q_heads / c.num_kv_heads;
+  if (g > 128 || (g & (g - 1))) return fail(NIYAMA_EUNSUPPORTED, "num_q_heads/num_kv_heads must be a power of two <= 128");
+  if (c.world_size < 1 || c.rank < 0 || c.rank >= c.world_size) return fail(NIYAMA_EINVAL, "world_size/rank");
+  if (c.num_kv_heads % c.world_size) return fail(NIYAMA_EINVAL, "num_kv_heads must divide by world_size");
+  if (c.dtype != NIYAMA_BF16 && c.dtype != NIYAMA_F32) return fail(NIYAMA_EINVAL, "dtype");
+  const int elt = c.dtype == NIYAMA_BF16 ? 2 : 4;
+  if (c.head_dim < 1 || (c.head_dim * elt) % 128) return fail(NIYAMA_EUNSUPPORTED, "head_dim*elt must be a multiple of 128 bytes");
+  if (c.block_size != 16 && c.block_size != 32 && c.block_size != 64 && c.block_size != 128)
+    return fail(NIYAMA_EUNSUPPORTED, "block_size must be 16, 32, 64 or 128");
+  if (c.num_blocks < 1) return fail(NIYAMA_EINVAL, "num_blocks < 1");
+  if (static_cast<int64_t>(c.num_blocks) * c.block_size >= (int64_t(1) << 31))
+    return fail(NIYAMA_EINVAL, "num_blocks*block_size must be < 2^31");
+  auto* kv = new niyama_kv();
+  kv->cfg = c;
+  kv->hq = c.num_q_heads / c.world_size;
+  kv->hkv = c.num_kv_heads / c.world_size;
+  kv->d = c.head_dim;
+  kv->B = c.block_size;
+  kv->elt = elt;
+  kv->g = g;
+  kv->row_bytes = c.head_dim * elt;
+  kv->chunk_bytes = static_cast<int64_t>(c.block_size) * kv->row_bytes;
+  kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
+  for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
+  if (c.device != NIYAMA_DEVICE_NONE) {
+    kv->has_device = true;
+    cudaError_t e = cudaSetDevice(c.device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&kv->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+    const size_t bytes = static_cast<size_t>(kv->half_bytes) * 2 * c.num_layers;
+    if (e == cudaSuccess) e = cudaMalloc(&kv->pool, bytes);
+    if (e == cudaSuccess) e = cudaMemset(kv->pool, 0, bytes);  // stale slots stay finite (masked, P = 0)
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->staging_ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      if (kv->pool) cudaFree(kv->pool);
+      delete kv;
+      return fail(NIYAMA_ECUDA, std::string("kv_create: ") + cudaGetErrorString(e));
+    }
+  }
+  *out = kv;
+  return NIYAMA_OK;
+}
+
+extern "C" void niyama_kv_destroy(niyama_kv* kv) {
+  if (!kv) return;
+  if (kv->has_device) {
+    cudaSetDevice(kv->cfg.device);
+    cudaDeviceSynchronize();
+    if (kv->comm) ncclCommDestroy(kv->comm);
+    if (kv->pool) cudaFree(kv->pool);
+    if (kv->staging) cudaFreeHost(kv->staging);
+    if (kv->staging_ev) cudaEventDestroy(kv->staging_ev);
+  }
+  delete kv;
+}
+
+extern "C" niyama_status niyama_kv_release(niyama_kv* kv, int64_t seq_id) {
+  if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");
+  auto it = kv->seqs.find(seq_id);
+  if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "release: unknown seq " + std::to_string(seq_id));
+  for (int32_t b : it->second.blocks) kv->free_.insert(b);
+  kv->seqs.erase(it);
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_truncate(niyama_kv* kv, int64_t seq_id, int32_t new_len) {
+  if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");
+  auto it = kv->seqs.find(seq_id);
+  if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "truncate: unknown seq " + std::to_string(seq_id));
+  Seq& q = it->second;
+  if (new_len < 0 || new_len > q.len) return fail(NIYAMA_EINVAL, "truncate: new_len outside [0, cached length]");
+  const size_t keep = static_cast<size_t>(ceil_div(new_len, kv->B));
+  for (size_t k = keep; k < q.blocks.size(); ++k) kv->free_.insert(q.blocks[k]);
+  q.blocks.resize(keep);
+  q.len = new_len;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_block_table(const niyama_kv* kv, int64_t seq_id, int32_t* out, int32_t cap,
+                                               int32_t* n) {
+  if (!kv || !n) return fail(NIYAMA_EINVAL, "kv/n is NULL");
+  auto it = kv->seqs.find(seq_id);
+  if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "block_table: unknown seq " + std::to_string(seq_id));
+  *n = static_cast<int32_t>(it->second.blocks.size());
+  if (out && cap > 0)
+    std::memcpy(out, it->second.blocks.data(), sizeof(int32_t) * std::min<size_t>(cap, it->second.blocks.size()));
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_seq_len(const niyama_kv* kv, int64_t seq_id, int32_t* len) {
+  if (!kv || !len) return fail(NIYAMA_EINVAL, "kv/len is NULL");
+  auto it = kv->seqs.find(seq_id);
+  if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "seq_len: unknown seq " + std::to_string(seq_id));
+  *len = it->second.len;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_num_free(const niyama_kv* kv, int32_t* n) {
+  if (!kv || !n) return fail(NIYAMA_EINVAL, "kv/n is NULL");
+  *n = static_cast<int32_t>(kv->free_.size());
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t seq_id, int32_t len, void* k_out,
+                                          void* v_out, niyama_stream stream) {
+  if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");
+  if (!kv->has_device) return fail(NIYAMA_EUNSUPPORTED, "no device (NIYAMA_DEVICE_NONE)");
+  if (layer < 0 || layer >= kv->cfg.num_layers) return fail(NIYAMA_EINVAL, "layer out of range");
+  auto it = kv->seqs.find(seq_id);
+  if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "gather: unknown seq " + std::to_string(seq_id));
+  if (len < 0 || len > it->second.len) return fail(NIYAMA_EINVAL, "gather: len exceeds cached length");
+  if (len == 0) return NIYAMA_OK;
+  if (!k_out || !v_out) return fail(NIYAMA_EINVAL, "k_out/v_out is NULL");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const auto& tbl = it->second.blocks;
+  int32_t* d_tbl = nullptr;
+  NY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tbl), tbl.size() * sizeof(int32_t), s));
+  NY_CUDA(cudaMemcpyAsync(d_tbl, tbl.data(), tbl.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  const uint8_t* pk = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
+  NY_CUDA(launch_gather(pk, pk + kv->half_bytes, d_tbl, len, kv->hkv, kv->row_bytes, kv->B, kv->chunk_bytes,
+                        static_cast<uint8_t*>(k_out), static_cast<uint8_t*>(v_out), s));
+  NY_CUDA(cudaFreeAsync(d_tbl, s));
+  NY_CUDA(cudaStreamSynchronize(s));  // the host table must outlive the pageable copy
+  return NIYAMA_OK;
+}
+
+// ================================================================ planner
+namespace {
+
+// Decode split length (a5): a power of two >= 64 chosen from batch totals only
+// (sum ctx * Hkv against 4 units per resident warp), so split boundaries never
+// depend on scheduling and results stay bitwise deterministic.
+int32_t choose_split_len(int64_t sum_ctx, int hkv, int num_sms) {
+  const int64_t target = 4LL * num_sms * 8;
+  const int64_t raw = ceil_div(std::max<int64_t>(1, sum_ctx * hkv), target);
+  int32_t s = 64;
+  while (s < raw && s < 8192) s *= 2;
+  return s;
+}
+
+}  // namespace
+
+extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_desc* desc, niyama_stream stream,
+                                            niyama_plan** out) {
+  if (!kv || !desc || !out) return fail(NIYAMA_EINVAL, "kv/desc/out is NULL");
+  *out = nullptr;
+  const int P = desc->num_prefill, D = desc->num_decode;
+  if (P < 0 || D < 0) return fail(NIYAMA_EINVAL, "num_prefill/num_decode < 0");
+  if (P > 0 && (!desc->prefill_seq || !desc->prefill_offset || !desc->prefill_len))
+    return fail(NIYAMA_EINVAL, "prefill arrays are NULL");
+  if (D > 0 && (!desc->decode_seq || !desc->decode_ctx)) return fail(NIYAMA_EINVAL, "decode arrays are NULL");
+  std::unordered_set<int64_t> seen;
+  for (int i = 0; i < P; ++i)
+    if (!seen.insert(desc->prefill_seq[i]).second)
+      return fail(NIYAMA_EINVAL, "seq " + std::to_string(desc->prefill_seq[i]) + " appears twice in one batch");
+  for (int j = 0; j < D; ++j)
+    if (!seen.insert(desc->decode_seq[j]).second)
+      return fail(NIYAMA_EINVAL, "seq " + std::to_string(desc->decode_seq[j]) + " appears twice in one batch");
+  // ---- validate (no side effects)
+  std::vector<std::pair<int64_t, int32_t>> new_len;
+  new_len.reserve(P + D);
+  int64_t T = 0;
+  for (int i = 0; i < P; ++i) {
+    const int64_t s = desc->prefill_seq[i];
+    const int32_t o = desc->prefill_offset[i], c = desc->prefill_len[i];
+    if (o < 0 || c < 0) return fail(NIYAMA_EINVAL, "prefill_offset/prefill_len < 0 (slice " + std::to_string(i) + ")");
+    if (static_cast<int64_t>(o) + c > std::numeric_limits<int32_t>::max() / 2)
+      return fail(NIYAMA_EINVAL, "prefill_offset+prefill_len too large");
+    auto it = kv->seqs.find(s);
+    const int32_t cur = it == kv->seqs.end() ? 0 : it->second.len;
+    if (cur != o)
+      return fail(NIYAMA_ESTATE, "seq " + std::to_string(s) + ": cached " + std::to_string(cur) +
+                                     " != prefill_offset " + std::to_string(o));
+    new_len.emplace_back(s, o + c);
+    T += c;
+  }
+  for (int j = 0; j < D; ++j) {
+    const int64_t s = desc->decode_seq[j];
+    const int32_t ctx = desc->decode_ctx[j];
+    if (ctx < 1) return fail(NIYAMA_EINVAL, "decode_ctx < 1 (decode " + std::to_string(j) + ")");
+    auto it = kv->seqs.find(s);
+    if (it == kv->seqs.end()) return fail(NIYAMA_ENOSEQ, "decode of unknown seq " + std::to_string(s));
+    if (it->second.len != ctx - 1)
+      return fail(NIYAMA_ESTATE, "seq " + std::to_string(s) + ": cached " + std::to_string(it->second.len) +
+                                     " != decode_ctx-1 " + std::to_string(ctx - 1));
+    new_len.emplace_back(s, ctx);
+    T += 1;
+  }
+  if (T > std::numeric_limits<int32_t>::max() / 4) return fail(NIYAMA_EINVAL, "batch too large");
+  int64_t need_total = 0;
+  for (auto& [s, n] : new_len) {
+    auto it = kv->seqs.find(s);
+    const int64_t have = it == kv->seqs.end() ? 0 : static_cast<int64_t>(it->second.blocks.size());
+    need_total += std::max<int64_t>(0, ceil_div(n, kv->B) - have);
+  }
+  if (need_total > static_cast<int64_t>(kv->free_.size()))
+    return fail(NIYAMA_ENOBLOCKS, "need " + std::to_string(need_total) + " blocks, " +
+                                      std::to_string(kv->free_.size()) + " free");
+  // staging buffer of the previous plan must be free before we reuse it
+  if (kv->has_device && kv->staging_pending) {
+    NY_CUDA(cudaEventSynchronize(kv->staging_ev));
+    kv->staging_pending = false;
+  }
+  // ---- commit: smallest free ids, descriptor order (R9); remember how to undo it
+  struct Undo { int64_t seq; bool existed; size_t nblocks; int32_t len; };
+  std::vector<Undo> undo;
+  undo.reserve(new_len.size());
+  for (auto& [s, n] : new_len) {
+    auto it = kv->seqs.find(s);
+    undo.push_back(it == kv->seqs.end() ? Undo{s, false, 0, 0} : Undo{s, true, it->second.blocks.size(), it->second.len});
+  }
+  auto rollback = [&]() {
+    for (auto it = undo.rbegin(); it != undo.rend(); ++it) {
+      Seq& q = kv->seqs[it->seq];
+      for (size_t k = it->nblocks; k < q.blocks.size(); ++k) kv->free_.insert(q.blocks[k]);
+      if (!it->existed) {
+        kv->seqs.erase(it->seq);
+      } else {
+        q.blocks.resize(it->nblocks);
+        q.len = it->len;
+      }
+    }
+  };
+  for (auto& [s, n] : new_len) {
+    Seq& q = kv->seqs[s];
+    const int64_t need = std::max<int64_t>(0, ceil_div(n, kv->B) - static_cast<int64_t>(q.blocks.size()));
+    for (int64_t k = 0; k < need; ++k) {
+      auto fit = kv->free_.begin();
+      q.blocks.push_back(*fit);
+      kv->free_.erase(fit);
+    }
+    q.len = n;
+  }
+  // ---- host metadata
+  auto* pl = new niyama_plan();
+  pl->kv = kv;
+  pl->stream = reinterpret_cast<cudaStream_t>(stream);
+  pl->T = static_cast<int32_t>(T);
+  pl->D = D;
+  const int B = kv->B, g = kv->g, hkv = kv->hkv;
+  std::vector<int32_t> tbl_off(P + D);
+  for (int k = 0; k < P + D; ++k) {
+    const Seq& q = kv->seqs[new_len[k].first];
+    tbl_off[k] = static_cast<int32_t>(pl->tables.size());
+    pl->tables.insert(pl->tables.end(), q.blocks.begin(), q.blocks.end());
+  }
+  if (pl->tables.empty()) pl->tables.push_back(0);
+  pl->slot_map.reserve(T);
+  pl->rows.reserve(T);
+  std::vector<int32_t> row0(P);
+  int32_t row = 0;
+  for (int i = 0; i < P; ++i) {
+    const Seq& q = kv->seqs[desc->prefill_seq[i]];
+    row0[i] = row;
+    const int32_t o = desc->prefill_offset[i];
+    for (int32_t k = 0; k < desc->prefill_len[i]; ++k, ++row) {
+      const int32_t pos = o + k;
+      pl->slot_map.push_back(q.blocks[pos / B] * B + pos % B);
+      pl->rows.push_back(RowInfo{tbl_off[i], pos + 1});
+    }
+  }
+  pl->prefill_rows = row;
+  for (int j = 0; j < D; ++j, ++row) {
+    const Seq& q = kv->seqs[desc->decode_seq[j]];
+    const int32_t pos = desc->decode_ctx[j] - 1;
+    pl->slot_map.push_back(q.blocks[pos / B] * B + pos % B);
+    pl->rows.push_back(RowInfo{tbl_off[P + j], pos + 1});
+    pl->sum_ctx += desc->decode_ctx[j];
+  }
+  auto tier_of = [&](int k) -> int { return desc->tier ? desc->tier[k] : 0; };
+  // prefill tiles (a4): 128 MMA rows = g heads x R rows; longest first
+  pl->R = 128 / g;
+  {
+    struct Key { int32_t nkeys; int tier; int idx; };
+    std::vector<Key> keys;
+    for (int i = 0; i < P; ++i) {
+      const int32_t o = desc->prefill_offset[i], c = desc->prefill_len[i];
+      for (int32_t t0 = 0; t0 < c; t0 += pl->R) {
+        const int32_t nkeys = o + std::min(t0 + pl->R, c);
+        for (int h = 0; h < hkv; ++h) {
+          PrefillTile t{tbl_off[i], o, c, t0, row0[i], h, nkeys, static_cast<int32_t>(ceil_div(nkeys, B))};
+          keys.push_back(Key{nkeys, tier_of(i), static_cast<int>(pl->tiles.size())});
+          pl->tiles.push_back(t);
+        }
+      }
+    }
+    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+      return a.nkeys != b.nkeys ? a.nkeys > b.nkeys : a.tier < b.tier;
+    });
+    std::vector<PrefillTile> sorted;
+    sorted.reserve(keys.size());
+    for (auto& k : keys) sorted.push_back(pl->tiles[k.idx]);
+    pl->tiles.swap(sorted);
+  }
+  // decode units (a5): split [0, ctx) into split_len pieces; longest first
+  pl->split_len = choose_split_len(pl->sum_ctx, hkv, kv->num_sms);
+  {
+    struct Key { int32_t len; int tier; int idx; };
+    std::vector<Key> keys;
+    int32_t pbase = 0;
+    for (int j = 0; j < D; ++j) {
+      const int32_t ctx = desc->decode_ctx[j];
+      const int32_t ns = static_cast<int32_t>(ceil_div(ctx, pl->split_len));
+      for (int h = 0; h < hkv; ++h) {
+        for (int32_t s = 0; s < ns; ++s) {
+          DecodeUnit u{};
+          u.tbl = tbl_off[P + j];
+          u.ctx = ctx;
+          u.row = pl->prefill_rows + j;
+          u.kvh = h;
+          u.k0 = s * pl->split_len;
+          u.k1 = std::min(ctx, u.k0 + pl->split_len);
+          u.split = s;
+          u.nsplit = ns;
+          u.pbase = ns > 1 ? pbase : -1;
+          u.pair = j * hkv + h;
+          keys.push_back(Key{u.k1 - u.k0, tier_of(P + j), static_cast<int>(pl->units.size())});
+          pl->units.push_back(u);
+        }
+        if (ns > 1) pbase += ns;
+      }
+    }
+    pl->n_partials = pbase;
+    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
+      return a.len != b.len ? a.len > b.len : a.tier < b.tier;
+    });
+    std::vector<DecodeUnit> sorted;
+    sorted.reserve(keys.size());
+    for (auto& k : keys) sorted.push_back(pl->units[k.idx]);
+    pl->units.swap(sorted);
+  }
+  // ---- device copy: one allocation, one H2D
+  if (kv->has_device) {
+    const size_t A = 256;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+      size_t o = off;
+      off = align_up(off + std::max<size_t>(bytes, 4), A);
+      return o;
+    };
+    const size_t o_slot = take(pl->slot_map.size() * 4);
+    const size_t o_tbl = take(pl->tables.size() * 4);
+    const size_t o_tiles = take(pl->tiles.size() * sizeof(PrefillTile));
+    const size_t o_units = take(pl->units.size() * sizeof(DecodeUnit));
+    const size_t o_rows = take(pl->rows.size() * sizeof(RowInfo));
+    const size_t meta_bytes = off;
+    const size_t o_part_o = take(static_cast<size_t>(pl->n_partials) * g * kv->d * 4);
+    const size_t o_part_ml = take(static_cast<size_t>(pl->n_partials) * g * 2 * 4);
+    const size_t o_cnt = take(static_cast<size_t>(D) * hkv * 4);
+    const size_t o_work = take(16);
+    const size_t total = off;
+    cudaStream_t s = pl->stream;
+    cudaError_t e = cudaSetDevice(kv->cfg.device);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&pl->dbuf), total, s);
+    if (e == cudaSuccess && kv->staging_cap < meta_bytes) {
+      if (kv->staging) cudaFreeHost(kv->staging);
+      kv->staging = nullptr;
+      kv->staging_cap = 0;
+      e = cudaMallocHost(&kv->staging, std::max<size_t>(meta_bytes, 1 << 20));
+      if (e == cudaSuccess) kv->staging_cap = std::max<size_t>(meta_bytes, 1 << 20);
+    }
+    if (e == cudaSuccess) {
+      uint8_t* h = static_cast<uint8_t*>(kv->staging);
+      std::memcpy(h + o_slot, pl->slot_map.data(), pl->slot_map.size() * 4);
+      std::memcpy(h + o_tbl, pl->tables.data(), pl->tables.size() * 4);
+      std::memcpy(h + o_tiles, pl->tiles.data(), pl->tiles.size() * sizeof(PrefillTile));
+      std::memcpy(h + o_units, pl->units.data(), pl->units.size() * sizeof(DecodeUnit));
+      std::memcpy(h + o_rows, pl->rows.data(), pl->rows.size() * sizeof(RowInfo));
+      e = cudaMemcpyAsync(pl->dbuf, h, meta_bytes, cudaMemcpyHostToDevice, s);
+    }
+    if (e == cudaSuccess) e = cudaMemsetAsync(pl->dbuf + o_cnt, 0, total - o_cnt, s);
+    if (e == cudaSuccess) e = cudaEventRecord(kv->staging_ev, s);
+    if (e != cudaSuccess) {
+      rollback();  // the error leaves the pool as it was
+      if (pl->dbuf) cudaFreeAsync(pl->dbuf, s);
+      delete pl;
+      return fail(NIYAMA_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
+    }
+    kv->staging_pending = true;
+    pl->d_slot = reinterpret_cast<int32_t*>(pl->dbuf + o_slot);
+    pl->d_tables = reinterpret_cast<int32_t*>(pl->dbuf + o_tbl);
+    pl->d_tiles = reinterpret_cast<PrefillTile*>(pl->dbuf + o_tiles);
+    pl->d_units = reinterpret_cast<DecodeUnit*>(pl->dbuf + o_units);
+    pl->d_rows = reinterpret_cast<RowInfo*>(pl->dbuf + o_rows);
+    pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
+    pl->d_part_ml = reinterpret_cast<float*>(pl->dbuf + o_part_ml);
+    pl->d_counters = reinterpret_cast<int32_t*>(pl->dbuf + o_cnt);
+    pl->d_work = reinterpret_cast<int32_t*>(pl->dbuf + o_work);
+  }
+  *out = pl;
+  return NIYAMA_OK;
+}
+
+extern "C" void niyama_plan_destroy(niyama_plan* plan) {
+  if (!plan) return;
+  if (plan->dbuf) {
+    cudaSetDevice(plan->kv->cfg.device);
+    cudaFreeAsync(plan->dbuf, plan->stream);
+  }
+  delete plan;
+}
+
+extern "C" niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_plan_info* out) {
+  if (!plan || !out) return fail(NIYAMA_EINVAL, "plan/out is NULL");
+  out->num_rows = plan->T;
+  out->num_prefill_rows = plan->prefill_rows;
+  out->num_decode = plan->D;
+  out->num_prefill_tiles = static_cast<int32_t>(plan->tiles.size());
+  out->num_decode_units = static_cast<int32_t>(plan->units.size());
+  out->split_len = plan->split_len;
+  out->rows_per_tile = plan->R;
+  out->reserved = 0;
+  out->sum_ctx = plan->sum_ctx;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_plan_slots(const niyama_plan* plan, int32_t* block_out, int32_t* slot_out,
+                                           int32_t cap) {
+  if (!plan || !block_out || !slot_out) return fail(NIYAMA_EINVAL, "plan/block_out/slot_out is NULL");
+  const int B = plan->kv->B;
+  for (int32_t r = 0; r < plan->T && r < cap; ++r) {
+    block_out[r] = plan->slot_map[r] / B;
+    slot_out[r] = plan->slot_map[r] % B;
+  }
+  return NIYAMA_OK;
+}
+
+// ================================================================ launches
+namespace {
+niyama_status check_launch(niyama_kv* kv, const niyama_plan* plan, int32_t layer) {
+  if (!kv || !plan) return fail(NIYAMA_EINVAL, "kv/plan is NULL");
+  if (plan->kv != kv) return fail(NIYAMA_EINVAL, "plan belongs to another niyama_kv");
+  if (!kv->has_device) return fail(NIYAMA_EUNSUPPORTED, "no device (NIYAMA_DEVICE_NONE): there is no CPU path");
+  if (layer < 0 || layer >= kv->cfg.num_layers) return fail(NIYAMA_EINVAL, "layer out of range");
+  return NIYAMA_OK;
+}
+}  // namespace
+
+extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
+                                          const void* v_new, niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, layer);
+  if (st != NIYAMA_OK) return st;
+  if (plan->T == 0) return NIYAMA_OK;
+  if (!k_new || !v_new) return fail(NIYAMA_EINVAL, "k_new/v_new is NULL");
+  if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15)
+    return fail(NIYAMA_EINVAL, "k_new/v_new must be 16-byte aligned");
+  AppendParams p{};
+  p.pool_k = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
+  p.pool_v = p.pool_k + kv->half_bytes;
+  p.k_new = static_cast<const uint8_t*>(k_new);
+  p.v_new = static_cast<const uint8_t*>(v_new);
+  p.slot_map = plan->d_slot;
+  p.chunk_bytes = kv->chunk_bytes;
+  p.T = plan->T;
+  p.Hkv = kv->hkv;
+  p.row_bytes = kv->row_bytes;
+  p.B = kv->B;
+  NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer,
+                                                 const void* q, void* o, float* lse, float softmax_scale,
+                                                 niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, layer);
+  if (st != NIYAMA_OK) return st;
+  if (plan->T == 0) return NIYAMA_OK;
+  if (!q || !o) return fail(NIYAMA_EINVAL, "q/o is NULL");
+  if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) & 15)
+    return fail(NIYAMA_EINVAL, "q/o must be 16-byte aligned");
+  const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(static_cast<float>(kv->d));
+  AttnParams p{};
+  p.pool_k = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
+  p.pool_v = p.pool_k + kv->half_bytes;
+  p.q = q;
+  p.o = o;
+  p.lse = lse;
+  p.tables = plan->d_tables;
+  p.tiles = plan->d_tiles;
+  p.units = plan->d_units;
+  p.rows = plan->d_rows;
+  p.part_o = plan->d_part_o;
+  p.part_ml = plan->d_part_ml;
+  p.counters = plan->d_counters;
+  p.work = plan->d_work;
+  p.chunk_bytes = kv->chunk_bytes;
+  p.T = plan->T;
+  p.Hq = kv->hq;
+  p.Hkv = kv->hkv;
+  p.d = kv->d;
+  p.B = kv->B;
+  p.g = kv->g;
+  p.R = plan->R;
+  p.n_tiles = static_cast<int32_t>(plan->tiles.size());
+  p.n_units = static_cast<int32_t>(plan->units.size());
+  p.scale_log2 = scale * 1.4426950408889634f;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (kv->cfg.dtype == NIYAMA_BF16) {
+    if (kv->d != 128 || kv->g > 8)
+      return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
+    const int64_t want = static_cast<int64_t>(p.n_tiles) + ceil_div(p.n_units, 8);
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kv->num_sms, want)));
+    NY_CUDA(launch_attention_bf16(p, grid, s));
+  } else {
+    if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
+    NY_CUDA(launch_attention_generic_f32(p, s));
+  }
+  return NIYAMA_OK;
+}
+
+// ================================================================ NCCL (a7)
+extern "C" niyama_status niyama_get_unique_id(void* out128) {
+  if (!out128) return fail(NIYAMA_EINVAL, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NY_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_comm_init(niyama_kv* kv, const void* nccl_unique_id) {
+  if (!kv || !nccl_unique_id) return fail(NIYAMA_EINVAL, "kv/unique_id is NULL");
+  if (!kv->has_device) return fail(NIYAMA_EUNSUPPORTED, "no device");
+  if (kv->comm) return fail(NIYAMA_EINVAL, "communicator already initialised");
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_unique_id, sizeof(id));
+  NY_CUDA(cudaSetDevice(kv->cfg.device));
+  NY_NCCL(ncclCommInitRank(&kv->comm, kv->cfg.world_size, id, kv->cfg.rank));
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, void* o_full,
+                                                float* lse_full, niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, 0);
+  if (st != NIYAMA_OK) return st;
+  if (!o_full) return fail(NIYAMA_EINVAL, "o_full is NULL");
+  if (kv->cfg.world_size == 1 || plan->T == 0) return NIYAMA_OK;
+  if (!kv->comm) return fail(NIYAMA_EINVAL, "niyama_comm_init was not called");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t count = static_cast<size_t>(kv->hq) * plan->T * kv->d;
+  uint8_t* base = static_cast<uint8_t*>(o_full);
+  const ncclDataType_t ty = kv->cfg.dtype == NIYAMA_BF16 ? ncclBfloat16 : ncclFloat32;
+  NY_NCCL(ncclGroupStart());
+  NY_NCCL(ncclAllGather(base + count * kv->elt * kv->cfg.rank, base, count, ty, kv->comm, s));
+  if (lse_full) {
+    const size_t lc = static_cast<size_t>(kv->hq) * plan->T;
+    NY_NCCL(ncclAllGather(lse_full + lc * kv->cfg.rank, lse_full, lc, ncclFloat32, kv->comm, s));
+  }
+  NY_NCCL(ncclGroupEnd());
+  return NIYAMA_OK;
+}
+
+// ================================================================ predictor (a8)
+namespace {
+
+void features(const niyama_predictor& p, int64_t c, int64_t o_c_tok, int64_t pairs, int64_t D, double* phi) {
+  const double B = static_cast<double>(o_c_tok) * p.hkv * p.d * 2 * p.elt;
+  const double F = 4.0 * p.d * p.hq * static_cast<double>(pairs);
+  phi[0] = 1.0;
+  phi[1] = static_cast<double>(c);
+  phi[2] = static_cast<double>(D);
+  phi[3] = B;
+  phi[4] = F;
+  phi[5] = std::max(F / p.fpeak, B / NIYAMA_B_PEAK);
+}
+
+// phi of {slices (o_i, c_i) with c_i > 0} + decodes (D, sum ctx)
+void features_batch(const niyama_predictor& p, const int32_t* o, const int32_t* c, int n_slices, int64_t D,
+                    int64_t sum_ctx, double* phi) {
+  int64_t rows = 0, tok = sum_ctx, pairs = sum_ctx;
+  for (int i = 0; i < n_slices; ++i) {
+    if (c[i] <= 0) continue;
+    rows += c[i];
+    tok += static_cast<int64_t>(o[i]) + c[i];
+    pairs += static_cast<int64_t>(c[i]) * o[i] + static_cast<int64_t>(c[i]) * (c[i] + 1) / 2;
+  }
+  features(p, rows, tok, pairs, D, phi);
+}
+
+double dot6(const double* a, const double* b) {
+  double s = 0;
+  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) s += a[k] * b[k];
+  return s;
+}
+
+// Least squares on the columns `cols` of A (m x n, row-major) by Householder QR.
+bool lsq_subset(const std::vector<double>& A, int m, int n, const std::vector<double>& b, const std::vector<int>& cols,
+                std::vector<double>& z) {
+  const int k = static_cast<int>(cols.size());
+  std::vector<double> M(static_cast<size_t>(m) * k), y(b);
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < k; ++j) M[static_cast<size_t>(i) * k + j] = A[static_cast<size_t>(i) * n + cols[j]];
+  for (int j = 0; j < k; ++j) {
+    double norm = 0;
+    for (int i = j; i < m; ++i) norm += M[static_cast<size_t>(i) * k + j] * M[static_cast<size_t>(i) * k + j];
+    norm = std::sqrt(norm);
+    if (norm == 0) return false;
+    const double alpha = M[static_cast<size_t>(j) * k + j] > 0 ? -norm : norm;
+    std::vector<double> v(m, 0.0);
+    for (int i = j; i < m; ++i) v[i] = M[static_cast<size_t>(i) * k + j];
+    v[j] -= alpha;
+    double vn = 0;
+    for (int i = j; i < m; ++i) vn += v[i] * v[i];
+    if (vn == 0) continue;
+    for (int jj = j; jj < k; ++jj) {
+      double s = 0;
+      for (int i = j; i < m; ++i) s += v[i] * M[static_cast<size_t>(i) * k + jj];
+      s = 2 * s / vn;
+      for (int i = j; i < m; ++i) M[static_cast<size_t>(i) * k + jj] -= s * v[i];
+    }
+    double s = 0;
+    for (int i = j; i < m; ++i) s += v[i] * y[i];
+    s = 2 * s / vn;
+    for (int i = j; i < m; ++i) y[i] -= s * v[i];
+  }
+  z.assign(k, 0.0);
+  for (int j = k - 1; j >= 0; --j) {
+    double s = y[j];
+    for (int jj = j + 1; jj < k; ++jj) s -= M[static_cast<size_t>(j) * k + jj] * z[jj];
+    const double diag = M[static_cast<size_t>(j) * k + j];
+    if (std::fabs(diag) < 1e-300) return false;
+    z[j] = s / diag;
+  }
+  return true;
+}
+
+// Lawson-Hanson active-set NNLS: min ||A x - b||, x >= 0.
+std::vector<double> nnls(const std::vector<double>& A, int m, int n, const std::vector<double>& b) {
+  std::vector<double> x(n, 0.0);
+  std::vector<bool> inP(n, false);
+  double norm1 = 0;
+  for (int j = 0; j < n; ++j) {
+    double s = 0;
+    for (int i = 0; i < m; ++i) s += std::fabs(A[static_cast<size_t>(i) * n + j]);
+    norm1 = std::max(norm1, s);
+  }
+  const double tol = 10.0 * std::max(m, n) * norm1 * std::numeric_limits<double>::epsilon();
+  auto gradient = [&](std::vector<double>& w) {
+    std::vector<double> r(b);
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < n; ++j) r[i] -= A[static_cast<size_t>(i) * n + j] * x[j];
+    w.assign(n, 0.0);
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < m; ++i) w[j] += A[static_cast<size_t>(i) * n + j] * r[i];
+  };
+  std::vector<double> w;
+  for (int outer = 0; outer < 3 * n + 10; ++outer) {
+    gradient(w);
+    int t = -1;
+    double best = tol;
+    for (int j = 0; j < n; ++j)
+      if (!inP[j] && w[j] > best) best = w[j], t = j;
+    if (t < 0) break;
+    inP[t] = true;
+    for (int inner = 0; inner < 3 * n + 10; ++inner) {
+      std::vector<int> cols;
+      for (int j = 0; j < n; ++j)
+        if (inP[j]) cols.push_back(j);
+      std::vector<double> zc;
+      if (!lsq_subset(A, m, n, b, cols, zc)) {
+        inP[cols.back()] = false;
+        break;
+      }
+      std::vector<double> z(n, 0.0);
+      for (size_t k = 0; k < cols.size(); ++k) z[cols[k]] = zc[k];
+      bool allpos = true;
+      for (int j : cols)
+        if (z[j] <= 0) allpos = false;
+      if (allpos) {
+        x = z;
+        break;
+      }
+      double alpha = 2.0;
+      for (int j : cols)
+        if (z[j] <= 0) alpha = std::min(alpha, x[j] / (x[j] - z[j]));
+      for (int j = 0; j < n; ++j) x[j] += alpha * (z[j] - x[j]);
+      for (int j : cols)
+        if (x[j] <= tol) {
+          x[j] = 0;
+          inP[j] = false;
+        }
+    }
+  }
+  return x;
+}
+
+niyama_status pred_shape(const niyama_kv_config* s, niyama_predictor* p) {
+  if (!s) return fail(NIYAMA_EINVAL, "shape is NULL");
+  if (s->world_size < 1 || s->num_kv_heads < 1 || s->num_q_heads < 1 || s->head_dim < 1 ||
+      s->num_kv_heads % s->world_size || s->num_q_heads % s->world_size)
+    return fail(NIYAMA_EINVAL, "predictor shape");
+  p->hq = s->num_q_heads / s->world_size;
+  p->hkv = s->num_kv_heads / s->world_size;
+  p->d = s->head_dim;
+  p->elt = s->dtype == NIYAMA_BF16 ? 2 : 4;
+  p->fpeak = s->dtype == NIYAMA_BF16 ? NIYAMA_F_PEAK_BF16 : NIYAMA_F_PEAK_F32;
+  return NIYAMA_OK;
+}
+
+bool feasible(double t, double slack) { return t <= slack + 1e-12 * std::max(1.0, std::fabs(slack)); }
+
+}  // namespace
+
+extern "C" niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
+                                              niyama_predictor** out) {
+  if (!out) return fail(NIYAMA_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (!samples || n < 1) return fail(NIYAMA_EINVAL, "no samples");
+  niyama_predictor p;
+  niyama_status st = pred_shape(shape, &p);
+  if (st != NIYAMA_OK) return st;
+  const int F = NIYAMA_NUM_FEATURES;
+  std::vector<double> A(static_cast<size_t>(n) * F), b(n, 1.0);
+  for (int i = 0; i < n; ++i) {
+    const niyama_sample& s = samples[i];
+    if (!(s.seconds > 0) || s.chunk_len < 0 || s.chunk_offset < 0 || s.num_decode < 0 || s.sum_ctx < 0)
+      return fail(NIYAMA_EINVAL, "sample " + std::to_string(i) + " is invalid");
+    double phi[F];
+    features_batch(p, &s.chunk_offset, &s.chunk_len, 1, s.num_decode, s.sum_ctx, phi);
+    for (int k = 0; k < F; ++k) A[static_cast<size_t>(i) * F + k] = phi[k] / s.seconds;
+  }
+  double colmax[F];
+  for (int k = 0; k < F; ++k) {
+    colmax[k] = 0;
+    for (int i = 0; i < n; ++i) colmax[k] = std::max(colmax[k], std::fabs(A[static_cast<size_t>(i) * F + k]));
+    if (colmax[k] == 0) colmax[k] = 1;
+    for (int i = 0; i < n; ++i) A[static_cast<size_t>(i) * F + k] /= colmax[k];
+  }
+  std::vector<double> z = nnls(A, n, F, b);
+  auto* res = new niyama_predictor(p);
+  for (int k = 0; k < F; ++k) res->theta[k] = z[k] / colmax[k];
+  *out = res;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta6,
+                                                      niyama_predictor** out) {
+  if (!out || !theta6) return fail(NIYAMA_EINVAL, "out/theta is NULL");
+  *out = nullptr;
+  niyama_predictor p;
+  niyama_status st = pred_shape(shape, &p);
+  if (st != NIYAMA_OK) return st;
+  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) {
+    if (!(theta6[k] >= 0) || !std::isfinite(theta6[k])) return fail(NIYAMA_EINVAL, "theta must be finite and >= 0");
+    p.theta[k] = theta6[k];
+  }
+  *out = new niyama_predictor(p);
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta6_out) {
+  if (!p || !theta6_out) return fail(NIYAMA_EINVAL, "p/out is NULL");
+  std::memcpy(theta6_out, p->theta, sizeof(p->theta));
+  return NIYAMA_OK;
+}
+
+extern "C" double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc) {
+  if (!p || !desc || desc->num_prefill < 0 || desc->num_decode < 0) return -1.0;
+  if (desc->num_prefill > 0 && (!desc->prefill_offset || !desc->prefill_len)) return -1.0;
+  if (desc->num_decode > 0 && !desc->decode_ctx) return -1.0;
+  int64_t sum_ctx = 0;
+  for (int j = 0; j < desc->num_decode; ++j) {
+    if (desc->decode_ctx[j] < 1) return -1.0;
+    sum_ctx += desc->decode_ctx[j];
+  }
+  for (int i = 0; i < desc->num_prefill; ++i)
+    if (desc->prefill_offset[i] < 0 || desc->prefill_len[i] < 0) return -1.0;
+  double phi[NIYAMA_NUM_FEATURES];
+  features_batch(*p, desc->prefill_offset, desc->prefill_len, desc->num_prefill, desc->num_decode, sum_ctx, phi);
+  return dot6(p->theta, phi);
+}
+
+extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_batch_desc* decodes_only,
+                                                   int32_t chunk_offset, int32_t prefill_remaining, double slack_s,
+                                                   int32_t max_chunk, int32_t* chunk_out, int32_t* infeasible_out) {
+  if (!p || !decodes_only || !chunk_out || !infeasible_out) return fail(NIYAMA_EINVAL, "NULL argument");
+  if (chunk_offset < 0 || max_chunk < 0 || std::isnan(slack_s)) return fail(NIYAMA_EINVAL, "chunk_offset/max_chunk/slack");
+  if (decodes_only->num_decode < 0 || (decodes_only->num_decode > 0 && !decodes_only->decode_ctx))
+    return fail(NIYAMA_EINVAL, "decode arrays");
+  int64_t sum_ctx = 0;
+  for (int j = 0; j < decodes_only->num_decode; ++j) {
+    if (decodes_only->decode_ctx[j] < 1) return fail(NIYAMA_EINVAL, "decode_ctx < 1");
+    sum_ctx += decodes_only->decode_ctx[j];
+  }
+  const int64_t D = decodes_only->num_decode;
+  auto t_of = [&](int32_t C) {
+    double phi[NIYAMA_NUM_FEATURES];
+    features_batch(*p, &chunk_offset, &C, 1, D, sum_ctx, phi);
+    return dot6(p->theta, phi);
+  };
+  const int32_t cap = std::max(0, std::min(max_chunk, prefill_remaining));
+  if (!feasible(t_of(0), slack_s)) {
+    *chunk_out = 0;
+    *infeasible_out = 1;
+    return NIYAMA_OK;
+  }
+  // theta >= 0 => t_hat non-decreasing in C: binary search the last feasible C.
+  int32_t lo = 0, hi = cap;
+  while (lo < hi) {
+    const int32_t mid = lo + (hi - lo + 1) / 2;
+    if (feasible(t_of(mid), slack_s))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  *chunk_out = lo;
+  *infeasible_out = 0;
+  return NIYAMA_OK;
+}
+
+extern "C" void niyama_predictor_destroy(niyama_predictor* p) { delete p; }
+
+// ================================================================ slack (a1)
+extern "C" niyama_status niyama_min_slack(const niyama_decode_qos* decodes, int32_t n, double now, double* slack_out) {
+  if (!slack_out || n < 0 || (n > 0 && !decodes)) return fail(NIYAMA_EINVAL, "NULL argument or n < 0");
+  double s = std::numeric_limits<double>::infinity();
+  for (int32_t i = 0; i < n; ++i) {
+    const niyama_decode_qos& q = decodes[i];
+    double si;
+    if (q.interactive) {
+      if (q.next_token < 1) return fail(NIYAMA_EINVAL, "next_token < 1 (Eq. 2 needs n >= 1)");
+      si = q.t_arrival + q.slo_ttft + (q.next_token - 1) * q.slo_tbt - now;  // Eq. 2
+    } else {
+      si = (q.t_arrival + q.slo_ttlt - now) / std::max(1, q.est_remaining);  // Eq. 3, pacing bound
+    }
+    s = std::min(s, si);
+  }
+  *slack_out = s;
+  return NIYAMA_OK;
+}

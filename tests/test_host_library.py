@@ -1,0 +1,248 @@
+"""CPU tests of the C-ABI library (no GPU): every declared symbol is exported,
+and the host logic behind the boundary (block allocator, planner slot map,
+work-list sizing, predictor, slack) agrees with the oracle.  The pool is
+created with device = NIYAMA_DEVICE_NONE (host bookkeeping only); every call
+that would touch the GPU must refuse with EUNSUPPORTED (no CPU fallback)."""
+import json
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+import workloads as W
+from oracle import kvcache as OK_
+from oracle import predictor as OP
+from oracle import sched as OS
+import paper_2503_22562_b200 as ny
+from paper_2503_22562_b200 import _binding as NB
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+
+
+def test_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "niyama.h")).read()
+    hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
+    names = set(re.findall(r"\b(niyama_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 20
+    for n in sorted(names):
+        assert hasattr(NB.lib, n), n
+    assert b"sm_100a" in NB.lib.niyama_version()
+
+
+def host_kv(shape: W.Shape, num_blocks: int, world=1, rank=0):
+    return ny.KVCache(shape.num_layers, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, num_blocks,
+                      block_size=shape.block_size, dtype=shape.dtype, world_size=world, rank=rank, device=None)
+
+
+def test_golden_tables_through_c_abi():
+    fx = json.load(open(os.path.join(GOLDEN, "kv_tables_scenario.json")))
+    p = fx["pool"]
+    # the library needs block_size >= 16: scale the fixture's block size 4 -> 16 by
+    # scaling every length by 4 (ceil(4n/16) == ceil(n/4)); slots scale the same way.
+    kv = ny.KVCache(1, 1, 1, 64, p["num_blocks"], block_size=16, dtype="bf16", device=None)
+    codes = {"EINVAL": NB.EINVAL, "ENOBLOCKS": NB.ENOBLOCKS, "ENOSEQ": NB.ENOSEQ, "ESTATE": NB.ESTATE}
+    for st in fx["steps"]:
+        if st["op"] == "release":
+            kv.release(st["seq"])
+            continue
+        desc = W.BatchDesc(prefill_seq=[x[0] for x in st["prefill"]], prefill_offset=[4 * x[1] for x in st["prefill"]],
+                           prefill_len=[4 * x[2] for x in st["prefill"]], decode_seq=[x[0] for x in st["decode"]],
+                           decode_ctx=[x[1] for x in st["decode"]])
+        if st["decode"] and "expect_error" not in st:
+            # decodes add one token: express them as 4-token prefill slices after scaling
+            desc = W.BatchDesc(prefill_seq=desc.prefill_seq + desc.decode_seq,
+                               prefill_offset=desc.prefill_offset + [4 * (c - 1) for c in desc.decode_ctx],
+                               prefill_len=desc.prefill_len + [4] * len(desc.decode_seq))
+        if "expect_error" in st:
+            nfree = kv.num_free()
+            with pytest.raises(ny.NiyamaError) as e:
+                kv.plan(desc)
+            assert e.value.status == codes[st["expect_error"]]
+            assert kv.num_free() == nfree
+        else:
+            kv.plan(desc)
+        if "expect_tables" in st:
+            for s, t in st["expect_tables"].items():
+                assert kv.block_table(int(s)) == t
+
+
+def replay_both(wl: W.Workload):
+    s = wl.shape
+    kv = host_kv(s, wl.num_blocks)
+    pool = OK_.KVPool(1, s.num_kv_heads, s.head_dim, s.block_size, wl.num_blocks, s.dtype)
+    plans = []
+    for st in wl.steps:
+        p = kv.plan(st.desc)
+        o = pool.plan(st.desc)
+        assert p.slots() == [tuple(x) for x in o.slots]
+        plans.append((p, o))
+    for seq in pool.table:
+        assert kv.block_table(seq) == pool.table[seq]
+        assert kv.seq_len(seq) == pool.length[seq]
+    assert kv.num_free() == len(pool.free)
+    return kv, pool, plans
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3])
+def test_random_tables_and_slots_match_oracle(seed):
+    shape = W.Shape(num_q_heads=8, num_kv_heads=2, head_dim=128, block_size=16, dtype="bf16")
+    wl = W.random_hybrid(shape, seed=seed, num_prefill=3, max_chunk=200, num_decode=6, max_ctx=500)
+    kv, pool, _ = replay_both(wl)
+    # release + reuse keeps the smallest-free-id policy
+    for seq in list(pool.table)[::2]:
+        kv.release(seq)
+        pool.release(seq)
+    d = W.BatchDesc(prefill_seq=[1000], prefill_offset=[0], prefill_len=[333])
+    assert kv.plan(d).slots() == [tuple(x) for x in pool.plan(d).slots]
+    assert kv.block_table(1000) == pool.table[1000]
+
+
+def test_error_codes_match_oracle():
+    shape = W.Shape(num_q_heads=4, num_kv_heads=2, head_dim=128, block_size=16, dtype="bf16")
+    kv = host_kv(shape, 8)
+    pool = OK_.KVPool(1, 2, 128, 16, 8, "bf16")
+    cases = [
+        W.BatchDesc(decode_seq=[5], decode_ctx=[1]),                         # ENOSEQ
+        W.BatchDesc([1], [3], [4]),                                           # ESTATE (new seq, offset 3)
+        W.BatchDesc([1, 1], [0, 0], [4, 4]),                                  # EINVAL duplicate
+        W.BatchDesc([1], [0], [16 * 9]),                                      # ENOBLOCKS
+        W.BatchDesc([1], [0], [-1]),                                          # EINVAL
+    ]
+    for d in cases:
+        with pytest.raises(OK_.OracleError) as eo:
+            pool.plan(d)
+        with pytest.raises(ny.NiyamaError) as ec:
+            kv.plan(d)
+        assert ec.value.status == eo.value.code
+    assert kv.num_free() == 8
+    kv.plan(W.BatchDesc([1], [0], [20]))
+    for d in [W.BatchDesc(decode_seq=[1], decode_ctx=[20]), W.BatchDesc(decode_seq=[1], decode_ctx=[0])]:
+        pool.plan(W.BatchDesc([1], [0], [20])) if 1 not in pool.length else None
+        with pytest.raises(OK_.OracleError) as eo:
+            pool.plan(d)
+        with pytest.raises(ny.NiyamaError) as ec:
+            kv.plan(d)
+        assert ec.value.status == eo.value.code
+
+
+def test_device_calls_refuse_without_gpu():
+    kv = host_kv(W.L8B, 16)
+    p = kv.plan(W.BatchDesc([0], [0], [10]))
+    for call in (lambda: kv.append(p, 0, 16, 16), lambda: kv.attention(p, 0, 16, 16),
+                 lambda: kv.gather(0, 0, 10, 16, 16)):
+        with pytest.raises(ny.NiyamaError) as e:
+            call()
+        assert e.value.status == NB.EUNSUPPORTED
+
+
+def test_work_list_sizing():
+    """a2: tiles = sum ceil(c/R) * Hkv with R = 128/g; units = sum ceil(ctx/split) * Hkv;
+    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 4 * 148 * 8."""
+    ctx = W.l8b_decode_ctx()
+    wl = W.hybrid(W.L8B, "sizing", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
+    kv = host_kv(W.L8B, wl.num_blocks)
+    for st in wl.steps:
+        p = kv.plan(st.desc)
+    info = p.info()
+    assert info.rows_per_tile == 32
+    assert info.num_prefill_tiles == (512 // 32) * 8
+    assert info.split_len == 256                      # 133674*8/4736 = 225.8 -> 256
+    assert info.num_decode_units == sum(-(-int(c) // 256) for c in ctx) * 8
+    assert info.sum_ctx == 133674 and info.num_rows == 576
+
+
+def test_head_shard_config():
+    kv = ny.KVCache(1, 64, 8, 128, 64, dtype="bf16", world_size=8, rank=3, device=None)
+    p = kv.plan(W.BatchDesc([0], [0], [100]))
+    assert p.info().num_prefill_tiles == 100 // 16 + 1     # g = 8, R = 16, 1 local kv head
+    with pytest.raises(ny.NiyamaError):
+        ny.KVCache(1, 64, 8, 128, 64, world_size=3, rank=0, device=None)
+
+
+# ------------------------------------------------------------------ predictor
+SHAPE = OP.PredShape(num_q_heads=32, num_kv_heads=8, head_dim=128, elt_bytes=2)
+CFG = ny.Predictor.shape_cfg(32, 8, 128)
+
+
+def test_predictor_eval_matches_oracle():
+    theta = np.array([4e-6, 2e-9, 5e-8, 1.1e-13, 3e-16, 0.9])
+    pr = ny.Predictor.from_params(CFG, theta)
+    np.testing.assert_array_equal(pr.params(), theta)
+    g = np.random.default_rng(0)
+    for _ in range(50):
+        P = int(g.integers(0, 3))
+        D = int(g.integers(0, 50))
+        offs = [int(x) for x in g.integers(0, 5000, size=P)]
+        lens = [int(x) for x in g.integers(0, 2049, size=P)]
+        ctx = [int(x) for x in g.integers(1, 8193, size=D)]
+        d = W.BatchDesc(list(range(P)), offs, lens, list(range(100, 100 + D)), ctx)
+        want = OP.predict(theta, OP.features(SHAPE, list(zip(offs, lens)), ctx))
+        assert pr.predict(d) == pytest.approx(want, rel=1e-13, abs=0)
+
+
+def test_predictor_fit_matches_oracle():
+    g = np.random.default_rng(1)
+    samples = []
+    for _ in range(80):
+        c = int(g.choice([0, 256, 512, 1024, 2048]))
+        o = int(g.integers(0, 6000)) if c else 0
+        D = int(g.integers(0, 257))
+        L = int(g.integers(D, D * 4096 + 1)) if D else 0
+        t = 5e-6 + 1.3 * max(4 * 128 * 32 * (c * o + c * (c + 1) / 2 + L) / 2.25e15,
+                             ((o + c if c else 0) + L) * 4096 / 8e12) * (1 + 0.05 * g.standard_normal())
+        samples.append(OP.Sample(c, o, D, L, max(t, 1e-6)))
+    th_o = OP.fit(SHAPE, samples)
+    th_c = ny.Predictor.fit(CFG, samples).params()
+    pred_o = np.array([th_o @ OP.features_sample(SHAPE, s) for s in samples])
+    pred_c = np.array([th_c @ OP.features_sample(SHAPE, s) for s in samples])
+    np.testing.assert_allclose(pred_c, pred_o, rtol=1e-7)
+    assert (th_c >= 0).all()
+
+
+def test_max_feasible_chunk_matches_bruteforce():
+    theta = np.array([4e-6, 2e-9, 5e-8, 1.1e-13, 3e-16, 0.9])
+    pr = ny.Predictor.from_params(CFG, theta)
+    g = np.random.default_rng(2)
+    for _ in range(25):
+        ctx = [int(x) for x in g.integers(1, 4097, size=int(g.integers(0, 64)))]
+        o = int(g.integers(0, 4000))
+        rem = int(g.integers(0, 3000))
+        t0 = OP.predict(theta, OP.features(SHAPE, [], ctx))
+        slack = float(t0 * g.uniform(0.8, 3.0))
+        assert pr.max_feasible_chunk(ctx, o, rem, slack, 2048) == \
+            OP.max_feasible_chunk(theta, SHAPE, ctx, o, rem, slack, 2048)
+
+
+def test_spec_examples_through_c_abi():
+    fx = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
+    cm = fx["cost_model"]
+    per_tok = 8 * 128 * 2 * 2
+    pr = ny.Predictor.from_params(CFG, [cm["c0"], cm["c1"], cm["c1"], cm["c2"] / per_tok, 0, 0])
+    assert pr.predict(W.BatchDesc()) == pytest.approx(cm["c0"], abs=1e-15)
+    assert pr.predict(W.BatchDesc([0], [0], [256])) == pytest.approx(cm["chunk256_s"], rel=1e-12)
+    assert pr.max_feasible_chunk([], 0, 10**6, cm["inverse"]["slack"], 2048) == (256, False)
+    assert pr.max_feasible_chunk([], 0, 10**6, math.inf, 2048) == (2048, False)
+    assert pr.max_feasible_chunk([100], 0, 10**6, 0.001, 2048) == (0, True)
+    for ex in fx["slack"]:
+        decs = [OS.DecodeQoS(**d) for d in ex["decodes"]]
+        got = ny.min_slack(decs, ex["now"])
+        want = OS.min_slack(decs, ex["now"])
+        assert got == want
+
+
+def test_min_slack_random_matches_oracle():
+    g = np.random.default_rng(3)
+    for _ in range(30):
+        decs = []
+        for _ in range(int(g.integers(0, 20))):
+            if g.random() < 0.5:
+                decs.append(OS.DecodeQoS(True, float(g.uniform(0, 100)), slo_ttft=6.0, slo_tbt=0.05,
+                                         next_token=int(g.integers(1, 500))))
+            else:
+                decs.append(OS.DecodeQoS(False, float(g.uniform(0, 100)), slo_ttlt=float(g.choice([600, 1800])),
+                                         est_remaining=int(g.integers(0, 900))))
+        now = float(g.uniform(0, 200))
+        assert ny.min_slack(decs, now) == pytest.approx(OS.min_slack(decs, now), rel=1e-15, abs=1e-15)
