@@ -280,8 +280,6 @@ def main():
     o = o_full[q0:q0 + hq]
     lse = lse_full[q0:q0 + hq]
     stream = torch.cuda.current_stream()
-    rewind = [(sq, o_) for sq, o_ in zip(desc.prefill_seq, desc.prefill_offset)] + \
-             [(sq, c - 1) for sq, c in zip(desc.decode_seq, desc.decode_ctx)]
 
     # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
     fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
@@ -291,31 +289,33 @@ def main():
         fj = json.load(open(fit_path))
         theta = fj.get("theta", theta) if fj.get("world", 1) == world and fj.get("config") == args.config else theta
     pred = ny.Predictor.from_params(cfg, theta)
-    # a1 inputs: decodes carry Table 3 tiers, interactive ones are mid-stream
+    # a1 inputs: decodes carry Table 3 tiers; interactive ones are mid-stream
+    from oracle.sched import DecodeQoS  # plain dataclass used only to describe the synthetic QoS state
     tiers = desc.tiers()
     qos = []
-    for j, c in enumerate(desc.decode_ctx):
+    for j in range(desc.num_decode):
         tier = tiers[desc.num_prefill + j] % 3
         if tier == 0:
-            qos.append(ny._binding.DecodeQoSC(1, 40, 1, 0, 0.0, 6.0, 0.05, 0.0))
+            qos.append(DecodeQoS(True, 0.0, slo_ttft=6.0, slo_tbt=0.05, next_token=40))
         else:
-            qos.append(ny._binding.DecodeQoSC(0, 1, 400, 0, 0.0, 0.0, 0.0, 600.0 if tier == 1 else 1800.0))
+            qos.append(DecodeQoS(False, 0.0, slo_ttlt=600.0 if tier == 1 else 1800.0, est_remaining=400))
+    qos_arr = ny.QoSArray(qos)
+    batch = ny.Batch(desc)                              # marshalled once, reused every step
+    dec_only = ny.Batch(W.BatchDesc(decode_seq=desc.decode_seq, decode_ctx=desc.decode_ctx))
+    c_off = desc.prefill_offset[0] if desc.num_prefill else 0
+    c_rem = desc.prefill_len[0] if desc.num_prefill else 0
     a1 = {}
 
     def a1_step():
-        import ctypes as C
-        arr = (ny._binding.DecodeQoSC * max(1, len(qos)))(*qos)
-        sl = C.c_double()
-        ny._binding.lib.niyama_min_slack(arr, len(qos), 7.9, C.byref(sl))
-        c, inf = pred.max_feasible_chunk(desc.decode_ctx, desc.prefill_offset[0] if desc.num_prefill else 0,
-                                         desc.prefill_len[0] if desc.num_prefill else 0, sl.value, 2048)
-        a1["slack_s"], a1["chunk"], a1["infeasible"] = sl.value, c, inf
+        sl = qos_arr.min_slack(7.9)
+        c, inf = pred.max_feasible_chunk(dec_only, c_off, c_rem, sl, 2048)
+        a1["slack_s"], a1["chunk"], a1["infeasible"] = sl, c, inf
 
     ev = []
 
     def step(record=None):
         a1_step()                                       # a1 (host)
-        plan = kv.plan(desc, stream)                    # a2
+        plan = kv.plan(batch, stream)                   # a2
         kv.append(plan, 0, k_new, v_new, stream)        # a3
         if record is not None:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -326,9 +326,8 @@ def main():
             record.append((a, b))
         if world > 1:
             kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
-        pred.predict(desc)                              # a8
-        for sq, n in rewind:
-            kv.truncate(sq, n)
+        pred.predict(batch)                             # a8
+        plan.rollback()                                 # replay the same batch next step (host only)
         plan.close()
 
     clocks = ClockSampler(local)
@@ -375,14 +374,13 @@ def main():
         d_k.copy_(h_k, non_blocking=True)
         d_v.copy_(h_v, non_blocking=True)
         a1_step()
-        plan = kv.plan(desc, stream)
+        plan = kv.plan(batch, stream)
         kv.append(plan, 0, d_k, d_v, stream)
         kv.attention(plan, 0, d_q, o, lse, 0.0, stream)
         if world > 1:
             kv.allgather_heads(plan, o_full, lse_full, stream)
-        pred.predict(desc)
-        for sq, n in rewind:
-            kv.truncate(sq, n)
+        pred.predict(batch)
+        plan.rollback()
         plan.close()
         h_o.copy_(o_full, non_blocking=True)
 

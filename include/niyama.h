@@ -146,6 +146,11 @@ typedef struct {
 niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_desc* desc, niyama_stream stream,
                                  niyama_plan** out);
 void niyama_plan_destroy(niyama_plan* plan); /* stream-ordered free on the plan's stream */
+/* Undo the plan's host bookkeeping: every sequence of the batch returns to its
+ * length before niyama_plan_create (sequences the plan created are removed);
+ * blocks past the old lengths are freed (R9).  The plan's device buffers stay
+ * valid for launches already enqueued.  Used to abort or replay an iteration. */
+niyama_status niyama_plan_rollback(niyama_kv* kv, niyama_plan* plan);
 
 typedef struct {
   int32_t num_rows;           /* T = sum prefill_len + num_decode */
@@ -180,6 +185,12 @@ niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t l
  * T = 0 is a no-op. */
 niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q,
                                       void* o, float* lse, float softmax_scale, niyama_stream stream);
+
+/* Diagnostics: when device_buf (DEVICE, int64 [#SMs][4]) is non-NULL every
+ * later niyama_hybrid_attention writes, per CTA, globaltimer ns at start, at
+ * the end of its prefill tiles, at exit, and the number of prefill tiles it
+ * ran.  NULL turns tracing off (the default). */
+niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
 
 /* a7 — head sharding across the GPUs of one node (§8e).  comm_init creates
  * the library's own NCCL communicator from a 128-byte ncclUniqueId produced

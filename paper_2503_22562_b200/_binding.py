@@ -76,9 +76,11 @@ def _load():
         "niyama_plan_create": ([vp, C.POINTER(BatchDescC), vp, C.POINTER(vp)], st),
         "niyama_plan_destroy": ([vp], None),
         "niyama_plan_get_info": ([vp, C.POINTER(PlanInfo)], st),
+        "niyama_plan_rollback": ([vp, vp], st),
         "niyama_plan_slots": ([vp, C.POINTER(i32), C.POINTER(i32), i32], st),
         "niyama_kv_append": ([vp, vp, i32, vp, vp, vp], st),
         "niyama_hybrid_attention": ([vp, vp, i32, vp, vp, vp, C.c_float, vp], st),
+        "niyama_debug_trace": ([vp, vp], st),
         "niyama_comm_init": ([vp, vp], st),
         "niyama_get_unique_id": ([vp], st),
         "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
@@ -182,6 +184,9 @@ class Plan:
                                      slot.ctypes.data_as(C.POINTER(C.c_int32)), n))
         return list(zip(blk[:n].tolist(), slot[:n].tolist()))
 
+    def rollback(self):
+        _check(lib.niyama_plan_rollback(self.kv.handle, self.handle))
+
     def close(self):
         if self.handle:
             lib.niyama_plan_destroy(self.handle)
@@ -209,7 +214,7 @@ class KVCache:
 
     # -- bookkeeping
     def plan(self, desc, stream=None) -> Plan:
-        d = _Desc(desc)
+        d = desc if isinstance(desc, _Desc) else _Desc(desc)
         h = C.c_void_p()
         _check(lib.niyama_plan_create(self.handle, C.byref(d.c), _stream(stream), C.byref(h)))
         return Plan(self, h.value)
@@ -248,6 +253,9 @@ class KVCache:
 
     def gather(self, layer: int, seq: int, n: int, k_out, v_out, stream=None):
         _check(lib.niyama_kv_gather(self.handle, layer, int(seq), n, _ptr(k_out), _ptr(v_out), _stream(stream)))
+
+    def debug_trace(self, buf):
+        _check(lib.niyama_debug_trace(self.handle, _ptr(buf)))
 
     def comm_init(self, unique_id: bytes):
         buf = C.create_string_buffer(bytes(unique_id), 128)
@@ -305,16 +313,20 @@ class Predictor:
         return np.array(list(th))
 
     def predict(self, desc) -> float:
-        d = _Desc(desc)
+        d = desc if isinstance(desc, _Desc) else _Desc(desc)
         return lib.niyama_predict_iter_time(self.handle, C.byref(d.c))
 
     def max_feasible_chunk(self, decode_ctx, chunk_offset, prefill_remaining, slack, max_chunk):
-        class _D:
-            pass
-        dd = _D()
-        dd.decode_seq = list(range(len(decode_ctx)))
-        dd.decode_ctx = list(decode_ctx)
-        d = _Desc(dd)
+        """decode_ctx: a list of contexts or a prebuilt `Batch` holding the decodes."""
+        if isinstance(decode_ctx, _Desc):
+            d = decode_ctx
+        else:
+            class _D:
+                pass
+            dd = _D()
+            dd.decode_seq = list(range(len(decode_ctx)))
+            dd.decode_ctx = list(decode_ctx)
+            d = _Desc(dd)
         c, inf = C.c_int32(), C.c_int32()
         _check(lib.niyama_max_feasible_chunk(self.handle, C.byref(d.c), chunk_offset, prefill_remaining,
                                              float(slack), max_chunk, C.byref(c), C.byref(inf)))
@@ -327,6 +339,24 @@ class Predictor:
                 self.handle = None
         except Exception:
             pass
+
+
+Batch = _Desc  # a batch descriptor marshalled once and reusable across calls
+
+
+class QoSArray:
+    """niyama_decode_qos[] marshalled once (for per-iteration min_slack calls)."""
+
+    def __init__(self, decodes):
+        self.n = len(decodes)
+        self.arr = (DecodeQoSC * max(1, self.n))(*[
+            DecodeQoSC(int(bool(q.interactive)), int(q.next_token), int(q.est_remaining), 0, float(q.t_arrival),
+                       float(q.slo_ttft), float(q.slo_tbt), float(q.slo_ttlt)) for q in decodes])
+
+    def min_slack(self, now: float) -> float:
+        out = C.c_double()
+        _check(lib.niyama_min_slack(self.arr, self.n, float(now), C.byref(out)))
+        return out.value
 
 
 def min_slack(decodes, now: float) -> float:

@@ -17,31 +17,34 @@ namespace niyama {
 // therefore already a canonical UMMA SW128 operand (K-major for K, MN-major
 // for V) and is bank-conflict free for ldmatrix.
 
-// Prefill tile: 128 MMA rows = g query heads x R chunk rows (R = 128/g) of one
-// kv head, over keys [0, nkeys).  (a4)
-struct PrefillTile {
+// Compact work list (a2 -> a4/a5).  The kernel expands item indices itself, so
+// the per-iteration H2D stays small (tables + one record per slice / decode).
+//
+// Prefill slice: its tiles are [tbase, tbase + nqt*Hkv); tile t of the slice is
+// q-tile qt = nqt-1 - (t-tbase)/Hkv (largest key range first), kv head
+// (t-tbase)%Hkv, rows [qt*R, min(qt*R+R, c)) with R = 128/g chunk rows per tile
+// (128 MMA rows = g query heads x R rows).  (a4)
+struct PrefillSlice {
   int32_t tbl;    // offset of the sequence's block table in the tables array
-  int32_t o;      // slice offset (positions of rows are o + t0 + i)
+  int32_t o;      // slice offset (positions of rows are o + i)
   int32_t c;      // slice length
-  int32_t t0;     // first slice row of this tile
   int32_t row0;   // batch row of slice row 0
-  int32_t kvh;    // local kv head
-  int32_t nkeys;  // o + min(t0 + R, c): keys visible to the tile's last row
-  int32_t nblk;   // blocks of the table covering nkeys
+  int32_t nqt;    // q tiles = ceil(c / R)
+  int32_t tbase;  // first tile index
+  int32_t pad0, pad1;
 };
 
-// Decode unit: one decode row, one kv head, keys [k0, k1).  (a5)
-struct DecodeUnit {
+// Decode row (sorted by ctx, longest first): its units are [ubase, ubase +
+// nsplit*Hkv); unit u has split s = (u-ubase)/Hkv over keys [s*L, min(ctx,
+// (s+1)*L)) with L = split_len, kv head (u-ubase)%Hkv.  Unit u's partial (when
+// nsplit > 1) lives at index u; merge counter = sorted_row*Hkv + head.  (a5, a6)
+struct DecodeRow {
   int32_t tbl;
   int32_t ctx;
   int32_t row;     // batch row
-  int32_t kvh;
-  int32_t k0, k1;  // k0 multiple of 16
-  int32_t split;   // split index within the (row, kv head) pair
   int32_t nsplit;
-  int32_t pbase;   // partial index of split 0 of this pair
-  int32_t pair;    // decode index * Hkv_loc + kvh (merge counter)
-  int32_t pad0, pad1;
+  int32_t ubase;
+  int32_t pad0, pad1, pad2;
 };
 
 // Per-row info for the generic (f32) path.
@@ -57,16 +60,19 @@ struct AttnParams {
   void* o;
   float* lse;
   const int32_t* tables;
-  const PrefillTile* tiles;
-  const DecodeUnit* units;
+  const PrefillSlice* slices;
+  const DecodeRow* drows;
+  const int32_t* urow;   // [n_units] sorted row index of each decode unit
   const RowInfo* rows;
-  float* part_o;    // [n_partials][g][d]
-  float* part_ml;   // [n_partials][g][2]
+  float* part_o;    // [n_units][g][d]
+  float* part_ml;   // [n_units][g][2]
   int32_t* counters;  // [num_decode * Hkv] merge counters (self-resetting)
-  int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter (self-resetting)
+  int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] grid barrier (self-resetting)
   int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
   int32_t T, Hq, Hkv, d, B, g, R;
-  int32_t n_tiles, n_units;
+  int32_t n_tiles, n_units, n_slices, n_drows, split_len;
+  int32_t n_merge_rows;  // rows with nsplit > 1 (a prefix of drows)
+  int64_t* trace;  // optional per-CTA timeline [grid][4] (globaltimer ns), nullptr = off
   float scale_log2;     // softmax scale * log2(e)
 };
 

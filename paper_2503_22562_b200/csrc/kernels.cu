@@ -102,35 +102,40 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 // ===================================================== fused bf16 attention
 // Shared memory map (bytes from the 1024-aligned base):
 //   [0, 32K)            Q tile   (2 panels x 128 rows x 128 B, SW128)
-//   [32K, 32K+NS*32K)   K stages (128 keys x 256 B each)
-//   [.., +NS*32K)       V stages
+//   [32K, +3*32K)       K stages (128 keys x 256 B each)
+//   [.., +2*32K)        V stages
 //   [.., +32K)          P tile   (2 panels x 128 rows x 128 B, SW128, bf16)
 // The decode role reuses [0, 192K) as 8 warps x 3 stages x 8 KB.
 namespace fa {
 constexpr int kD = 128;            // head dim (bf16 path)
 constexpr int kBN = 128;           // keys per prefill tile
-constexpr int kNS = 2;             // K/V stages
+constexpr int kNSK = 3;            // K stages (released by the QK^T commit)
+constexpr int kNSV = 2;            // V stages (released by the PV commit)
 constexpr int kPanel = 128 * 128;  // one 64-column panel of a 128-row tile
 constexpr int kTile = 2 * kPanel;  // 128 rows x 256 B
 constexpr int kQOff = 0;
 constexpr int kKOff = kTile;
-constexpr int kVOff = kKOff + kNS * kTile;
-constexpr int kPOff = kVOff + kNS * kTile;
-constexpr int kDataBytes = kPOff + kTile;  // 192 KB
+constexpr int kVOff = kKOff + kNSK * kTile;
+constexpr int kPOff = kVOff + kNSV * kTile;
+constexpr int kDataBytes = kPOff + kTile;  // 224 KB
 constexpr int kDecStages = 3;
 constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V (4 KB)
 static_assert(8 * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
 // barrier indices
 constexpr int kBarKFull = 0;
-constexpr int kBarVFull = kBarKFull + kNS;
-constexpr int kBarKVEmpty = kBarVFull + kNS;
-constexpr int kBarSFull = kBarKVEmpty + kNS;
+constexpr int kBarKEmpty = kBarKFull + kNSK;
+constexpr int kBarVFull = kBarKEmpty + kNSK;
+constexpr int kBarVEmpty = kBarVFull + kNSV;
+constexpr int kBarSFull = kBarVEmpty + kNSV;
 constexpr int kBarSFree = kBarSFull + 2;
 constexpr int kBarPFull = kBarSFree + 2;
 constexpr int kBarODone = kBarPFull + 1;
 constexpr int kBarDec = kBarODone + 1;  // 8 warps x 3 stages
 constexpr int kNumBars = kBarDec + 8 * kDecStages;
-constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kNumBars * 8 + 64;
+constexpr int kMiscBytes = 64 + 8 * 16;               // tmem slot, item slot, per-warp desc counters
+constexpr int kDescBytes = 8 * 4 * 40;                 // per-warp 4-entry UnitDesc rings
+constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kNumBars * 8 + kMiscBytes + kDescBytes;
+static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kTmemO = 256;  // O accumulator columns [256, 384); S buffers at 0 and 128
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
@@ -138,9 +143,31 @@ constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 1);
 }  // namespace fa
 
 // -------------------------------------------------------------- prefill tile
+struct TileDesc {
+  int tbl, o, c, t0, row0, kvh, nkeys, nblk;
+};
+
+// Expand tile index t (PrefillSlice records; see internal.h).
+__device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
+  int i = 0;
+  while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= t) ++i;
+  const PrefillSlice sl = p.slices[i];
+  const int local = t - sl.tbase;
+  const int qt = sl.nqt - 1 - local / p.Hkv;
+  TileDesc d;
+  d.tbl = sl.tbl;
+  d.o = sl.o;
+  d.c = sl.c;
+  d.t0 = qt * p.R;
+  d.row0 = sl.row0;
+  d.kvh = local % p.Hkv;
+  d.nkeys = sl.o + min(d.t0 + p.R, sl.c);
+  d.nblk = (d.nkeys + p.B - 1) / p.B;
+  return d;
+}
 // Roles inside the 256-thread CTA: warp 0 lane 0 = bulk-copy producer, warp 1
 // lane 0 = tcgen05 issuer, warps 4-7 = softmax (thread = TMEM lane = tile row).
-__device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillTile& t, uint8_t* smem,
+__device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc& t, uint8_t* smem,
                                              uint32_t sbase, uint32_t bars, uint32_t tmem, uint32_t& kv_iter,
                                              uint32_t& s_iter, uint32_t& pv_iter) {
   using namespace fa;
@@ -168,29 +195,30 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillT
     __syncthreads();
   }
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 2) {
     if (lane == 0) {
-      // ---------------- producer: K and V tiles of 128 keys, block by block
+      // ---------------- producers: warp 0 streams K tiles, warp 2 streams V tiles (128 keys, block by block)
+      const bool isK = warp == 0;
+      const int ns = isK ? kNSK : kNSV;
+      const uint8_t* pool = isK ? p.pool_k : p.pool_v;
+      const uint32_t ring = sbase + (isK ? kKOff : kVOff);
+      const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
       const int bpt = kBN / p.B;  // blocks per tile
       const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
       for (int j = 0; j < nk; ++j) {
         const uint32_t it = kv_iter + j;
-        const int st = it % kNS;
-        const uint32_t ph = (it / kNS) & 1;
-        mbar_wait(bars + 8 * (kBarKVEmpty + st), ph ^ 1);
-        const uint32_t kfull = bars + 8 * (kBarKFull + st), vfull = bars + 8 * (kBarVFull + st);
-        mbar_expect_tx(kfull, kTile);
-        mbar_expect_tx(vfull, kTile);
+        const int st = it % ns;
+        const uint32_t ph = (it / ns) & 1;
+        mbar_wait(bars + 8 * (bar_empty + st), ph ^ 1);
+        const uint32_t full = bars + 8 * (bar_full + st);
+        mbar_expect_tx(full, kTile);
         for (int b = 0; b < bpt; ++b) {
           int lb = j * bpt + b;
           if (lb >= t.nblk) lb = t.nblk - 1;  // finite data; masked out (P = 0)
           const int64_t phys = p.tables[t.tbl + lb];
           const int64_t off = (phys * p.Hkv + t.kvh) * p.chunk_bytes;
-          for (int pn = 0; pn < 2; ++pn) {
-            const uint32_t dst = pn * kPanel + b * seg;
-            bulk_g2s(sbase + kKOff + st * kTile + dst, p.pool_k + off + pn * seg, seg, kfull);
-            bulk_g2s(sbase + kVOff + st * kTile + dst, p.pool_v + off + pn * seg, seg, vfull);
-          }
+          for (int pn = 0; pn < 2; ++pn)
+            bulk_g2s(ring + st * kTile + pn * kPanel + b * seg, pool + off + pn * seg, seg, full);
         }
       }
     }
@@ -202,8 +230,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillT
           const uint32_t si = s_iter + j;
           const uint32_t sb = si & 1, sph = (si >> 1) & 1;
           const uint32_t it = kv_iter + j;
-          const int st = it % kNS;
-          const uint32_t ph = (it / kNS) & 1;
+          const int st = it % kNSK;
+          const uint32_t ph = (it / kNSK) & 1;
           mbar_wait(bars + 8 * (kBarSFree + sb), sph ^ 1);
           mbar_wait(bars + 8 * (kBarKFull + st), ph);
           tc_fence_after();
@@ -215,12 +243,13 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillT
                      kk > 0);
           }
           umma_commit(bars + 8 * (kBarSFull + sb));
+          umma_commit(bars + 8 * (kBarKEmpty + st));
         }
         if (j >= 1) {
           const int jj = j - 1;
           const uint32_t it = kv_iter + jj;
-          const int st = it % kNS;
-          const uint32_t ph = (it / kNS) & 1;
+          const int st = it % kNSV;
+          const uint32_t ph = (it / kNSV) & 1;
           mbar_wait(bars + 8 * kBarPFull, (pv_iter + jj) & 1);
           mbar_wait(bars + 8 * (kBarVFull + st), ph);
           tc_fence_after();
@@ -231,7 +260,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillT
             umma_f16(tmem + kTmemO, sw128_desc(pa + poff, 16, 1024), sw128_desc(va + kk * 2048, kPanel, 1024),
                      kIdescPV, (jj > 0 || kk > 0) ? 1u : 0u);
           }
-          umma_commit(bars + 8 * (kBarKVEmpty + st));
+          umma_commit(bars + 8 * (kBarVEmpty + st));
           umma_commit(bars + 8 * kBarODone);
         }
       }
@@ -349,22 +378,120 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const PrefillT
 }
 
 // --------------------------------------------------------------- decode unit
-__device__ __forceinline__ void decode_issue(const AttnParams& p, const DecodeUnit& u, int s, uint32_t stage,
+struct UnitDesc {
+  int id, tbl, ctx, row, kvh, k0, k1, nsplit, ubase, pad;
+};
+
+__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int id) {
+  const int local = id - r.ubase;
+  const int s = local / p.Hkv;
+  UnitDesc d;
+  d.id = id;
+  d.tbl = r.tbl;
+  d.ctx = r.ctx;
+  d.row = r.row;
+  d.kvh = local - s * p.Hkv;
+  d.k0 = s * p.split_len;
+  d.k1 = min(r.ctx, d.k0 + p.split_len);
+  d.nsplit = r.nsplit;
+  d.ubase = r.ubase;
+  d.pad = 0;
+  return d;
+}
+
+// Stage s of a unit = 16 tokens of one kv head: K then V (4 KB each at d = 128 bf16).
+__device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, uint32_t stage,
                                              uint32_t bar) {
   const int tok = u.k0 + 16 * s;
   const int lb = tok / p.B;
   const int sub = (tok - lb * p.B) >> 4;
-  const int64_t phys = p.tables[u.tbl + lb];
+  const int64_t phys = __ldg(p.tables + u.tbl + lb);
   const int64_t off = (phys * p.Hkv + u.kvh) * p.chunk_bytes + sub * 2048;
   const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
   mbar_expect_tx(bar, fa::kDecStage);
-  bulk_g2s(stage, p.pool_k + off, 2048, bar);
-  bulk_g2s(stage + 2048, p.pool_k + off + seg, 2048, bar);
-  bulk_g2s(stage + 4096, p.pool_v + off, 2048, bar);
-  bulk_g2s(stage + 6144, p.pool_v + off + seg, 2048, bar);
+  if (seg == 2048) {  // B = 16: the (block, head) chunk is one contiguous 4 KB run per K / V
+    bulk_g2s(stage, p.pool_k + off, 4096, bar);
+    bulk_g2s(stage + 4096, p.pool_v + off, 4096, bar);
+  } else {
+    bulk_g2s(stage, p.pool_k + off, 2048, bar);
+    bulk_g2s(stage + 2048, p.pool_k + off + seg, 2048, bar);
+    bulk_g2s(stage + 4096, p.pool_v + off, 2048, bar);
+    bulk_g2s(stage + 6144, p.pool_v + off + seg, 2048, bar);
+  }
 }
 
-__device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars) {
+// Load side of a decode warp (lane 0 only).  It walks a continuous stream of
+// 16-token stages across unit boundaries, keeping kDecStages in flight, and
+// prepares the NEXT unit one dependent step per issued stage (queue atomic ->
+// unit's row index -> row record) so the latency of that chain is hidden behind
+// the current unit.  Each new unit's descriptor is published to the compute
+// lanes through a 4-entry per-warp ring in shared memory (+ a counter).
+struct DecodeLoader {
+  UnitDesc cur;
+  int s, nst;
+  int nxt_id, nxt_row, nxt_step;  // 0: nothing, 1: id requested, 2: row loaded, 3: ready
+  DecodeRow nxt_r;
+  bool done;
+  uint32_t issued;
+
+  __device__ __forceinline__ void advance(const AttnParams& p) {
+    if (nxt_step == 0) {
+      nxt_id = atomicAdd(p.work + 1, 1);
+      nxt_step = 1;
+    } else if (nxt_step == 1) {
+      if (nxt_id < p.n_units) nxt_row = __ldg(p.urow + nxt_id);
+      nxt_step = 2;
+    } else if (nxt_step == 2) {
+      if (nxt_id < p.n_units) nxt_r = p.drows[nxt_row];
+      nxt_step = 3;
+    }
+  }
+  __device__ __forceinline__ void issue_next(const AttnParams& p, uint32_t ring, uint32_t bar0, UnitDesc* descs,
+                                             volatile int* n_desc) {
+    using namespace fa;
+    if (done) return;
+    if (s == nst) {
+      while (nxt_step < 3) advance(p);
+      const int k = *n_desc;
+      if (nxt_id >= p.n_units) {
+        done = true;
+        descs[k & 3].id = -1;  // end of stream
+        *n_desc = k + 1;
+        return;
+      }
+      cur = make_unit(p, nxt_r, nxt_id);
+      s = 0;
+      nst = (cur.k1 - cur.k0 + 15) >> 4;
+      nxt_step = 0;
+      descs[k & 3] = cur;
+      *n_desc = k + 1;
+    }
+    const uint32_t slot = issued % kDecStages;
+    decode_issue(p, cur, s, ring + slot * kDecStage, bar0 + 8 * slot);
+    ++s;
+    ++issued;
+    advance(p);
+  }
+};
+
+__device__ __forceinline__ void load_q_frags(const AttnParams& p, const UnitDesc& u, int gid, int tig,
+                                             uint32_t (&qa0)[8], uint32_t (&qa2)[8]) {
+  const int g = p.g;
+  const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(p.q) +
+                              (static_cast<int64_t>(u.row) * p.Hq + u.kvh * g + (gid < g ? gid : 0)) * fa::kD;
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) {
+    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tig));
+    const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tig));
+    qa0[kk] = gid < g ? a : 0u;
+    qa2[kk] = gid < g ? b : 0u;
+  }
+}
+
+// Compute side: every lane of the warp.  Split rows write an fp32 partial
+// (m, l, o~) at index `unit id` (fire and forget); unsplit rows write O / LSE.
+__device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars,
+                                                 UnitDesc* descs, volatile int* n_desc) {
   using namespace fa;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -374,37 +501,37 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   const uint32_t bar0 = bars + 8 * (kBarDec + warp * kDecStages);
   uint32_t dec_iter = 0;
   const float sl2 = p.scale_log2;
-  // ldmatrix lane geometry
   const int mi = lane >> 3, rr = lane & 7;
   const int ktok = (mi >> 1) * 8 + rr;  // K (non-trans): matrices (tok 0-7,c),(0-7,c+1),(8-15,c),(8-15,c+1)
   const int vtok = (mi & 1) * 8 + rr;   // V (trans):     matrices (tok 0-7,d),(8-15,d),(0-7,d+8),(8-15,d+8)
-  while (true) {
-    int ui = 0;
-    if (lane == 0) ui = atomicAdd(p.work + 1, 1);
-    ui = __shfl_sync(0xffffffffu, ui, 0);
-    if (ui >= p.n_units) break;
-    const DecodeUnit u = p.units[ui];
+
+  DecodeLoader ld;
+  ld.s = ld.nst = 0;
+  ld.nxt_step = 0;
+  ld.nxt_id = ld.nxt_row = 0;
+  ld.done = false;
+  ld.issued = 0;
+  if (lane == 0) {
+    *n_desc = 0;
+    for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
+  }
+  __syncwarp();
+
+  uint32_t qn0[8], qn2[8];
+  bool qn_valid = false;
+  for (int ck = 0;; ++ck) {
+    __syncwarp();
+    const UnitDesc u = descs[ck & 3];
+    if (u.id < 0) break;
     const int nst = (u.k1 - u.k0 + 15) >> 4;
-    if (lane == 0) {
-      const int pre = nst < kDecStages ? nst : kDecStages;
-      for (int s = 0; s < pre; ++s) {
-        const uint32_t slot = (dec_iter + s) % kDecStages;
-        decode_issue(p, u, s, ring + slot * kDecStage, bar0 + 8 * slot);
-      }
-    }
-    // Q fragments (A operand, rows = heads of the group, rows >= g are zero)
     uint32_t qa0[8], qa2[8];
-    {
-      const __nv_bfloat16* qrow = static_cast<const __nv_bfloat16*>(p.q) +
-                                  (static_cast<int64_t>(u.row) * p.Hq + u.kvh * g + (gid < g ? gid : 0)) * kD;
+    if (qn_valid) {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tig));
-        uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tig));
-        qa0[kk] = gid < g ? a : 0u;
-        qa2[kk] = gid < g ? b : 0u;
-      }
+      for (int kk = 0; kk < 8; ++kk) qa0[kk] = qn0[kk], qa2[kk] = qn2[kk];
+    } else {
+      load_q_frags(p, u, gid, tig, qa0, qa2);
     }
+    qn_valid = false;
     float o[16][4];
 #pragma unroll
     for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -462,71 +589,104 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
       }
       __syncwarp();
-      if (lane == 0 && s + kDecStages < nst) decode_issue(p, u, s + kDecStages, stg, bar0 + 8 * slot);
+      if (lane == 0) ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
       ++dec_iter;
+      // prefetch the next unit's Q fragments once its descriptor is published
+      if (!qn_valid && s + 2 >= nst) {
+        __syncwarp();
+        if (*n_desc > ck + 1) {
+          const UnitDesc nu = descs[(ck + 1) & 3];
+          if (nu.id >= 0) {
+            load_q_frags(p, nu, gid, tig, qn0, qn2);
+            qn_valid = true;
+          }
+        }
+      }
     }
     l += __shfl_xor_sync(0xffffffffu, l, 1);
     l += __shfl_xor_sync(0xffffffffu, l, 2);
-    const int D = kD;
-    if (u.nsplit == 1) {
-      if (gid < g) {
+    if (gid < g) {
+      const float inv = 1.f / l;
+      if (u.nsplit == 1) {
         const int h = u.kvh * g + gid;
-        const float inv = 1.f / l;
-        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + u.row) * D;
+        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + u.row) * kD;
 #pragma unroll
         for (int n = 0; n < 16; ++n)
           *reinterpret_cast<uint32_t*>(orow + n * 8 + 2 * tig) = pack_bf16(o[n][0] * inv, o[n][1] * inv);
         if (tig == 0 && p.lse != nullptr)
           p.lse[static_cast<int64_t>(h) * p.T + u.row] = (m + __log2f(l)) * 0.69314718055994530942f;
-      }
-    } else {
-      const int pidx = u.pbase + u.split;
-      if (gid < g) {
-        const float inv = 1.f / l;
-        float* po = p.part_o + (static_cast<int64_t>(pidx) * g + gid) * D;
+      } else {
+        float* po = p.part_o + (static_cast<int64_t>(u.id) * g + gid) * kD;
 #pragma unroll
         for (int n = 0; n < 16; ++n)
           __stcg(reinterpret_cast<float2*>(po + n * 8 + 2 * tig), make_float2(o[n][0] * inv, o[n][1] * inv));
-        if (tig == 0) __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(pidx) * g + gid) * 2),
-                             make_float2(m, l));
-      }
-      __threadfence();
-      __syncwarp();
-      int prev = 0;
-      if (lane == 0) prev = atomicAdd(p.counters + u.pair, 1);
-      prev = __shfl_sync(0xffffffffu, prev, 0);
-      if (prev == u.nsplit - 1) {
-        // a6: last split merges all partials of this (row, kv head), in split order.
-        __threadfence();
-        for (int hh = 0; hh < g; ++hh) {
-          float M = -INFINITY;
-          for (int sp = 0; sp < u.nsplit; ++sp)
-            M = fmaxf(M, __ldcg(p.part_ml + (static_cast<int64_t>(u.pbase + sp) * g + hh) * 2));
-          float L = 0.f;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          for (int sp = 0; sp < u.nsplit; ++sp) {
-            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + (static_cast<int64_t>(u.pbase + sp) * g + hh) * 2));
-            const float w = ex2(ml.x - M) * ml.y;
-            L += w;
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(p.part_o + (static_cast<int64_t>(u.pbase + sp) * g + hh) * D + lane * 4));
-            acc.x += w * v.x;
-            acc.y += w * v.y;
-            acc.z += w * v.z;
-            acc.w += w * v.w;
-          }
-          const float inv = 1.f / L;
-          const int h = u.kvh * g + hh;
-          __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + u.row) * D;
-          uint2 w2;
-          w2.x = pack_bf16(acc.x * inv, acc.y * inv);
-          w2.y = pack_bf16(acc.z * inv, acc.w * inv);
-          *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
-          if (lane == 0 && p.lse != nullptr)
-            p.lse[static_cast<int64_t>(h) * p.T + u.row] = (M + __log2f(L)) * 0.69314718055994530942f;
-        }
-        if (lane == 0) p.counters[u.pair] = 0;  // ready for the next launch
+        if (tig == 0)
+          __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(u.id) * g + gid) * 2), make_float2(m, l));
       }
     }
+  }
+}
+
+// a6 — after the grid barrier: merge the partials of every split (row, kv head, q head)
+// item, one warp per item, splits folded in index order (deterministic).  Rows with
+// nsplit > 1 form the prefix [0, n_merge_rows) of the sorted DecodeRow records.
+__device__ __forceinline__ void merge_phase(const AttnParams& p) {
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int g = p.g;
+  const int items = p.n_merge_rows * p.Hkv * g;
+  for (int it = gw; it < items; it += nw) {
+    const int hh = it % g;
+    const int pair = it / g;
+    const int r = pair / p.Hkv, kvh = pair - r * p.Hkv;
+    const DecodeRow dr = p.drows[r];
+    float M = -INFINITY, L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int sp = 0;
+    for (; sp + 4 <= dr.nsplit; sp += 4) {
+      float2 ml[4];
+      float4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int64_t pi = (static_cast<int64_t>(dr.ubase + (sp + k) * p.Hkv + kvh)) * g + hh;
+        ml[k] = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pi * 2));
+        v[k] = __ldcg(reinterpret_cast<const float4*>(p.part_o + pi * fa::kD + lane * 4));
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float Mn = fmaxf(M, ml[k].x);
+        const float a = ex2(M - Mn), w = ex2(ml[k].x - Mn) * ml[k].y;
+        L = L * a + w;
+        acc.x = acc.x * a + w * v[k].x;
+        acc.y = acc.y * a + w * v[k].y;
+        acc.z = acc.z * a + w * v[k].z;
+        acc.w = acc.w * a + w * v[k].w;
+        M = Mn;
+      }
+    }
+    for (; sp < dr.nsplit; ++sp) {
+      const int64_t pi = (static_cast<int64_t>(dr.ubase + sp * p.Hkv + kvh)) * g + hh;
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pi * 2));
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.part_o + pi * fa::kD + lane * 4));
+      const float Mn = fmaxf(M, ml.x);
+      const float a = ex2(M - Mn), w = ex2(ml.x - Mn) * ml.y;
+      L = L * a + w;
+      acc.x = acc.x * a + w * v.x;
+      acc.y = acc.y * a + w * v.y;
+      acc.z = acc.z * a + w * v.z;
+      acc.w = acc.w * a + w * v.w;
+      M = Mn;
+    }
+    const float inv = 1.f / L;
+    const int h = kvh * g + hh;
+    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + dr.row) * fa::kD;
+    uint2 w2;
+    w2.x = pack_bf16(acc.x * inv, acc.y * inv);
+    w2.y = pack_bf16(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
+    if (lane == 0 && p.lse != nullptr)
+      p.lse[static_cast<int64_t>(h) * p.T + dr.row] = (M + __log2f(L)) * 0.69314718055994530942f;
   }
 }
 
@@ -542,7 +702,7 @@ __global__ void __launch_bounds__(256, 1) hybrid_attn_bf16_kernel(const AttnPara
   const int warp = tid >> 5;
 
   if (tid == 0) {
-    for (int b = kBarKFull; b < kBarKVEmpty + kNS; ++b) mbar_init(bars + 8 * b, 1);
+    for (int b = kBarKFull; b < kBarVEmpty + kNSV; ++b) mbar_init(bars + 8 * b, 1);
     mbar_init(bars + 8 * (kBarSFull + 0), 1);
     mbar_init(bars + 8 * (kBarSFull + 1), 1);
     mbar_init(bars + 8 * (kBarSFree + 0), 128);
@@ -562,6 +722,9 @@ __global__ void __launch_bounds__(256, 1) hybrid_attn_bf16_kernel(const AttnPara
   tc_fence_after();
   const uint32_t tmem = any_tiles ? *tmem_slot : 0u;
 
+  uint64_t t_start = 0;
+  if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  int n_done_tiles = 0;
   uint32_t kv_iter = 0, s_iter = 0, pv_iter = 0;
   while (any_tiles) {
     if (tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
@@ -569,15 +732,44 @@ __global__ void __launch_bounds__(256, 1) hybrid_attn_bf16_kernel(const AttnPara
     const int item = *item_slot;
     __syncthreads();
     if (item >= p.n_tiles) break;
-    prefill_tile(p, p.tiles[item], smem, sbase, bars, tmem, kv_iter, s_iter, pv_iter);
+    prefill_tile(p, tile_desc(p, item), smem, sbase, bars, tmem, kv_iter, s_iter, pv_iter);
+    ++n_done_tiles;
   }
+  uint64_t t_prefill = 0;
+  if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prefill));
   // Switch roles: the ring overwrites prefill buffers through the async proxy.
   fence_proxy_async_smem();
   __syncthreads();
-  if (p.n_units > 0) decode_warp_loop(p, sbase, bars);
+  if (p.n_units > 0) {
+    uint8_t* misc = smem + kDataBytes + kNumBars * 8;
+    UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
+    volatile int* n_desc = reinterpret_cast<volatile int*>(misc + 64 + 16 * warp);
+    decode_warp_loop(p, sbase, bars, descs, n_desc);
+  }
+  if (p.n_merge_rows > 0) {
+    // grid barrier (cooperative launch: every CTA is resident), then the a6 merge phase
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(p.work + 3, 1);
+      while (atomicAdd(p.work + 3, 0) < static_cast<int>(gridDim.x)) __nanosleep(100);
+      __threadfence();
+    }
+    __syncthreads();
+    merge_phase(p);
+  }
 
   tc_fence_before();
   __syncthreads();
+  if (p.trace != nullptr && tid == 0) {
+    uint64_t t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    int64_t* tr = p.trace + 4 * blockIdx.x;
+    tr[0] = static_cast<int64_t>(t_start);
+    tr[1] = static_cast<int64_t>(t_prefill);
+    tr[2] = static_cast<int64_t>(t_end);
+    tr[3] = n_done_tiles;
+  }
   if (any_tiles && warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -589,6 +781,7 @@ __global__ void __launch_bounds__(256, 1) hybrid_attn_bf16_kernel(const AttnPara
       p.work[0] = 0;
       p.work[1] = 0;
       p.work[2] = 0;
+      p.work[3] = 0;
       __threadfence();
     }
   }
@@ -604,8 +797,19 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  hybrid_attn_bf16_kernel<<<grid, 256, fa::kSmemBytes, s>>>(p);
-  return cudaGetLastError();
+  // Cooperative launch: the decode merge phase follows a grid-wide barrier, which
+  // needs every CTA resident (1 CTA/SM, grid <= #SMs).
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = fa::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = p.n_merge_rows > 0 ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);
 }
 
 // ==================================================== generic f32 (config 1)

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <set>
@@ -66,24 +67,31 @@ struct niyama_kv {
   size_t staging_cap = 0;
   cudaEvent_t staging_ev = nullptr;
   bool staging_pending = false;
+  int64_t* trace = nullptr;  // niyama_debug_trace
+  int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
 };
 
 struct niyama_plan {
   niyama_kv* kv = nullptr;
   cudaStream_t stream = nullptr;
-  int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0, n_partials = 0;
+  int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0;
   int64_t sum_ctx = 0;
   std::vector<int32_t> slot_map;
   std::vector<int32_t> tables;
-  std::vector<PrefillTile> tiles;
-  std::vector<DecodeUnit> units;
+  struct Prev { int64_t seq; bool existed; int32_t len; };
+  std::vector<Prev> prev;  // bookkeeping before this plan (niyama_plan_rollback)
+  std::vector<PrefillSlice> slices;
+  std::vector<DecodeRow> drows;
+  std::vector<int32_t> urow;  // unit -> sorted decode row
+  int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;
   std::vector<RowInfo> rows;
   uint8_t* dbuf = nullptr;
   int32_t* d_slot = nullptr;
   int32_t* d_tables = nullptr;
-  PrefillTile* d_tiles = nullptr;
-  DecodeUnit* d_units = nullptr;
+  PrefillSlice* d_slices = nullptr;
+  DecodeRow* d_drows = nullptr;
   RowInfo* d_rows = nullptr;
+  int32_t* d_urow = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   int32_t* d_counters = nullptr;
@@ -131,6 +139,10 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->chunk_bytes = static_cast<int64_t>(c.block_size) * kv->row_bytes;
   kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
+  if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
+    const int v = std::atoi(sl);
+    if (v >= 16 && v % 16 == 0) kv->split_override = v;
+  }
   if (c.device != NIYAMA_DEVICE_NONE) {
     kv->has_device = true;
     cudaError_t e = cudaSetDevice(c.device);
@@ -236,10 +248,10 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
 namespace {
 
 // Decode split length (a5): a power of two >= 64 chosen from batch totals only
-// (sum ctx * Hkv against 4 units per resident warp), so split boundaries never
+// (sum ctx * Hkv against 8 units per resident warp), so split boundaries never
 // depend on scheduling and results stay bitwise deterministic.
 int32_t choose_split_len(int64_t sum_ctx, int hkv, int num_sms) {
-  const int64_t target = 4LL * num_sms * 8;
+  const int64_t target = 8LL * num_sms * 8;
   const int64_t raw = ceil_div(std::max<int64_t>(1, sum_ctx * hkv), target);
   int32_t s = 64;
   while (s < raw && s < 8192) s *= 2;
@@ -342,6 +354,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   // ---- host metadata
   auto* pl = new niyama_plan();
   pl->kv = kv;
+  for (const auto& u : undo) pl->prev.push_back(niyama_plan::Prev{u.seq, u.existed, u.len});
   pl->stream = reinterpret_cast<cudaStream_t>(stream);
   pl->T = static_cast<int32_t>(T);
   pl->D = D;
@@ -376,66 +389,54 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     pl->sum_ctx += desc->decode_ctx[j];
   }
   auto tier_of = [&](int k) -> int { return desc->tier ? desc->tier[k] : 0; };
-  // prefill tiles (a4): 128 MMA rows = g heads x R rows; longest first
+  // prefill slices (a4): 128 MMA rows = g heads x R rows; slices with the most keys first
   pl->R = 128 / g;
   {
-    struct Key { int32_t nkeys; int tier; int idx; };
-    std::vector<Key> keys;
-    for (int i = 0; i < P; ++i) {
-      const int32_t o = desc->prefill_offset[i], c = desc->prefill_len[i];
-      for (int32_t t0 = 0; t0 < c; t0 += pl->R) {
-        const int32_t nkeys = o + std::min(t0 + pl->R, c);
-        for (int h = 0; h < hkv; ++h) {
-          PrefillTile t{tbl_off[i], o, c, t0, row0[i], h, nkeys, static_cast<int32_t>(ceil_div(nkeys, B))};
-          keys.push_back(Key{nkeys, tier_of(i), static_cast<int>(pl->tiles.size())});
-          pl->tiles.push_back(t);
-        }
-      }
-    }
-    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
-      return a.nkeys != b.nkeys ? a.nkeys > b.nkeys : a.tier < b.tier;
+    std::vector<int> order;
+    for (int i = 0; i < P; ++i)
+      if (desc->prefill_len[i] > 0) order.push_back(i);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const int64_t ka = static_cast<int64_t>(desc->prefill_offset[a]) + desc->prefill_len[a];
+      const int64_t kb = static_cast<int64_t>(desc->prefill_offset[b]) + desc->prefill_len[b];
+      return ka != kb ? ka > kb : tier_of(a) < tier_of(b);
     });
-    std::vector<PrefillTile> sorted;
-    sorted.reserve(keys.size());
-    for (auto& k : keys) sorted.push_back(pl->tiles[k.idx]);
-    pl->tiles.swap(sorted);
+    int32_t tbase = 0;
+    for (int i : order) {
+      PrefillSlice sl{};
+      sl.tbl = tbl_off[i];
+      sl.o = desc->prefill_offset[i];
+      sl.c = desc->prefill_len[i];
+      sl.row0 = row0[i];
+      sl.nqt = static_cast<int32_t>(ceil_div(sl.c, pl->R));
+      sl.tbase = tbase;
+      tbase += sl.nqt * hkv;
+      pl->slices.push_back(sl);
+    }
+    pl->n_tiles = tbase;
   }
-  // decode units (a5): split [0, ctx) into split_len pieces; longest first
-  pl->split_len = choose_split_len(pl->sum_ctx, hkv, kv->num_sms);
+  // decode rows (a5): split [0, ctx) into split_len pieces; longest rows first
+  pl->split_len = kv->split_override > 0 ? kv->split_override : choose_split_len(pl->sum_ctx, hkv, kv->num_sms);
   {
-    struct Key { int32_t len; int tier; int idx; };
-    std::vector<Key> keys;
-    int32_t pbase = 0;
-    for (int j = 0; j < D; ++j) {
-      const int32_t ctx = desc->decode_ctx[j];
-      const int32_t ns = static_cast<int32_t>(ceil_div(ctx, pl->split_len));
-      for (int h = 0; h < hkv; ++h) {
-        for (int32_t s = 0; s < ns; ++s) {
-          DecodeUnit u{};
-          u.tbl = tbl_off[P + j];
-          u.ctx = ctx;
-          u.row = pl->prefill_rows + j;
-          u.kvh = h;
-          u.k0 = s * pl->split_len;
-          u.k1 = std::min(ctx, u.k0 + pl->split_len);
-          u.split = s;
-          u.nsplit = ns;
-          u.pbase = ns > 1 ? pbase : -1;
-          u.pair = j * hkv + h;
-          keys.push_back(Key{u.k1 - u.k0, tier_of(P + j), static_cast<int>(pl->units.size())});
-          pl->units.push_back(u);
-        }
-        if (ns > 1) pbase += ns;
-      }
-    }
-    pl->n_partials = pbase;
-    std::stable_sort(keys.begin(), keys.end(), [](const Key& a, const Key& b) {
-      return a.len != b.len ? a.len > b.len : a.tier < b.tier;
+    std::vector<int> order(D);
+    for (int j = 0; j < D; ++j) order[j] = j;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      return desc->decode_ctx[a] != desc->decode_ctx[b] ? desc->decode_ctx[a] > desc->decode_ctx[b]
+                                                         : tier_of(P + a) < tier_of(P + b);
     });
-    std::vector<DecodeUnit> sorted;
-    sorted.reserve(keys.size());
-    for (auto& k : keys) sorted.push_back(pl->units[k.idx]);
-    pl->units.swap(sorted);
+    int32_t ubase = 0;
+    for (int j : order) {
+      DecodeRow r{};
+      r.tbl = tbl_off[P + j];
+      r.ctx = desc->decode_ctx[j];
+      r.row = pl->prefill_rows + j;
+      r.nsplit = static_cast<int32_t>(ceil_div(r.ctx, pl->split_len));
+      r.ubase = ubase;
+      ubase += r.nsplit * hkv;
+      if (r.nsplit > 1) ++pl->n_merge_rows;
+      for (int32_t u = 0; u < r.nsplit * hkv; ++u) pl->urow.push_back(static_cast<int32_t>(pl->drows.size()));
+      pl->drows.push_back(r);
+    }
+    pl->n_units = ubase;
   }
   // ---- device copy: one allocation, one H2D
   if (kv->has_device) {
@@ -448,12 +449,13 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     };
     const size_t o_slot = take(pl->slot_map.size() * 4);
     const size_t o_tbl = take(pl->tables.size() * 4);
-    const size_t o_tiles = take(pl->tiles.size() * sizeof(PrefillTile));
-    const size_t o_units = take(pl->units.size() * sizeof(DecodeUnit));
+    const size_t o_tiles = take(pl->slices.size() * sizeof(PrefillSlice));
+    const size_t o_units = take(pl->drows.size() * sizeof(DecodeRow));
     const size_t o_rows = take(pl->rows.size() * sizeof(RowInfo));
+    const size_t o_urow = take(pl->urow.size() * 4);
     const size_t meta_bytes = off;
-    const size_t o_part_o = take(static_cast<size_t>(pl->n_partials) * g * kv->d * 4);
-    const size_t o_part_ml = take(static_cast<size_t>(pl->n_partials) * g * 2 * 4);
+    const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
+    const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
     const size_t o_cnt = take(static_cast<size_t>(D) * hkv * 4);
     const size_t o_work = take(16);
     const size_t total = off;
@@ -471,9 +473,10 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       uint8_t* h = static_cast<uint8_t*>(kv->staging);
       std::memcpy(h + o_slot, pl->slot_map.data(), pl->slot_map.size() * 4);
       std::memcpy(h + o_tbl, pl->tables.data(), pl->tables.size() * 4);
-      std::memcpy(h + o_tiles, pl->tiles.data(), pl->tiles.size() * sizeof(PrefillTile));
-      std::memcpy(h + o_units, pl->units.data(), pl->units.size() * sizeof(DecodeUnit));
+      std::memcpy(h + o_tiles, pl->slices.data(), pl->slices.size() * sizeof(PrefillSlice));
+      std::memcpy(h + o_units, pl->drows.data(), pl->drows.size() * sizeof(DecodeRow));
       std::memcpy(h + o_rows, pl->rows.data(), pl->rows.size() * sizeof(RowInfo));
+      std::memcpy(h + o_urow, pl->urow.data(), pl->urow.size() * 4);
       e = cudaMemcpyAsync(pl->dbuf, h, meta_bytes, cudaMemcpyHostToDevice, s);
     }
     if (e == cudaSuccess) e = cudaMemsetAsync(pl->dbuf + o_cnt, 0, total - o_cnt, s);
@@ -487,9 +490,10 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     kv->staging_pending = true;
     pl->d_slot = reinterpret_cast<int32_t*>(pl->dbuf + o_slot);
     pl->d_tables = reinterpret_cast<int32_t*>(pl->dbuf + o_tbl);
-    pl->d_tiles = reinterpret_cast<PrefillTile*>(pl->dbuf + o_tiles);
-    pl->d_units = reinterpret_cast<DecodeUnit*>(pl->dbuf + o_units);
+    pl->d_slices = reinterpret_cast<PrefillSlice*>(pl->dbuf + o_tiles);
+    pl->d_drows = reinterpret_cast<DecodeRow*>(pl->dbuf + o_units);
     pl->d_rows = reinterpret_cast<RowInfo*>(pl->dbuf + o_rows);
+    pl->d_urow = reinterpret_cast<int32_t*>(pl->dbuf + o_urow);
     pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
     pl->d_part_ml = reinterpret_cast<float*>(pl->dbuf + o_part_ml);
     pl->d_counters = reinterpret_cast<int32_t*>(pl->dbuf + o_cnt);
@@ -508,13 +512,34 @@ extern "C" void niyama_plan_destroy(niyama_plan* plan) {
   delete plan;
 }
 
+extern "C" niyama_status niyama_plan_rollback(niyama_kv* kv, niyama_plan* plan) {
+  if (!kv || !plan || plan->kv != kv) return fail(NIYAMA_EINVAL, "kv/plan mismatch");
+  for (auto it = plan->prev.rbegin(); it != plan->prev.rend(); ++it) {
+    auto sit = kv->seqs.find(it->seq);
+    if (sit == kv->seqs.end()) continue;  // released meanwhile
+    if (!it->existed) {
+      for (int32_t b : sit->second.blocks) kv->free_.insert(b);
+      kv->seqs.erase(sit);
+      continue;
+    }
+    Seq& q = sit->second;
+    if (it->len > q.len) return fail(NIYAMA_ESTATE, "rollback: sequence shorter than before the plan");
+    const size_t keep = static_cast<size_t>(ceil_div(it->len, kv->B));
+    for (size_t k = keep; k < q.blocks.size(); ++k) kv->free_.insert(q.blocks[k]);
+    q.blocks.resize(keep);
+    q.len = it->len;
+  }
+  plan->prev.clear();
+  return NIYAMA_OK;
+}
+
 extern "C" niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_plan_info* out) {
   if (!plan || !out) return fail(NIYAMA_EINVAL, "plan/out is NULL");
   out->num_rows = plan->T;
   out->num_prefill_rows = plan->prefill_rows;
   out->num_decode = plan->D;
-  out->num_prefill_tiles = static_cast<int32_t>(plan->tiles.size());
-  out->num_decode_units = static_cast<int32_t>(plan->units.size());
+  out->num_prefill_tiles = plan->n_tiles;
+  out->num_decode_units = plan->n_units;
   out->split_len = plan->split_len;
   out->rows_per_tile = plan->R;
   out->reserved = 0;
@@ -584,8 +609,8 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.o = o;
   p.lse = lse;
   p.tables = plan->d_tables;
-  p.tiles = plan->d_tiles;
-  p.units = plan->d_units;
+  p.slices = plan->d_slices;
+  p.drows = plan->d_drows;
   p.rows = plan->d_rows;
   p.part_o = plan->d_part_o;
   p.part_ml = plan->d_part_ml;
@@ -599,9 +624,15 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.B = kv->B;
   p.g = kv->g;
   p.R = plan->R;
-  p.n_tiles = static_cast<int32_t>(plan->tiles.size());
-  p.n_units = static_cast<int32_t>(plan->units.size());
+  p.n_tiles = plan->n_tiles;
+  p.n_units = plan->n_units;
+  p.n_slices = static_cast<int32_t>(plan->slices.size());
+  p.n_drows = static_cast<int32_t>(plan->drows.size());
+  p.split_len = plan->split_len;
+  p.urow = plan->d_urow;
+  p.n_merge_rows = plan->n_merge_rows;
   p.scale_log2 = scale * 1.4426950408889634f;
+  p.trace = kv->trace;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (kv->cfg.dtype == NIYAMA_BF16) {
     if (kv->d != 128 || kv->g > 8)
@@ -613,6 +644,12 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
     if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
     NY_CUDA(launch_attention_generic_f32(p, s));
   }
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf) {
+  if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");
+  kv->trace = device_buf;
   return NIYAMA_OK;
 }
 

@@ -140,7 +140,7 @@ def test_device_calls_refuse_without_gpu():
 
 def test_work_list_sizing():
     """a2: tiles = sum ceil(c/R) * Hkv with R = 128/g; units = sum ceil(ctx/split) * Hkv;
-    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 4 * 148 * 8."""
+    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 8 * 148 * 8."""
     ctx = W.l8b_decode_ctx()
     wl = W.hybrid(W.L8B, "sizing", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
     kv = host_kv(W.L8B, wl.num_blocks)
@@ -149,9 +149,29 @@ def test_work_list_sizing():
     info = p.info()
     assert info.rows_per_tile == 32
     assert info.num_prefill_tiles == (512 // 32) * 8
-    assert info.split_len == 256                      # 133674*8/4736 = 225.8 -> 256
-    assert info.num_decode_units == sum(-(-int(c) // 256) for c in ctx) * 8
+    assert info.split_len == 128                      # 133674*8/9472 = 112.9 -> 128
+    assert info.num_decode_units == sum(-(-int(c) // 128) for c in ctx) * 8
     assert info.sum_ctx == 133674 and info.num_rows == 576
+
+
+def test_plan_rollback_matches_oracle_truncate():
+    shape = W.Shape(num_q_heads=8, num_kv_heads=2, head_dim=128, block_size=16, dtype="bf16")
+    wl = W.random_hybrid(shape, seed=9, num_prefill=2, max_chunk=200, num_decode=6, max_ctx=500, extra_blocks=64)
+    kv, pool, _ = replay_both(wl)
+    free0 = kv.num_free()
+    d = wl.final.desc
+    nxt = W.BatchDesc(prefill_seq=list(d.prefill_seq) + [777], prefill_offset=[o + c for o, c in zip(
+        d.prefill_offset, d.prefill_len)] + [0], prefill_len=[33] * len(d.prefill_seq) + [40],
+        decode_seq=list(d.decode_seq), decode_ctx=[c + 1 for c in d.decode_ctx])
+    tables = {s: kv.block_table(s) for s in pool.table}
+    p = kv.plan(nxt)
+    p.rollback()
+    assert kv.num_free() == free0
+    assert {s: kv.block_table(s) for s in pool.table} == tables
+    with pytest.raises(ny.NiyamaError):
+        kv.seq_len(777)
+    # replaying the same plan lands in the same blocks and slots
+    assert kv.plan(nxt).slots() == [tuple(x) for x in pool.plan(nxt).slots]
 
 
 def test_head_shard_config():
