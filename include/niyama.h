@@ -186,10 +186,14 @@ niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t l
 niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q,
                                       void* o, float* lse, float softmax_scale, niyama_stream stream);
 
-/* Diagnostics: when device_buf (DEVICE, int64 [#SMs][4]) is non-NULL every
- * later niyama_hybrid_attention writes, per CTA, globaltimer ns at start, at
- * the end of its prefill tiles, at exit, and the number of prefill tiles it
- * ran.  NULL turns tracing off (the default). */
+/* Diagnostics: when device_buf (DEVICE, int64, >= 160*8 + 10*64 entries,
+ * zeroed by the caller) is non-NULL every later niyama_hybrid_attention
+ * writes, per CTA c at [8c..8c+5]: globaltimer ns at start, end of its
+ * prefill tiles, exit, #prefill tiles, end of its decode units, grid barrier
+ * passed; and at [1280 + 64*role + j] CTA 0's clock64 when key tile j of its
+ * first prefill tile passed role's step (0 K issue, 1 V issue, 2 QK issue,
+ * 3 PV issue, 4 S ready, 5 row max done, 6 P written, 7 rescale done, 8-9 P half
+ * written).  NULL = off (default). */
 niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
 
 /* a7 — head sharding across the GPUs of one node (§8e).  comm_init creates

@@ -20,10 +20,10 @@ namespace niyama {
 // Compact work list (a2 -> a4/a5).  The kernel expands item indices itself, so
 // the per-iteration H2D stays small (tables + one record per slice / decode).
 //
-// Prefill slice: its tiles are [tbase, tbase + nqt*Hkv); tile t of the slice is
-// q-tile qt = nqt-1 - (t-tbase)/Hkv (largest key range first), kv head
-// (t-tbase)%Hkv, rows [qt*R, min(qt*R+R, c)) with R = 128/g chunk rows per tile
-// (128 MMA rows = g query heads x R rows).  (a4)
+// Prefill slice: its work items are [tbase, tbase + ceil(nqt/2)*Hkv); item t is the
+// pair qp = npair-1 - (t-tbase)/Hkv (largest key ranges first) of q tiles 2qp and
+// 2qp+1 of kv head (t-tbase)%Hkv; q tile k covers rows [k*R, min(k*R+R, c)) with
+// R = 128/g chunk rows (128 MMA rows = g query heads x R rows).  (a4)
 struct PrefillSlice {
   int32_t tbl;    // offset of the sequence's block table in the tables array
   int32_t o;      // slice offset (positions of rows are o + i)
@@ -34,10 +34,10 @@ struct PrefillSlice {
   int32_t pad0, pad1;
 };
 
-// Decode row (sorted by ctx, longest first): its units are [ubase, ubase +
-// nsplit*Hkv); unit u has split s = (u-ubase)/Hkv over keys [s*L, min(ctx,
-// (s+1)*L)) with L = split_len, kv head (u-ubase)%Hkv.  Unit u's partial (when
-// nsplit > 1) lives at index u; merge counter = sorted_row*Hkv + head.  (a5, a6)
+// Decode row (sorted by ctx, longest first): unit (row, split s, kv head h) covers
+// keys [s*L, min(ctx, (s+1)*L)) with L = split_len; its partial (when nsplit > 1)
+// lives at the canonical index ubase + s*Hkv + h.  The device queue visits units in
+// the order of `urow` (one entry per (row, split), heads consecutive).  (a5, a6)
 struct DecodeRow {
   int32_t tbl;
   int32_t ctx;
@@ -62,7 +62,7 @@ struct AttnParams {
   const int32_t* tables;
   const PrefillSlice* slices;
   const DecodeRow* drows;
-  const int32_t* urow;   // [n_units] sorted row index of each decode unit
+  const int32_t* urow;   // [n_units / Hkv] queue entry -> (sorted row << 12) | split
   const RowInfo* rows;
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]

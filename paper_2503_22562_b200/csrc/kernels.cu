@@ -21,6 +21,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -30,26 +31,25 @@ namespace niyama {
 using namespace ptx;
 
 // ============================================================= append (a3)
-// One thread per 16-byte piece of a (row, kv head) vector.  Source rows are
-// dense [T][Hkv][row_bytes]; the destination piece j of the row at (block,
-// slot) lands in panel j/8 at chunk position (j%8) ^ (slot%8).
-__global__ void kv_append_kernel(const AppendParams p) {
-  const int pieces = p.row_bytes >> 4;
-  const int64_t total = static_cast<int64_t>(p.T) * p.Hkv * pieces;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int j = static_cast<int>(idx % pieces);
-    const int64_t rh = idx / pieces;
-    const int h = static_cast<int>(rh % p.Hkv);
-    const int r = static_cast<int>(rh / p.Hkv);
-    const int32_t sm = p.slot_map[r];
-    const int64_t blk = sm / p.B;
-    const int slot = sm - static_cast<int>(blk) * p.B;
-    const int64_t src_off = rh * p.row_bytes + (static_cast<int64_t>(j) << 4);
-    const int64_t dst_off = (blk * p.Hkv + h) * p.chunk_bytes + static_cast<int64_t>(j >> 3) * p.B * 128 +
+// One thread per 16-byte piece of a (row, kv head) vector, 32-bit index math (the
+// launcher guarantees T*Hkv*pieces < 2^31).  Source rows are dense [T][Hkv][row_bytes];
+// piece j of the row at (block, slot) lands in panel j/8 at chunk position
+// (j%8) ^ (slot%8).  K and V move together; all loads are issued before the stores.
+__global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
+  const int pieces = p.row_bytes >> 4;  // 16 at d = 128 bf16
+  const int total = p.T * p.Hkv * pieces;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int j = idx % pieces;
+    const int rh = idx / pieces;
+    const int h = rh % p.Hkv;
+    const int r = rh / p.Hkv;
+    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(p.k_new) + idx);
+    const uint4 vv = __ldg(reinterpret_cast<const uint4*>(p.v_new) + idx);
+    const int32_t sm = __ldg(p.slot_map + r);
+    const int blk = sm / p.B;
+    const int slot = sm - blk * p.B;
+    const int64_t dst_off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + (j >> 3) * p.B * 128 +
                             slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
-    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(p.k_new + src_off));
-    const uint4 vv = __ldg(reinterpret_cast<const uint4*>(p.v_new + src_off));
     *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
     *reinterpret_cast<uint4*>(p.pool_v + dst_off) = vv;
   }
@@ -58,8 +58,9 @@ __global__ void kv_append_kernel(const AppendParams p) {
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(p.T) * p.Hkv * (p.row_bytes >> 4);
   if (total == 0) return cudaSuccess;
+  if (total >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   int64_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks > 148 * 8) blocks = 148 * 8;
   kv_append_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(p);
   return cudaGetLastError();
 }
@@ -100,280 +101,363 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 }
 
 // ===================================================== fused bf16 attention
+// CTA = 384 threads (3 warpgroups), 1 CTA/SM, 512 TMEM columns.  Warpgroups 0-1 (softmax,
+// decode, merge) run with 224 registers, warpgroup 2 (bulk-copy producers, MMA issuer) with 56.
 // Shared memory map (bytes from the 1024-aligned base):
-//   [0, 32K)            Q tile   (2 panels x 128 rows x 128 B, SW128)
-//   [32K, +3*32K)       K stages (128 keys x 256 B each)
+//   [0, 64K)            Q_A, Q_B tiles (2 panels x 128 rows x 128 B each, SW128)
+//   [64K, +3*32K)       K stages (128 keys x 256 B each)
 //   [.., +2*32K)        V stages
-//   [.., +32K)          P tile   (2 panels x 128 rows x 128 B, SW128, bf16)
+// TMEM: S_A/P_A cols [0,128), S_B/P_B [128,256), O_A [256,384), O_B [384,512).
 // The decode role reuses [0, 192K) as 8 warps x 3 stages x 8 KB.
 namespace fa {
 constexpr int kD = 128;            // head dim (bf16 path)
-constexpr int kBN = 128;           // keys per prefill tile
-constexpr int kNSK = 3;            // K stages (released by the QK^T commit)
-constexpr int kNSV = 2;            // V stages (released by the PV commit)
+constexpr int kBN = 128;           // keys per prefill key tile
+constexpr int kNSK = 3;            // K stages (released after both QK^T of a key tile)
+constexpr int kNSV = 2;            // V stages (released after both PV of a key tile)
 constexpr int kPanel = 128 * 128;  // one 64-column panel of a 128-row tile
 constexpr int kTile = 2 * kPanel;  // 128 rows x 256 B
-constexpr int kQOff = 0;
-constexpr int kKOff = kTile;
+constexpr int kQOff = 0;           // Q_X at kQOff + X * kTile
+constexpr int kKOff = 2 * kTile;
 constexpr int kVOff = kKOff + kNSK * kTile;
-constexpr int kPOff = kVOff + kNSV * kTile;
-constexpr int kDataBytes = kPOff + kTile;  // 224 KB
+constexpr int kDataBytes = kVOff + kNSV * kTile;  // 224 KB
+constexpr int kThreads = 384;
+constexpr int kWarpLoad = 8, kWarpMMA = 9;  // warp 8: lane 0 streams K, lane 1 streams V; warp 9 lane 0: MMA
+constexpr int kRegsMath = 216, kRegsCtl = 72;  // setmaxnreg budgets: warpgroups 0-1 / warpgroup 2
+static_assert(2 * kRegsMath + kRegsCtl <= 65536 / kThreads / 8 * 8 * 3, "setmaxnreg budgets exceed the launch allocation");
+constexpr int kDecWarps = 8;
 constexpr int kDecStages = 3;
 constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V (4 KB)
-static_assert(8 * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
+static_assert(kDecWarps * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
 // barrier indices
 constexpr int kBarKFull = 0;
 constexpr int kBarKEmpty = kBarKFull + kNSK;
 constexpr int kBarVFull = kBarKEmpty + kNSK;
 constexpr int kBarVEmpty = kBarVFull + kNSV;
-constexpr int kBarSFull = kBarVEmpty + kNSV;
-constexpr int kBarSFree = kBarSFull + 2;
-constexpr int kBarPFull = kBarSFree + 2;
-constexpr int kBarODone = kBarPFull + 1;
-constexpr int kBarDec = kBarODone + 1;  // 8 warps x 3 stages
-constexpr int kNumBars = kBarDec + 8 * kDecStages;
-constexpr int kMiscBytes = 64 + 8 * 16;               // tmem slot, item slot, per-warp desc counters
-constexpr int kDescBytes = 8 * 4 * 40;                 // per-warp 4-entry UnitDesc rings
+constexpr int kBarSFull = kBarVEmpty + kNSV;  // [2] per Q tile: QK^T committed
+constexpr int kBarPFull = kBarSFull + 2;      // [2] per Q tile: P written to TMEM (128 arrivals)
+constexpr int kBarODone = kBarPFull + 2;      // [2] per Q tile: PV committed
+constexpr int kBarDec = kBarODone + 2;        // kDecWarps x kDecStages
+constexpr int kNumBars = kBarDec + kDecWarps * kDecStages;
+constexpr int kMiscBytes = 64 + kDecWarps * 16;      // tmem slot, item slot, per-warp desc counters
+constexpr int kDescBytes = kDecWarps * 4 * 40;       // per-warp 4-entry UnitDesc rings
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kNumBars * 8 + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemO = 256;  // O accumulator columns [256, 384); S buffers at 0 and 128
+constexpr uint32_t kTmemS = 0;    // S_X / P_X at kTmemS + 128 X
+constexpr uint32_t kTmemO = 256;  // O_X at kTmemO + 128 X
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 1);
 }  // namespace fa
 
-// -------------------------------------------------------------- prefill tile
-struct TileDesc {
-  int tbl, o, c, t0, row0, kvh, nkeys, nblk;
+// -------------------------------------------------------------- prefill pair
+// Debug event log (niyama_debug_trace): CTA 0's first item, key tiles < 64, clock64 per role.
+__device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
+  if (ev != nullptr && j < 64) {
+    int64_t c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    ev[role * 64 + j] = c;
+  }
+}
+
+// A prefill work item = a PAIR of 128-row Q tiles (X = 0: q-tile 2qp, X = 1: q-tile
+// 2qp+1) of one kv head; both stream the same K/V tiles.  Tile X's rows r = hh*R + i
+// hold chunk row t0[X] + i of query head kvh*g + hh (GQA packing, R = 128/g).
+struct PairDesc {
+  int tbl, o, c, row0, kvh, nblk;
+  int t0[2], vrows[2], nk[2];
 };
 
-// Expand tile index t (PrefillSlice records; see internal.h).
-__device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
+__device__ __forceinline__ PairDesc pair_desc(const AttnParams& p, int item) {
   int i = 0;
-  while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= t) ++i;
+  while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= item) ++i;
   const PrefillSlice sl = p.slices[i];
-  const int local = t - sl.tbase;
-  const int qt = sl.nqt - 1 - local / p.Hkv;
-  TileDesc d;
+  const int local = item - sl.tbase;
+  const int npair = (sl.nqt + 1) >> 1;
+  const int qp = npair - 1 - local / p.Hkv;  // largest key ranges first
+  PairDesc d;
   d.tbl = sl.tbl;
   d.o = sl.o;
   d.c = sl.c;
-  d.t0 = qt * p.R;
   d.row0 = sl.row0;
   d.kvh = local % p.Hkv;
-  d.nkeys = sl.o + min(d.t0 + p.R, sl.c);
-  d.nblk = (d.nkeys + p.B - 1) / p.B;
+  int nkeys_max = 0;
+#pragma unroll
+  for (int X = 0; X < 2; ++X) {
+    d.t0[X] = (2 * qp + X) * p.R;
+    d.vrows[X] = max(0, min(p.R, sl.c - d.t0[X]));
+    const int nkeys = d.vrows[X] > 0 ? sl.o + d.t0[X] + d.vrows[X] : 0;
+    d.nk[X] = (nkeys + fa::kBN - 1) / fa::kBN;
+    nkeys_max = max(nkeys_max, nkeys);
+  }
+  d.nblk = (nkeys_max + p.B - 1) / p.B;
   return d;
 }
-// Roles inside the 256-thread CTA: warp 0 lane 0 = bulk-copy producer, warp 1
-// lane 0 = tcgen05 issuer, warps 4-7 = softmax (thread = TMEM lane = tile row).
-__device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc& t, uint8_t* smem,
-                                             uint32_t sbase, uint32_t bars, uint32_t tmem, uint32_t& kv_iter,
-                                             uint32_t& s_iter, uint32_t& pv_iter) {
+
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Roles: warp 8 lane 0 streams K tiles and lane 1 V tiles (bulk copies of pre-swizzled
+// paged blocks), warp 9 lane 0 issues tcgen05 MMAs, warps 0-3 run the
+// softmax of tile A and warps 4-7 that of tile B (thread = TMEM lane = tile row).
+// MMA order per key tile j:  PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1) — the tensor pipe
+// executes in issue order, so "S_X(j+1) ready" implies "PV_X(j) done": the softmax of
+// tile X may rescale O_X right after S_X(j+1) lands, and P_X(j) (bf16, written into
+// the first 64 columns of S_X) is consumed by PV_X(j) from TMEM before QK_X(j+1)
+// overwrites S_X.
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
+// kMath = true: warpgroups 0-1 (Q load, softmax of tiles A/B); false: warpgroup 2
+// (bulk-copy producers, MMA issuer).  Both instantiations run the same named-barrier
+// sequence, so the two register budgets never share a code path.
+template <bool kMath>
+__device__ __forceinline__ void prefill_pair(const AttnParams& p, const PairDesc& t, uint32_t sbase, uint32_t bars,
+                                             uint32_t tmem, uint32_t& kv_it, uint32_t (&it)[2]) {
   using namespace fa;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
   const int g = p.g, R = p.R;
-  const int vrows = min(R, t.c - t.t0);
-  const int nk = (t.nkeys + kBN - 1) / kBN;
+  const int nk = max(t.nk[0], t.nk[1]);
+  int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && kv_it == 0) ? p.trace + 8 * 160 : nullptr;  // [10 roles][64]
 
-  // ---- Q tile: rows r = hh*R + i  <-  q[row0 + t0 + i][kvh*g + hh][:]
-  {
+  // ---- Q tiles: tile X row r = hh*R + i  <-  q[row0 + t0[X] + i][kvh*g + hh][:]
+  if constexpr (kMath) {
     const uint8_t* q = static_cast<const uint8_t*>(p.q);
-    for (int idx = tid; idx < 128 * 16; idx += 256) {
-      const int r = idx >> 4, j = idx & 15;
+    for (int idx = tid; idx < 2 * 128 * 16; idx += 256) {
+      const int X = idx >> 11, r = (idx >> 4) & 127, j = idx & 15;
       const int hh = r / R, i = r - hh * R;
+      const int vrowsX = X ? t.vrows[1] : t.vrows[0], t0X = X ? t.t0[1] : t.t0[0];
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < vrows) {
-        const int64_t row = t.row0 + t.t0 + i;
+      if (i < vrowsX) {
+        const int64_t row = t.row0 + t0X + i;
         v = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
       }
-      st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
+      st_shared_v4(sbase + kQOff + X * kTile + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), v.x, v.y,
+                   v.z, v.w);
     }
     fence_proxy_async_smem();
-    __syncthreads();
   }
+  named_bar_sync(1, kThreads);  // Q tiles in smem
 
-  if (warp == 0 || warp == 2) {
-    if (lane == 0) {
-      // ---------------- producers: warp 0 streams K tiles, warp 2 streams V tiles (128 keys, block by block)
-      const bool isK = warp == 0;
+  if (!kMath && warp == kWarpLoad) {
+    if (lane < 2) {
+      // ---------------- producers (two lanes, independent thread scheduling): 128-key K / V tiles
+      const bool isK = lane == 0;
       const int ns = isK ? kNSK : kNSV;
       const uint8_t* pool = isK ? p.pool_k : p.pool_v;
       const uint32_t ring = sbase + (isK ? kKOff : kVOff);
       const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
-      const int bpt = kBN / p.B;  // blocks per tile
+      const int bpt = kBN / p.B;  // blocks per key tile
       const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
       for (int j = 0; j < nk; ++j) {
-        const uint32_t it = kv_iter + j;
-        const int st = it % ns;
-        const uint32_t ph = (it / ns) & 1;
+        const uint32_t k_it = kv_it + j;
+        const int st = k_it % ns;
+        const uint32_t ph = (k_it / ns) & 1;
         mbar_wait(bars + 8 * (bar_empty + st), ph ^ 1);
+        ev_stamp(ev, isK ? 0 : 1, j);
         const uint32_t full = bars + 8 * (bar_full + st);
         mbar_expect_tx(full, kTile);
         for (int b = 0; b < bpt; ++b) {
           int lb = j * bpt + b;
           if (lb >= t.nblk) lb = t.nblk - 1;  // finite data; masked out (P = 0)
-          const int64_t phys = p.tables[t.tbl + lb];
+          const int64_t phys = __ldg(p.tables + t.tbl + lb);
           const int64_t off = (phys * p.Hkv + t.kvh) * p.chunk_bytes;
           for (int pn = 0; pn < 2; ++pn)
             bulk_g2s(ring + st * kTile + pn * kPanel + b * seg, pool + off + pn * seg, seg, full);
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (!kMath && warp == kWarpMMA) {
     if (lane == 0) {
       // ---------------- tcgen05 issuer
-      for (int j = 0; j <= nk; ++j) {
-        if (j < nk) {
-          const uint32_t si = s_iter + j;
-          const uint32_t sb = si & 1, sph = (si >> 1) & 1;
-          const uint32_t it = kv_iter + j;
-          const int st = it % kNSK;
-          const uint32_t ph = (it / kNSK) & 1;
-          mbar_wait(bars + 8 * (kBarSFree + sb), sph ^ 1);
-          mbar_wait(bars + 8 * (kBarKFull + st), ph);
-          tc_fence_after();
-          const uint32_t qa = sbase + kQOff, ka = sbase + kKOff + st * kTile;
+      auto qk = [&](int X, int j) {
+        const uint32_t k_it = kv_it + j;
+        const int st = k_it % kNSK;
+        mbar_wait(bars + 8 * (kBarKFull + st), (k_it / kNSK) & 1);
+        tc_fence_after();
+        if (X == 0) ev_stamp(ev, 2, j);
+        const uint32_t qa = sbase + kQOff + X * kTile, ka = sbase + kKOff + st * kTile;
 #pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk) {
-            const uint32_t koff = (kk >> 2) * kPanel + (kk & 3) * 32;
-            umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), sw128_desc(ka + koff, 16, 1024), kIdescQK,
-                     kk > 0);
-          }
-          umma_commit(bars + 8 * (kBarSFull + sb));
-          umma_commit(bars + 8 * (kBarKEmpty + st));
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t koff = (kk >> 2) * kPanel + (kk & 3) * 32;
+          umma_f16(tmem + kTmemS + 128 * X, sw128_desc(qa + koff, 16, 1024), sw128_desc(ka + koff, 16, 1024),
+                   kIdescQK, kk > 0);
         }
-        if (j >= 1) {
-          const int jj = j - 1;
-          const uint32_t it = kv_iter + jj;
-          const int st = it % kNSV;
-          const uint32_t ph = (it / kNSV) & 1;
-          mbar_wait(bars + 8 * kBarPFull, (pv_iter + jj) & 1);
-          mbar_wait(bars + 8 * (kBarVFull + st), ph);
-          tc_fence_after();
-          const uint32_t pa = sbase + kPOff, va = sbase + kVOff + st * kTile;
+        umma_commit(bars + 8 * (kBarSFull + X));
+      };
+      auto pv = [&](int X, int j) {
+        const uint32_t k_it = kv_it + j;
+        const int st = k_it % kNSV;
+        mbar_wait(bars + 8 * (kBarPFull + X), (it[X] + j) & 1);
+        mbar_wait(bars + 8 * (kBarVFull + st), (k_it / kNSV) & 1);
+        tc_fence_after();
+        if (X == 0) ev_stamp(ev, 3, j);
+        const uint32_t va = sbase + kVOff + st * kTile;
 #pragma unroll
-          for (int kk = 0; kk < kBN / 16; ++kk) {
-            const uint32_t poff = (kk >> 2) * kPanel + (kk & 3) * 32;
-            umma_f16(tmem + kTmemO, sw128_desc(pa + poff, 16, 1024), sw128_desc(va + kk * 2048, kPanel, 1024),
-                     kIdescPV, (jj > 0 || kk > 0) ? 1u : 0u);
-          }
-          umma_commit(bars + 8 * (kBarVEmpty + st));
-          umma_commit(bars + 8 * kBarODone);
-        }
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tmem + kTmemO + 128 * X, tmem + kTmemS + 128 * X + kk * 8, sw128_desc(va + kk * 2048, kPanel, 1024),
+                  kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(bars + 8 * (kBarODone + X));
+      };
+      if (t.nk[0] > 0) qk(0, 0);
+      if (t.nk[1] > 0) qk(1, 0);
+      umma_commit(bars + 8 * (kBarKEmpty + kv_it % kNSK));
+      for (int j = 0; j < nk; ++j) {
+        if (j < t.nk[0]) pv(0, j);
+        if (j + 1 < t.nk[0]) qk(0, j + 1);
+        if (j < t.nk[1]) pv(1, j);
+        umma_commit(bars + 8 * (kBarVEmpty + (kv_it + j) % kNSV));
+        if (j + 1 < t.nk[1]) qk(1, j + 1);
+        if (j + 1 < nk) umma_commit(bars + 8 * (kBarKEmpty + (kv_it + j + 1) % kNSK));
       }
     }
-  } else if (warp >= 4) {
-    // ---------------- softmax: this thread owns tile row r (TMEM lane r)
-    const int quarter = warp - 4;
+  } else if (kMath) {
+    // ---------------- softmax of tile X: this thread owns tile row r (TMEM lane r)
+    const int X = warp >> 2;
+    const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const int hh = r / R, i = r - hh * R;
-    const bool valid = i < vrows;
-    const int pos = t.o + t.t0 + (valid ? i : 0);  // last visible key of this row
+    const int vrowsX = X ? t.vrows[1] : t.vrows[0], t0X = X ? t.t0[1] : t.t0[0];
+    const int nkX = X ? t.nk[1] : t.nk[0];
+    const uint32_t itX = X ? it[1] : it[0];
+    const bool valid = i < vrowsX;
+    const int pos = t.o + t0X + (valid ? i : 0);  // last visible key of this row
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+    const uint32_t s_addr = lane_addr + kTmemS + 128 * X, o_addr = lane_addr + kTmemO + 128 * X;
     float m_ref = -INFINITY, l = 0.f;
     const float sl2 = p.scale_log2;
-    for (int j = 0; j < nk; ++j) {
-      const uint32_t si = s_iter + j;
-      const uint32_t sb = si & 1, sph = (si >> 1) & 1;
-      mbar_wait(bars + 8 * (kBarSFull + sb), sph);
+    for (int j = 0; j < nkX; ++j) {
+      mbar_wait(bars + 8 * (kBarSFull + X), (itX + j) & 1);
       tc_fence_after();
-      float s[kBN];
-#pragma unroll
-      for (int c = 0; c < kBN / 32; ++c) {
-        uint32_t raw[32];
-        tmem_ld32(lane_addr + sb * 128 + c * 32, raw);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(raw[e]);
-      }
-      tc_fence_before();
-      mbar_arrive(bars + 8 * (kBarSFree + sb));
+      if (X == 0 && r == 0) ev_stamp(ev, 4, j);
       const int kbase = j * kBN;
-      float mx = -INFINITY;
-      if (kbase + kBN - 1 <= pos) {
+      const bool diag = kbase + kBN - 1 > pos;  // diagonal / tail tile: causal mask on raw scores
+      // exp pass: p = 2^(s*scale*log2e - m_ref) (one FFMA + one MUFU.EX2 each), row max of the
+      // raw scores tracked on the side (scale > 0 commutes with max).  P stays in registers
+      // (bf16x2) until the reference is verified.
+      uint32_t pk[64];
+      float sum0 = 0.f, sum1 = 0.f;
+      auto exp_pass = [&](float ref, float& mxraw) {
+        const float nm = -ref;
+        float m8[8];
 #pragma unroll
-        for (int e = 0; e < kBN; ++e) {
-          s[e] *= sl2;
-          mx = fmaxf(mx, s[e]);
-        }
-      } else {
+        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+        sum0 = sum1 = 0.f;
 #pragma unroll
-        for (int e = 0; e < kBN; ++e) {
-          s[e] = (kbase + e <= pos) ? s[e] * sl2 : -INFINITY;
-          mx = fmaxf(mx, s[e]);
-        }
-      }
-      const float m_new = fmaxf(m_ref, mx);
-      const bool need = m_new > m_ref + 8.0f;  // lazy rescale (p <= 2^8 otherwise)
-      if (j > 0) {
-        mbar_wait(bars + 8 * kBarODone, (pv_iter + j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, need)) {
-          const float alpha = need ? ex2(m_ref - m_new) : 1.f;
-#pragma unroll 1
-          for (int c = 0; c < kD / 32; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(lane_addr + kTmemO + c * 32, ov);
+        for (int q4 = 0; q4 < 4; ++q4) {  // 32 columns per TMEM load keeps register pressure low
+          uint32_t sr[32];
+          tmem_ld32(s_addr + q4 * 32, sr);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-            tmem_st32(lane_addr + kTmemO + c * 32, ov);
+          for (int c = 0; c < 16; ++c) {
+            const int e = q4 * 32 + 2 * c;
+            const float s0 = (diag && kbase + e > pos) ? -INFINITY : __uint_as_float(sr[2 * c]);
+            const float s1 = (diag && kbase + e + 1 > pos) ? -INFINITY : __uint_as_float(sr[2 * c + 1]);
+            m8[(2 * c) & 7] = fmaxf(m8[(2 * c) & 7], s0);
+            m8[(2 * c + 1) & 7] = fmaxf(m8[(2 * c + 1) & 7], s1);
+            const float e0 = ex2(fmaf(s0, sl2, nm)), e1 = ex2(fmaf(s1, sl2, nm));
+            if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
+            pk[q4 * 16 + c] = pack_bf16(e0, e1);
           }
-          tmem_wait_st();
         }
-      }
-      if (need) {
-        l *= ex2(m_ref - m_new);  // 0 on the first tile (m_ref = -inf)
-        m_ref = m_new;
-      }
-      float sum = 0.f;
-      const uint32_t prow = sbase + kPOff + r * 128;
+        mxraw = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      };
+      if (j == 0) {
+        // first key tile: the reference is the tile's own row max (max pass, then exps)
+        float m8[8];
 #pragma unroll
-      for (int c = 0; c < kBN / 8; ++c) {
-        float e0 = ex2(s[c * 8 + 0] - m_ref), e1 = ex2(s[c * 8 + 1] - m_ref);
-        float e2 = ex2(s[c * 8 + 2] - m_ref), e3 = ex2(s[c * 8 + 3] - m_ref);
-        float e4 = ex2(s[c * 8 + 4] - m_ref), e5 = ex2(s[c * 8 + 5] - m_ref);
-        float e6 = ex2(s[c * 8 + 6] - m_ref), e7 = ex2(s[c * 8 + 7] - m_ref);
-        sum += ((e0 + e1) + (e2 + e3)) + ((e4 + e5) + (e6 + e7));
-        st_shared_v4(prow + (c >> 3) * kPanel + (((c & 7) ^ (r & 7)) << 4), pack_bf16(e0, e1), pack_bf16(e2, e3),
-                     pack_bf16(e4, e5), pack_bf16(e6, e7));
+        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          uint32_t sr[32];
+          tmem_ld32(s_addr + q4 * 32, sr);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const float v = (diag && kbase + q4 * 32 + e > pos) ? -INFINITY : __uint_as_float(sr[e]);
+            m8[e & 7] = fmaxf(m8[e & 7], v);
+          }
+        }
+        m_ref = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) *
+                sl2;
       }
-      l += sum;
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(bars + 8 * kBarPFull);
-    }
-    // ---------------- epilogue: O / l -> bf16, LSE
-    mbar_wait(bars + 8 * kBarODone, (pv_iter + nk - 1) & 1);
-    tc_fence_after();
-    const float inv_l = 1.f / l;
-    const int h = t.kvh * g + hh;
-    const int64_t trow = t.row0 + t.t0 + i;
-    uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD) * 2;
+      float mxraw;
+      exp_pass(m_ref, mxraw);
+      if (X == 0 && r == 0) ev_stamp(ev, 5, j);
+      const float m_new = fmaxf(m_ref, mxraw * sl2);
+      const bool need = m_new > m_ref + 8.0f;  // lazy rescale: p <= 2^8 otherwise
+      if (__any_sync(0xffffffffu, need)) {
+        // rare: rescale O_X (PV_X(j-1) completed before QK_X(j) ran; PV_X(j) waits for our P),
+        // then redo the exps against the new reference (S is intact: P is not written yet)
+        const float alpha = need ? ex2(m_ref - m_new) : 1.f;
 #pragma unroll 1
-    for (int c = 0; c < kD / 32; ++c) {
-      uint32_t ov[32];
-      tmem_ld32(lane_addr + kTmemO + c * 32, ov);
-      if (valid) {
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t ov[32];
+          tmem_ld32(o_addr + c * 32, ov);
 #pragma unroll
-        for (int e = 0; e < 32; e += 8) {
-          uint4 w;
-          w.x = pack_bf16(__uint_as_float(ov[e + 0]) * inv_l, __uint_as_float(ov[e + 1]) * inv_l);
-          w.y = pack_bf16(__uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l);
-          w.z = pack_bf16(__uint_as_float(ov[e + 4]) * inv_l, __uint_as_float(ov[e + 5]) * inv_l);
-          w.w = pack_bf16(__uint_as_float(ov[e + 6]) * inv_l, __uint_as_float(ov[e + 7]) * inv_l);
-          *reinterpret_cast<uint4*>(orow + (c * 32 + e) * 2) = w;
+          for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
+          tmem_st32(o_addr + c * 32, ov);
+        }
+        if (need) {
+          l *= alpha;
+          m_ref = m_new;
+        }
+        float unused;
+        exp_pass(m_ref, unused);
+      }
+      if (X == 0 && r == 0) ev_stamp(ev, 7, j);
+      {
+        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
+        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
+        tmem_st32(s_addr, p0);  // P_X(j) as bf16x2 over S_X's first 64 columns
+        tmem_st32(s_addr + 32, p1);
+      }
+      l += sum0 + sum1;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bars + 8 * (kBarPFull + X));
+      if (X == 0 && r == 0) ev_stamp(ev, 6, j);
+    }
+    if (nkX > 0) {
+      // ---------------- epilogue: O / l -> bf16, LSE
+      mbar_wait(bars + 8 * (kBarODone + X), (itX + nkX - 1) & 1);
+      tc_fence_after();
+      const float inv_l = 1.f / l;
+      const int h = t.kvh * g + hh;
+      const int64_t trow = t.row0 + t0X + i;
+      uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD) * 2;
+#pragma unroll 1
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(o_addr + c * 32, ov);
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 w;
+            w.x = pack_bf16(__uint_as_float(ov[e + 0]) * inv_l, __uint_as_float(ov[e + 1]) * inv_l);
+            w.y = pack_bf16(__uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l);
+            w.z = pack_bf16(__uint_as_float(ov[e + 4]) * inv_l, __uint_as_float(ov[e + 5]) * inv_l);
+            w.w = pack_bf16(__uint_as_float(ov[e + 6]) * inv_l, __uint_as_float(ov[e + 7]) * inv_l);
+            *reinterpret_cast<uint4*>(orow + (c * 32 + e) * 2) = w;
+          }
         }
       }
+      if (valid && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
     }
-    if (valid && p.lse != nullptr) p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
   }
-  kv_iter += nk;
-  s_iter += nk;
-  pv_iter += nk;
+  kv_it += nk;
+  it[0] += t.nk[0];
+  it[1] += t.nk[1];
   tc_fence_before();
-  __syncthreads();
+  named_bar_sync(2, kThreads);  // item done: Q/K/V smem and TMEM free for the next item
   tc_fence_after();
 }
 
@@ -382,15 +466,14 @@ struct UnitDesc {
   int id, tbl, ctx, row, kvh, k0, k1, nsplit, ubase, pad;
 };
 
-__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int id) {
-  const int local = id - r.ubase;
-  const int s = local / p.Hkv;
+// Unit = (row, split s, kv head h); d.id = its canonical partial index ubase + s*Hkv + h.
+__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int s, int h) {
   UnitDesc d;
-  d.id = id;
+  d.id = r.ubase + s * p.Hkv + h;
   d.tbl = r.tbl;
   d.ctx = r.ctx;
   d.row = r.row;
-  d.kvh = local - s * p.Hkv;
+  d.kvh = h;
   d.k0 = s * p.split_len;
   d.k1 = min(r.ctx, d.k0 + p.split_len);
   d.nsplit = r.nsplit;
@@ -400,12 +483,11 @@ __device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeR
 }
 
 // Stage s of a unit = 16 tokens of one kv head: K then V (4 KB each at d = 128 bf16).
-__device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, uint32_t stage,
-                                             uint32_t bar) {
+// `phys` is the physical block holding the stage (looked up one stage ahead).
+__device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, int64_t phys,
+                                             uint32_t stage, uint32_t bar) {
   const int tok = u.k0 + 16 * s;
-  const int lb = tok / p.B;
-  const int sub = (tok - lb * p.B) >> 4;
-  const int64_t phys = __ldg(p.tables + u.tbl + lb);
+  const int sub = (tok % p.B) >> 4;
   const int64_t off = (phys * p.Hkv + u.kvh) * p.chunk_bytes + sub * 2048;
   const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
   mbar_expect_tx(bar, fa::kDecStage);
@@ -421,37 +503,47 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
 }
 
 // Load side of a decode warp (lane 0 only).  It walks a continuous stream of
-// 16-token stages across unit boundaries, keeping kDecStages in flight, and
-// prepares the NEXT unit one dependent step per issued stage (queue atomic ->
-// unit's row index -> row record) so the latency of that chain is hidden behind
-// the current unit.  Each new unit's descriptor is published to the compute
-// lanes through a 4-entry per-warp ring in shared memory (+ a counter).
+// 16-token stages across unit boundaries, keeping kDecStages in flight.  Every
+// dependent global load is issued one step before its value is needed: the
+// block-table entry of the NEXT stage is fetched while the current one is issued,
+// and the next unit is prepared one step per issued stage (queue atomic -> its
+// row index -> row record -> descriptor + first block), so lane 0 never waits on
+// memory in the issue path.  Each new unit's descriptor is published to the
+// compute lanes through a 4-entry per-warp ring in shared memory (+ a counter).
 struct DecodeLoader {
   UnitDesc cur;
   int s, nst;
-  int nxt_id, nxt_row, nxt_step;  // 0: nothing, 1: id requested, 2: row loaded, 3: ready
+  int64_t phys;  // block of stage s of cur
+  int nxt_id, nxt_row, nxt_step;  // 0 nothing, 1 id requested, 2 row index, 3 row record, 4 ready
   DecodeRow nxt_r;
+  UnitDesc nxt;
+  int64_t nxt_phys0;
   bool done;
   uint32_t issued;
 
   __device__ __forceinline__ void advance(const AttnParams& p) {
     if (nxt_step == 0) {
       nxt_id = atomicAdd(p.work + 1, 1);
-      nxt_step = 1;
     } else if (nxt_step == 1) {
-      if (nxt_id < p.n_units) nxt_row = __ldg(p.urow + nxt_id);
-      nxt_step = 2;
+      if (nxt_id < p.n_units) nxt_row = __ldg(p.urow + nxt_id / p.Hkv);  // row << 12 | split
     } else if (nxt_step == 2) {
-      if (nxt_id < p.n_units) nxt_r = p.drows[nxt_row];
-      nxt_step = 3;
+      if (nxt_id < p.n_units) nxt_r = p.drows[nxt_row >> 12];
+    } else if (nxt_step == 3) {
+      if (nxt_id < p.n_units) {
+        nxt = make_unit(p, nxt_r, nxt_row & 4095, nxt_id % p.Hkv);
+        nxt_phys0 = __ldg(p.tables + nxt.tbl + nxt.k0 / p.B);
+      }
+    } else {
+      return;
     }
+    ++nxt_step;
   }
   __device__ __forceinline__ void issue_next(const AttnParams& p, uint32_t ring, uint32_t bar0, UnitDesc* descs,
                                              volatile int* n_desc) {
     using namespace fa;
     if (done) return;
     if (s == nst) {
-      while (nxt_step < 3) advance(p);
+      while (nxt_step < 4) advance(p);
       const int k = *n_desc;
       if (nxt_id >= p.n_units) {
         done = true;
@@ -459,7 +551,8 @@ struct DecodeLoader {
         *n_desc = k + 1;
         return;
       }
-      cur = make_unit(p, nxt_r, nxt_id);
+      cur = nxt;
+      phys = nxt_phys0;
       s = 0;
       nst = (cur.k1 - cur.k0 + 15) >> 4;
       nxt_step = 0;
@@ -467,13 +560,20 @@ struct DecodeLoader {
       *n_desc = k + 1;
     }
     const uint32_t slot = issued % kDecStages;
-    decode_issue(p, cur, s, ring + slot * kDecStage, bar0 + 8 * slot);
+    decode_issue(p, cur, s, phys, ring + slot * kDecStage, bar0 + 8 * slot);
     ++s;
     ++issued;
+    if (s < nst) {
+      const int lb_prev = (cur.k0 + 16 * (s - 1)) / p.B, lb = (cur.k0 + 16 * s) / p.B;
+      if (lb != lb_prev) phys = __ldg(p.tables + cur.tbl + lb);  // consumed by the next call
+    }
     advance(p);
   }
 };
 
+// Raw Q fragments of unit u (A operand rows = the g heads of its group; lanes with
+// gid >= g load a valid row and are zeroed by q_mask at use, so no instruction
+// depends on the loads until the fragments are consumed).
 __device__ __forceinline__ void load_q_frags(const AttnParams& p, const UnitDesc& u, int gid, int tig,
                                              uint32_t (&qa0)[8], uint32_t (&qa2)[8]) {
   const int g = p.g;
@@ -481,10 +581,8 @@ __device__ __forceinline__ void load_q_frags(const AttnParams& p, const UnitDesc
                               (static_cast<int64_t>(u.row) * p.Hq + u.kvh * g + (gid < g ? gid : 0)) * fa::kD;
 #pragma unroll
   for (int kk = 0; kk < 8; ++kk) {
-    const uint32_t a = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tig));
-    const uint32_t b = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tig));
-    qa0[kk] = gid < g ? a : 0u;
-    qa2[kk] = gid < g ? b : 0u;
+    qa0[kk] = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 2 * tig));
+    qa2[kk] = __ldg(reinterpret_cast<const uint32_t*>(qrow + kk * 16 + 8 + 2 * tig));
   }
 }
 
@@ -511,6 +609,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   ld.nxt_id = ld.nxt_row = 0;
   ld.done = false;
   ld.issued = 0;
+  ld.phys = ld.nxt_phys0 = 0;
   if (lane == 0) {
     *n_desc = 0;
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
@@ -532,6 +631,10 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       load_q_frags(p, u, gid, tig, qa0, qa2);
     }
     qn_valid = false;
+    if (gid >= g) {
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) qa0[kk] = qa2[kk] = 0u;
+    }
     float o[16][4];
 #pragma unroll
     for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
@@ -628,12 +731,15 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
 }
 
 // a6 — after the grid barrier: merge the partials of every split (row, kv head, q head)
-// item, one warp per item, splits folded in index order (deterministic).  Rows with
-// nsplit > 1 form the prefix [0, n_merge_rows) of the sorted DecodeRow records.
+// item, one warp per item (m = max_s m_s, w_s = e^(m_s - m) l_s,
+// o = sum_s w_s o~_s / sum_s w_s, lse = m + ln sum_s w_s).  Lane s reads split s's
+// (m, l); the o slices are read 16 splits at a time (16 loads in flight per lane) and
+// accumulated in split order, so the result is deterministic.  Rows with nsplit > 1
+// form the prefix [0, n_merge_rows) of the sorted DecodeRow records.
 __device__ __forceinline__ void merge_phase(const AttnParams& p) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int gw = blockIdx.x * fa::kDecWarps + (threadIdx.x >> 5);  // warps 0..kDecWarps-1 of each CTA
+  const int nw = gridDim.x * fa::kDecWarps;
   const int g = p.g;
   const int items = p.n_merge_rows * p.Hkv * g;
   for (int it = gw; it < items; it += nw) {
@@ -641,42 +747,44 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
     const int pair = it / g;
     const int r = pair / p.Hkv, kvh = pair - r * p.Hkv;
     const DecodeRow dr = p.drows[r];
-    float M = -INFINITY, L = 0.f;
+    const int ns = dr.nsplit;
+    auto pidx = [&](int sp) -> int64_t {
+      return static_cast<int64_t>(dr.ubase + sp * p.Hkv + kvh) * g + hh;
+    };
+    float M = -INFINITY;
+    for (int base = 0; base < ns; base += 32)
+      if (base + lane < ns) M = fmaxf(M, __ldcg(p.part_ml + pidx(base + lane) * 2));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    float L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int sp = 0;
-    for (; sp + 4 <= dr.nsplit; sp += 4) {
-      float2 ml[4];
-      float4 v[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int64_t pi = (static_cast<int64_t>(dr.ubase + (sp + k) * p.Hkv + kvh)) * g + hh;
-        ml[k] = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pi * 2));
-        v[k] = __ldcg(reinterpret_cast<const float4*>(p.part_o + pi * fa::kD + lane * 4));
+    for (int base = 0; base < ns; base += 32) {
+      float w = 0.f;
+      if (base + lane < ns) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pidx(base + lane) * 2));
+        w = ex2(ml.x - M) * ml.y;
       }
+      float ws = w;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float Mn = fmaxf(M, ml[k].x);
-        const float a = ex2(M - Mn), w = ex2(ml[k].x - Mn) * ml[k].y;
-        L = L * a + w;
-        acc.x = acc.x * a + w * v[k].x;
-        acc.y = acc.y * a + w * v[k].y;
-        acc.z = acc.z * a + w * v[k].z;
-        acc.w = acc.w * a + w * v[k].w;
-        M = Mn;
+      for (int off = 16; off > 0; off >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, off);
+      L += ws;
+      const int cnt = min(32, ns - base);
+      for (int k0 = 0; k0 < cnt; k0 += 16) {
+        float4 v[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          v[k] = (k0 + k < cnt) ? __ldcg(reinterpret_cast<const float4*>(p.part_o + pidx(base + k0 + k) * fa::kD +
+                                                                         lane * 4))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float wk = __shfl_sync(0xffffffffu, w, k0 + k);
+          acc.x += wk * v[k].x;
+          acc.y += wk * v[k].y;
+          acc.z += wk * v[k].z;
+          acc.w += wk * v[k].w;
+        }
       }
-    }
-    for (; sp < dr.nsplit; ++sp) {
-      const int64_t pi = (static_cast<int64_t>(dr.ubase + sp * p.Hkv + kvh)) * g + hh;
-      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pi * 2));
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.part_o + pi * fa::kD + lane * 4));
-      const float Mn = fmaxf(M, ml.x);
-      const float a = ex2(M - Mn), w = ex2(ml.x - Mn) * ml.y;
-      L = L * a + w;
-      acc.x = acc.x * a + w * v.x;
-      acc.y = acc.y * a + w * v.y;
-      acc.z = acc.z * a + w * v.z;
-      acc.w = acc.w * a + w * v.w;
-      M = Mn;
     }
     const float inv = 1.f / L;
     const int h = kvh * g + hh;
@@ -690,89 +798,107 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
   }
 }
 
-__global__ void __launch_bounds__(256, 1) hybrid_attn_bf16_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const AttnParams p) {
   using namespace fa;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bars = sbase + kDataBytes;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kDataBytes + kNumBars * 8);
-  int* item_slot = reinterpret_cast<int*>(smem + kDataBytes + kNumBars * 8 + 16);
+  uint8_t* misc = smem + kDataBytes + kNumBars * 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(misc);
+  volatile int* item_slot = reinterpret_cast<volatile int*>(misc + 16);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
   if (tid == 0) {
     for (int b = kBarKFull; b < kBarVEmpty + kNSV; ++b) mbar_init(bars + 8 * b, 1);
-    mbar_init(bars + 8 * (kBarSFull + 0), 1);
-    mbar_init(bars + 8 * (kBarSFull + 1), 1);
-    mbar_init(bars + 8 * (kBarSFree + 0), 128);
-    mbar_init(bars + 8 * (kBarSFree + 1), 128);
-    mbar_init(bars + 8 * kBarPFull, 128);
-    mbar_init(bars + 8 * kBarODone, 1);
+    for (int X = 0; X < 2; ++X) {
+      mbar_init(bars + 8 * (kBarSFull + X), 1);
+      mbar_init(bars + 8 * (kBarPFull + X), 128);
+      mbar_init(bars + 8 * (kBarODone + X), 1);
+    }
     for (int b = kBarDec; b < kNumBars; ++b) mbar_init(bars + 8 * b, 1);
     fence_mbar_init();
   }
-  const bool any_tiles = p.n_tiles > 0;
-  if (any_tiles && warp == 1) {
+  const bool any_items = p.n_tiles > 0;
+  if (any_items && warp == kWarpMMA) {
     tmem_alloc(smem_u32(tmem_slot), kTmemCols);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = any_tiles ? *tmem_slot : 0u;
+  const uint32_t tmem = any_items ? *tmem_slot : 0u;
+  uint32_t kv_it = 0, it[2] = {0, 0};
 
+  if (warp >= 8) {
+    // ===== warpgroup 2: producers + MMA issuer (few registers); never rejoins the math path
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
+    while (any_items) {
+      named_bar_sync(3, kThreads);  // item id published by thread 0
+      const int item = *item_slot;
+      named_bar_sync(4, kThreads);  // everyone has read it
+      if (item >= p.n_tiles) break;
+      prefill_pair<false>(p, pair_desc(p, item), sbase, bars, tmem, kv_it, it);
+    }
+    if (any_items && warp == kWarpMMA) {  // all TMEM reads ended before the last item barrier
+      tc_fence_after();
+      tmem_dealloc(tmem, kTmemCols);
+    }
+    return;
+  }
+
+  // ===== warpgroups 0-1: Q load + softmax, then decode and merge (many registers)
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsMath));
   uint64_t t_start = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-  int n_done_tiles = 0;
-  uint32_t kv_iter = 0, s_iter = 0, pv_iter = 0;
-  while (any_tiles) {
+  int n_done_items = 0;
+  while (any_items) {
     if (tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
-    __syncthreads();
+    named_bar_sync(3, kThreads);
     const int item = *item_slot;
-    __syncthreads();
+    named_bar_sync(4, kThreads);
     if (item >= p.n_tiles) break;
-    prefill_tile(p, tile_desc(p, item), smem, sbase, bars, tmem, kv_iter, s_iter, pv_iter);
-    ++n_done_tiles;
+    prefill_pair<true>(p, pair_desc(p, item), sbase, bars, tmem, kv_it, it);
+    ++n_done_items;
   }
   uint64_t t_prefill = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_prefill));
-  // Switch roles: the ring overwrites prefill buffers through the async proxy.
+  // Switch roles: the decode rings overwrite prefill buffers through the async proxy.  All
+  // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
-  __syncthreads();
+  named_bar_sync(5, 256);
   if (p.n_units > 0) {
-    uint8_t* misc = smem + kDataBytes + kNumBars * 8;
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     volatile int* n_desc = reinterpret_cast<volatile int*>(misc + 64 + 16 * warp);
     decode_warp_loop(p, sbase, bars, descs, n_desc);
   }
+  uint64_t t_decode = 0, t_barrier = 0;
   if (p.n_merge_rows > 0) {
     // grid barrier (cooperative launch: every CTA is resident), then the a6 merge phase
-    __syncthreads();
+    named_bar_sync(6, 256);
     if (tid == 0) {
+      if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_decode));
       __threadfence();
       atomicAdd(p.work + 3, 1);
       while (atomicAdd(p.work + 3, 0) < static_cast<int>(gridDim.x)) __nanosleep(100);
       __threadfence();
+      if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_barrier));
     }
-    __syncthreads();
+    named_bar_sync(7, 256);
     merge_phase(p);
   }
-
-  tc_fence_before();
-  __syncthreads();
+  named_bar_sync(8, 256);
   if (p.trace != nullptr && tid == 0) {
     uint64_t t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-    int64_t* tr = p.trace + 4 * blockIdx.x;
+    int64_t* tr = p.trace + 8 * blockIdx.x;
     tr[0] = static_cast<int64_t>(t_start);
     tr[1] = static_cast<int64_t>(t_prefill);
     tr[2] = static_cast<int64_t>(t_end);
-    tr[3] = n_done_tiles;
-  }
-  if (any_tiles && warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tr[3] = n_done_items;
+    tr[4] = static_cast<int64_t>(t_decode);
+    tr[5] = static_cast<int64_t>(t_barrier);
   }
   if (tid == 0) {
     __threadfence();
@@ -801,12 +927,15 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
   // needs every CTA resident (1 CTA/SM, grid <= #SMs).
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(fa::kThreads);
   cfg.dynamicSmemBytes = fa::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.n_merge_rows > 0 ? 1 : 0;
+  // NIYAMA_NO_COOP=1: diagnostic switch to measure the cooperative-launch overhead (the
+  // grid is <= #SMs at 1 CTA/SM, so all CTAs are resident on an otherwise idle GPU).
+  static const bool no_coop = std::getenv("NIYAMA_NO_COOP") != nullptr;
+  attr[0].val.cooperative = (p.n_merge_rows > 0 && !no_coop) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);

@@ -82,8 +82,9 @@ struct niyama_plan {
   std::vector<Prev> prev;  // bookkeeping before this plan (niyama_plan_rollback)
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
-  std::vector<int32_t> urow;  // unit -> sorted decode row
-  int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;
+  std::vector<int32_t> urow;  // queue entry (row, split) -> sorted row << 12 | split
+  int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q-tile pairs)
+  int32_t q_tiles = 0;
   std::vector<RowInfo> rows;
   uint8_t* dbuf = nullptr;
   int32_t* d_slot = nullptr;
@@ -248,13 +249,13 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
 namespace {
 
 // Decode split length (a5): a power of two >= 64 chosen from batch totals only
-// (sum ctx * Hkv against 8 units per resident warp), so split boundaries never
+// (sum ctx * Hkv against 4 units per resident warp), so split boundaries never
 // depend on scheduling and results stay bitwise deterministic.
-int32_t choose_split_len(int64_t sum_ctx, int hkv, int num_sms) {
-  const int64_t target = 8LL * num_sms * 8;
+int32_t choose_split_len(int64_t sum_ctx, int32_t max_ctx, int hkv, int num_sms) {
+  const int64_t target = 4LL * num_sms * 8;
   const int64_t raw = ceil_div(std::max<int64_t>(1, sum_ctx * hkv), target);
   int32_t s = 64;
-  while (s < raw && s < 8192) s *= 2;
+  while ((s < raw || ceil_div(max_ctx, s) > 4095) && s < (1 << 20)) s *= 2;  // split index fits 12 bits
   return s;
 }
 
@@ -409,13 +410,17 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       sl.row0 = row0[i];
       sl.nqt = static_cast<int32_t>(ceil_div(sl.c, pl->R));
       sl.tbase = tbase;
-      tbase += sl.nqt * hkv;
+      tbase += static_cast<int32_t>(ceil_div(sl.nqt, 2)) * hkv;  // work items = pairs of q tiles
+      pl->q_tiles += sl.nqt * hkv;
       pl->slices.push_back(sl);
     }
     pl->n_tiles = tbase;
   }
   // decode rows (a5): split [0, ctx) into split_len pieces; longest rows first
-  pl->split_len = kv->split_override > 0 ? kv->split_override : choose_split_len(pl->sum_ctx, hkv, kv->num_sms);
+  int32_t max_ctx = 0;
+  for (int j = 0; j < D; ++j) max_ctx = std::max(max_ctx, desc->decode_ctx[j]);
+  pl->split_len = choose_split_len(pl->sum_ctx, max_ctx, hkv, kv->num_sms);
+  if (kv->split_override > 0 && ceil_div(max_ctx, kv->split_override) <= 4095) pl->split_len = kv->split_override;
   {
     std::vector<int> order(D);
     for (int j = 0; j < D; ++j) order[j] = j;
@@ -433,9 +438,24 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       r.ubase = ubase;
       ubase += r.nsplit * hkv;
       if (r.nsplit > 1) ++pl->n_merge_rows;
-      for (int32_t u = 0; u < r.nsplit * hkv; ++u) pl->urow.push_back(static_cast<int32_t>(pl->drows.size()));
       pl->drows.push_back(r);
     }
+    // Queue order (LPT): every full-length split of every row first (row-major,
+    // longest rows first), then each row's partial last split, longest first, so
+    // the queue ends with the smallest units.  uinfo[(row,split)] = row << 12 | split;
+    // heads of one (row, split) are consecutive queue entries.
+    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
+      const DecodeRow& dr = pl->drows[r];
+      const int32_t full = dr.ctx / pl->split_len;
+      for (int32_t sp = 0; sp < full; ++sp) pl->urow.push_back((r << 12) | sp);
+    }
+    std::vector<int32_t> tails;
+    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r)
+      if (pl->drows[r].ctx % pl->split_len) tails.push_back(r);
+    std::stable_sort(tails.begin(), tails.end(), [&](int32_t a, int32_t b) {
+      return pl->drows[a].ctx % pl->split_len > pl->drows[b].ctx % pl->split_len;
+    });
+    for (int32_t r : tails) pl->urow.push_back((r << 12) | (pl->drows[r].ctx / pl->split_len));
     pl->n_units = ubase;
   }
   // ---- device copy: one allocation, one H2D
@@ -538,7 +558,7 @@ extern "C" niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_pl
   out->num_rows = plan->T;
   out->num_prefill_rows = plan->prefill_rows;
   out->num_decode = plan->D;
-  out->num_prefill_tiles = plan->n_tiles;
+  out->num_prefill_tiles = plan->q_tiles;
   out->num_decode_units = plan->n_units;
   out->split_len = plan->split_len;
   out->rows_per_tile = plan->R;

@@ -140,7 +140,7 @@ def test_device_calls_refuse_without_gpu():
 
 def test_work_list_sizing():
     """a2: tiles = sum ceil(c/R) * Hkv with R = 128/g; units = sum ceil(ctx/split) * Hkv;
-    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 8 * 148 * 8."""
+    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 4 * 148 * 8."""
     ctx = W.l8b_decode_ctx()
     wl = W.hybrid(W.L8B, "sizing", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
     kv = host_kv(W.L8B, wl.num_blocks)
@@ -149,8 +149,8 @@ def test_work_list_sizing():
     info = p.info()
     assert info.rows_per_tile == 32
     assert info.num_prefill_tiles == (512 // 32) * 8
-    assert info.split_len == 128                      # 133674*8/9472 = 112.9 -> 128
-    assert info.num_decode_units == sum(-(-int(c) // 128) for c in ctx) * 8
+    assert info.split_len == 256                      # 133674*8/4736 = 225.8 -> 256
+    assert info.num_decode_units == sum(-(-int(c) // 256) for c in ctx) * 8
     assert info.sum_ctx == 133674 and info.num_rows == 576
 
 

@@ -36,22 +36,23 @@ def time_it(wl, reps=50, trace=False):
     kv, plan, q, o, lse = setup(wl)
     for _ in range(5):
         kv.attention(plan, 0, q, o, lse)
-    ts = []
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
+    # back-to-back launches (no host sync in between, so host launch latency is hidden)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    evs[0].record()
+    for i in range(reps):
         kv.attention(plan, 0, q, o, lse)
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
+        evs[i + 1].record()
+    torch.cuda.synchronize()
+    ts = [evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(reps)]
     tr = None
     if trace:
-        buf = torch.zeros((148, 4), dtype=torch.int64, device="cuda")
+        buf = torch.zeros((160 * 8 + 10 * 64,), dtype=torch.int64, device="cuda")
         kv.debug_trace(buf)
         kv.attention(plan, 0, q, o, lse)
         torch.cuda.synchronize()
         kv.debug_trace(None)
-        tr = buf.cpu().numpy()
+        tr = buf.cpu().numpy()[:160 * 8].reshape(160, 8)
+        tr = tr[tr[:, 0] > 0]
     d = wl.final.desc
     tok = sum(o_ + c for o_, c in zip(d.prefill_offset, d.prefill_len)) + sum(d.decode_ctx)
     B = tok * wl.shape.num_kv_heads * wl.shape.head_dim * 4

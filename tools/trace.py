@@ -1,0 +1,54 @@
+"""Per-CTA phase timeline + CTA 0 prefill pipeline event log (niyama_debug_trace)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import workloads as W  # noqa: E402
+from kbench import setup  # noqa: E402
+
+ROLES = ["K issue", "V issue", "QK issue", "PV issue", "S ready", "max done", "P written", "rescaled", "half0", "half1"]
+
+
+def run(wl):
+    kv, plan, q, o, lse = setup(wl)
+    for _ in range(3):
+        kv.attention(plan, 0, q, o, lse)
+    buf = torch.zeros(160 * 8 + 10 * 64, dtype=torch.int64, device="cuda")
+    kv.debug_trace(buf)
+    kv.attention(plan, 0, q, o, lse)
+    torch.cuda.synchronize()
+    kv.debug_trace(None)
+    b = buf.cpu().numpy()
+    cta = b[:160 * 8].reshape(160, 8)
+    cta = cta[cta[:, 0] > 0]
+    t0 = cta[:, 0].min()
+    us = lambda x: (x - t0) / 1e3  # noqa: E731
+    print(f"== {wl.name}: {len(cta)} CTAs")
+    pre = cta[cta[:, 3] > 0]
+    if len(pre):
+        print(f"  prefill CTAs {len(pre)}: prefill end {us(pre[:,1].min()):.1f} .. {us(pre[:,1].max()):.1f} us")
+    dec = cta[cta[:, 4] > 0]
+    if len(dec):
+        print(f"  decode end   {us(dec[:,4].min()):.1f} / {us(np.median(dec[:,4])):.1f} / {us(dec[:,4].max()):.1f} us "
+              f"(min/med/max); barrier passed {us(dec[:,5].min()):.1f} .. {us(dec[:,5].max()):.1f}")
+    print(f"  CTA exit     {us(cta[:,2].min()):.1f} / {us(np.median(cta[:,2])):.1f} / {us(cta[:,2].max()):.1f} us")
+    ev = b[160 * 8:].reshape(10, 64)
+    if (ev > 0).any():
+        base = ev[ev > 0].min()
+        n = int((ev[4] > 0).sum())
+        print("  CTA0 prefill tile events (kcycles from first event):")
+        print("   j " + " ".join(f"{r:>9s}" for r in ROLES))
+        for j in range(n):
+            print(f"  {j:2d} " + " ".join(f"{(ev[r, j] - base) / 1e3:9.2f}" if ev[r, j] > 0 else f"{'-':>9s}"
+                                          for r in range(10)))
+
+
+if __name__ == "__main__":
+    run(W.hybrid(W.L8B, "prefill-only-c512-o1536", prefill_offset=1536, chunk=512, decode_ctx=[], seed=2))
+    if len(sys.argv) < 2:
+        run(W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2))
+        run(W.config2_l8b())
