@@ -10,20 +10,25 @@ namespace niyama {
 // KV pool physical layout:
 //   pool[layer][K=0|V=1][block][kv_head][panel][slot][128 B]
 // A (block, kv head) chunk is block_size * head_dim * elt bytes, contiguous.
-// Each token row (head_dim * elt bytes) is cut into 128-byte panels; inside a
+// K: each token row (head_dim * elt bytes) is cut into 128-byte panels; inside a
 // panel the 16-byte chunk c of the row at slot s is stored at chunk position
 // c ^ (s & 7) — the tcgen05 / TMA SWIZZLE_128B pattern.  A bulk copy of any
 // 8-row-aligned run of a panel into 1024-byte aligned shared memory is
-// therefore already a canonical UMMA SW128 operand (K-major for K, MN-major
-// for V) and is bank-conflict free for ldmatrix.
+// therefore already a canonical K-major UMMA SW128 operand for S = Q K^T.
+// V (bf16): stored TRANSPOSED in 16-key sub-blocks: sub-block u of a chunk is
+// V^T [head_dim rows][16 keys] (32 B per row), 16-byte half c of row e at
+// c ^ ((e >> 2) & 1) — the SWIZZLE_32B pattern.  One 4 KB sub-block is a
+// canonical K-major UMMA SW32 operand (N = head_dim, K = 16 keys) for O += P V:
+// K-major operands run at full tensor rate, MN-major ones at half rate.
+// V (f32 path) keeps the row layout of K.
 
 // Compact work list (a2 -> a4/a5).  The kernel expands item indices itself, so
 // the per-iteration H2D stays small (tables + one record per slice / decode).
 //
-// Prefill slice: its work items are [tbase, tbase + ceil(nqt/2)*Hkv); item t is the
-// pair qp = npair-1 - (t-tbase)/Hkv (largest key ranges first) of q tiles 2qp and
-// 2qp+1 of kv head (t-tbase)%Hkv; q tile k covers rows [k*R, min(k*R+R, c)) with
-// R = 128/g chunk rows (128 MMA rows = g query heads x R rows).  (a4)
+// Prefill slice: its work items are [tbase, tbase + nqt*Hkv); item t is q tile
+// qt = nqt-1 - (t-tbase)/Hkv (largest key ranges first) of kv head (t-tbase)%Hkv,
+// rows [qt*R, min(qt*R+R, c)) with R = 128/g chunk rows (128 MMA rows = g query
+// heads x R rows).  (a4)
 struct PrefillSlice {
   int32_t tbl;    // offset of the sequence's block table in the tables array
   int32_t o;      // slice offset (positions of rows are o + i)
@@ -66,12 +71,13 @@ struct AttnParams {
   const RowInfo* rows;
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]
-  int32_t* counters;  // [num_decode * Hkv] merge counters (self-resetting)
+  int32_t* counters;  // [num_decode * Hkv] split-completion counters (reset by the merging warp)
   int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] grid barrier (self-resetting)
   int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
   int32_t T, Hq, Hkv, d, B, g, R;
   int32_t n_tiles, n_units, n_slices, n_drows, split_len;
   int32_t n_merge_rows;  // rows with nsplit > 1 (a prefix of drows)
+  int32_t prefill_ctas;  // CTAs [0, prefill_ctas) serve prefill items first; the rest decode at once
   int64_t* trace;  // optional per-CTA timeline [grid][4] (globaltimer ns), nullptr = off
   float scale_log2;     // softmax scale * log2(e)
 };
@@ -84,12 +90,13 @@ struct AppendParams {
   const int32_t* slot_map;  // [T] block * B + slot
   int64_t chunk_bytes;
   int32_t T, Hkv, row_bytes, B;
+  int32_t v_t;  // 1: V stored transposed in 16-key SW32 sub-blocks (bf16 path)
 };
 
 // Launchers (kernels.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
 cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const int32_t* table, int32_t len,
-                          int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, uint8_t* k_out,
+                          int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, int32_t v_t, uint8_t* k_out,
                           uint8_t* v_out, cudaStream_t s);
 cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s);
 cudaError_t launch_attention_generic_f32(const AttnParams& p, cudaStream_t s);

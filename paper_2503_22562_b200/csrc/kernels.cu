@@ -31,10 +31,18 @@ namespace niyama {
 using namespace ptx;
 
 // ============================================================= append (a3)
+// Byte offset, inside a (block, kv head) chunk, of V element (slot, dim e) in the
+// transposed SW32 sub-block layout (internal.h): sub-block slot/16, row e, key slot%16.
+__device__ __forceinline__ int vt_offset(int slot, int e, int head_dim) {
+  const int k = slot & 15;
+  return (slot >> 4) * (head_dim * 32) + e * 32 + ((((k >> 3) ^ (e >> 2)) & 1) << 4) + ((k & 7) << 1);
+}
+
 // One thread per 16-byte piece of a (row, kv head) vector, 32-bit index math (the
 // launcher guarantees T*Hkv*pieces < 2^31).  Source rows are dense [T][Hkv][row_bytes];
-// piece j of the row at (block, slot) lands in panel j/8 at chunk position
-// (j%8) ^ (slot%8).  K and V move together; all loads are issued before the stores.
+// piece j of the K row at (block, slot) lands in panel j/8 at chunk position
+// (j%8) ^ (slot%8).  V pieces go to the same place (f32) or are scattered element by
+// element into the transposed sub-block (bf16, v_t).
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
   const int pieces = p.row_bytes >> 4;  // 16 at d = 128 bf16
   const int total = p.T * p.Hkv * pieces;
@@ -48,10 +56,19 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
     const int32_t sm = __ldg(p.slot_map + r);
     const int blk = sm / p.B;
     const int slot = sm - blk * p.B;
-    const int64_t dst_off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + (j >> 3) * p.B * 128 +
-                            slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
+    const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
+    const int64_t dst_off = chunk + (j >> 3) * p.B * 128 + slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
     *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
-    *reinterpret_cast<uint4*>(p.pool_v + dst_off) = vv;
+    if (p.v_t) {
+      const int d = p.row_bytes >> 1;
+      const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint16_t*>(p.pool_v + chunk + vt_offset(slot, j * 8 + q, d)) =
+            static_cast<uint16_t>(w[q >> 1] >> ((q & 1) * 16));
+    } else {
+      *reinterpret_cast<uint4*>(p.pool_v + dst_off) = vv;
+    }
   }
 }
 
@@ -68,7 +85,7 @@ cudaError_t launch_append(const AppendParams& p, cudaStream_t s) {
 // ================================================================= gather
 __global__ void kv_gather_kernel(const uint8_t* __restrict__ pool_k, const uint8_t* __restrict__ pool_v,
                                  const int32_t* __restrict__ table, int32_t len, int32_t Hkv, int32_t row_bytes,
-                                 int32_t B, int64_t chunk_bytes, uint8_t* __restrict__ k_out,
+                                 int32_t B, int64_t chunk_bytes, int32_t v_t, uint8_t* __restrict__ k_out,
                                  uint8_t* __restrict__ v_out) {
   const int pieces = row_bytes >> 4;
   const int64_t total = static_cast<int64_t>(len) * Hkv * pieces;
@@ -80,76 +97,81 @@ __global__ void kv_gather_kernel(const uint8_t* __restrict__ pool_k, const uint8
     const int t = static_cast<int>(th / Hkv);
     const int64_t blk = table[t / B];
     const int slot = t % B;
-    const int64_t src = (blk * Hkv + h) * chunk_bytes + static_cast<int64_t>(j >> 3) * B * 128 + slot * 128 +
-                        (((j & 7) ^ (slot & 7)) << 4);
+    const int64_t chunk = (blk * Hkv + h) * chunk_bytes;
+    const int64_t src = chunk + static_cast<int64_t>(j >> 3) * B * 128 + slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
     const int64_t dst = th * row_bytes + (static_cast<int64_t>(j) << 4);
     *reinterpret_cast<uint4*>(k_out + dst) = *reinterpret_cast<const uint4*>(pool_k + src);
-    *reinterpret_cast<uint4*>(v_out + dst) = *reinterpret_cast<const uint4*>(pool_v + src);
+    if (v_t) {
+      const int d = row_bytes >> 1;
+      uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        w[q >> 1] |= static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(pool_v + chunk + vt_offset(slot, j * 8 + q, d)))
+                     << ((q & 1) * 16);
+      *reinterpret_cast<uint4*>(v_out + dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      *reinterpret_cast<uint4*>(v_out + dst) = *reinterpret_cast<const uint4*>(pool_v + src);
+    }
   }
 }
 
 cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const int32_t* table, int32_t len,
-                          int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, uint8_t* k_out,
+                          int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, int32_t v_t, uint8_t* k_out,
                           uint8_t* v_out, cudaStream_t s) {
   const int64_t total = static_cast<int64_t>(len) * Hkv * (row_bytes >> 4);
   if (total == 0) return cudaSuccess;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   kv_gather_kernel<<<static_cast<int>(blocks), 256, 0, s>>>(pool_k, pool_v, table, len, Hkv, row_bytes, B,
-                                                           chunk_bytes, k_out, v_out);
+                                                           chunk_bytes, v_t, k_out, v_out);
   return cudaGetLastError();
 }
 
 // ===================================================== fused bf16 attention
-// CTA = 384 threads (3 warpgroups), 1 CTA/SM, 512 TMEM columns.  Warpgroups 0-1 (softmax,
-// decode, merge) run with 224 registers, warpgroup 2 (bulk-copy producers, MMA issuer) with 56.
-// Shared memory map (bytes from the 1024-aligned base):
-//   [0, 64K)            Q_A, Q_B tiles (2 panels x 128 rows x 128 B each, SW128)
-//   [64K, +3*32K)       K stages (128 keys x 256 B each)
-//   [.., +2*32K)        V stages
-// TMEM: S_A/P_A cols [0,128), S_B/P_B [128,256), O_A [256,384), O_B [384,512).
+// CTA = 256 threads (8 warps), 1 CTA/SM, 512 TMEM columns.
+// Shared memory map (32 KB regions from the 1024-aligned base; the two operands of
+// every MMA sit in different regions, which the tensor core needs for full rate):
+//   [0,32K) Q tile | [32K,96K) K stages x2 | [96K,160K) V^T stages x2 | [160K,224K) P x2
+// Q, K, P: 2 panels x 128 rows x 128 B (SW128, K-major).  V^T stage: 8 sub-blocks of
+// [128 d][16 keys] (SW32, K-major).  TMEM: S0 [0,128), S1 [128,256), O [256,384).
 // The decode role reuses [0, 192K) as 8 warps x 3 stages x 8 KB.
 namespace fa {
-constexpr int kD = 128;            // head dim (bf16 path)
-constexpr int kBN = 128;           // keys per prefill key tile
-constexpr int kNSK = 3;            // K stages (released after both QK^T of a key tile)
-constexpr int kNSV = 2;            // V stages (released after both PV of a key tile)
-constexpr int kPanel = 128 * 128;  // one 64-column panel of a 128-row tile
-constexpr int kTile = 2 * kPanel;  // 128 rows x 256 B
-constexpr int kQOff = 0;           // Q_X at kQOff + X * kTile
-constexpr int kKOff = 2 * kTile;
-constexpr int kVOff = kKOff + kNSK * kTile;
-constexpr int kDataBytes = kVOff + kNSV * kTile;  // 224 KB
-constexpr int kThreads = 384;
-constexpr int kWarpLoad = 8, kWarpMMA = 9;  // warp 8: lane 0 streams K, lane 1 streams V; warp 9 lane 0: MMA
-constexpr int kRegsMath = 216, kRegsCtl = 72;  // setmaxnreg budgets: warpgroups 0-1 / warpgroup 2
-static_assert(2 * kRegsMath + kRegsCtl <= 65536 / kThreads / 8 * 8 * 3, "setmaxnreg budgets exceed the launch allocation");
+constexpr int kD = 128;             // head dim (bf16 path)
+constexpr int kBN = 128;            // keys per prefill key tile
+constexpr int kPanel = 128 * 128;   // one 64-column panel of a 128-row tile
+constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
+constexpr int kQOff = 0;
+constexpr int kKOff = kTile;        // K stage s at kKOff + s * kTile
+constexpr int kVOff = 3 * kTile;    // V^T stage s at kVOff + s * kTile
+constexpr int kPOff = 5 * kTile;    // P buffer b at kPOff + b * kTile
+constexpr int kDataBytes = 7 * kTile;  // 224 KB
+constexpr int kThreads = 256;
 constexpr int kDecWarps = 8;
 constexpr int kDecStages = 3;
-constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V (4 KB)
+constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
 static_assert(kDecWarps * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
-// barrier indices
+// barrier indices (all [2]: double-buffered resources)
 constexpr int kBarKFull = 0;
-constexpr int kBarKEmpty = kBarKFull + kNSK;
-constexpr int kBarVFull = kBarKEmpty + kNSK;
-constexpr int kBarVEmpty = kBarVFull + kNSV;
-constexpr int kBarSFull = kBarVEmpty + kNSV;  // [2] per Q tile: QK^T committed
-constexpr int kBarPFull = kBarSFull + 2;      // [2] per Q tile: P written to TMEM (128 arrivals)
-constexpr int kBarODone = kBarPFull + 2;      // [2] per Q tile: PV committed
-constexpr int kBarDec = kBarODone + 2;        // kDecWarps x kDecStages
+constexpr int kBarKEmpty = 2;
+constexpr int kBarVFull = 4;
+constexpr int kBarVEmpty = 6;
+constexpr int kBarSFull = 8;    // QK^T committed into S[b]
+constexpr int kBarSFree = 10;   // softmax read S[b] (128 arrivals)
+constexpr int kBarPFull = 12;   // softmax wrote P[b] (128 arrivals)
+constexpr int kBarODone = 14;   // PV from P[b] committed (P[b] free, O includes it)
+constexpr int kBarDec = 16;     // kDecWarps x kDecStages
 constexpr int kNumBars = kBarDec + kDecWarps * kDecStages;
 constexpr int kMiscBytes = 64 + kDecWarps * 16;      // tmem slot, item slot, per-warp desc counters
 constexpr int kDescBytes = kDecWarps * 4 * 40;       // per-warp 4-entry UnitDesc rings
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kNumBars * 8 + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemS = 0;    // S_X / P_X at kTmemS + 128 X
-constexpr uint32_t kTmemO = 256;  // O_X at kTmemO + 128 X
+constexpr uint32_t kTmemO = 256;  // O accumulator columns [256, 384); S buffers at 0 and 128
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
-constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 1);
+constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 0);  // both operands K-major
 }  // namespace fa
 
-// -------------------------------------------------------------- prefill pair
+// -------------------------------------------------------------- prefill tile
 // Debug event log (niyama_debug_trace): CTA 0's first item, key tiles < 64, clock64 per role.
 __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
   if (ev != nullptr && j < 64) {
@@ -159,315 +181,259 @@ __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
   }
 }
 
-// A prefill work item = a PAIR of 128-row Q tiles (X = 0: q-tile 2qp, X = 1: q-tile
-// 2qp+1) of one kv head; both stream the same K/V tiles.  Tile X's rows r = hh*R + i
-// hold chunk row t0[X] + i of query head kvh*g + hh (GQA packing, R = 128/g).
-struct PairDesc {
-  int tbl, o, c, row0, kvh, nblk;
-  int t0[2], vrows[2], nk[2];
+struct TileDesc {
+  int tbl, o, c, t0, row0, kvh, nkeys, nblk;
 };
 
-__device__ __forceinline__ PairDesc pair_desc(const AttnParams& p, int item) {
+// Expand work item t (PrefillSlice records; see internal.h): one 128-row q tile.
+__device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
   int i = 0;
-  while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= item) ++i;
+  while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= t) ++i;
   const PrefillSlice sl = p.slices[i];
-  const int local = item - sl.tbase;
-  const int npair = (sl.nqt + 1) >> 1;
-  const int qp = npair - 1 - local / p.Hkv;  // largest key ranges first
-  PairDesc d;
+  const int local = t - sl.tbase;
+  const int qt = sl.nqt - 1 - local / p.Hkv;  // largest key ranges first
+  TileDesc d;
   d.tbl = sl.tbl;
   d.o = sl.o;
   d.c = sl.c;
+  d.t0 = qt * p.R;
   d.row0 = sl.row0;
   d.kvh = local % p.Hkv;
-  int nkeys_max = 0;
-#pragma unroll
-  for (int X = 0; X < 2; ++X) {
-    d.t0[X] = (2 * qp + X) * p.R;
-    d.vrows[X] = max(0, min(p.R, sl.c - d.t0[X]));
-    const int nkeys = d.vrows[X] > 0 ? sl.o + d.t0[X] + d.vrows[X] : 0;
-    d.nk[X] = (nkeys + fa::kBN - 1) / fa::kBN;
-    nkeys_max = max(nkeys_max, nkeys);
-  }
-  d.nblk = (nkeys_max + p.B - 1) / p.B;
+  d.nkeys = sl.o + min(d.t0 + p.R, sl.c);
+  d.nblk = (d.nkeys + p.B - 1) / p.B;
   return d;
 }
 
-__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-
-// Roles: warp 8 lane 0 streams K tiles and lane 1 V tiles (bulk copies of pre-swizzled
-// paged blocks), warp 9 lane 0 issues tcgen05 MMAs, warps 0-3 run the
-// softmax of tile A and warps 4-7 that of tile B (thread = TMEM lane = tile row).
-// MMA order per key tile j:  PV_A(j), QK_A(j+1), PV_B(j), QK_B(j+1) — the tensor pipe
-// executes in issue order, so "S_X(j+1) ready" implies "PV_X(j) done": the softmax of
-// tile X may rescale O_X right after S_X(j+1) lands, and P_X(j) (bf16, written into
-// the first 64 columns of S_X) is consumed by PV_X(j) from TMEM before QK_X(j+1)
-// overwrites S_X.
-__device__ __forceinline__ void named_bar_sync(int id, int count) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
-}
-
-// kMath = true: warpgroups 0-1 (Q load, softmax of tiles A/B); false: warpgroup 2
-// (bulk-copy producers, MMA issuer).  Both instantiations run the same named-barrier
-// sequence, so the two register budgets never share a code path.
-template <bool kMath>
-__device__ __forceinline__ void prefill_pair(const AttnParams& p, const PairDesc& t, uint32_t sbase, uint32_t bars,
-                                             uint32_t tmem, uint32_t& kv_it, uint32_t (&it)[2]) {
+// Roles inside the 256-thread CTA: warp 0 lane 0 streams K tiles, warp 2 lane 0 V^T
+// tiles (bulk copies of pre-swizzled paged blocks), warp 1 lane 0 issues tcgen05 MMAs,
+// warps 4-7 run the softmax (thread = TMEM lane = tile row r = hh*R + i, GQA packing).
+// Pipeline per key tile j (global iteration g = it + j; buffers g % 2):
+//   MMA:     QK_{j+1} -> S[(g+1)%2] (once the softmax read S_{j-1}),  PV_j from P[g%2]
+//   softmax: S_g -> max -> exps (P in registers) -> [rare: wait PV_{j-1}, rescale O in
+//            TMEM] -> [wait PV_{j-2} done: P[g%2] free] -> P -> smem -> arrive
+__device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc& t, uint32_t sbase, uint32_t bars,
+                                             uint32_t tmem, uint32_t& kv_it, uint32_t& it) {
   using namespace fa;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
   const int g = p.g, R = p.R;
-  const int nk = max(t.nk[0], t.nk[1]);
-  int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && kv_it == 0) ? p.trace + 8 * 160 : nullptr;  // [10 roles][64]
+  const int vrows = min(R, t.c - t.t0);
+  const int nk = (t.nkeys + kBN - 1) / kBN;
+  int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && it == 0) ? p.trace + 8 * 160 : nullptr;  // [10][64]
 
-  // ---- Q tiles: tile X row r = hh*R + i  <-  q[row0 + t0[X] + i][kvh*g + hh][:]
-  if constexpr (kMath) {
+  // ---- Q tile: rows r = hh*R + i  <-  q[row0 + t0 + i][kvh*g + hh][:]
+  {
     const uint8_t* q = static_cast<const uint8_t*>(p.q);
-    for (int idx = tid; idx < 2 * 128 * 16; idx += 256) {
-      const int X = idx >> 11, r = (idx >> 4) & 127, j = idx & 15;
+    for (int idx = tid; idx < 128 * 16; idx += kThreads) {
+      const int r = idx >> 4, j = idx & 15;
       const int hh = r / R, i = r - hh * R;
-      const int vrowsX = X ? t.vrows[1] : t.vrows[0], t0X = X ? t.t0[1] : t.t0[0];
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < vrowsX) {
-        const int64_t row = t.row0 + t0X + i;
+      if (i < vrows) {
+        const int64_t row = t.row0 + t.t0 + i;
         v = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
       }
-      st_shared_v4(sbase + kQOff + X * kTile + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), v.x, v.y,
-                   v.z, v.w);
+      st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
     }
     fence_proxy_async_smem();
+    __syncthreads();
   }
-  named_bar_sync(1, kThreads);  // Q tiles in smem
 
-  if (!kMath && warp == kWarpLoad) {
-    if (lane < 2) {
-      // ---------------- producers (two lanes, independent thread scheduling): 128-key K / V tiles
-      const bool isK = lane == 0;
-      const int ns = isK ? kNSK : kNSV;
+  if (warp == 0 || warp == 2) {
+    if (lane == 0) {
+      // ---------------- producers: 128-key K tiles (warp 0), V^T tiles (warp 2)
+      const bool isK = warp == 0;
       const uint8_t* pool = isK ? p.pool_k : p.pool_v;
       const uint32_t ring = sbase + (isK ? kKOff : kVOff);
       const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
-      const int bpt = kBN / p.B;  // blocks per key tile
       const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
       for (int j = 0; j < nk; ++j) {
         const uint32_t k_it = kv_it + j;
-        const int st = k_it % ns;
-        const uint32_t ph = (k_it / ns) & 1;
-        mbar_wait(bars + 8 * (bar_empty + st), ph ^ 1);
+        const int st = k_it & 1;
+        mbar_wait(bars + 8 * (bar_empty + st), ((k_it >> 1) & 1) ^ 1);
         ev_stamp(ev, isK ? 0 : 1, j);
         const uint32_t full = bars + 8 * (bar_full + st);
+        const uint32_t dst0 = ring + st * kTile;
         mbar_expect_tx(full, kTile);
-        for (int b = 0; b < bpt; ++b) {
-          int lb = j * bpt + b;
-          if (lb >= t.nblk) lb = t.nblk - 1;  // finite data; masked out (P = 0)
-          const int64_t phys = __ldg(p.tables + t.tbl + lb);
-          const int64_t off = (phys * p.Hkv + t.kvh) * p.chunk_bytes;
-          for (int pn = 0; pn < 2; ++pn)
-            bulk_g2s(ring + st * kTile + pn * kPanel + b * seg, pool + off + pn * seg, seg, full);
+        if (isK) {
+          const int bpt = kBN / p.B;  // blocks per key tile
+          for (int b = 0; b < bpt; ++b) {
+            int lb = j * bpt + b;
+            if (lb >= t.nblk) lb = t.nblk - 1;  // finite data; masked out (P = 0)
+            const int64_t off = (__ldg(p.tables + t.tbl + lb) * p.Hkv + t.kvh) * p.chunk_bytes;
+            for (int pn = 0; pn < 2; ++pn) bulk_g2s(dst0 + pn * kPanel + b * seg, pool + off + pn * seg, seg, full);
+          }
+        } else {
+          for (int u = 0; u < kBN / 16; ++u) {  // one 4 KB V^T sub-block per 16 keys
+            const int key = j * kBN + 16 * u;
+            const int lb = min(key / p.B, t.nblk - 1);
+            const int64_t off = (__ldg(p.tables + t.tbl + lb) * p.Hkv + t.kvh) * p.chunk_bytes +
+                                static_cast<int64_t>((key % p.B) >> 4) * 4096;
+            bulk_g2s(dst0 + u * 4096, pool + off, 4096, full);
+          }
         }
       }
     }
-  } else if (!kMath && warp == kWarpMMA) {
+  } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- tcgen05 issuer
-      auto qk = [&](int X, int j) {
-        const uint32_t k_it = kv_it + j;
-        const int st = k_it % kNSK;
-        mbar_wait(bars + 8 * (kBarKFull + st), (k_it / kNSK) & 1);
+      // ---------------- tcgen05 issuer (single thread, in order)
+      auto qk = [&](int j) {
+        const uint32_t k_it = kv_it + j, gj = it + j;
+        const int st = k_it & 1, sb = gj & 1;
+        if (gj >= 2) mbar_wait(bars + 8 * (kBarSFree + sb), ((gj >> 1) & 1) ^ 1);
+        mbar_wait(bars + 8 * (kBarKFull + st), (k_it >> 1) & 1);
         tc_fence_after();
-        if (X == 0) ev_stamp(ev, 2, j);
-        const uint32_t qa = sbase + kQOff + X * kTile, ka = sbase + kKOff + st * kTile;
+        ev_stamp(ev, 2, j);
+        const uint32_t qa = sbase + kQOff, ka = sbase + kKOff + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t koff = (kk >> 2) * kPanel + (kk & 3) * 32;
-          umma_f16(tmem + kTmemS + 128 * X, sw128_desc(qa + koff, 16, 1024), sw128_desc(ka + koff, 16, 1024),
-                   kIdescQK, kk > 0);
+          umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), sw128_desc(ka + koff, 16, 1024), kIdescQK,
+                   kk > 0);
         }
-        umma_commit(bars + 8 * (kBarSFull + X));
+        umma_commit(bars + 8 * (kBarSFull + sb));
+        umma_commit(bars + 8 * (kBarKEmpty + st));
       };
-      auto pv = [&](int X, int j) {
-        const uint32_t k_it = kv_it + j;
-        const int st = k_it % kNSV;
-        mbar_wait(bars + 8 * (kBarPFull + X), (it[X] + j) & 1);
-        mbar_wait(bars + 8 * (kBarVFull + st), (k_it / kNSV) & 1);
-        tc_fence_after();
-        if (X == 0) ev_stamp(ev, 3, j);
-        const uint32_t va = sbase + kVOff + st * kTile;
-#pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk)
-          umma_ts(tmem + kTmemO + 128 * X, tmem + kTmemS + 128 * X + kk * 8, sw128_desc(va + kk * 2048, kPanel, 1024),
-                  kIdescPV, (j > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(bars + 8 * (kBarODone + X));
-      };
-      if (t.nk[0] > 0) qk(0, 0);
-      if (t.nk[1] > 0) qk(1, 0);
-      umma_commit(bars + 8 * (kBarKEmpty + kv_it % kNSK));
+      qk(0);
       for (int j = 0; j < nk; ++j) {
-        if (j < t.nk[0]) pv(0, j);
-        if (j + 1 < t.nk[0]) qk(0, j + 1);
-        if (j < t.nk[1]) pv(1, j);
-        umma_commit(bars + 8 * (kBarVEmpty + (kv_it + j) % kNSV));
-        if (j + 1 < t.nk[1]) qk(1, j + 1);
-        if (j + 1 < nk) umma_commit(bars + 8 * (kBarKEmpty + (kv_it + j + 1) % kNSK));
+        if (j + 1 < nk) qk(j + 1);
+        const uint32_t k_it = kv_it + j, gj = it + j;
+        const int st = k_it & 1, pb = gj & 1;
+        mbar_wait(bars + 8 * (kBarPFull + pb), (gj >> 1) & 1);
+        mbar_wait(bars + 8 * (kBarVFull + st), (k_it >> 1) & 1);
+        tc_fence_after();
+        ev_stamp(ev, 3, j);
+        const uint32_t pa = sbase + kPOff + pb * kTile, va = sbase + kVOff + st * kTile;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk) {
+          const uint32_t poff = (kk >> 2) * kPanel + (kk & 3) * 32;
+          umma_f16(tmem + kTmemO, sw128_desc(pa + poff, 16, 1024), sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
+                   (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(bars + 8 * (kBarODone + pb));
+        umma_commit(bars + 8 * (kBarVEmpty + st));
       }
     }
-  } else if (kMath) {
-    // ---------------- softmax of tile X: this thread owns tile row r (TMEM lane r)
-    const int X = warp >> 2;
-    const int quarter = warp & 3;
+  } else if (warp >= 4) {
+    // ---------------- softmax: this thread owns tile row r (TMEM lane r)
+    const int quarter = warp - 4;
     const int r = quarter * 32 + lane;
     const int hh = r / R, i = r - hh * R;
-    const int vrowsX = X ? t.vrows[1] : t.vrows[0], t0X = X ? t.t0[1] : t.t0[0];
-    const int nkX = X ? t.nk[1] : t.nk[0];
-    const uint32_t itX = X ? it[1] : it[0];
-    const bool valid = i < vrowsX;
-    const int pos = t.o + t0X + (valid ? i : 0);  // last visible key of this row
+    const bool valid = i < vrows;
+    const int pos = t.o + t.t0 + (valid ? i : 0);  // last visible key of this row
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    const uint32_t s_addr = lane_addr + kTmemS + 128 * X, o_addr = lane_addr + kTmemO + 128 * X;
     float m_ref = -INFINITY, l = 0.f;
     const float sl2 = p.scale_log2;
-    for (int j = 0; j < nkX; ++j) {
-      mbar_wait(bars + 8 * (kBarSFull + X), (itX + j) & 1);
+    for (int j = 0; j < nk; ++j) {
+      const uint32_t gj = it + j;
+      const int sb = gj & 1;
+      mbar_wait(bars + 8 * (kBarSFull + sb), (gj >> 1) & 1);
       tc_fence_after();
-      if (X == 0 && r == 0) ev_stamp(ev, 4, j);
+      if (r == 0) ev_stamp(ev, 4, j);
+      uint32_t sr[kBN];
+      tmem_ld128(lane_addr + sb * 128, sr);
+      tc_fence_before();
+      mbar_arrive(bars + 8 * (kBarSFree + sb));  // S[sb] may be overwritten by QK_{j+2}
+      float s[kBN];
+#pragma unroll
+      for (int e = 0; e < kBN; ++e) s[e] = __uint_as_float(sr[e]);
       const int kbase = j * kBN;
-      const bool diag = kbase + kBN - 1 > pos;  // diagonal / tail tile: causal mask on raw scores
-      // exp pass: p = 2^(s*scale*log2e - m_ref) (one FFMA + one MUFU.EX2 each), row max of the
-      // raw scores tracked on the side (scale > 0 commutes with max).  P stays in registers
-      // (bf16x2) until the reference is verified.
-      uint32_t pk[64];
-      float sum0 = 0.f, sum1 = 0.f;
-      auto exp_pass = [&](float ref, float& mxraw) {
-        const float nm = -ref;
-        float m8[8];
+      if (kbase + kBN - 1 > pos) {  // diagonal / tail tile: causal mask on raw scores
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
-        sum0 = sum1 = 0.f;
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {  // 32 columns per TMEM load keeps register pressure low
-          uint32_t sr[32];
-          tmem_ld32(s_addr + q4 * 32, sr);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) {
-            const int e = q4 * 32 + 2 * c;
-            const float s0 = (diag && kbase + e > pos) ? -INFINITY : __uint_as_float(sr[2 * c]);
-            const float s1 = (diag && kbase + e + 1 > pos) ? -INFINITY : __uint_as_float(sr[2 * c + 1]);
-            m8[(2 * c) & 7] = fmaxf(m8[(2 * c) & 7], s0);
-            m8[(2 * c + 1) & 7] = fmaxf(m8[(2 * c + 1) & 7], s1);
-            const float e0 = ex2(fmaf(s0, sl2, nm)), e1 = ex2(fmaf(s1, sl2, nm));
-            if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
-            pk[q4 * 16 + c] = pack_bf16(e0, e1);
-          }
-        }
-        mxraw = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      };
-      if (j == 0) {
-        // first key tile: the reference is the tile's own row max (max pass, then exps)
-        float m8[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = -INFINITY;
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          uint32_t sr[32];
-          tmem_ld32(s_addr + q4 * 32, sr);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float v = (diag && kbase + q4 * 32 + e > pos) ? -INFINITY : __uint_as_float(sr[e]);
-            m8[e & 7] = fmaxf(m8[e & 7], v);
-          }
-        }
-        m_ref = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))) *
-                sl2;
+        for (int e = 0; e < kBN; ++e)
+          if (kbase + e > pos) s[e] = -INFINITY;
       }
-      float mxraw;
-      exp_pass(m_ref, mxraw);
-      if (X == 0 && r == 0) ev_stamp(ev, 5, j);
-      const float m_new = fmaxf(m_ref, mxraw * sl2);
+      float m8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m8[k] = s[k];
+#pragma unroll
+      for (int e = 8; e < kBN; ++e) m8[e & 7] = fmaxf(m8[e & 7], s[e]);
+      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      const float m_new = fmaxf(m_ref, mx * sl2);
       const bool need = m_new > m_ref + 8.0f;  // lazy rescale: p <= 2^8 otherwise
-      if (__any_sync(0xffffffffu, need)) {
-        // rare: rescale O_X (PV_X(j-1) completed before QK_X(j) ran; PV_X(j) waits for our P),
-        // then redo the exps against the new reference (S is intact: P is not written yet)
-        const float alpha = need ? ex2(m_ref - m_new) : 1.f;
+      const float alpha = need ? ex2(m_ref - m_new) : 1.f;  // 0 on the first tile (m_ref = -inf)
+      if (need) {
+        l *= alpha;
+        m_ref = m_new;
+      }
+      if (r == 0) ev_stamp(ev, 5, j);
+      const float nm = -m_ref;
+      uint32_t pk[kBN / 2];
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll
+      for (int c = 0; c < kBN / 2; ++c) {  // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each
+        const float e0 = ex2(fmaf(s[2 * c], sl2, nm)), e1 = ex2(fmaf(s[2 * c + 1], sl2, nm));
+        if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
+        pk[c] = pack_bf16(e0, e1);
+      }
+      l += sum0 + sum1;
+      if (r == 0) ev_stamp(ev, 8, j);
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // rare: rescale O after PV_{j-1} (PV_j waits for our P)
+        mbar_wait(bars + 8 * (kBarODone + ((gj - 1) & 1)), ((gj - 1) >> 1) & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < kD / 32; ++c) {
           uint32_t ov[32];
-          tmem_ld32(o_addr + c * 32, ov);
+          tmem_ld32(lane_addr + kTmemO + c * 32, ov);
 #pragma unroll
           for (int e = 0; e < 32; ++e) ov[e] = __float_as_uint(__uint_as_float(ov[e]) * alpha);
-          tmem_st32(o_addr + c * 32, ov);
+          tmem_st32(lane_addr + kTmemO + c * 32, ov);
         }
-        if (need) {
-          l *= alpha;
-          m_ref = m_new;
-        }
-        float unused;
-        exp_pass(m_ref, unused);
+        tmem_wait_st();
       }
-      if (X == 0 && r == 0) ev_stamp(ev, 7, j);
-      {
-        uint32_t (&p0)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[0]);
-        uint32_t (&p1)[32] = *reinterpret_cast<uint32_t(*)[32]>(&pk[32]);
-        tmem_st32(s_addr, p0);  // P_X(j) as bf16x2 over S_X's first 64 columns
-        tmem_st32(s_addr + 32, p1);
-      }
-      l += sum0 + sum1;
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(bars + 8 * (kBarPFull + X));
-      if (X == 0 && r == 0) ev_stamp(ev, 6, j);
-    }
-    if (nkX > 0) {
-      // ---------------- epilogue: O / l -> bf16, LSE
-      mbar_wait(bars + 8 * (kBarODone + X), (itX + nkX - 1) & 1);
-      tc_fence_after();
-      const float inv_l = 1.f / l;
-      const int h = t.kvh * g + hh;
-      const int64_t trow = t.row0 + t0X + i;
-      uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD) * 2;
-#pragma unroll 1
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t ov[32];
-        tmem_ld32(o_addr + c * 32, ov);
-        if (valid) {
+      if (j >= 2) mbar_wait(bars + 8 * (kBarODone + sb), ((gj - 2) >> 1) & 1);  // PV_{j-2} released P[sb]
+      if (r == 0) ev_stamp(ev, 7, j);
+      const uint32_t prow = sbase + kPOff + sb * kTile + r * 128;
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 w;
-            w.x = pack_bf16(__uint_as_float(ov[e + 0]) * inv_l, __uint_as_float(ov[e + 1]) * inv_l);
-            w.y = pack_bf16(__uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l);
-            w.z = pack_bf16(__uint_as_float(ov[e + 4]) * inv_l, __uint_as_float(ov[e + 5]) * inv_l);
-            w.w = pack_bf16(__uint_as_float(ov[e + 6]) * inv_l, __uint_as_float(ov[e + 7]) * inv_l);
-            *reinterpret_cast<uint4*>(orow + (c * 32 + e) * 2) = w;
-          }
+      for (int c = 0; c < kBN / 8; ++c)
+        st_shared_v4(prow + (c >> 3) * kPanel + (((c & 7) ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                     pk[4 * c + 3]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(bars + 8 * (kBarPFull + sb));
+      if (r == 0) ev_stamp(ev, 6, j);
+    }
+    // ---------------- epilogue: O / l -> bf16, LSE
+    mbar_wait(bars + 8 * (kBarODone + ((it + nk - 1) & 1)), ((it + nk - 1) >> 1) & 1);
+    tc_fence_after();
+    const float inv_l = 1.f / l;
+    const int h = t.kvh * g + hh;
+    const int64_t trow = t.row0 + t.t0 + i;
+    uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD) * 2;
+#pragma unroll 1
+    for (int c = 0; c < kD / 32; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(lane_addr + kTmemO + c * 32, ov);
+      if (valid) {
+#pragma unroll
+        for (int e = 0; e < 32; e += 8) {
+          uint4 w;
+          w.x = pack_bf16(__uint_as_float(ov[e + 0]) * inv_l, __uint_as_float(ov[e + 1]) * inv_l);
+          w.y = pack_bf16(__uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l);
+          w.z = pack_bf16(__uint_as_float(ov[e + 4]) * inv_l, __uint_as_float(ov[e + 5]) * inv_l);
+          w.w = pack_bf16(__uint_as_float(ov[e + 6]) * inv_l, __uint_as_float(ov[e + 7]) * inv_l);
+          *reinterpret_cast<uint4*>(orow + (c * 32 + e) * 2) = w;
         }
       }
-      if (valid && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
     }
+    if (valid && p.lse != nullptr)
+      p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
   }
   kv_it += nk;
-  it[0] += t.nk[0];
-  it[1] += t.nk[1];
+  it += nk;
   tc_fence_before();
-  named_bar_sync(2, kThreads);  // item done: Q/K/V smem and TMEM free for the next item
+  __syncthreads();
   tc_fence_after();
 }
 
 // --------------------------------------------------------------- decode unit
 struct UnitDesc {
-  int id, tbl, ctx, row, kvh, k0, k1, nsplit, ubase, pad;
+  int id, tbl, ctx, row, kvh, k0, k1, nsplit, ubase, pair;  // pair = sorted row * Hkv + kvh (merge counter)
 };
 
 // Unit = (row, split s, kv head h); d.id = its canonical partial index ubase + s*Hkv + h.
-__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int s, int h) {
+__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int ridx, int s, int h) {
   UnitDesc d;
   d.id = r.ubase + s * p.Hkv + h;
   d.tbl = r.tbl;
@@ -478,7 +444,7 @@ __device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeR
   d.k1 = min(r.ctx, d.k0 + p.split_len);
   d.nsplit = r.nsplit;
   d.ubase = r.ubase;
-  d.pad = 0;
+  d.pair = ridx * p.Hkv + h;
   return d;
 }
 
@@ -487,19 +453,17 @@ __device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeR
 __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, int64_t phys,
                                              uint32_t stage, uint32_t bar) {
   const int tok = u.k0 + 16 * s;
-  const int sub = (tok % p.B) >> 4;
-  const int64_t off = (phys * p.Hkv + u.kvh) * p.chunk_bytes + sub * 2048;
+  const int sub = (tok % p.B) >> 4;  // 16-token sub-block of the block
+  const int64_t chunk = (phys * p.Hkv + u.kvh) * p.chunk_bytes;
   const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
   mbar_expect_tx(bar, fa::kDecStage);
-  if (seg == 2048) {  // B = 16: the (block, head) chunk is one contiguous 4 KB run per K / V
-    bulk_g2s(stage, p.pool_k + off, 4096, bar);
-    bulk_g2s(stage + 4096, p.pool_v + off, 4096, bar);
-  } else {
-    bulk_g2s(stage, p.pool_k + off, 2048, bar);
-    bulk_g2s(stage + 2048, p.pool_k + off + seg, 2048, bar);
-    bulk_g2s(stage + 4096, p.pool_v + off, 2048, bar);
-    bulk_g2s(stage + 6144, p.pool_v + off + seg, 2048, bar);
+  if (seg == 2048) {  // B = 16: the K chunk is one contiguous 4 KB run
+    bulk_g2s(stage, p.pool_k + chunk, 4096, bar);
+  } else {            // 16 rows of each of the two 128-byte K panels
+    bulk_g2s(stage, p.pool_k + chunk + sub * 2048, 2048, bar);
+    bulk_g2s(stage + 2048, p.pool_k + chunk + seg + sub * 2048, 2048, bar);
   }
+  bulk_g2s(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar);  // V^T sub-block [128 d][16 keys]
 }
 
 // Load side of a decode warp (lane 0 only).  It walks a continuous stream of
@@ -530,7 +494,7 @@ struct DecodeLoader {
       if (nxt_id < p.n_units) nxt_r = p.drows[nxt_row >> 12];
     } else if (nxt_step == 3) {
       if (nxt_id < p.n_units) {
-        nxt = make_unit(p, nxt_r, nxt_row & 4095, nxt_id % p.Hkv);
+        nxt = make_unit(p, nxt_r, nxt_row >> 12, nxt_row & 4095, nxt_id % p.Hkv);
         nxt_phys0 = __ldg(p.tables + nxt.tbl + nxt.k0 / p.B);
       }
     } else {
@@ -601,7 +565,6 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   const float sl2 = p.scale_log2;
   const int mi = lane >> 3, rr = lane & 7;
   const int ktok = (mi >> 1) * 8 + rr;  // K (non-trans): matrices (tok 0-7,c),(0-7,c+1),(8-15,c),(8-15,c+1)
-  const int vtok = (mi & 1) * 8 + rr;   // V (trans):     matrices (tok 0-7,d),(8-15,d),(0-7,d+8),(8-15,d+8)
 
   DecodeLoader ld;
   ld.s = ld.nst = 0;
@@ -681,13 +644,13 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       const float p0 = ex2(x0 - m), p1 = ex2(x1 - m), p2 = ex2(x2 - m), p3 = ex2(x3 - m);
       l += (p0 + p1) + (p2 + p3);
       const uint32_t pa0 = pack_bf16(p0, p1), pa2 = pack_bf16(p2, p3);
-      // O += P V  (16 tokens x 128 dims = 16 n-tiles)
+      // O += P V  (16 tokens x 128 dims = 16 n-tiles); V^T sub-block rows = dims (SW32)
 #pragma unroll
       for (int n2 = 0; n2 < 8; ++n2) {
-        const int dchunk = 2 * n2 + (mi >> 1);
-        const uint32_t addr = stg + 4096 + (dchunk >> 3) * 2048 + vtok * 128 + (((dchunk & 7) ^ (vtok & 7)) << 4);
+        const int dr = 16 * n2 + (mi >> 1) * 8 + rr;
+        const uint32_t addr = stg + 4096 + dr * 32 + ((((mi & 1) ^ (dr >> 2)) & 1) << 4);
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(addr, b0, b1, b2, b3);
+        ldsm_x4(addr, b0, b1, b2, b3);
         mma_bf16_16816(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
         mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
       }
@@ -811,17 +774,13 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   const int warp = tid >> 5;
 
   if (tid == 0) {
-    for (int b = kBarKFull; b < kBarVEmpty + kNSV; ++b) mbar_init(bars + 8 * b, 1);
-    for (int X = 0; X < 2; ++X) {
-      mbar_init(bars + 8 * (kBarSFull + X), 1);
-      mbar_init(bars + 8 * (kBarPFull + X), 128);
-      mbar_init(bars + 8 * (kBarODone + X), 1);
-    }
+    for (int b = 0; b < kBarDec; ++b)
+      mbar_init(bars + 8 * b, (b == kBarSFree || b == kBarSFree + 1 || b == kBarPFull || b == kBarPFull + 1) ? 128 : 1);
     for (int b = kBarDec; b < kNumBars; ++b) mbar_init(bars + 8 * b, 1);
     fence_mbar_init();
   }
-  const bool any_items = p.n_tiles > 0;
-  if (any_items && warp == kWarpMMA) {
+  const bool any_items = p.n_tiles > 0 && static_cast<int>(blockIdx.x) < p.prefill_ctas;
+  if (any_items && warp == 1) {
     tmem_alloc(smem_u32(tmem_slot), kTmemCols);
     tmem_relinquish();
   }
@@ -829,37 +788,18 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = any_items ? *tmem_slot : 0u;
-  uint32_t kv_it = 0, it[2] = {0, 0};
 
-  if (warp >= 8) {
-    // ===== warpgroup 2: producers + MMA issuer (few registers); never rejoins the math path
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsCtl));
-    while (any_items) {
-      named_bar_sync(3, kThreads);  // item id published by thread 0
-      const int item = *item_slot;
-      named_bar_sync(4, kThreads);  // everyone has read it
-      if (item >= p.n_tiles) break;
-      prefill_pair<false>(p, pair_desc(p, item), sbase, bars, tmem, kv_it, it);
-    }
-    if (any_items && warp == kWarpMMA) {  // all TMEM reads ended before the last item barrier
-      tc_fence_after();
-      tmem_dealloc(tmem, kTmemCols);
-    }
-    return;
-  }
-
-  // ===== warpgroups 0-1: Q load + softmax, then decode and merge (many registers)
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsMath));
   uint64_t t_start = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   int n_done_items = 0;
+  uint32_t kv_it = 0, it = 0;
   while (any_items) {
     if (tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
-    named_bar_sync(3, kThreads);
+    __syncthreads();
     const int item = *item_slot;
-    named_bar_sync(4, kThreads);
+    __syncthreads();
     if (item >= p.n_tiles) break;
-    prefill_pair<true>(p, pair_desc(p, item), sbase, bars, tmem, kv_it, it);
+    prefill_tile(p, tile_desc(p, item), sbase, bars, tmem, kv_it, it);
     ++n_done_items;
   }
   uint64_t t_prefill = 0;
@@ -867,7 +807,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // Switch roles: the decode rings overwrite prefill buffers through the async proxy.  All
   // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
-  named_bar_sync(5, 256);
+  __syncthreads();
   if (p.n_units > 0) {
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     volatile int* n_desc = reinterpret_cast<volatile int*>(misc + 64 + 16 * warp);
@@ -876,7 +816,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   uint64_t t_decode = 0, t_barrier = 0;
   if (p.n_merge_rows > 0) {
     // grid barrier (cooperative launch: every CTA is resident), then the a6 merge phase
-    named_bar_sync(6, 256);
+    __syncthreads();
     if (tid == 0) {
       if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_decode));
       __threadfence();
@@ -885,10 +825,11 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
       __threadfence();
       if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_barrier));
     }
-    named_bar_sync(7, 256);
+    __syncthreads();
     merge_phase(p);
   }
-  named_bar_sync(8, 256);
+  tc_fence_before();
+  __syncthreads();
   if (p.trace != nullptr && tid == 0) {
     uint64_t t_end;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -899,6 +840,10 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     tr[3] = n_done_items;
     tr[4] = static_cast<int64_t>(t_decode);
     tr[5] = static_cast<int64_t>(t_barrier);
+  }
+  if (any_items && warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
   }
   if (tid == 0) {
     __threadfence();
@@ -932,10 +877,7 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  // NIYAMA_NO_COOP=1: diagnostic switch to measure the cooperative-launch overhead (the
-  // grid is <= #SMs at 1 CTA/SM, so all CTAs are resident on an otherwise idle GPU).
-  static const bool no_coop = std::getenv("NIYAMA_NO_COOP") != nullptr;
-  attr[0].val.cooperative = (p.n_merge_rows > 0 && !no_coop) ? 1 : 0;
+  attr[0].val.cooperative = p.n_merge_rows > 0 ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);

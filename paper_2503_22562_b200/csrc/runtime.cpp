@@ -69,6 +69,7 @@ struct niyama_kv {
   bool staging_pending = false;
   int64_t* trace = nullptr;  // niyama_debug_trace
   int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
+  int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
 };
 
 struct niyama_plan {
@@ -83,7 +84,7 @@ struct niyama_plan {
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
   std::vector<int32_t> urow;  // queue entry (row, split) -> sorted row << 12 | split
-  int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q-tile pairs)
+  int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
   std::vector<RowInfo> rows;
   uint8_t* dbuf = nullptr;
@@ -140,6 +141,7 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->chunk_bytes = static_cast<int64_t>(c.block_size) * kv->row_bytes;
   kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
+  if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
   if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
     const int v = std::atoi(sl);
     if (v >= 16 && v % 16 == 0) kv->split_override = v;
@@ -239,7 +241,8 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
   NY_CUDA(cudaMemcpyAsync(d_tbl, tbl.data(), tbl.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   const uint8_t* pk = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
   NY_CUDA(launch_gather(pk, pk + kv->half_bytes, d_tbl, len, kv->hkv, kv->row_bytes, kv->B, kv->chunk_bytes,
-                        static_cast<uint8_t*>(k_out), static_cast<uint8_t*>(v_out), s));
+                        kv->cfg.dtype == NIYAMA_BF16 ? 1 : 0, static_cast<uint8_t*>(k_out), static_cast<uint8_t*>(v_out),
+                        s));
   NY_CUDA(cudaFreeAsync(d_tbl, s));
   NY_CUDA(cudaStreamSynchronize(s));  // the host table must outlive the pageable copy
   return NIYAMA_OK;
@@ -410,7 +413,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       sl.row0 = row0[i];
       sl.nqt = static_cast<int32_t>(ceil_div(sl.c, pl->R));
       sl.tbase = tbase;
-      tbase += static_cast<int32_t>(ceil_div(sl.nqt, 2)) * hkv;  // work items = pairs of q tiles
+      tbase += sl.nqt * hkv;  // work items = 128-row q tiles
       pl->q_tiles += sl.nqt * hkv;
       pl->slices.push_back(sl);
     }
@@ -608,6 +611,7 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
   p.Hkv = kv->hkv;
   p.row_bytes = kv->row_bytes;
   p.B = kv->B;
+  p.v_t = kv->cfg.dtype == NIYAMA_BF16 ? 1 : 0;
   NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
   return NIYAMA_OK;
 }
@@ -659,6 +663,12 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
       return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
     const int64_t want = static_cast<int64_t>(p.n_tiles) + ceil_div(p.n_units, 8);
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kv->num_sms, want)));
+    // Prefill tiles are tensor/MUFU-bound and decode streaming is HBM-bound: confining
+    // the tiles to about half the SMs (each CTA then runs ~2 tiles) lets the other half
+    // stream decode KV from the start (measured on config 2: 132 -> 123 us).
+    const int cap = kv->prefill_cap > 0 ? kv->prefill_cap
+                                        : std::max(1, std::min<int>(grid / 2, static_cast<int>(ceil_div(p.n_tiles, 2))));
+    p.prefill_ctas = std::min(cap, grid);
     NY_CUDA(launch_attention_bf16(p, grid, s));
   } else {
     if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
