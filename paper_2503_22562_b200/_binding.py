@@ -344,6 +344,18 @@ class Predictor:
 Batch = _Desc  # a batch descriptor marshalled once and reusable across calls
 
 
+class DecodeQoS:
+    """Python-side record of one running decode's QoS state (fields of `niyama_decode_qos`, include/niyama.h)."""
+
+    __slots__ = ("interactive", "t_arrival", "slo_ttft", "slo_tbt", "slo_ttlt", "next_token", "est_remaining")
+
+    def __init__(self, interactive, t_arrival, slo_ttft=0.0, slo_tbt=0.0, slo_ttlt=0.0, next_token=1,
+                 est_remaining=1):
+        self.interactive, self.t_arrival = bool(interactive), float(t_arrival)
+        self.slo_ttft, self.slo_tbt, self.slo_ttlt = float(slo_ttft), float(slo_tbt), float(slo_ttlt)
+        self.next_token, self.est_remaining = int(next_token), int(est_remaining)
+
+
 class QoSArray:
     """niyama_decode_qos[] marshalled once (for per-iteration min_slack calls)."""
 

@@ -91,6 +91,12 @@ struct AppendParams {
   int64_t chunk_bytes;
   int32_t T, Hkv, row_bytes, B;
   int32_t v_t;  // 1: V stored transposed in 16-key SW32 sub-blocks (bf16 path)
+  // v_t only: V^T writes are grouped — vgrp[k] = first batch row of 8 consecutive rows
+  // whose positions form one 8-aligned half of a 16-key sub-block (written as one 16-byte
+  // V^T row segment per dim); velem[k] = every other row (element-wise 2-byte writes).
+  const int32_t* vgrp;
+  const int32_t* velem;
+  int32_t n_grp, n_elem;
 };
 
 // Launchers (kernels.cu).  Return cudaSuccess or the launch error.

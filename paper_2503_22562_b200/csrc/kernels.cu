@@ -45,35 +45,68 @@ __device__ __forceinline__ int vt_offset(int slot, int e, int head_dim) {
 // element into the transposed sub-block (bf16, v_t).
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
   const int pieces = p.row_bytes >> 4;  // 16 at d = 128 bf16
-  const int total = p.T * p.Hkv * pieces;
+  const int nk = p.T * p.Hkv * pieces;  // K pieces (and V pieces when !v_t)
+  const int d = p.row_bytes >> 1;       // head_dim (bf16)
+  const int ng = p.v_t ? p.n_grp * p.Hkv * d : 0;
+  const int ne = p.v_t ? p.n_elem * p.Hkv * pieces : 0;
+  const int total = nk + ng + ne;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
-    const int j = idx % pieces;
-    const int rh = idx / pieces;
-    const int h = rh % p.Hkv;
-    const int r = rh / p.Hkv;
-    const uint4 kv = __ldg(reinterpret_cast<const uint4*>(p.k_new) + idx);
-    const uint4 vv = __ldg(reinterpret_cast<const uint4*>(p.v_new) + idx);
-    const int32_t sm = __ldg(p.slot_map + r);
-    const int blk = sm / p.B;
-    const int slot = sm - blk * p.B;
-    const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
-    const int64_t dst_off = chunk + (j >> 3) * p.B * 128 + slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
-    *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
-    if (p.v_t) {
-      const int d = p.row_bytes >> 1;
+    if (idx < nk) {  // K row pieces (and V when stored row-major)
+      const int j = idx % pieces;
+      const int rh = idx / pieces;
+      const int h = rh % p.Hkv;
+      const int r = rh / p.Hkv;
+      const uint4 kv = __ldg(reinterpret_cast<const uint4*>(p.k_new) + idx);
+      const int32_t sm = __ldg(p.slot_map + r);
+      const int blk = sm / p.B;
+      const int slot = sm - blk * p.B;
+      const int64_t dst_off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + (j >> 3) * p.B * 128 +
+                              slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
+      *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
+      if (!p.v_t) *reinterpret_cast<uint4*>(p.pool_v + dst_off) = __ldg(reinterpret_cast<const uint4*>(p.v_new) + idx);
+    } else if (idx < nk + ng) {  // V^T: 8 tokens x one dim -> one 16-byte segment of row e
+      const int k = idx - nk;
+      const int e = k % d;
+      const int gh = k / d;
+      const int h = gh % p.Hkv;
+      const int r0 = __ldg(p.vgrp + gh / p.Hkv);
+      const uint16_t* src = reinterpret_cast<const uint16_t*>(p.v_new) + (static_cast<int64_t>(r0) * p.Hkv + h) * d + e;
+      uint32_t w[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w[q] = static_cast<uint32_t>(__ldg(src + static_cast<int64_t>(2 * q) * p.Hkv * d)) |
+               (static_cast<uint32_t>(__ldg(src + static_cast<int64_t>(2 * q + 1) * p.Hkv * d)) << 16);
+      const int32_t sm = __ldg(p.slot_map + r0);
+      const int blk = sm / p.B;
+      const int slot = sm - blk * p.B;  // 8-aligned
+      const int64_t off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + vt_offset(slot, e, d);
+      *reinterpret_cast<uint4*>(p.pool_v + off) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {  // V^T element-wise: row r, dims 8j..8j+7
+      const int k = idx - nk - ng;
+      const int j = k % pieces;
+      const int rh = k / pieces;
+      const int h = rh % p.Hkv;
+      const int r = __ldg(p.velem + rh / p.Hkv);
+      const uint4 vv = __ldg(reinterpret_cast<const uint4*>(p.v_new) + (static_cast<int64_t>(r) * p.Hkv + h) * pieces + j);
+      const int32_t sm = __ldg(p.slot_map + r);
+      const int blk = sm / p.B;
+      const int slot = sm - blk * p.B;
+      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
       const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         *reinterpret_cast<uint16_t*>(p.pool_v + chunk + vt_offset(slot, j * 8 + q, d)) =
             static_cast<uint16_t>(w[q >> 1] >> ((q & 1) * 16));
-    } else {
-      *reinterpret_cast<uint4*>(p.pool_v + dst_off) = vv;
     }
   }
 }
 
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s) {
-  const int64_t total = static_cast<int64_t>(p.T) * p.Hkv * (p.row_bytes >> 4);
+  const int64_t pieces = p.row_bytes >> 4;
+  const int64_t total = static_cast<int64_t>(p.T) * p.Hkv * pieces +
+                        (p.v_t ? static_cast<int64_t>(p.n_grp) * p.Hkv * (p.row_bytes >> 1) +
+                                     static_cast<int64_t>(p.n_elem) * p.Hkv * pieces
+                               : 0);
   if (total == 0) return cudaSuccess;
   if (total >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
   int64_t blocks = (total + 255) / 256;

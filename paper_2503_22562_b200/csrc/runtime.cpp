@@ -63,10 +63,21 @@ struct niyama_kv {
   std::set<int32_t> free_;
   std::unordered_map<int64_t, Seq> seqs;
   ncclComm_t comm = nullptr;
-  void* staging = nullptr;
-  size_t staging_cap = 0;
-  cudaEvent_t staging_ev = nullptr;
-  bool staging_pending = false;
+  // Plan metadata goes host -> device through a ring of pinned staging buffers;
+  // a buffer is reused only after its previous H2D completed (its event), so the
+  // host can plan up to kStaging steps ahead of the device.
+  static constexpr int kStaging = 8;
+  struct Staging {
+    void* h = nullptr;
+    size_t cap = 0;
+    cudaEvent_t ev = nullptr;
+    bool pending = false;
+  } stg[kStaging];
+  int stg_next = 0;
+  // Plan device buffers come from a library-owned stream-ordered pool that never
+  // returns memory to the OS (release threshold = max): the per-step
+  // allocate/free is then a pointer bump, never a page map.
+  cudaMemPool_t mempool = nullptr;
   int64_t* trace = nullptr;  // niyama_debug_trace
   int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
   int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
@@ -84,6 +95,7 @@ struct niyama_plan {
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
   std::vector<int32_t> urow;  // queue entry (row, split) -> sorted row << 12 | split
+  std::vector<int32_t> vgrp, velem;  // V^T append groups / element rows
   int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
   std::vector<RowInfo> rows;
@@ -94,6 +106,8 @@ struct niyama_plan {
   DecodeRow* d_drows = nullptr;
   RowInfo* d_rows = nullptr;
   int32_t* d_urow = nullptr;
+  int32_t* d_vgrp = nullptr;
+  int32_t* d_velem = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   int32_t* d_counters = nullptr;
@@ -153,8 +167,22 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
     const size_t bytes = static_cast<size_t>(kv->half_bytes) * 2 * c.num_layers;
     if (e == cudaSuccess) e = cudaMalloc(&kv->pool, bytes);
     if (e == cudaSuccess) e = cudaMemset(kv->pool, 0, bytes);  // stale slots stay finite (masked, P = 0)
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->staging_ev, cudaEventDisableTiming);
+    for (int i = 0; i < niyama_kv::kStaging && e == cudaSuccess; ++i)
+      e = cudaEventCreateWithFlags(&kv->stg[i].ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = c.device;
+      e = cudaMemPoolCreate(&kv->mempool, &props);
+      uint64_t keep = ~uint64_t(0);
+      if (e == cudaSuccess) e = cudaMemPoolSetAttribute(kv->mempool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     if (e != cudaSuccess) {
+      for (auto& st : kv->stg)
+        if (st.ev) cudaEventDestroy(st.ev);
+      if (kv->mempool) cudaMemPoolDestroy(kv->mempool);
       if (kv->pool) cudaFree(kv->pool);
       delete kv;
       return fail(NIYAMA_ECUDA, std::string("kv_create: ") + cudaGetErrorString(e));
@@ -171,8 +199,11 @@ extern "C" void niyama_kv_destroy(niyama_kv* kv) {
     cudaDeviceSynchronize();
     if (kv->comm) ncclCommDestroy(kv->comm);
     if (kv->pool) cudaFree(kv->pool);
-    if (kv->staging) cudaFreeHost(kv->staging);
-    if (kv->staging_ev) cudaEventDestroy(kv->staging_ev);
+    for (auto& st : kv->stg) {
+      if (st.h) cudaFreeHost(st.h);
+      if (st.ev) cudaEventDestroy(st.ev);
+    }
+    if (kv->mempool) cudaMemPoolDestroy(kv->mempool);
   }
   delete kv;
 }
@@ -273,13 +304,13 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   if (P > 0 && (!desc->prefill_seq || !desc->prefill_offset || !desc->prefill_len))
     return fail(NIYAMA_EINVAL, "prefill arrays are NULL");
   if (D > 0 && (!desc->decode_seq || !desc->decode_ctx)) return fail(NIYAMA_EINVAL, "decode arrays are NULL");
-  std::unordered_set<int64_t> seen;
-  for (int i = 0; i < P; ++i)
-    if (!seen.insert(desc->prefill_seq[i]).second)
-      return fail(NIYAMA_EINVAL, "seq " + std::to_string(desc->prefill_seq[i]) + " appears twice in one batch");
-  for (int j = 0; j < D; ++j)
-    if (!seen.insert(desc->decode_seq[j]).second)
-      return fail(NIYAMA_EINVAL, "seq " + std::to_string(desc->decode_seq[j]) + " appears twice in one batch");
+  {
+    std::vector<int64_t> ids(desc->prefill_seq, desc->prefill_seq + (P > 0 ? P : 0));
+    if (D > 0) ids.insert(ids.end(), desc->decode_seq, desc->decode_seq + D);
+    std::sort(ids.begin(), ids.end());
+    const auto dup = std::adjacent_find(ids.begin(), ids.end());
+    if (dup != ids.end()) return fail(NIYAMA_EINVAL, "seq " + std::to_string(*dup) + " appears twice in one batch");
+  }
   // ---- validate (no side effects)
   std::vector<std::pair<int64_t, int32_t>> new_len;
   new_len.reserve(P + D);
@@ -320,10 +351,14 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   if (need_total > static_cast<int64_t>(kv->free_.size()))
     return fail(NIYAMA_ENOBLOCKS, "need " + std::to_string(need_total) + " blocks, " +
                                       std::to_string(kv->free_.size()) + " free");
-  // staging buffer of the previous plan must be free before we reuse it
-  if (kv->has_device && kv->staging_pending) {
-    NY_CUDA(cudaEventSynchronize(kv->staging_ev));
-    kv->staging_pending = false;
+  // the staging buffer this plan will use must have finished its previous H2D
+  niyama_kv::Staging* stg = nullptr;
+  if (kv->has_device) {
+    stg = &kv->stg[kv->stg_next];
+    if (stg->pending) {
+      NY_CUDA(cudaEventSynchronize(stg->ev));
+      stg->pending = false;
+    }
   }
   // ---- commit: smallest free ids, descriptor order (R9); remember how to undo it
   struct Undo { int64_t seq; bool existed; size_t nblocks; int32_t len; };
@@ -364,8 +399,17 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   pl->D = D;
   const int B = kv->B, g = kv->g, hkv = kv->hkv;
   std::vector<int32_t> tbl_off(P + D);
+  std::vector<Seq*> seq_of(P + D);
+  {
+    size_t nb = 0;
+    for (int k = 0; k < P + D; ++k) {
+      seq_of[k] = &kv->seqs[new_len[k].first];
+      nb += seq_of[k]->blocks.size();
+    }
+    pl->tables.reserve(nb + 1);
+  }
   for (int k = 0; k < P + D; ++k) {
-    const Seq& q = kv->seqs[new_len[k].first];
+    const Seq& q = *seq_of[k];
     tbl_off[k] = static_cast<int32_t>(pl->tables.size());
     pl->tables.insert(pl->tables.end(), q.blocks.begin(), q.blocks.end());
   }
@@ -375,7 +419,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   std::vector<int32_t> row0(P);
   int32_t row = 0;
   for (int i = 0; i < P; ++i) {
-    const Seq& q = kv->seqs[desc->prefill_seq[i]];
+    const Seq& q = *seq_of[i];
     row0[i] = row;
     const int32_t o = desc->prefill_offset[i];
     for (int32_t k = 0; k < desc->prefill_len[i]; ++k, ++row) {
@@ -385,8 +429,24 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     }
   }
   pl->prefill_rows = row;
+  // V^T append groups (see AppendParams): 8-aligned runs of 8 positions inside a slice
+  for (int i = 0; i < P; ++i) {
+    const int32_t o = desc->prefill_offset[i], c = desc->prefill_len[i];
+    int32_t k = 0;
+    while (k < c) {
+      const int32_t pos = o + k;
+      if ((pos & 7) == 0 && k + 8 <= c) {
+        pl->vgrp.push_back(row0[i] + k);
+        k += 8;
+      } else {
+        pl->velem.push_back(row0[i] + k);
+        k += 1;
+      }
+    }
+  }
+  for (int j = 0; j < D; ++j) pl->velem.push_back(row + j);
   for (int j = 0; j < D; ++j, ++row) {
-    const Seq& q = kv->seqs[desc->decode_seq[j]];
+    const Seq& q = *seq_of[P + j];
     const int32_t pos = desc->decode_ctx[j] - 1;
     pl->slot_map.push_back(q.blocks[pos / B] * B + pos % B);
     pl->rows.push_back(RowInfo{tbl_off[P + j], pos + 1});
@@ -427,11 +487,13 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   {
     std::vector<int> order(D);
     for (int j = 0; j < D; ++j) order[j] = j;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
-      return desc->decode_ctx[a] != desc->decode_ctx[b] ? desc->decode_ctx[a] > desc->decode_ctx[b]
-                                                         : tier_of(P + a) < tier_of(P + b);
+    std::sort(order.begin(), order.end(), [&](int a, int b) {  // ties: tier, then descriptor order
+      if (desc->decode_ctx[a] != desc->decode_ctx[b]) return desc->decode_ctx[a] > desc->decode_ctx[b];
+      if (tier_of(P + a) != tier_of(P + b)) return tier_of(P + a) < tier_of(P + b);
+      return a < b;
     });
     int32_t ubase = 0;
+    pl->drows.reserve(D);
     for (int j : order) {
       DecodeRow r{};
       r.tbl = tbl_off[P + j];
@@ -447,6 +509,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     // longest rows first), then each row's partial last split, longest first, so
     // the queue ends with the smallest units.  uinfo[(row,split)] = row << 12 | split;
     // heads of one (row, split) are consecutive queue entries.
+    pl->urow.reserve(static_cast<size_t>(ubase / std::max(hkv, 1)) + 1);
     for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
       const DecodeRow& dr = pl->drows[r];
       const int32_t full = dr.ctx / pl->split_len;
@@ -455,8 +518,9 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     std::vector<int32_t> tails;
     for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r)
       if (pl->drows[r].ctx % pl->split_len) tails.push_back(r);
-    std::stable_sort(tails.begin(), tails.end(), [&](int32_t a, int32_t b) {
-      return pl->drows[a].ctx % pl->split_len > pl->drows[b].ctx % pl->split_len;
+    std::sort(tails.begin(), tails.end(), [&](int32_t a, int32_t b) {
+      const int32_t ra = pl->drows[a].ctx % pl->split_len, rb = pl->drows[b].ctx % pl->split_len;
+      return ra != rb ? ra > rb : a < b;
     });
     for (int32_t r : tails) pl->urow.push_back((r << 12) | (pl->drows[r].ctx / pl->split_len));
     pl->n_units = ubase;
@@ -476,47 +540,54 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_units = take(pl->drows.size() * sizeof(DecodeRow));
     const size_t o_rows = take(pl->rows.size() * sizeof(RowInfo));
     const size_t o_urow = take(pl->urow.size() * 4);
+    const size_t o_vgrp = take(pl->vgrp.size() * 4);
+    const size_t o_velem = take(pl->velem.size() * 4);
+    const size_t o_cnt = take(static_cast<size_t>(D) * hkv * 4);  // zero-initialised through the H2D
+    const size_t o_work = take(16);
     const size_t meta_bytes = off;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
-    const size_t o_cnt = take(static_cast<size_t>(D) * hkv * 4);
-    const size_t o_work = take(16);
     const size_t total = off;
     cudaStream_t s = pl->stream;
     cudaError_t e = cudaSetDevice(kv->cfg.device);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&pl->dbuf), total, s);
-    if (e == cudaSuccess && kv->staging_cap < meta_bytes) {
-      if (kv->staging) cudaFreeHost(kv->staging);
-      kv->staging = nullptr;
-      kv->staging_cap = 0;
-      e = cudaMallocHost(&kv->staging, std::max<size_t>(meta_bytes, 1 << 20));
-      if (e == cudaSuccess) kv->staging_cap = std::max<size_t>(meta_bytes, 1 << 20);
+    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pl->dbuf), total, kv->mempool, s);
+    if (e == cudaSuccess && stg->cap < meta_bytes) {
+      if (stg->h) cudaFreeHost(stg->h);
+      stg->h = nullptr;
+      stg->cap = 0;
+      e = cudaMallocHost(&stg->h, std::max<size_t>(meta_bytes, 1 << 20));
+      if (e == cudaSuccess) stg->cap = std::max<size_t>(meta_bytes, 1 << 20);
     }
     if (e == cudaSuccess) {
-      uint8_t* h = static_cast<uint8_t*>(kv->staging);
+      uint8_t* h = static_cast<uint8_t*>(stg->h);
       std::memcpy(h + o_slot, pl->slot_map.data(), pl->slot_map.size() * 4);
       std::memcpy(h + o_tbl, pl->tables.data(), pl->tables.size() * 4);
       std::memcpy(h + o_tiles, pl->slices.data(), pl->slices.size() * sizeof(PrefillSlice));
       std::memcpy(h + o_units, pl->drows.data(), pl->drows.size() * sizeof(DecodeRow));
       std::memcpy(h + o_rows, pl->rows.data(), pl->rows.size() * sizeof(RowInfo));
       std::memcpy(h + o_urow, pl->urow.data(), pl->urow.size() * 4);
+      std::memcpy(h + o_vgrp, pl->vgrp.data(), pl->vgrp.size() * 4);
+      std::memcpy(h + o_velem, pl->velem.data(), pl->velem.size() * 4);
+      std::memset(h + o_cnt, 0, meta_bytes - o_cnt);
       e = cudaMemcpyAsync(pl->dbuf, h, meta_bytes, cudaMemcpyHostToDevice, s);
     }
-    if (e == cudaSuccess) e = cudaMemsetAsync(pl->dbuf + o_cnt, 0, total - o_cnt, s);
-    if (e == cudaSuccess) e = cudaEventRecord(kv->staging_ev, s);
+    if (e == cudaSuccess) e = cudaEventRecord(stg->ev, s);
     if (e != cudaSuccess) {
       rollback();  // the error leaves the pool as it was
       if (pl->dbuf) cudaFreeAsync(pl->dbuf, s);
       delete pl;
       return fail(NIYAMA_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
     }
-    kv->staging_pending = true;
+    stg->pending = true;
+    kv->stg_next = (kv->stg_next + 1) % niyama_kv::kStaging;
     pl->d_slot = reinterpret_cast<int32_t*>(pl->dbuf + o_slot);
     pl->d_tables = reinterpret_cast<int32_t*>(pl->dbuf + o_tbl);
     pl->d_slices = reinterpret_cast<PrefillSlice*>(pl->dbuf + o_tiles);
     pl->d_drows = reinterpret_cast<DecodeRow*>(pl->dbuf + o_units);
     pl->d_rows = reinterpret_cast<RowInfo*>(pl->dbuf + o_rows);
     pl->d_urow = reinterpret_cast<int32_t*>(pl->dbuf + o_urow);
+    pl->d_vgrp = reinterpret_cast<int32_t*>(pl->dbuf + o_vgrp);
+    pl->d_velem = reinterpret_cast<int32_t*>(pl->dbuf + o_velem);
     pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
     pl->d_part_ml = reinterpret_cast<float*>(pl->dbuf + o_part_ml);
     pl->d_counters = reinterpret_cast<int32_t*>(pl->dbuf + o_cnt);
@@ -612,6 +683,10 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
   p.row_bytes = kv->row_bytes;
   p.B = kv->B;
   p.v_t = kv->cfg.dtype == NIYAMA_BF16 ? 1 : 0;
+  p.vgrp = plan->d_vgrp;
+  p.velem = plan->d_velem;
+  p.n_grp = static_cast<int32_t>(plan->vgrp.size());
+  p.n_elem = static_cast<int32_t>(plan->velem.size());
   NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
   return NIYAMA_OK;
 }
