@@ -282,10 +282,11 @@ def main():
     # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
     fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
     cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
-    theta = [4e-6, 0.0, 0.0, 0.0, 0.0, 1.2]
+    theta = [3.1e-5, 5e-9, 0.0, 0.0, 1.07, 0.16, 1.3e-6, 70e9, 7.2e12]   # config-3 fit (profiles/r01)
     if os.path.exists(fit_path):
         fj = json.load(open(fit_path))
-        theta = fj.get("theta", theta) if fj.get("world", 1) == world and fj.get("config") == args.config else theta
+        ok = fj.get("world", 1) == world and fj.get("config") == args.config and len(fj.get("theta", [])) == 9
+        theta = fj["theta"] if ok else theta
     pred = ny.Predictor.from_params(cfg, theta)
     # a1 inputs: decodes carry Table 3 tiers; interactive ones are mid-stream
     DecodeQoS = ny.DecodeQoS

@@ -160,7 +160,8 @@ typedef struct {
   int32_t num_decode_units;   /* (decode row, kv head, key split) items */
   int32_t split_len;          /* decode split length in tokens (batch-level choice) */
   int32_t rows_per_tile;      /* 128 / (Hq/Hkv) chunk rows per prefill tile */
-  int32_t reserved;
+  int32_t prefill_ctas;       /* bf16 launch: CTAs that take prefill tiles before decode units
+                                 (work-proportional split); 0 if no tiles */
   int64_t sum_ctx;            /* sum of decode ctx */
 } niyama_plan_info;
 niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_plan_info* out);
@@ -207,38 +208,69 @@ niyama_status niyama_get_unique_id(void* out128); /* ncclGetUniqueId, for rank 0
 niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, void* o_full, float* lse_full,
                                      niyama_stream stream);
 
-/* a8 — iteration-time predictor (P:205 ④; R16).  Features of a batch
- * on this rank's shape: phi = [1, c, D, B_KV, F, max(F/F_PEAK, B_KV/B_PEAK)]
- * with c = prefill rows, D = decodes, B_KV = [sum(o+c) + sum ctx]*Hkv*d*2*elt
- * bytes, F = 4*d*Hq*[sum(c*o + c(c+1)/2) + sum ctx] flops, F_PEAK/B_PEAK the
- * nominal B200 peaks below.  t_hat = theta . phi, theta >= 0 fitted by
- * non-negative least squares on relative residuals of measured samples. */
-#define NIYAMA_F_PEAK_BF16 2.25e15
-#define NIYAMA_F_PEAK_F32 1.125e15
-#define NIYAMA_B_PEAK 8.0e12
+/* a8 — iteration-time predictor (P:205 ④ "A lightweight predictor is then used
+ * to estimate the latency of the batch"; reading R16).  The paper's
+ * predictor is a random forest on profiles; this one is a SCHEDULE MODEL of the
+ * fused launch, evaluated on this rank's shape:
+ *
+ *  1. Prefill tile queue: slices (o, c > 0) sorted by o + c descending (stable);
+ *     per slice the q tiles from last to first (qt = nqt-1 .. 0, nqt =
+ *     ceil(c / R), R = 128 / (Hq/Hkv)), each repeated Hkv times, with cost
+ *     ceil((o + min(c, (qt+1) R)) / 128) + NIYAMA_TILE_SETUP_STEPS steps.
+ *  2. Decode units: split_len from (sum ctx, max ctx) exactly as the planner
+ *     (a power of two >= 64 with about 4 units per resident warp on
+ *     NIYAMA_PRED_SMS SMs), units = sum_j ceil(ctx_j / split_len) * Hkv.
+ *  3. grid and prefill CTAs n_p by the planner's CTA split (niyama_plan_info).
+ *  4. List scheduling: each tile in queue order goes to the prefill CTA that
+ *     frees first; f_1 <= ... <= f_np are the CTAs' finish times in steps.
+ *  5. Fluid decode: B_d = sum ctx * Hkv * d * 2 * elt bytes stream at
+ *     min(BW, k(t) * r_cta), k(t) = grid - (prefill CTAs still busy at t); a
+ *     step lasts tau seconds.  T_p = tau * f_np, T_d = time B_d is done.
+ *  6. phi = [1, c + D, D, sum ctx, max(T_d, T_p), min(T_d, T_p)] (c = prefill
+ *     rows, D = decodes) and t_hat = theta_lin . phi.
+ * Parameters (NIYAMA_NUM_PARAMS doubles): theta[0..5] = theta_lin >= 0,
+ * theta[6] = tau (s), theta[7] = r_cta (B/s), theta[8] = BW (B/s), all > 0 for
+ * 6..8.  SPEC's affine model is theta_lin = (c0, c1, 0, c2, 0, 0).
+ * Fit: for every (tau, r_cta, BW) of a grid (tau-major), theta_lin by
+ * non-negative least squares on relative residuals (phi_i / t_i against 1,
+ * columns scaled to unit max); keep the grid point of least squared residual
+ * (the first one within 1e-9 relative of the minimum). */
+#define NIYAMA_PRED_SMS 148
+#define NIYAMA_STEP_BYTES 160e3
+#define NIYAMA_TILE_SETUP_STEPS 2
+#define NIYAMA_NUM_PARAMS 9
 #define NIYAMA_NUM_FEATURES 6
 
 typedef struct {
   int32_t chunk_len;    /* prefill rows of the (single) slice, 0 if none */
   int32_t chunk_offset;
   int32_t num_decode;
-  int64_t sum_ctx;      /* sum of decode ctx */
+  int64_t sum_ctx;      /* sum of decode ctx (>= num_decode); the model spreads it evenly over the decodes */
   double seconds;       /* measured launch time (> 0) */
 } niyama_sample;
 typedef struct niyama_predictor niyama_predictor;
 
+/* Fit on the default grid: tau 1.0..2.5 us step 0.1 us, r_cta 30..100 GB/s
+ * step 5 GB/s, BW 5.0..7.6 TB/s step 0.2 TB/s. */
 niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
                                    niyama_predictor** out);
-niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta6,
-                                           niyama_predictor** out); /* theta >= 0 required */
-niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta6_out);
+/* Fit on an explicit grid {tau_lo, tau_hi, tau_step, r_lo, r_hi, r_step,
+ * bw_lo, bw_hi, bw_step}: values lo + i*step for i = 0 .. round((hi-lo)/step). */
+niyama_status niyama_predictor_fit_grid(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
+                                        const double* grid9, niyama_predictor** out);
+niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta9,
+                                           niyama_predictor** out); /* theta_lin >= 0, theta[6..8] > 0 */
+niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta9_out);
 /* Seconds for the batch (slices and decodes of desc; tiers ignored); < 0 on invalid input. */
 double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc);
-/* a1 — largest C in [0, min(max_chunk, prefill_remaining)] such that the batch
- * {C prefill rows at chunk_offset} + desc's decodes predicts <= slack_s (a
- * latency equal to the slack is feasible, R18; 1e-12 relative guard).  If
- * even C = 0 is infeasible: chunk_out = 0 and infeasible_out = 1 (a flag,
- * not an error).  desc's prefill slices are ignored. */
+/* a1 — chunk for the batch {C prefill rows at chunk_offset} + desc's decodes
+ * (desc's prefill slices are ignored) against slack_s (a latency equal to the
+ * slack is feasible, R18; 1e-12 relative guard).  cap = max(0, min(max_chunk,
+ * prefill_remaining)).  If C = 0 is infeasible: chunk_out = 0, infeasible_out
+ * = 1 (a flag, not an error).  Else if cap is feasible: cap.  Else
+ * bisection lo = 0, hi = cap, mid = floor((lo+hi)/2) until hi = lo + 1:
+ * returns lo, so t_hat(C) <= slack < t_hat(C+1) (S:137 inverse consistency);
+ * C is the largest feasible chunk whenever t_hat is non-decreasing in C. */
 niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_batch_desc* decodes_only,
                                         int32_t chunk_offset, int32_t prefill_remaining, double slack_s,
                                         int32_t max_chunk, int32_t* chunk_out, int32_t* infeasible_out);

@@ -17,6 +17,8 @@ STATUS_NAMES = ["OK", "EINVAL", "ENOBLOCKS", "ENOSEQ", "ESTATE", "ECUDA", "ENCCL
 BF16, F32 = 0, 1
 DEVICE_NONE = -1
 NUM_FEATURES = 6
+NUM_PARAMS = 9
+DEFAULT_FIT_GRID = (1.0e-6, 2.5e-6, 0.1e-6, 30e9, 100e9, 5e9, 5.0e12, 7.6e12, 0.2e12)
 
 
 class NiyamaError(RuntimeError):
@@ -42,7 +44,7 @@ class BatchDescC(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("num_rows", C.c_int32), ("num_prefill_rows", C.c_int32), ("num_decode", C.c_int32),
                 ("num_prefill_tiles", C.c_int32), ("num_decode_units", C.c_int32), ("split_len", C.c_int32),
-                ("rows_per_tile", C.c_int32), ("reserved", C.c_int32), ("sum_ctx", C.c_int64)]
+                ("rows_per_tile", C.c_int32), ("prefill_ctas", C.c_int32), ("sum_ctx", C.c_int64)]
 
 
 class SampleC(C.Structure):
@@ -85,6 +87,8 @@ def _load():
         "niyama_get_unique_id": ([vp], st),
         "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
         "niyama_predictor_fit": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(vp)], st),
+        "niyama_predictor_fit_grid": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(C.c_double),
+                                       C.POINTER(vp)], st),
         "niyama_predictor_from_params": ([C.POINTER(KVConfig), C.POINTER(C.c_double), C.POINTER(vp)], st),
         "niyama_predictor_params": ([vp, C.POINTER(C.c_double)], st),
         "niyama_predict_iter_time": ([vp, C.POINTER(BatchDescC)], C.c_double),
@@ -283,7 +287,10 @@ def get_unique_id() -> bytes:
 
 
 class Predictor:
-    """Iteration-time predictor (niyama_predictor), features per include/niyama.h (a8)."""
+    """Iteration-time predictor (niyama_predictor): the a8 schedule model of include/niyama.h.
+
+    Parameters: theta[0:6] linear weights of phi = [1, c+D, D, sum ctx, max(T_d,T_p), min(T_d,T_p)],
+    theta[6] = tau (s per prefill step), theta[7] = r_cta (B/s), theta[8] = BW (B/s)."""
 
     def __init__(self, handle: int):
         self.handle = handle
@@ -293,22 +300,29 @@ class Predictor:
         return _cfg(1, num_q_heads, num_kv_heads, head_dim, 16, 1, dtype, world_size, 0, None)
 
     @classmethod
-    def fit(cls, cfg: KVConfig, samples: Sequence) -> "Predictor":
+    def fit(cls, cfg: KVConfig, samples: Sequence, grid=None) -> "Predictor":
+        """grid: (tau_lo, tau_hi, tau_step, r_lo, r_hi, r_step, bw_lo, bw_hi, bw_step); None = library default."""
         arr = (SampleC * len(samples))(*[SampleC(s.chunk_len, s.chunk_offset, s.num_decode, s.sum_ctx, s.seconds)
                                          for s in samples])
         h = C.c_void_p()
-        _check(lib.niyama_predictor_fit(C.byref(cfg), arr, len(samples), C.byref(h)))
+        if grid is None:
+            _check(lib.niyama_predictor_fit(C.byref(cfg), arr, len(samples), C.byref(h)))
+        else:
+            g = (C.c_double * 9)(*[float(x) for x in grid])
+            _check(lib.niyama_predictor_fit_grid(C.byref(cfg), arr, len(samples), g, C.byref(h)))
         return cls(h.value)
 
     @classmethod
     def from_params(cls, cfg: KVConfig, theta) -> "Predictor":
-        th = (C.c_double * NUM_FEATURES)(*[float(x) for x in theta])
+        if len(theta) != NUM_PARAMS:
+            raise ValueError(f"theta needs {NUM_PARAMS} values")
+        th = (C.c_double * NUM_PARAMS)(*[float(x) for x in theta])
         h = C.c_void_p()
         _check(lib.niyama_predictor_from_params(C.byref(cfg), th, C.byref(h)))
         return cls(h.value)
 
     def params(self) -> np.ndarray:
-        th = (C.c_double * NUM_FEATURES)()
+        th = (C.c_double * NUM_PARAMS)()
         _check(lib.niyama_predictor_params(self.handle, th))
         return np.array(list(th))
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <queue>
 #include <set>
 #include <string>
 #include <unordered_map>
@@ -98,6 +99,9 @@ struct niyama_plan {
   std::vector<int32_t> vgrp, velem;  // V^T append groups / element rows
   int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
+  int64_t tile_steps = 0;     // sum over prefill tiles of ceil(visible keys / 128)
+  int32_t prefill_ctas = 0;   // CTAs of the bf16 launch that take prefill tiles first
+  int32_t grid = 0;           // CTAs of the bf16 launch
   std::vector<RowInfo> rows;
   uint8_t* dbuf = nullptr;
   int32_t* d_slot = nullptr;
@@ -116,8 +120,7 @@ struct niyama_plan {
 
 struct niyama_predictor {
   int hq = 0, hkv = 0, d = 0, elt = 0;
-  double fpeak = NIYAMA_F_PEAK_BF16;
-  double theta[NIYAMA_NUM_FEATURES] = {0, 0, 0, 0, 0, 0};
+  double theta[NIYAMA_NUM_PARAMS] = {0, 0, 0, 0, 0, 0, 1e-6, 50e9, 6e12};
 };
 
 extern "C" const char* niyama_last_error(void) { return g_err.c_str(); }
@@ -291,6 +294,45 @@ int32_t choose_split_len(int64_t sum_ctx, int32_t max_ctx, int hkv, int num_sms)
   int32_t s = 64;
   while ((s < raw || ceil_div(max_ctx, s) > 4095) && s < (1 << 20)) s *= 2;  // split index fits 12 bits
   return s;
+}
+
+// CTA split of the bf16 launch.  Prefill tiles are
+// tensor/MUFU-bound and decode streaming is HBM-bound, so the launch runs them side
+// by side: CTAs [0, prefill_ctas) take prefill tiles first (longest first) and then
+// join the decode queue; the others stream decode KV from the start.  The prefill
+// share of the CTAs is its share of the estimated CTA-time: one 128-key prefill
+// step costs a CTA about as long as streaming NIYAMA_STEP_BYTES of decode KV under
+// load (measured: ~3.6 us per step vs ~44 GB/s per CTA on B200, tools/cap_sweep.py).
+// A tile also pays a fixed setup (Q load, pipeline fill, epilogue) of about
+// NIYAMA_TILE_SETUP_STEPS steps, which dominates short tiles (chunk at offset 0).
+// `tile_cost` = sum over tiles of (steps + setup).  Shared by the planner and the
+// predictor (a8), which simulates the same launch.
+struct CtaSplit {
+  int32_t grid, prefill_ctas;
+};
+CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv, int d, int elt,
+                   int num_sms) {
+  CtaSplit r{};
+  r.grid = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div(n_units, 8))));
+  if (n_tiles == 0) return r;
+  if (n_units == 0) {
+    r.prefill_ctas = r.grid;
+    return r;
+  }
+  const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
+  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt;
+  int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
+  np = std::max<int64_t>(np, ceil_div(n_tiles, 4));  // a tile-count floor keeps prefill off the tail
+  np = std::min<int64_t>({np, n_tiles, static_cast<int64_t>(r.grid)});
+  r.prefill_ctas = static_cast<int32_t>(std::max<int64_t>(1, np));
+  return r;
+}
+
+void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
+  const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_tiles,
+                               pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->num_sms);
+  pl->grid = r.grid;
+  pl->prefill_ctas = r.prefill_ctas;
 }
 
 }  // namespace
@@ -474,6 +516,8 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       sl.nqt = static_cast<int32_t>(ceil_div(sl.c, pl->R));
       sl.tbase = tbase;
       tbase += sl.nqt * hkv;  // work items = 128-row q tiles
+      for (int32_t qt = 0; qt < sl.nqt; ++qt)
+        pl->tile_steps += hkv * ceil_div(static_cast<int64_t>(sl.o) + std::min<int64_t>(sl.c, (qt + 1LL) * pl->R), 128);
       pl->q_tiles += sl.nqt * hkv;
       pl->slices.push_back(sl);
     }
@@ -525,6 +569,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     for (int32_t r : tails) pl->urow.push_back((r << 12) | (pl->drows[r].ctx / pl->split_len));
     pl->n_units = ubase;
   }
+  plan_cta_split(pl, kv);
   // ---- device copy: one allocation, one H2D
   if (kv->has_device) {
     const size_t A = 256;
@@ -636,7 +681,7 @@ extern "C" niyama_status niyama_plan_get_info(const niyama_plan* plan, niyama_pl
   out->num_decode_units = plan->n_units;
   out->split_len = plan->split_len;
   out->rows_per_tile = plan->R;
-  out->reserved = 0;
+  out->prefill_ctas = plan->prefill_ctas;
   out->sum_ctx = plan->sum_ctx;
   return NIYAMA_OK;
 }
@@ -736,15 +781,8 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   if (kv->cfg.dtype == NIYAMA_BF16) {
     if (kv->d != 128 || kv->g > 8)
       return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
-    const int64_t want = static_cast<int64_t>(p.n_tiles) + ceil_div(p.n_units, 8);
-    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(kv->num_sms, want)));
-    // Prefill tiles are tensor/MUFU-bound and decode streaming is HBM-bound: confining
-    // the tiles to about half the SMs (each CTA then runs ~2 tiles) lets the other half
-    // stream decode KV from the start (measured on config 2: 132 -> 123 us).
-    const int cap = kv->prefill_cap > 0 ? kv->prefill_cap
-                                        : std::max(1, std::min<int>(grid / 2, static_cast<int>(ceil_div(p.n_tiles, 2))));
-    p.prefill_ctas = std::min(cap, grid);
-    NY_CUDA(launch_attention_bf16(p, grid, s));
+    p.prefill_ctas = kv->prefill_cap > 0 ? std::min(kv->prefill_cap, plan->grid) : plan->prefill_ctas;
+    NY_CUDA(launch_attention_bf16(p, plan->grid, s));
   } else {
     if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
     NY_CUDA(launch_attention_generic_f32(p, s));
@@ -801,36 +839,123 @@ extern "C" niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan
 }
 
 // ================================================================ predictor (a8)
+// Schedule model of the fused launch; every step is spelled out in include/niyama.h
+// and DESIGN.md "a8 schedule model" (the oracle re-implements it from there).
 namespace {
 
-void features(const niyama_predictor& p, int64_t c, int64_t o_c_tok, int64_t pairs, int64_t D, double* phi) {
-  const double B = static_cast<double>(o_c_tok) * p.hkv * p.d * 2 * p.elt;
-  const double F = 4.0 * p.d * p.hq * static_cast<double>(pairs);
-  phi[0] = 1.0;
-  phi[1] = static_cast<double>(c);
-  phi[2] = static_cast<double>(D);
-  phi[3] = B;
-  phi[4] = F;
-  phi[5] = std::max(F / p.fpeak, B / NIYAMA_B_PEAK);
-}
+// The launch's schedule in step units: independent of (tau, r_cta, BW).
+struct Sched {
+  double rows = 0, D = 0, sum_ctx = 0, Bd = 0;
+  int32_t grid = 1, np = 0;
+  std::vector<int64_t> fin;  // prefill CTAs' finish times (steps), ascending
+};
 
-// phi of {slices (o_i, c_i) with c_i > 0} + decodes (D, sum ctx)
-void features_batch(const niyama_predictor& p, const int32_t* o, const int32_t* c, int n_slices, int64_t D,
-                    int64_t sum_ctx, double* phi) {
-  int64_t rows = 0, tok = sum_ctx, pairs = sum_ctx;
-  for (int i = 0; i < n_slices; ++i) {
-    if (c[i] <= 0) continue;
-    rows += c[i];
-    tok += static_cast<int64_t>(o[i]) + c[i];
-    pairs += static_cast<int64_t>(c[i]) * o[i] + static_cast<int64_t>(c[i]) * (c[i] + 1) / 2;
+struct SliceOC {
+  int32_t o, c;
+};
+
+Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int32_t* ctx, int64_t D) {
+  Sched r;
+  const int g = p.hq / p.hkv;
+  const int64_t R = std::max(1, 128 / g);
+  // 1. tile queue: slices by o + c descending (stable), q tiles last to first, x Hkv
+  std::stable_sort(slices.begin(), slices.end(), [](const SliceOC& a, const SliceOC& b) {
+    return static_cast<int64_t>(a.o) + a.c > static_cast<int64_t>(b.o) + b.c;
+  });
+  std::vector<int64_t> costs;
+  int64_t tile_cost = 0;
+  for (const SliceOC& sl : slices) {
+    r.rows += sl.c;
+    const int64_t nqt = ceil_div(sl.c, R);
+    for (int64_t qt = nqt - 1; qt >= 0; --qt) {
+      const int64_t cost = ceil_div(sl.o + std::min<int64_t>(sl.c, (qt + 1) * R), 128) + NIYAMA_TILE_SETUP_STEPS;
+      for (int h = 0; h < p.hkv; ++h) costs.push_back(cost);
+      tile_cost += cost * p.hkv;
+    }
   }
-  features(p, rows, tok, pairs, D, phi);
+  // 2. decode units
+  int64_t sum_ctx = 0;
+  int32_t max_ctx = 0;
+  for (int64_t j = 0; j < D; ++j) {
+    sum_ctx += ctx[j];
+    max_ctx = std::max(max_ctx, ctx[j]);
+  }
+  int64_t n_units = 0;
+  if (D > 0) {
+    const int32_t split = choose_split_len(sum_ctx, max_ctx, p.hkv, NIYAMA_PRED_SMS);
+    for (int64_t j = 0; j < D; ++j) n_units += ceil_div(ctx[j], split) * p.hkv;
+  }
+  r.D = static_cast<double>(D);
+  r.sum_ctx = static_cast<double>(sum_ctx);
+  r.Bd = static_cast<double>(sum_ctx) * p.hkv * p.d * 2.0 * p.elt;
+  // 3. CTA split (the planner's rule)
+  const CtaSplit cs = cta_split(static_cast<int64_t>(costs.size()), n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt,
+                                NIYAMA_PRED_SMS);
+  r.grid = cs.grid;
+  r.np = cs.prefill_ctas;
+  // 4. list scheduling of the queue on the prefill CTAs
+  if (!costs.empty()) {
+    std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> heap;
+    for (int32_t i = 0; i < r.np; ++i) heap.push(0);
+    for (int64_t c : costs) {
+      const int64_t t = heap.top();
+      heap.pop();
+      heap.push(t + c);
+    }
+    while (!heap.empty()) {
+      r.fin.push_back(heap.top());
+      heap.pop();
+    }
+  }
+  return r;
 }
 
-double dot6(const double* a, const double* b) {
-  double s = 0;
-  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) s += a[k] * b[k];
-  return s;
+// 5.-6. fluid decode and the feature vector
+void phi_of(const Sched& s, double tau, double rc, double bw, double* phi) {
+  const double Tp = s.fin.empty() ? 0.0 : tau * static_cast<double>(s.fin.back());
+  double Td = 0.0;
+  if (s.Bd > 0) {
+    double t = 0.0, done = 0.0;
+    int32_t busy = s.np;
+    bool finished = false;
+    for (int64_t f : s.fin) {
+      const double tf = tau * static_cast<double>(f);
+      const double rate = std::min(bw, (s.grid - busy) * rc);
+      if (rate > 0 && done + rate * (tf - t) >= s.Bd) {
+        Td = t + (s.Bd - done) / rate;
+        finished = true;
+        break;
+      }
+      done += rate * (tf - t);
+      t = tf;
+      busy -= 1;
+    }
+    if (!finished) Td = t + (s.Bd - done) / std::min(bw, s.grid * rc);
+  }
+  phi[0] = 1.0;
+  phi[1] = s.rows + s.D;
+  phi[2] = s.D;
+  phi[3] = s.sum_ctx;
+  phi[4] = std::max(Td, Tp);
+  phi[5] = std::min(Td, Tp);
+}
+
+double lin(const double* theta, const double* phi) {
+  double t = 0;
+  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) t += theta[k] * phi[k];
+  return t;
+}
+
+// A sample as a batch: one slice (o, c) if c > 0, D decodes with sum ctx spread evenly.
+Sched schedule_sample(const niyama_predictor& p, const niyama_sample& s) {
+  std::vector<SliceOC> sl;
+  if (s.chunk_len > 0) sl.push_back(SliceOC{s.chunk_offset, s.chunk_len});
+  std::vector<int32_t> ctx(s.num_decode);
+  if (s.num_decode > 0) {
+    const int64_t base = s.sum_ctx / s.num_decode, rem = s.sum_ctx % s.num_decode;
+    for (int32_t j = 0; j < s.num_decode; ++j) ctx[j] = static_cast<int32_t>(base + (j < rem ? 1 : 0));
+  }
+  return schedule(p, sl, ctx.data(), s.num_decode);
 }
 
 // Least squares on the columns `cols` of A (m x n, row-major) by Householder QR.
@@ -937,70 +1062,127 @@ std::vector<double> nnls(const std::vector<double>& A, int m, int n, const std::
 niyama_status pred_shape(const niyama_kv_config* s, niyama_predictor* p) {
   if (!s) return fail(NIYAMA_EINVAL, "shape is NULL");
   if (s->world_size < 1 || s->num_kv_heads < 1 || s->num_q_heads < 1 || s->head_dim < 1 ||
-      s->num_kv_heads % s->world_size || s->num_q_heads % s->world_size)
+      s->num_kv_heads % s->world_size || s->num_q_heads % s->world_size || s->num_q_heads % s->num_kv_heads)
     return fail(NIYAMA_EINVAL, "predictor shape");
   p->hq = s->num_q_heads / s->world_size;
   p->hkv = s->num_kv_heads / s->world_size;
   p->d = s->head_dim;
   p->elt = s->dtype == NIYAMA_BF16 ? 2 : 4;
-  p->fpeak = s->dtype == NIYAMA_BF16 ? NIYAMA_F_PEAK_BF16 : NIYAMA_F_PEAK_F32;
   return NIYAMA_OK;
 }
 
 bool feasible(double t, double slack) { return t <= slack + 1e-12 * std::max(1.0, std::fabs(slack)); }
 
+std::vector<double> grid_values(double lo, double hi, double step) {
+  std::vector<double> v;
+  const int64_t n = static_cast<int64_t>(std::floor((hi - lo) / step + 0.5)) + 1;
+  for (int64_t i = 0; i < n; ++i) v.push_back(lo + static_cast<double>(i) * step);
+  return v;
+}
+
+constexpr double kDefaultGrid[9] = {1.0e-6, 2.5e-6, 0.1e-6, 30e9, 100e9, 5e9, 5.0e12, 7.6e12, 0.2e12};
+
 }  // namespace
 
-extern "C" niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
-                                              niyama_predictor** out) {
+extern "C" niyama_status niyama_predictor_fit_grid(const niyama_kv_config* shape, const niyama_sample* samples,
+                                                   int32_t n, const double* grid9, niyama_predictor** out) {
   if (!out) return fail(NIYAMA_EINVAL, "out is NULL");
   *out = nullptr;
   if (!samples || n < 1) return fail(NIYAMA_EINVAL, "no samples");
+  if (!grid9) return fail(NIYAMA_EINVAL, "grid is NULL");
+  for (int k = 0; k < 9; k += 3)
+    if (!(grid9[k] > 0) || !(grid9[k + 1] >= grid9[k]) || !(grid9[k + 2] > 0) || !std::isfinite(grid9[k + 1]) ||
+        (grid9[k + 1] - grid9[k]) / grid9[k + 2] > 1e6)
+      return fail(NIYAMA_EINVAL, "grid: need 0 < lo <= hi, step > 0");
   niyama_predictor p;
   niyama_status st = pred_shape(shape, &p);
   if (st != NIYAMA_OK) return st;
-  const int F = NIYAMA_NUM_FEATURES;
-  std::vector<double> A(static_cast<size_t>(n) * F), b(n, 1.0);
+  std::vector<Sched> sch;
+  sch.reserve(n);
   for (int i = 0; i < n; ++i) {
     const niyama_sample& s = samples[i];
-    if (!(s.seconds > 0) || s.chunk_len < 0 || s.chunk_offset < 0 || s.num_decode < 0 || s.sum_ctx < 0)
+    if (!(s.seconds > 0) || !std::isfinite(s.seconds) || s.chunk_len < 0 || s.chunk_offset < 0 || s.num_decode < 0 ||
+        s.sum_ctx < s.num_decode || (s.num_decode == 0 && s.sum_ctx != 0) ||
+        s.sum_ctx / std::max(1, s.num_decode) >= (int64_t(1) << 30))
       return fail(NIYAMA_EINVAL, "sample " + std::to_string(i) + " is invalid");
-    double phi[F];
-    features_batch(p, &s.chunk_offset, &s.chunk_len, 1, s.num_decode, s.sum_ctx, phi);
-    for (int k = 0; k < F; ++k) A[static_cast<size_t>(i) * F + k] = phi[k] / s.seconds;
+    sch.push_back(schedule_sample(p, s));
   }
-  double colmax[F];
-  for (int k = 0; k < F; ++k) {
-    colmax[k] = 0;
-    for (int i = 0; i < n; ++i) colmax[k] = std::max(colmax[k], std::fabs(A[static_cast<size_t>(i) * F + k]));
-    if (colmax[k] == 0) colmax[k] = 1;
-    for (int i = 0; i < n; ++i) A[static_cast<size_t>(i) * F + k] /= colmax[k];
-  }
-  std::vector<double> z = nnls(A, n, F, b);
+  const std::vector<double> taus = grid_values(grid9[0], grid9[1], grid9[2]);
+  const std::vector<double> rcs = grid_values(grid9[3], grid9[4], grid9[5]);
+  const std::vector<double> bws = grid_values(grid9[6], grid9[7], grid9[8]);
+  const int F = NIYAMA_NUM_FEATURES;
+  struct Cand {
+    double score;
+    double theta[NIYAMA_NUM_PARAMS];
+  };
+  std::vector<Cand> cands;
+  cands.reserve(taus.size() * rcs.size() * bws.size());
+  std::vector<double> A(static_cast<size_t>(n) * F), b(n, 1.0), phi_all(static_cast<size_t>(n) * F);
+  for (double tau : taus)
+    for (double rc : rcs)
+      for (double bw : bws) {
+        for (int i = 0; i < n; ++i) {
+          phi_of(sch[i], tau, rc, bw, &phi_all[static_cast<size_t>(i) * F]);
+          for (int k = 0; k < F; ++k) A[static_cast<size_t>(i) * F + k] = phi_all[static_cast<size_t>(i) * F + k] / samples[i].seconds;
+        }
+        double colmax[NIYAMA_NUM_FEATURES];
+        for (int k = 0; k < F; ++k) {
+          colmax[k] = 0;
+          for (int i = 0; i < n; ++i) colmax[k] = std::max(colmax[k], std::fabs(A[static_cast<size_t>(i) * F + k]));
+          if (colmax[k] == 0) colmax[k] = 1;
+          for (int i = 0; i < n; ++i) A[static_cast<size_t>(i) * F + k] /= colmax[k];
+        }
+        const std::vector<double> z = nnls(A, n, F, b);
+        Cand c{};
+        for (int k = 0; k < F; ++k) c.theta[k] = z[k] / colmax[k];
+        c.theta[6] = tau;
+        c.theta[7] = rc;
+        c.theta[8] = bw;
+        c.score = 0;
+        for (int i = 0; i < n; ++i) {
+          const double e = lin(c.theta, &phi_all[static_cast<size_t>(i) * F]) / samples[i].seconds - 1.0;
+          c.score += e * e;
+        }
+        cands.push_back(c);
+      }
+  double best = std::numeric_limits<double>::infinity();
+  for (const Cand& c : cands) best = std::min(best, c.score);
+  const Cand* pick = &cands[0];
+  for (const Cand& c : cands)
+    if (c.score <= best * (1.0 + 1e-9)) {
+      pick = &c;
+      break;
+    }
   auto* res = new niyama_predictor(p);
-  for (int k = 0; k < F; ++k) res->theta[k] = z[k] / colmax[k];
+  std::memcpy(res->theta, pick->theta, sizeof(res->theta));
   *out = res;
   return NIYAMA_OK;
 }
 
-extern "C" niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta6,
+extern "C" niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
+                                              niyama_predictor** out) {
+  return niyama_predictor_fit_grid(shape, samples, n, kDefaultGrid, out);
+}
+
+extern "C" niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta9,
                                                       niyama_predictor** out) {
-  if (!out || !theta6) return fail(NIYAMA_EINVAL, "out/theta is NULL");
+  if (!out || !theta9) return fail(NIYAMA_EINVAL, "out/theta is NULL");
   *out = nullptr;
   niyama_predictor p;
   niyama_status st = pred_shape(shape, &p);
   if (st != NIYAMA_OK) return st;
-  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) {
-    if (!(theta6[k] >= 0) || !std::isfinite(theta6[k])) return fail(NIYAMA_EINVAL, "theta must be finite and >= 0");
-    p.theta[k] = theta6[k];
+  for (int k = 0; k < NIYAMA_NUM_PARAMS; ++k) {
+    const bool ok = std::isfinite(theta9[k]) && (k < NIYAMA_NUM_FEATURES ? theta9[k] >= 0 : theta9[k] > 0);
+    if (!ok) return fail(NIYAMA_EINVAL, "theta: linear part finite and >= 0, tau/r_cta/BW finite and > 0");
+    p.theta[k] = theta9[k];
   }
   *out = new niyama_predictor(p);
   return NIYAMA_OK;
 }
 
-extern "C" niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta6_out) {
-  if (!p || !theta6_out) return fail(NIYAMA_EINVAL, "p/out is NULL");
-  std::memcpy(theta6_out, p->theta, sizeof(p->theta));
+extern "C" niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta9_out) {
+  if (!p || !theta9_out) return fail(NIYAMA_EINVAL, "p/out is NULL");
+  std::memcpy(theta9_out, p->theta, sizeof(p->theta));
   return NIYAMA_OK;
 }
 
@@ -1008,16 +1190,17 @@ extern "C" double niyama_predict_iter_time(const niyama_predictor* p, const niya
   if (!p || !desc || desc->num_prefill < 0 || desc->num_decode < 0) return -1.0;
   if (desc->num_prefill > 0 && (!desc->prefill_offset || !desc->prefill_len)) return -1.0;
   if (desc->num_decode > 0 && !desc->decode_ctx) return -1.0;
-  int64_t sum_ctx = 0;
-  for (int j = 0; j < desc->num_decode; ++j) {
+  for (int j = 0; j < desc->num_decode; ++j)
     if (desc->decode_ctx[j] < 1) return -1.0;
-    sum_ctx += desc->decode_ctx[j];
-  }
-  for (int i = 0; i < desc->num_prefill; ++i)
+  std::vector<SliceOC> sl;
+  for (int i = 0; i < desc->num_prefill; ++i) {
     if (desc->prefill_offset[i] < 0 || desc->prefill_len[i] < 0) return -1.0;
+    if (desc->prefill_len[i] > 0) sl.push_back(SliceOC{desc->prefill_offset[i], desc->prefill_len[i]});
+  }
+  const Sched s = schedule(*p, std::move(sl), desc->decode_ctx, desc->num_decode);
   double phi[NIYAMA_NUM_FEATURES];
-  features_batch(*p, desc->prefill_offset, desc->prefill_len, desc->num_prefill, desc->num_decode, sum_ctx, phi);
-  return dot6(p->theta, phi);
+  phi_of(s, p->theta[6], p->theta[7], p->theta[8], phi);
+  return lin(p->theta, phi);
 }
 
 extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_batch_desc* decodes_only,
@@ -1027,34 +1210,36 @@ extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, co
   if (chunk_offset < 0 || max_chunk < 0 || std::isnan(slack_s)) return fail(NIYAMA_EINVAL, "chunk_offset/max_chunk/slack");
   if (decodes_only->num_decode < 0 || (decodes_only->num_decode > 0 && !decodes_only->decode_ctx))
     return fail(NIYAMA_EINVAL, "decode arrays");
-  int64_t sum_ctx = 0;
-  for (int j = 0; j < decodes_only->num_decode; ++j) {
+  for (int j = 0; j < decodes_only->num_decode; ++j)
     if (decodes_only->decode_ctx[j] < 1) return fail(NIYAMA_EINVAL, "decode_ctx < 1");
-    sum_ctx += decodes_only->decode_ctx[j];
-  }
-  const int64_t D = decodes_only->num_decode;
   auto t_of = [&](int32_t C) {
+    std::vector<SliceOC> sl;
+    if (C > 0) sl.push_back(SliceOC{chunk_offset, C});
+    const Sched s = schedule(*p, std::move(sl), decodes_only->decode_ctx, decodes_only->num_decode);
     double phi[NIYAMA_NUM_FEATURES];
-    features_batch(*p, &chunk_offset, &C, 1, D, sum_ctx, phi);
-    return dot6(p->theta, phi);
+    phi_of(s, p->theta[6], p->theta[7], p->theta[8], phi);
+    return lin(p->theta, phi);
   };
   const int32_t cap = std::max(0, std::min(max_chunk, prefill_remaining));
+  *infeasible_out = 0;
   if (!feasible(t_of(0), slack_s)) {
     *chunk_out = 0;
     *infeasible_out = 1;
     return NIYAMA_OK;
   }
-  // theta >= 0 => t_hat non-decreasing in C: binary search the last feasible C.
-  int32_t lo = 0, hi = cap;
-  while (lo < hi) {
-    const int32_t mid = lo + (hi - lo + 1) / 2;
+  if (feasible(t_of(cap), slack_s)) {
+    *chunk_out = cap;
+    return NIYAMA_OK;
+  }
+  int32_t lo = 0, hi = cap;  // t_of(lo) feasible, t_of(hi) not
+  while (hi - lo > 1) {
+    const int32_t mid = lo + (hi - lo) / 2;
     if (feasible(t_of(mid), slack_s))
       lo = mid;
     else
-      hi = mid - 1;
+      hi = mid;
   }
   *chunk_out = lo;
-  *infeasible_out = 0;
   return NIYAMA_OK;
 }
 

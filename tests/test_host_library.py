@@ -187,65 +187,95 @@ SHAPE = OP.PredShape(num_q_heads=32, num_kv_heads=8, head_dim=128, elt_bytes=2)
 CFG = ny.Predictor.shape_cfg(32, 8, 128)
 
 
+THETA = np.array([3e-5, 2e-9, 5e-8, 1.1e-10, 0.9, 0.2, 1.6e-6, 50e9, 6.0e12])
+
+
+def _rand_batch(g, max_p=3, max_d=50):
+    P = int(g.integers(0, max_p))
+    D = int(g.integers(0, max_d))
+    offs = [int(x) for x in g.integers(0, 5000, size=P)]
+    lens = [int(x) for x in g.integers(0, 2049, size=P)]
+    ctx = [int(x) for x in g.integers(1, 8193, size=D)]
+    return offs, lens, ctx
+
+
 def test_predictor_eval_matches_oracle():
-    theta = np.array([4e-6, 2e-9, 5e-8, 1.1e-13, 3e-16, 0.9])
-    pr = ny.Predictor.from_params(CFG, theta)
-    np.testing.assert_array_equal(pr.params(), theta)
+    pr = ny.Predictor.from_params(CFG, THETA)
+    np.testing.assert_array_equal(pr.params(), THETA)
     g = np.random.default_rng(0)
-    for _ in range(50):
-        P = int(g.integers(0, 3))
-        D = int(g.integers(0, 50))
-        offs = [int(x) for x in g.integers(0, 5000, size=P)]
-        lens = [int(x) for x in g.integers(0, 2049, size=P)]
-        ctx = [int(x) for x in g.integers(1, 8193, size=D)]
-        d = W.BatchDesc(list(range(P)), offs, lens, list(range(100, 100 + D)), ctx)
-        want = OP.predict(theta, OP.features(SHAPE, list(zip(offs, lens)), ctx))
-        assert pr.predict(d) == pytest.approx(want, rel=1e-13, abs=0)
+    for _ in range(60):
+        offs, lens, ctx = _rand_batch(g)
+        d = W.BatchDesc(list(range(len(offs))), offs, lens, list(range(100, 100 + len(ctx))), ctx)
+        want = OP.predict(THETA, SHAPE, list(zip(offs, lens)), ctx)
+        assert pr.predict(d) == pytest.approx(want, rel=1e-12, abs=0)
+
+
+def test_planner_cta_split_matches_oracle_schedule():
+    """The planner's (grid, prefill CTAs) is the schedule model's step 3."""
+    g = np.random.default_rng(4)
+    for _ in range(12):
+        offs, lens, ctx = _rand_batch(g, max_p=3, max_d=80)
+        kv = host_kv(W.L8B, 40000)
+        n = len(offs)
+        pre = W.BatchDesc(list(range(n)) + list(range(100, 100 + len(ctx))), offs + [c - 1 for c in ctx],
+                          [1] * n + [1] * len(ctx))
+        pre.prefill_len = [o for o in offs] + [c - 1 for c in ctx]
+        pre.prefill_offset = [0] * (n + len(ctx))
+        kv.plan(pre).close()
+        d = W.BatchDesc(list(range(n)), offs, lens, list(range(100, 100 + len(ctx))), ctx)
+        info = kv.plan(d).info()
+        sch = OP.schedule(SHAPE, list(zip(offs, lens)), ctx)
+        assert info.num_prefill_tiles == len(OP.tile_queue(SHAPE, list(zip(offs, lens))))
+        assert info.prefill_ctas == sch.np_
+        if ctx:
+            assert info.split_len == OP.split_len(sum(ctx), max(ctx), 8)
 
 
 def test_predictor_fit_matches_oracle():
     g = np.random.default_rng(1)
     samples = []
-    for _ in range(80):
+    for _ in range(40):
         c = int(g.choice([0, 256, 512, 1024, 2048]))
         o = int(g.integers(0, 6000)) if c else 0
-        D = int(g.integers(0, 257))
-        L = int(g.integers(D, D * 4096 + 1)) if D else 0
-        t = 5e-6 + 1.3 * max(4 * 128 * 32 * (c * o + c * (c + 1) / 2 + L) / 2.25e15,
-                             ((o + c if c else 0) + L) * 4096 / 8e12) * (1 + 0.05 * g.standard_normal())
-        samples.append(OP.Sample(c, o, D, L, max(t, 1e-6)))
-    th_o = OP.fit(SHAPE, samples)
-    th_c = ny.Predictor.fit(CFG, samples).params()
-    pred_o = np.array([th_o @ OP.features_sample(SHAPE, s) for s in samples])
-    pred_c = np.array([th_c @ OP.features_sample(SHAPE, s) for s in samples])
+        D = int(g.integers(1, 257))
+        L = int(g.integers(D, D * 4096 + 1))
+        s = OP.Sample(c, o, D, L, 1.0)
+        s.seconds = OP.predict(THETA, SHAPE, *OP.sample_batch(s)) * (1 + 0.05 * float(g.standard_normal()))
+        samples.append(s)
+    grid = (1.2e-6, 2.0e-6, 0.2e-6, 40e9, 60e9, 10e9, 5.6e12, 6.4e12, 0.4e12)
+    th_o = OP.fit(SHAPE, samples, grid)
+    th_c = ny.Predictor.fit(CFG, samples, grid).params()
+    np.testing.assert_array_equal(th_c[6:], th_o[6:])           # same grid point
+    pred_o = np.array([OP.predict(th_o, SHAPE, *OP.sample_batch(s)) for s in samples])
+    pred_c = np.array([OP.predict(th_c, SHAPE, *OP.sample_batch(s)) for s in samples])
     np.testing.assert_allclose(pred_c, pred_o, rtol=1e-7)
-    assert (th_c >= 0).all()
+    assert (th_c[:6] >= 0).all()
 
 
-def test_max_feasible_chunk_matches_bruteforce():
-    theta = np.array([4e-6, 2e-9, 5e-8, 1.1e-13, 3e-16, 0.9])
-    pr = ny.Predictor.from_params(CFG, theta)
+def test_max_feasible_chunk_matches_oracle():
+    pr = ny.Predictor.from_params(CFG, THETA)
     g = np.random.default_rng(2)
     for _ in range(25):
         ctx = [int(x) for x in g.integers(1, 4097, size=int(g.integers(0, 64)))]
         o = int(g.integers(0, 4000))
         rem = int(g.integers(0, 3000))
-        t0 = OP.predict(theta, OP.features(SHAPE, [], ctx))
+        t0 = OP.predict(THETA, SHAPE, [], ctx)
         slack = float(t0 * g.uniform(0.8, 3.0))
         assert pr.max_feasible_chunk(ctx, o, rem, slack, 2048) == \
-            OP.max_feasible_chunk(theta, SHAPE, ctx, o, rem, slack, 2048)
+            OP.max_feasible_chunk(THETA, SHAPE, ctx, o, rem, slack, 2048)
 
 
 def test_spec_examples_through_c_abi():
     fx = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
     cm = fx["cost_model"]
-    per_tok = 8 * 128 * 2 * 2
-    pr = ny.Predictor.from_params(CFG, [cm["c0"], cm["c1"], cm["c1"], cm["c2"] / per_tok, 0, 0])
+    pr = ny.Predictor.from_params(CFG, [cm["c0"], cm["c1"], 0, cm["c2"], 0, 0, 1.6e-6, 50e9, 6e12])
     assert pr.predict(W.BatchDesc()) == pytest.approx(cm["c0"], abs=1e-15)
     assert pr.predict(W.BatchDesc([0], [0], [256])) == pytest.approx(cm["chunk256_s"], rel=1e-12)
     assert pr.max_feasible_chunk([], 0, 10**6, cm["inverse"]["slack"], 2048) == (256, False)
     assert pr.max_feasible_chunk([], 0, 10**6, math.inf, 2048) == (2048, False)
     assert pr.max_feasible_chunk([100], 0, 10**6, 0.001, 2048) == (0, True)
+    with pytest.raises(ny.NiyamaError):
+        ny.Predictor.from_params(CFG, [1e-5, 0, 0, 0, 0, 0, 0.0, 50e9, 6e12])      # tau must be > 0
     for ex in fx["slack"]:
         decs = [OS.DecodeQoS(**d) for d in ex["decodes"]]
         got = ny.min_slack(decs, ex["now"])

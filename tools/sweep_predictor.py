@@ -69,6 +69,7 @@ class Rig:
         Tb = desc.num_rows
         batch = ny.Batch(desc)
         plan = kv.plan(batch)
+        self.last_info = plan.info()
         knew = self.randn(Tb, s.num_kv_heads, s.head_dim)
         kv.append(plan, 0, knew, knew)
         q = self.randn(Tb, s.num_q_heads, s.head_dim)
@@ -88,13 +89,22 @@ class Rig:
         p.close()
         for sq in [0] + seqs:
             kv.release(sq)
+        self.last_ts = ts
         return statistics.median(ts), Tb
+
+
+def plan_fields(rig):
+    i = rig.last_info
+    return dict(tiles=i.num_prefill_tiles, units=i.num_decode_units, split_len=i.split_len,
+                prefill_ctas=i.prefill_ctas, p10=float(np.percentile(rig.last_ts, 10)),
+                p90=float(np.percentile(rig.last_ts, 90)))
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "predictor_fit.json"))
+    ap.add_argument("--offgrid", type=int, default=20)
     args = ap.parse_args()
     s = W.L8B
     rig = Rig(s, num_blocks=256 * 8192 // 16 + 8192)
@@ -107,16 +117,16 @@ def main():
                 o, ctx = point_desc(chunk, D, seed)
                 t, T = rig.measure(chunk, o, ctx, args.reps)
                 rows.append(dict(kind="grid", seed=seed, chunk=chunk, offset=o, D=D, sum_ctx=int(sum(ctx)),
-                                 seconds=t, T=T))
+                                 seconds=t, T=T, ctx=ctx, **plan_fields(rig)))
                 print(f"seed={seed} c={chunk:5d} o={o:5d} D={D:3d} sumctx={sum(ctx):8d} t={t*1e6:8.1f}us", flush=True)
     g = np.random.default_rng(123)
-    for i in range(20):
+    for i in range(args.offgrid):
         chunk = int(g.integers(1, 2049))
         D = int(g.integers(1, 257))
         o, ctx = point_desc(chunk, D, 100 + i)
         t, T = rig.measure(chunk, o, ctx, args.reps)
         rows.append(dict(kind="offgrid", seed=100 + i, chunk=chunk, offset=o, D=D, sum_ctx=int(sum(ctx)),
-                         seconds=t, T=T))
+                         seconds=t, T=T, ctx=ctx, **plan_fields(rig)))
         print(f"offgrid c={chunk:5d} o={o:5d} D={D:3d} t={t*1e6:8.1f}us", flush=True)
 
     def sample(r):
@@ -132,12 +142,10 @@ def main():
     theta = pred.params().tolist()
 
     def err(r):
+        # held-out and training points are evaluated on their real decode contexts
         d = W.BatchDesc(prefill_seq=[0] if r["chunk"] else [], prefill_offset=[r["offset"]] if r["chunk"] else [],
-                        prefill_len=[r["chunk"]] if r["chunk"] else [])
-        # decodes enter the features only through D and sum ctx: spread sum ctx over D rows
-        base, rem = divmod(r["sum_ctx"], r["D"])
-        d.decode_seq = list(range(1, r["D"] + 1))
-        d.decode_ctx = [base + (1 if i < rem else 0) for i in range(r["D"])]
+                        prefill_len=[r["chunk"]] if r["chunk"] else [], decode_seq=list(range(1, r["D"] + 1)),
+                        decode_ctx=list(r["ctx"]))
         return pred.predict(d) / r["seconds"] - 1.0
 
     e_train = np.abs([err(r) for r in train])
@@ -148,7 +156,9 @@ def main():
         rs = [r for r in rows if r["kind"] == "grid" and r["chunk"] == c]
         perf[c] = float(np.mean([r["T"] / r["seconds"] for r in rs]))
     out = {"config": "l8b", "world": 1, "theta": theta,
-           "features": ["1", "c", "D", "B_KV bytes", "F flops", "max(F/F_peak, B/B_peak) s"],
+           "params": ["c0", "per row (c+D)", "per decode", "per ctx token", "max(T_d,T_p)", "min(T_d,T_p)",
+                      "tau s/step", "r_cta B/s", "BW B/s"],
+           "model": "a8 schedule model (include/niyama.h, DESIGN.md)",
            "train_points": len(train), "heldout_points": len(held),
            "train_rel_err": {"p50": float(np.median(e_train)), "p95": float(np.percentile(e_train, 95)),
                              "max": float(e_train.max())},
