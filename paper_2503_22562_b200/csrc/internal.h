@@ -41,8 +41,7 @@ struct PrefillSlice {
 
 // Decode row (sorted by ctx, longest first): unit (row, split s, kv head h) covers
 // keys [s*L, min(ctx, (s+1)*L)) with L = split_len; its partial (when nsplit > 1)
-// lives at the canonical index ubase + s*Hkv + h.  The device queue visits units in
-// the order of `urow` (one entry per (row, split), heads consecutive).  (a5, a6)
+// lives at the canonical index ubase + s*Hkv + h.  (a5, a6)
 struct DecodeRow {
   int32_t tbl;
   int32_t ctx;
@@ -50,6 +49,20 @@ struct DecodeRow {
   int32_t nsplit;
   int32_t ubase;
   int32_t pad0, pad1, pad2;
+};
+
+// Decode queue entry (a5): one per (row, split), in LPT order; unit id u of the
+// queue is entry u / Hkv, kv head u % Hkv.  Everything a warp needs to start the
+// unit is in this one 32-byte record, including the physical block of its first
+// 16-token stage, so claiming a unit costs one dependent load.
+struct UnitRec {
+  int32_t tbl;     // offset of the sequence's block table
+  int32_t row;     // batch row
+  int32_t k0, k1;  // key range [k0, k1)
+  int32_t nsplit;  // splits of the row (1: write O/LSE directly)
+  int32_t pbase;   // partial index of kv head 0: ubase + s * Hkv
+  int32_t phys0;   // physical block of key k0
+  int32_t pad;
 };
 
 // Per-row info for the generic (f32) path.
@@ -67,11 +80,10 @@ struct AttnParams {
   const int32_t* tables;
   const PrefillSlice* slices;
   const DecodeRow* drows;
-  const int32_t* urow;   // [n_units / Hkv] queue entry -> (sorted row << 12) | split
+  const UnitRec* uq;     // [n_units / Hkv] decode queue (LPT order)
   const RowInfo* rows;
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]
-  int32_t* counters;  // [num_decode * Hkv] split-completion counters (reset by the merging warp)
   int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] grid barrier (self-resetting)
   int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
   int32_t T, Hq, Hkv, d, B, g, R;

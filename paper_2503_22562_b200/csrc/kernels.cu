@@ -273,37 +273,48 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   }
 
   if (warp == 0 || warp == 2) {
-    if (lane == 0) {
-      // ---------------- producers: 128-key K tiles (warp 0), V^T tiles (warp 2)
-      const bool isK = warp == 0;
-      const uint8_t* pool = isK ? p.pool_k : p.pool_v;
-      const uint32_t ring = sbase + (isK ? kKOff : kVOff);
-      const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
-      const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
-      for (int j = 0; j < nk; ++j) {
-        const uint32_t k_it = kv_it + j;
-        const int st = k_it & 1;
+    // ---------------- producers: 128-key K tiles (warp 0), V^T tiles (warp 2).
+    // Lane u < 8 owns piece u of every step: K = block u of the step (two 128-byte
+    // panels of B rows, at B = 16), V^T = the 16-key sub-block u.  Its block-table
+    // lookup for step j+1 is issued before step j's copies, so the lookups of a
+    // step run in parallel and off the critical path; lane 0 arms the barrier.
+    const bool isK = warp == 0;
+    const uint8_t* pool = isK ? p.pool_k : p.pool_v;
+    const uint32_t ring = sbase + (isK ? kKOff : kVOff);
+    const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
+    const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
+    const int bpt = kBN / p.B;                  // K: blocks per key step
+    const int npc = isK ? bpt : kBN / 16;       // pieces per step
+    auto piece_off = [&](int j) -> int64_t {    // byte offset of this lane's piece of step j
+      if (lane >= npc || j >= nk) return 0;
+      if (isK) {
+        const int lb = min(j * bpt + lane, t.nblk - 1);  // past the end: finite data, masked (P = 0)
+        return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes;
+      }
+      const int key = j * kBN + 16 * lane;
+      const int lb = min(key / p.B, t.nblk - 1);
+      return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes +
+             static_cast<int64_t>((key % p.B) >> 4) * 4096;
+    };
+    int64_t next = piece_off(0);
+    for (int j = 0; j < nk; ++j) {
+      const int64_t cur = next;
+      next = piece_off(j + 1);
+      const uint32_t k_it = kv_it + j;
+      const int st = k_it & 1;
+      const uint32_t full = bars + 8 * (bar_full + st);
+      if (lane == 0) {
         mbar_wait(bars + 8 * (bar_empty + st), ((k_it >> 1) & 1) ^ 1);
         ev_stamp(ev, isK ? 0 : 1, j);
-        const uint32_t full = bars + 8 * (bar_full + st);
-        const uint32_t dst0 = ring + st * kTile;
         mbar_expect_tx(full, kTile);
+      }
+      __syncwarp();
+      const uint32_t dst0 = ring + st * kTile;
+      if (lane < npc) {
         if (isK) {
-          const int bpt = kBN / p.B;  // blocks per key tile
-          for (int b = 0; b < bpt; ++b) {
-            int lb = j * bpt + b;
-            if (lb >= t.nblk) lb = t.nblk - 1;  // finite data; masked out (P = 0)
-            const int64_t off = (__ldg(p.tables + t.tbl + lb) * p.Hkv + t.kvh) * p.chunk_bytes;
-            for (int pn = 0; pn < 2; ++pn) bulk_g2s(dst0 + pn * kPanel + b * seg, pool + off + pn * seg, seg, full);
-          }
+          for (int pn = 0; pn < 2; ++pn) bulk_g2s(dst0 + pn * kPanel + lane * seg, pool + cur + pn * seg, seg, full);
         } else {
-          for (int u = 0; u < kBN / 16; ++u) {  // one 4 KB V^T sub-block per 16 keys
-            const int key = j * kBN + 16 * u;
-            const int lb = min(key / p.B, t.nblk - 1);
-            const int64_t off = (__ldg(p.tables + t.tbl + lb) * p.Hkv + t.kvh) * p.chunk_bytes +
-                                static_cast<int64_t>((key % p.B) >> 4) * 4096;
-            bulk_g2s(dst0 + u * 4096, pool + off, 4096, full);
-          }
+          bulk_g2s(dst0 + lane * 4096, pool + cur, 4096, full);
         }
       }
     }
@@ -462,32 +473,29 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
 
 // --------------------------------------------------------------- decode unit
 struct UnitDesc {
-  int id, tbl, ctx, row, kvh, k0, k1, nsplit, ubase, pair;  // pair = sorted row * Hkv + kvh (merge counter)
+  int id, tbl, row, kvh, k0, k1, nsplit;
 };
 
 // Unit = (row, split s, kv head h); d.id = its canonical partial index ubase + s*Hkv + h.
-__device__ __forceinline__ UnitDesc make_unit(const AttnParams& p, const DecodeRow& r, int ridx, int s, int h) {
+__device__ __forceinline__ UnitDesc make_unit(const UnitRec& r, int h) {
   UnitDesc d;
-  d.id = r.ubase + s * p.Hkv + h;
+  d.id = r.pbase + h;
   d.tbl = r.tbl;
-  d.ctx = r.ctx;
   d.row = r.row;
   d.kvh = h;
-  d.k0 = s * p.split_len;
-  d.k1 = min(r.ctx, d.k0 + p.split_len);
+  d.k0 = r.k0;
+  d.k1 = r.k1;
   d.nsplit = r.nsplit;
-  d.ubase = r.ubase;
-  d.pair = ridx * p.Hkv + h;
   return d;
 }
 
 // Stage s of a unit = 16 tokens of one kv head: K then V (4 KB each at d = 128 bf16).
 // `phys` is the physical block holding the stage (looked up one stage ahead).
-__device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, int64_t phys,
+__device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, int phys,
                                              uint32_t stage, uint32_t bar) {
   const int tok = u.k0 + 16 * s;
   const int sub = (tok % p.B) >> 4;  // 16-token sub-block of the block
-  const int64_t chunk = (phys * p.Hkv + u.kvh) * p.chunk_bytes;
+  const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + u.kvh) * p.chunk_bytes;
   const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
   mbar_expect_tx(bar, fa::kDecStage);
   if (seg == 2048) {  // B = 16: the K chunk is one contiguous 4 KB run
@@ -510,25 +518,27 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
 struct DecodeLoader {
   UnitDesc cur;
   int s, nst;
-  int64_t phys;  // block of stage s of cur
-  int nxt_id, nxt_row, nxt_step;  // 0 nothing, 1 id requested, 2 row index, 3 row record, 4 ready
-  DecodeRow nxt_r;
-  UnitDesc nxt;
-  int64_t nxt_phys0;
+  int phys;  // block of stage s of cur (32-bit: loaded one stage before it is consumed)
+  int nxt_id, nxt_step;  // 0 nothing, 1 id claimed, 2 record requested
+  int reserved;          // this warp's pre-assigned first unit (decode-first CTAs), -1 if none
+  int id_base;           // ids [0, id_base) are pre-assigned; the queue counter hands out the rest
+  int4 nxt_a, nxt_b;     // raw UnitRec of the next unit, unpacked only when it starts
   bool done;
   uint32_t issued;
 
   __device__ __forceinline__ void advance(const AttnParams& p) {
     if (nxt_step == 0) {
-      nxt_id = atomicAdd(p.work + 1, 1);
+      if (reserved >= 0) {
+        nxt_id = reserved;
+        reserved = -1;
+      } else {
+        nxt_id = id_base + atomicAdd(p.work + 1, 1);
+      }
     } else if (nxt_step == 1) {
-      if (nxt_id < p.n_units) nxt_row = __ldg(p.urow + nxt_id / p.Hkv);  // row << 12 | split
-    } else if (nxt_step == 2) {
-      if (nxt_id < p.n_units) nxt_r = p.drows[nxt_row >> 12];
-    } else if (nxt_step == 3) {
       if (nxt_id < p.n_units) {
-        nxt = make_unit(p, nxt_r, nxt_row >> 12, nxt_row & 4095, nxt_id % p.Hkv);
-        nxt_phys0 = __ldg(p.tables + nxt.tbl + nxt.k0 / p.B);
+        const int4* rp = reinterpret_cast<const int4*>(p.uq + nxt_id / p.Hkv);
+        nxt_a = __ldg(rp);
+        nxt_b = __ldg(rp + 1);
       }
     } else {
       return;
@@ -540,7 +550,7 @@ struct DecodeLoader {
     using namespace fa;
     if (done) return;
     if (s == nst) {
-      while (nxt_step < 4) advance(p);
+      while (nxt_step < 2) advance(p);
       const int k = *n_desc;
       if (nxt_id >= p.n_units) {
         done = true;
@@ -548,8 +558,9 @@ struct DecodeLoader {
         *n_desc = k + 1;
         return;
       }
-      cur = nxt;
-      phys = nxt_phys0;
+      const UnitRec rec{nxt_a.x, nxt_a.y, nxt_a.z, nxt_a.w, nxt_b.x, nxt_b.y, nxt_b.z, nxt_b.w};
+      cur = make_unit(rec, nxt_id % p.Hkv);
+      phys = rec.phys0;
       s = 0;
       nst = (cur.k1 - cur.k0 + 15) >> 4;
       nxt_step = 0;
@@ -602,10 +613,20 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   DecodeLoader ld;
   ld.s = ld.nst = 0;
   ld.nxt_step = 0;
-  ld.nxt_id = ld.nxt_row = 0;
+  ld.nxt_id = 0;
+  {
+    // CTAs that start with decode get one pre-assigned unit per warp (LPT order), so
+    // the first claim is a plain load instead of an atomic; prefill-first CTAs and
+    // every later claim use the queue counter.
+    const int dec_first = p.n_tiles > 0 ? p.prefill_ctas : 0;
+    ld.id_base = (static_cast<int>(gridDim.x) - dec_first) * kDecWarps;
+    ld.reserved = static_cast<int>(blockIdx.x) >= dec_first
+                      ? (static_cast<int>(blockIdx.x) - dec_first) * kDecWarps + warp
+                      : -1;
+  }
   ld.done = false;
   ld.issued = 0;
-  ld.phys = ld.nxt_phys0 = 0;
+  ld.phys = 0;
   if (lane == 0) {
     *n_desc = 0;
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
@@ -738,15 +759,55 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
   const int nw = gridDim.x * fa::kDecWarps;
   const int g = p.g;
   const int items = p.n_merge_rows * p.Hkv * g;
+  // the row record of the next item is loaded one item ahead
+  DecodeRow dr_next{};
+  if (gw < items) dr_next = p.drows[gw / g / p.Hkv];
   for (int it = gw; it < items; it += nw) {
     const int hh = it % g;
     const int pair = it / g;
     const int r = pair / p.Hkv, kvh = pair - r * p.Hkv;
-    const DecodeRow dr = p.drows[r];
+    const DecodeRow dr = dr_next;
+    if (it + nw < items) dr_next = p.drows[(it + nw) / g / p.Hkv];
     const int ns = dr.nsplit;
     auto pidx = [&](int sp) -> int64_t {
       return static_cast<int64_t>(dr.ubase + sp * p.Hkv + kvh) * g + hh;
     };
+    const int h = kvh * g + hh;
+    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + dr.row) * fa::kD;
+    if (ns <= 16) {
+      // one round trip: (m, l) of split `lane` and the 16 o~ slices are loaded together
+      float2 ml = make_float2(-INFINITY, 0.f);
+      if (lane < ns) ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pidx(lane) * 2));
+      float4 v[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        v[k] = k < ns ? __ldcg(reinterpret_cast<const float4*>(p.part_o + pidx(k) * fa::kD + lane * 4))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      float M = ml.x;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float w = lane < ns ? ex2(ml.x - M) * ml.y : 0.f;
+      float L = w;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float wk = __shfl_sync(0xffffffffu, w, k);
+        acc.x += wk * v[k].x;
+        acc.y += wk * v[k].y;
+        acc.z += wk * v[k].z;
+        acc.w += wk * v[k].w;
+      }
+      const float inv = 1.f / L;
+      uint2 w2;
+      w2.x = pack_bf16(acc.x * inv, acc.y * inv);
+      w2.y = pack_bf16(acc.z * inv, acc.w * inv);
+      *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
+      if (lane == 0 && p.lse != nullptr)
+        p.lse[static_cast<int64_t>(h) * p.T + dr.row] = (M + __log2f(L)) * 0.69314718055994530942f;
+      continue;
+    }
     float M = -INFINITY;
     for (int base = 0; base < ns; base += 32)
       if (base + lane < ns) M = fmaxf(M, __ldcg(p.part_ml + pidx(base + lane) * 2));
@@ -783,8 +844,6 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
       }
     }
     const float inv = 1.f / L;
-    const int h = kvh * g + hh;
-    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + dr.row) * fa::kD;
     uint2 w2;
     w2.x = pack_bf16(acc.x * inv, acc.y * inv);
     w2.y = pack_bf16(acc.z * inv, acc.w * inv);
@@ -805,6 +864,8 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   volatile int* item_slot = reinterpret_cast<volatile int*>(misc + 16);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  uint64_t t_entry = 0;
+  if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
 
   if (tid == 0) {
     for (int b = 0; b < kBarDec; ++b)
@@ -873,6 +934,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     tr[3] = n_done_items;
     tr[4] = static_cast<int64_t>(t_decode);
     tr[5] = static_cast<int64_t>(t_barrier);
+    tr[6] = static_cast<int64_t>(t_entry);
   }
   if (any_items && warp == 1) {
     tc_fence_after();
@@ -910,7 +972,8 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = p.n_merge_rows > 0 ? 1 : 0;
+  static const bool no_coop = std::getenv("NIYAMA_NO_COOP") != nullptr;  // experiment knob (unsafe)
+  attr[0].val.cooperative = (p.n_merge_rows > 0 && !no_coop) ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);

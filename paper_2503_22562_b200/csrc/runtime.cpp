@@ -95,7 +95,7 @@ struct niyama_plan {
   std::vector<Prev> prev;  // bookkeeping before this plan (niyama_plan_rollback)
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
-  std::vector<int32_t> urow;  // queue entry (row, split) -> sorted row << 12 | split
+  std::vector<UnitRec> uq;    // decode queue, one record per (row, split), LPT order
   std::vector<int32_t> vgrp, velem;  // V^T append groups / element rows
   int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
@@ -109,12 +109,11 @@ struct niyama_plan {
   PrefillSlice* d_slices = nullptr;
   DecodeRow* d_drows = nullptr;
   RowInfo* d_rows = nullptr;
-  int32_t* d_urow = nullptr;
+  UnitRec* d_uq = nullptr;
   int32_t* d_vgrp = nullptr;
   int32_t* d_velem = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
-  int32_t* d_counters = nullptr;
   int32_t* d_work = nullptr;
 };
 
@@ -553,11 +552,22 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     // longest rows first), then each row's partial last split, longest first, so
     // the queue ends with the smallest units.  uinfo[(row,split)] = row << 12 | split;
     // heads of one (row, split) are consecutive queue entries.
-    pl->urow.reserve(static_cast<size_t>(ubase / std::max(hkv, 1)) + 1);
-    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
+    auto entry = [&](int32_t r, int32_t sp) {
       const DecodeRow& dr = pl->drows[r];
-      const int32_t full = dr.ctx / pl->split_len;
-      for (int32_t sp = 0; sp < full; ++sp) pl->urow.push_back((r << 12) | sp);
+      UnitRec u{};
+      u.tbl = dr.tbl;
+      u.row = dr.row;
+      u.k0 = sp * pl->split_len;
+      u.k1 = std::min(dr.ctx, u.k0 + pl->split_len);
+      u.nsplit = dr.nsplit;
+      u.pbase = dr.ubase + sp * hkv;
+      u.phys0 = pl->tables[dr.tbl + u.k0 / B];
+      pl->uq.push_back(u);
+    };
+    pl->uq.reserve(static_cast<size_t>(ubase / std::max(hkv, 1)) + 1);
+    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
+      const int32_t full = pl->drows[r].ctx / pl->split_len;
+      for (int32_t sp = 0; sp < full; ++sp) entry(r, sp);
     }
     std::vector<int32_t> tails;
     for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r)
@@ -566,7 +576,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       const int32_t ra = pl->drows[a].ctx % pl->split_len, rb = pl->drows[b].ctx % pl->split_len;
       return ra != rb ? ra > rb : a < b;
     });
-    for (int32_t r : tails) pl->urow.push_back((r << 12) | (pl->drows[r].ctx / pl->split_len));
+    for (int32_t r : tails) entry(r, pl->drows[r].ctx / pl->split_len);
     pl->n_units = ubase;
   }
   plan_cta_split(pl, kv);
@@ -584,11 +594,10 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_tiles = take(pl->slices.size() * sizeof(PrefillSlice));
     const size_t o_units = take(pl->drows.size() * sizeof(DecodeRow));
     const size_t o_rows = take(pl->rows.size() * sizeof(RowInfo));
-    const size_t o_urow = take(pl->urow.size() * 4);
+    const size_t o_uq = take(pl->uq.size() * sizeof(UnitRec));
     const size_t o_vgrp = take(pl->vgrp.size() * 4);
     const size_t o_velem = take(pl->velem.size() * 4);
-    const size_t o_cnt = take(static_cast<size_t>(D) * hkv * 4);  // zero-initialised through the H2D
-    const size_t o_work = take(16);
+    const size_t o_work = take(16);  // zero-initialised through the H2D
     const size_t meta_bytes = off;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
@@ -610,10 +619,10 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       std::memcpy(h + o_tiles, pl->slices.data(), pl->slices.size() * sizeof(PrefillSlice));
       std::memcpy(h + o_units, pl->drows.data(), pl->drows.size() * sizeof(DecodeRow));
       std::memcpy(h + o_rows, pl->rows.data(), pl->rows.size() * sizeof(RowInfo));
-      std::memcpy(h + o_urow, pl->urow.data(), pl->urow.size() * 4);
+      std::memcpy(h + o_uq, pl->uq.data(), pl->uq.size() * sizeof(UnitRec));
       std::memcpy(h + o_vgrp, pl->vgrp.data(), pl->vgrp.size() * 4);
       std::memcpy(h + o_velem, pl->velem.data(), pl->velem.size() * 4);
-      std::memset(h + o_cnt, 0, meta_bytes - o_cnt);
+      std::memset(h + o_work, 0, meta_bytes - o_work);
       e = cudaMemcpyAsync(pl->dbuf, h, meta_bytes, cudaMemcpyHostToDevice, s);
     }
     if (e == cudaSuccess) e = cudaEventRecord(stg->ev, s);
@@ -630,12 +639,11 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     pl->d_slices = reinterpret_cast<PrefillSlice*>(pl->dbuf + o_tiles);
     pl->d_drows = reinterpret_cast<DecodeRow*>(pl->dbuf + o_units);
     pl->d_rows = reinterpret_cast<RowInfo*>(pl->dbuf + o_rows);
-    pl->d_urow = reinterpret_cast<int32_t*>(pl->dbuf + o_urow);
+    pl->d_uq = reinterpret_cast<UnitRec*>(pl->dbuf + o_uq);
     pl->d_vgrp = reinterpret_cast<int32_t*>(pl->dbuf + o_vgrp);
     pl->d_velem = reinterpret_cast<int32_t*>(pl->dbuf + o_velem);
     pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
     pl->d_part_ml = reinterpret_cast<float*>(pl->dbuf + o_part_ml);
-    pl->d_counters = reinterpret_cast<int32_t*>(pl->dbuf + o_cnt);
     pl->d_work = reinterpret_cast<int32_t*>(pl->dbuf + o_work);
   }
   *out = pl;
@@ -758,7 +766,6 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.rows = plan->d_rows;
   p.part_o = plan->d_part_o;
   p.part_ml = plan->d_part_ml;
-  p.counters = plan->d_counters;
   p.work = plan->d_work;
   p.chunk_bytes = kv->chunk_bytes;
   p.T = plan->T;
@@ -773,7 +780,7 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.n_slices = static_cast<int32_t>(plan->slices.size());
   p.n_drows = static_cast<int32_t>(plan->drows.size());
   p.split_len = plan->split_len;
-  p.urow = plan->d_urow;
+  p.uq = plan->d_uq;
   p.n_merge_rows = plan->n_merge_rows;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = kv->trace;

@@ -14,6 +14,8 @@ ROLES = ["K issue", "V issue", "QK issue", "PV issue", "S ready", "max done", "P
 
 
 def run(wl):
+    from kbench import time_it
+    time_it(wl)
     kv, plan, q, o, lse = setup(wl)
     for _ in range(3):
         kv.attention(plan, 0, q, o, lse)
@@ -36,6 +38,9 @@ def run(wl):
         print(f"  decode end   {us(dec[:,4].min()):.1f} / {us(np.median(dec[:,4])):.1f} / {us(dec[:,4].max()):.1f} us "
               f"(min/med/max); barrier passed {us(dec[:,5].min()):.1f} .. {us(dec[:,5].max()):.1f}")
     print(f"  CTA exit     {us(cta[:,2].min()):.1f} / {us(np.median(cta[:,2])):.1f} / {us(cta[:,2].max()):.1f} us")
+    e0 = cta[:, 6].min()
+    print(f"  entry -> start: {(cta[:,0]-cta[:,6]).min()/1e3:.2f} .. {(cta[:,0]-cta[:,6]).max()/1e3:.2f} us; "
+          f"entry spread {(cta[:,6].max()-e0)/1e3:.2f} us; first entry -> last exit {(cta[:,2].max()-e0)/1e3:.1f} us")
     ev = b[160 * 8:].reshape(10, 64)
     if (ev > 0).any():
         base = ev[ev > 0].min()
@@ -47,8 +52,32 @@ def run(wl):
                                           for r in range(10)))
 
 
+def gap(wl):
+    """Last CTA exit of launch i vs first CTA entry of launch i+1 (back to back, no host sync)."""
+    kv, plan, q, o, lse = setup(wl)
+    for _ in range(3):
+        kv.attention(plan, 0, q, o, lse)
+    bufs = [torch.zeros(160 * 8 + 10 * 64, dtype=torch.int64, device="cuda") for _ in range(3)]
+    torch.cuda.synchronize()
+    for b in bufs:
+        kv.debug_trace(b)
+        kv.attention(plan, 0, q, o, lse)
+    torch.cuda.synchronize()
+    kv.debug_trace(None)
+    tr = [b.cpu().numpy()[:160 * 8].reshape(160, 8) for b in bufs]
+    tr = [t[t[:, 0] > 0] for t in tr]
+    for i in range(2):
+        print(f"  {wl.name}: launch {i} first entry -> last exit {(tr[i][:, 2].max() - tr[i][:, 6].min()) / 1e3:.1f} us; "
+              f"last exit -> next first entry {(tr[i + 1][:, 6].min() - tr[i][:, 2].max()) / 1e3:.2f} us")
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "gap":
+        gap(W.config2_l8b())
+        gap(W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2))
+        sys.exit(0)
     run(W.hybrid(W.L8B, "prefill-only-c512-o1536", prefill_offset=1536, chunk=512, decode_ctx=[], seed=2))
     if len(sys.argv) < 2:
         run(W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2))
         run(W.config2_l8b())
+
