@@ -62,7 +62,16 @@ struct UnitRec {
   int32_t nsplit;  // splits of the row (1: write O/LSE directly)
   int32_t pbase;   // partial index of kv head 0: ubase + s * Hkv
   int32_t phys0;   // physical block of key k0
-  int32_t pad;
+  int32_t crow;    // sorted row index: completion counter crow * Hkv + kv head
+};
+
+// Merge row (a6), in readiness order (by the queue position of the row's last
+// split): its items are (kv head, q head of the group).
+struct MergeRec {
+  int32_t row;     // batch row
+  int32_t ubase;   // partial index of split 0, kv head 0
+  int32_t nsplit;  // > 1
+  int32_t crow;    // completion counter row
 };
 
 // Per-row info for the generic (f32) path.
@@ -81,14 +90,17 @@ struct AttnParams {
   const PrefillSlice* slices;
   const DecodeRow* drows;
   const UnitRec* uq;     // [n_units / Hkv] decode queue (LPT order)
+  const MergeRec* mq;    // [n_merge_rows] merge queue (readiness order)
+  int32_t* counters;     // [n_drows * Hkv] split-completion counters, cumulative over launches
+  int32_t epoch;         // launches of this plan before this one (counter target (epoch+1)*nsplit)
   const RowInfo* rows;
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]
-  int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] grid barrier (self-resetting)
+  int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] merge queue (self-resetting)
   int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
   int32_t T, Hq, Hkv, d, B, g, R;
   int32_t n_tiles, n_units, n_slices, n_drows, split_len;
-  int32_t n_merge_rows;  // rows with nsplit > 1 (a prefix of drows)
+  int32_t n_merge_rows;  // rows with nsplit > 1
   int32_t prefill_ctas;  // CTAs [0, prefill_ctas) serve prefill items first; the rest decode at once
   int64_t* trace;  // optional per-CTA timeline [grid][4] (globaltimer ns), nullptr = off
   float scale_log2;     // softmax scale * log2(e)

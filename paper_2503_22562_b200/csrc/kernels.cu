@@ -473,7 +473,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
 
 // --------------------------------------------------------------- decode unit
 struct UnitDesc {
-  int id, tbl, row, kvh, k0, k1, nsplit;
+  int id, tbl, row, kvh, k0, k1, nsplit, crow;
 };
 
 // Unit = (row, split s, kv head h); d.id = its canonical partial index ubase + s*Hkv + h.
@@ -486,6 +486,7 @@ __device__ __forceinline__ UnitDesc make_unit(const UnitRec& r, int h) {
   d.k0 = r.k0;
   d.k1 = r.k1;
   d.nsplit = r.nsplit;
+  d.crow = r.crow;
   return d;
 }
 
@@ -594,6 +595,21 @@ __device__ __forceinline__ void load_q_frags(const AttnParams& p, const UnitDesc
   }
 }
 
+// Make split unit `c`'s partial (stored by every lane) visible, then count it
+// (a6 completion counter; c = crow * Hkv + kv head, -1 = nothing pending).
+__device__ __forceinline__ void publish_split(const AttnParams& p, int c, int lane) {
+  if (c < 0) return;
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) atomicAdd(p.counters + c, 1);
+}
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
 // Compute side: every lane of the warp.  Split rows write an fp32 partial
 // (m, l, o~) at index `unit id` (fire and forget); unsplit rows write O / LSE.
 __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars,
@@ -635,6 +651,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
 
   uint32_t qn0[8], qn2[8];
   bool qn_valid = false;
+  int pending = -1;  // completion counter of the last split unit, not yet published
   for (int ck = 0;; ++ck) {
     __syncwarp();
     const UnitDesc u = descs[ck & 3];
@@ -708,6 +725,12 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         mma_bf16_16816(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
         mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
       }
+      // Publish the previous split unit once two stages of this one have gone by: its
+      // partial stores have landed by then, so the fence costs nothing.
+      if (s == 1 || s == nst - 1) {
+        publish_split(p, pending, lane);
+        pending = -1;
+      }
       __syncwarp();
       if (lane == 0) ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
       ++dec_iter;
@@ -725,6 +748,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
     }
     l += __shfl_xor_sync(0xffffffffu, l, 1);
     l += __shfl_xor_sync(0xffffffffu, l, 2);
+    if (u.nsplit > 1) pending = u.crow * p.Hkv + u.kvh;  // published two stages into the next unit
     if (gid < g) {
       const float inv = 1.f / l;
       if (u.nsplit == 1) {
@@ -745,35 +769,47 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       }
     }
   }
+  publish_split(p, pending, lane);  // the last split unit of this warp
+
 }
 
-// a6 — after the grid barrier: merge the partials of every split (row, kv head, q head)
-// item, one warp per item (m = max_s m_s, w_s = e^(m_s - m) l_s,
-// o = sum_s w_s o~_s / sum_s w_s, lse = m + ln sum_s w_s).  Lane s reads split s's
-// (m, l); the o slices are read 16 splits at a time (16 loads in flight per lane) and
-// accumulated in split order, so the result is deterministic.  Rows with nsplit > 1
-// form the prefix [0, n_merge_rows) of the sorted DecodeRow records.
-__device__ __forceinline__ void merge_phase(const AttnParams& p) {
+// a6 — merge the partials of every split (row, kv head, q head) item (SURVEY §8 a6:
+// m = max_s m_s, w_s = e^(m_s - m) l_s, o = sum_s w_s o~_s / sum_s w_s, lse = m + ln
+// sum_s w_s).  Run by warps whose decode queue is exhausted, so it overlaps the
+// decode tail: items are claimed in readiness order (merge queue) and each waits
+// for its (row, kv head) completion counter.  No deadlock: every unit is claimed
+// before any warp merges, and unit processing never waits on a merge.  Lane s
+// reads split s's (m, l); o slices are accumulated in split order, so the result
+// is deterministic.
+__device__ __forceinline__ void merge_tail(const AttnParams& p) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * fa::kDecWarps + (threadIdx.x >> 5);  // warps 0..kDecWarps-1 of each CTA
-  const int nw = gridDim.x * fa::kDecWarps;
   const int g = p.g;
-  const int items = p.n_merge_rows * p.Hkv * g;
-  // the row record of the next item is loaded one item ahead
-  DecodeRow dr_next{};
-  if (gw < items) dr_next = p.drows[gw / g / p.Hkv];
-  for (int it = gw; it < items; it += nw) {
-    const int hh = it % g;
-    const int pair = it / g;
-    const int r = pair / p.Hkv, kvh = pair - r * p.Hkv;
-    const DecodeRow dr = dr_next;
-    if (it + nw < items) dr_next = p.drows[(it + nw) / g / p.Hkv];
-    const int ns = dr.nsplit;
+  const int per_row = p.Hkv * g;
+  const int items = p.n_merge_rows * per_row;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(p.work + 3, 1);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= items) break;
+    const MergeRec rec = p.mq[it / per_row];
+    const int kvh = (it / g) % p.Hkv, hh = it % g;
+    {
+      const int target = (p.epoch + 1) * rec.nsplit;
+      const int* cnt = p.counters + rec.crow * p.Hkv + kvh;
+      uint32_t polls = 0;
+      while (ld_acquire_gpu(cnt) < target) {
+        __nanosleep(64);
+#ifndef NIYAMA_NO_WATCHDOG
+        if (++polls == (1u << 26)) __trap();  // a lost completion: fail loudly, never hang
+#endif
+      }
+    }
+    const int ns = rec.nsplit;
     auto pidx = [&](int sp) -> int64_t {
-      return static_cast<int64_t>(dr.ubase + sp * p.Hkv + kvh) * g + hh;
+      return static_cast<int64_t>(rec.ubase + sp * p.Hkv + kvh) * g + hh;
     };
     const int h = kvh * g + hh;
-    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + dr.row) * fa::kD;
+    __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + rec.row) * fa::kD;
     if (ns <= 16) {
       // one round trip: (m, l) of split `lane` and the 16 o~ slices are loaded together
       float2 ml = make_float2(-INFINITY, 0.f);
@@ -805,7 +841,7 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
       w2.y = pack_bf16(acc.z * inv, acc.w * inv);
       *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
       if (lane == 0 && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(h) * p.T + dr.row] = (M + __log2f(L)) * 0.69314718055994530942f;
+        p.lse[static_cast<int64_t>(h) * p.T + rec.row] = (M + __log2f(L)) * 0.69314718055994530942f;
       continue;
     }
     float M = -INFINITY;
@@ -849,7 +885,7 @@ __device__ __forceinline__ void merge_phase(const AttnParams& p) {
     w2.y = pack_bf16(acc.z * inv, acc.w * inv);
     *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
     if (lane == 0 && p.lse != nullptr)
-      p.lse[static_cast<int64_t>(h) * p.T + dr.row] = (M + __log2f(L)) * 0.69314718055994530942f;
+      p.lse[static_cast<int64_t>(h) * p.T + rec.row] = (M + __log2f(L)) * 0.69314718055994530942f;
   }
 }
 
@@ -906,22 +942,10 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     volatile int* n_desc = reinterpret_cast<volatile int*>(misc + 64 + 16 * warp);
     decode_warp_loop(p, sbase, bars, descs, n_desc);
+    if (p.n_merge_rows > 0) merge_tail(p);
   }
   uint64_t t_decode = 0, t_barrier = 0;
-  if (p.n_merge_rows > 0) {
-    // grid barrier (cooperative launch: every CTA is resident), then the a6 merge phase
-    __syncthreads();
-    if (tid == 0) {
-      if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_decode));
-      __threadfence();
-      atomicAdd(p.work + 3, 1);
-      while (atomicAdd(p.work + 3, 0) < static_cast<int>(gridDim.x)) __nanosleep(100);
-      __threadfence();
-      if (p.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_barrier));
-    }
-    __syncthreads();
-    merge_phase(p);
-  }
+  if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_decode));
   tc_fence_before();
   __syncthreads();
   if (p.trace != nullptr && tid == 0) {
@@ -963,19 +987,12 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  // Cooperative launch: the decode merge phase follows a grid-wide barrier, which
-  // needs every CTA resident (1 CTA/SM, grid <= #SMs).
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(fa::kThreads);
   cfg.dynamicSmemBytes = fa::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  static const bool no_coop = std::getenv("NIYAMA_NO_COOP") != nullptr;  // experiment knob (unsafe)
-  attr[0].val.cooperative = (p.n_merge_rows > 0 && !no_coop) ? 1 : 0;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 0;
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);
 }
 

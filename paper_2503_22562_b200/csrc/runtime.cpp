@@ -96,6 +96,8 @@ struct niyama_plan {
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
   std::vector<UnitRec> uq;    // decode queue, one record per (row, split), LPT order
+  std::vector<MergeRec> mq;   // merge queue: split rows by the queue position of their last split
+  mutable int32_t launches = 0;  // bf16 attention launches issued with this plan (counter epoch)
   std::vector<int32_t> vgrp, velem;  // V^T append groups / element rows
   int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
@@ -110,6 +112,8 @@ struct niyama_plan {
   DecodeRow* d_drows = nullptr;
   RowInfo* d_rows = nullptr;
   UnitRec* d_uq = nullptr;
+  MergeRec* d_mq = nullptr;
+  int32_t* d_counters = nullptr;
   int32_t* d_vgrp = nullptr;
   int32_t* d_velem = nullptr;
   float* d_part_o = nullptr;
@@ -562,6 +566,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       u.nsplit = dr.nsplit;
       u.pbase = dr.ubase + sp * hkv;
       u.phys0 = pl->tables[dr.tbl + u.k0 / B];
+      u.crow = r;
       pl->uq.push_back(u);
     };
     pl->uq.reserve(static_cast<size_t>(ubase / std::max(hkv, 1)) + 1);
@@ -577,6 +582,17 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       return ra != rb ? ra > rb : a < b;
     });
     for (int32_t r : tails) entry(r, pl->drows[r].ctx / pl->split_len);
+    // merge queue (a6): rows with splits, in the order their last split is queued
+    std::vector<int32_t> last(pl->drows.size(), -1);
+    for (int32_t e = 0; e < static_cast<int32_t>(pl->uq.size()); ++e) last[pl->uq[e].crow] = e;
+    std::vector<int32_t> mrows;
+    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r)
+      if (pl->drows[r].nsplit > 1) mrows.push_back(r);
+    std::sort(mrows.begin(), mrows.end(), [&](int32_t a, int32_t b) { return last[a] < last[b]; });
+    for (int32_t r : mrows) {
+      const DecodeRow& dr = pl->drows[r];
+      pl->mq.push_back(MergeRec{dr.row, dr.ubase, dr.nsplit, r});
+    }
     pl->n_units = ubase;
   }
   plan_cta_split(pl, kv);
@@ -595,9 +611,11 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_units = take(pl->drows.size() * sizeof(DecodeRow));
     const size_t o_rows = take(pl->rows.size() * sizeof(RowInfo));
     const size_t o_uq = take(pl->uq.size() * sizeof(UnitRec));
+    const size_t o_mq = take(pl->mq.size() * sizeof(MergeRec));
     const size_t o_vgrp = take(pl->vgrp.size() * 4);
     const size_t o_velem = take(pl->velem.size() * 4);
-    const size_t o_work = take(16);  // zero-initialised through the H2D
+    const size_t o_work = take(16);  // zero-initialised through the H2D (with the counters)
+    const size_t o_cnt = take(pl->drows.size() * static_cast<size_t>(hkv) * 4);
     const size_t meta_bytes = off;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
@@ -620,6 +638,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       std::memcpy(h + o_units, pl->drows.data(), pl->drows.size() * sizeof(DecodeRow));
       std::memcpy(h + o_rows, pl->rows.data(), pl->rows.size() * sizeof(RowInfo));
       std::memcpy(h + o_uq, pl->uq.data(), pl->uq.size() * sizeof(UnitRec));
+      std::memcpy(h + o_mq, pl->mq.data(), pl->mq.size() * sizeof(MergeRec));
       std::memcpy(h + o_vgrp, pl->vgrp.data(), pl->vgrp.size() * 4);
       std::memcpy(h + o_velem, pl->velem.data(), pl->velem.size() * 4);
       std::memset(h + o_work, 0, meta_bytes - o_work);
@@ -640,6 +659,8 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     pl->d_drows = reinterpret_cast<DecodeRow*>(pl->dbuf + o_units);
     pl->d_rows = reinterpret_cast<RowInfo*>(pl->dbuf + o_rows);
     pl->d_uq = reinterpret_cast<UnitRec*>(pl->dbuf + o_uq);
+    pl->d_mq = reinterpret_cast<MergeRec*>(pl->dbuf + o_mq);
+    pl->d_counters = reinterpret_cast<int32_t*>(pl->dbuf + o_cnt);
     pl->d_vgrp = reinterpret_cast<int32_t*>(pl->dbuf + o_vgrp);
     pl->d_velem = reinterpret_cast<int32_t*>(pl->dbuf + o_velem);
     pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
@@ -781,6 +802,9 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.n_drows = static_cast<int32_t>(plan->drows.size());
   p.split_len = plan->split_len;
   p.uq = plan->d_uq;
+  p.mq = plan->d_mq;
+  p.counters = plan->d_counters;
+  p.epoch = plan->launches;
   p.n_merge_rows = plan->n_merge_rows;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = kv->trace;
@@ -790,6 +814,7 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
       return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
     p.prefill_ctas = kv->prefill_cap > 0 ? std::min(kv->prefill_cap, plan->grid) : plan->prefill_ctas;
     NY_CUDA(launch_attention_bf16(p, plan->grid, s));
+    ++plan->launches;
   } else {
     if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
     NY_CUDA(launch_attention_generic_f32(p, s));

@@ -44,6 +44,14 @@ def time_it(wl, reps=50, trace=False):
         evs[i + 1].record()
     torch.cuda.synchronize()
     ts = [evs[i].elapsed_time(evs[i + 1]) * 1e3 for i in range(reps)]
+    # the same launches with one event pair around all of them (no per-launch events)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(reps):
+        kv.attention(plan, 0, q, o, lse)
+    e1.record()
+    torch.cuda.synchronize()
+    batched = e0.elapsed_time(e1) * 1e3 / reps
     tr = None
     if trace:
         buf = torch.zeros((160 * 8 + 10 * 64,), dtype=torch.int64, device="cuda")
@@ -59,7 +67,8 @@ def time_it(wl, reps=50, trace=False):
     med = statistics.median(ts)
     info = plan.info()
     print(f"{wl.name:40s} T={d.num_rows:5d} tiles={info.num_prefill_tiles:4d} units={info.num_decode_units:5d} "
-          f"split={info.split_len:4d} median={med:8.1f}us  KV={B/1e6:7.1f}MB  {B/med/1e3:7.0f} GB/s", flush=True)
+          f"split={info.split_len:4d} median={med:8.1f}us batched={batched:8.1f}us  KV={B/1e6:7.1f}MB  "
+          f"{B/batched/1e3:7.0f} GB/s", flush=True)
     if tr is not None:
         t0 = tr[:, 0].min()
         pre = tr[tr[:, 3] > 0]
