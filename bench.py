@@ -310,7 +310,12 @@ def main():
         c, inf = pred.max_feasible_chunk(dec_only, c_off, c_rem, sl, 2048)
         a1["slack_s"], a1["chunk"], a1["infeasible"] = sl, c, inf
 
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    # Per-launch events cost device time (~1-2 us each) and break the programmatic
+    # launch overlap of append -> attention, so they bracket every EV_EVERY-th timed
+    # step only; the attention roofline uses the mean over those launches.
+    EV_EVERY = 4
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) if i % EV_EVERY == 0 else None
+          for i in range(args.steps)]
 
     def step(evs=None):
         a1_step()                                       # a1 (host)
@@ -356,8 +361,8 @@ def main():
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    attn_ms = [a.elapsed_time(b) for _, a, b in ev]
-    append_ms = [a0.elapsed_time(a) for a0, a, _ in ev]
+    attn_ms = [e[1].elapsed_time(e[2]) for e in ev if e is not None]
+    append_ms = [e[0].elapsed_time(e[1]) for e in ev if e is not None]
     attn_avg_ms = sum(attn_ms) / len(attn_ms)
     if dist:
         t = torch.tensor([ms, attn_avg_ms], device=dev)
@@ -470,6 +475,7 @@ def main():
                 "d2h_bytes_per_step": d2h, "output_matches_device_run": ok,
                 "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
         "gpu_launches": 2 * args.steps,
+        "timing_note": f"attention/append launch times from events on every {EV_EVERY}th timed step",
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
     }

@@ -44,6 +44,7 @@ __device__ __forceinline__ int vt_offset(int slot, int e, int head_dim) {
 // (j%8) ^ (slot%8).  V pieces go to the same place (f32) or are scattered element by
 // element into the transposed sub-block (bf16, v_t).
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
+  grid_dep_launch();  // the attention launch that follows may start its prologue
   const int pieces = p.row_bytes >> 4;  // 16 at d = 128 bf16
   const int nk = p.T * p.Hkv * pieces;  // K pieces (and V pieces when !v_t)
   const int d = p.row_bytes >> 1;       // head_dim (bf16)
@@ -918,6 +919,10 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = any_items ? *tmem_slot : 0u;
+  // Launched with programmatic stream serialization: everything above touched only
+  // on-chip state; every global access below comes after the preceding grid (the
+  // KV append) has completed and its writes are visible.
+  grid_dep_wait();
 
   uint64_t t_start = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
@@ -992,7 +997,11 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
   cfg.blockDim = dim3(fa::kThreads);
   cfg.dynamicSmemBytes = fa::kSmemBytes;
   cfg.stream = s;
-  cfg.numAttrs = 0;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);
 }
 

@@ -879,7 +879,8 @@ namespace {
 struct Sched {
   double rows = 0, D = 0, sum_ctx = 0, Bd = 0;
   int32_t grid = 1, np = 0;
-  std::vector<int64_t> fin;  // prefill CTAs' finish times (steps), ascending
+  // prefill CTAs' finish times (steps), ascending, as (time, number of CTAs)
+  std::vector<std::pair<int64_t, int32_t>> fin;
 };
 
 struct SliceOC {
@@ -890,19 +891,21 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   Sched r;
   const int g = p.hq / p.hkv;
   const int64_t R = std::max(1, 128 / g);
-  // 1. tile queue: slices by o + c descending (stable), q tiles last to first, x Hkv
+  // 1. tile queue: slices by o + c descending (stable), q tiles last to first, x Hkv.
+  //    Kept as (cost, Hkv) groups.
   std::stable_sort(slices.begin(), slices.end(), [](const SliceOC& a, const SliceOC& b) {
     return static_cast<int64_t>(a.o) + a.c > static_cast<int64_t>(b.o) + b.c;
   });
-  std::vector<int64_t> costs;
-  int64_t tile_cost = 0;
+  std::vector<int64_t> costs;  // one entry per group of Hkv equal tiles
+  int64_t tile_cost = 0, n_tiles = 0;
   for (const SliceOC& sl : slices) {
     r.rows += sl.c;
     const int64_t nqt = ceil_div(sl.c, R);
     for (int64_t qt = nqt - 1; qt >= 0; --qt) {
       const int64_t cost = ceil_div(sl.o + std::min<int64_t>(sl.c, (qt + 1) * R), 128) + NIYAMA_TILE_SETUP_STEPS;
-      for (int h = 0; h < p.hkv; ++h) costs.push_back(cost);
+      costs.push_back(cost);
       tile_cost += cost * p.hkv;
+      n_tiles += p.hkv;
     }
   }
   // 2. decode units
@@ -921,22 +924,32 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   r.sum_ctx = static_cast<double>(sum_ctx);
   r.Bd = static_cast<double>(sum_ctx) * p.hkv * p.d * 2.0 * p.elt;
   // 3. CTA split (the planner's rule)
-  const CtaSplit cs = cta_split(static_cast<int64_t>(costs.size()), n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt,
-                                NIYAMA_PRED_SMS);
+  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, NIYAMA_PRED_SMS);
   r.grid = cs.grid;
   r.np = cs.prefill_ctas;
-  // 4. list scheduling of the queue on the prefill CTAs
+  // 4. list scheduling of the queue on the prefill CTAs.  Each tile goes to a CTA
+  //    that frees first; CTAs with equal loads are interchangeable, so the loads are
+  //    kept as an ascending (load, count) list and up to `count` tiles of a group go
+  //    to the CTAs at the minimum load at once — the same finish-time multiset as
+  //    one-by-one list scheduling.
   if (!costs.empty()) {
-    std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> heap;
-    for (int32_t i = 0; i < r.np; ++i) heap.push(0);
+    auto& L = r.fin;
+    L.assign(1, {0, r.np});
     for (int64_t c : costs) {
-      const int64_t t = heap.top();
-      heap.pop();
-      heap.push(t + c);
-    }
-    while (!heap.empty()) {
-      r.fin.push_back(heap.top());
-      heap.pop();
+      int64_t left = p.hkv;
+      while (left > 0) {
+        const int64_t load = L.front().first;
+        const int32_t take = static_cast<int32_t>(std::min<int64_t>(left, L.front().second));
+        if ((L.front().second -= take) == 0) L.erase(L.begin());
+        left -= take;
+        const int64_t nl = load + c;
+        auto it = std::lower_bound(L.begin(), L.end(), nl,
+                                   [](const std::pair<int64_t, int32_t>& e, int64_t v) { return e.first < v; });
+        if (it != L.end() && it->first == nl)
+          it->second += take;
+        else
+          L.insert(it, {nl, take});
+      }
     }
   }
   return r;
@@ -944,14 +957,14 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
 
 // 5.-6. fluid decode and the feature vector
 void phi_of(const Sched& s, double tau, double rc, double bw, double* phi) {
-  const double Tp = s.fin.empty() ? 0.0 : tau * static_cast<double>(s.fin.back());
+  const double Tp = s.fin.empty() ? 0.0 : tau * static_cast<double>(s.fin.back().first);
   double Td = 0.0;
   if (s.Bd > 0) {
     double t = 0.0, done = 0.0;
     int32_t busy = s.np;
     bool finished = false;
-    for (int64_t f : s.fin) {
-      const double tf = tau * static_cast<double>(f);
+    for (const auto& f : s.fin) {  // CTAs with equal finish times leave together
+      const double tf = tau * static_cast<double>(f.first);
       const double rate = std::min(bw, (s.grid - busy) * rc);
       if (rate > 0 && done + rate * (tf - t) >= s.Bd) {
         Td = t + (s.Bd - done) / rate;
@@ -960,7 +973,7 @@ void phi_of(const Sched& s, double tau, double rc, double bw, double* phi) {
       }
       done += rate * (tf - t);
       t = tf;
-      busy -= 1;
+      busy -= f.second;
     }
     if (!finished) Td = t + (s.Bd - done) / std::min(bw, s.grid * rc);
   }
