@@ -59,10 +59,13 @@ class DecodeQoSC(C.Structure):
 
 
 def _load():
-    if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is not built: run `python paper_2503_22562_b200/build.py` "
+    # NIYAMA_LIB_PATH: load an alternate build of the same library (A/B experiments
+    # with tools/build_variant.py); the default is the in-tree libniyama.so.
+    path = os.environ.get("NIYAMA_LIB_PATH", LIB_PATH)
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is not built: run `python paper_2503_22562_b200/build.py` "
                           "(there is no CPU fallback)")
-    lib = C.CDLL(LIB_PATH)
+    lib = C.CDLL(path)
     vp, i32, i64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_int
     sigs = {
         "niyama_last_error": ([], C.c_char_p),

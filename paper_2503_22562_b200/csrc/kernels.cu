@@ -405,11 +405,16 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       const float nm = -m_ref;
       uint32_t pk[kBN / 2];
       float sum0 = 0.f, sum1 = 0.f;
+      // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each.  (Moving a share of
+      // them to a polynomial on the FMA pipe was measured slower: the step is bound
+      // by the MMA pipe and issue, not by MUFU.)
+      {
 #pragma unroll
-      for (int c = 0; c < kBN / 2; ++c) {  // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each
-        const float e0 = ex2(fmaf(s[2 * c], sl2, nm)), e1 = ex2(fmaf(s[2 * c + 1], sl2, nm));
-        if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
-        pk[c] = pack_bf16(e0, e1);
+        for (int c = 0; c < kBN / 2; ++c) {
+          const float e0 = ex2(fmaf(s[2 * c], sl2, nm)), e1 = ex2(fmaf(s[2 * c + 1], sl2, nm));
+          if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
+          pk[c] = pack_bf16(e0, e1);
+        }
       }
       l += sum0 + sum1;
       if (r == 0) ev_stamp(ev, 8, j);
