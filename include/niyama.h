@@ -217,9 +217,11 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  *     per slice the q tiles from last to first (qt = nqt-1 .. 0, nqt =
  *     ceil(c / R), R = 128 / (Hq/Hkv)), each repeated Hkv times, with cost
  *     ceil((o + min(c, (qt+1) R)) / 128) + NIYAMA_TILE_SETUP_STEPS steps.
- *  2. Decode units: split_len from (sum ctx, max ctx) exactly as the planner
+ *  2. Decode units: split_len q from (sum ctx, max ctx) exactly as the planner
  *     (a power of two >= 64 with about 4 units per resident warp on
- *     NIYAMA_PRED_SMS SMs), units = sum_j ceil(ctx_j / split_len) * Hkv.
+ *     NIYAMA_PRED_SMS SMs); a row of ctx L has n_f = ceil(L/q) - 1 pieces of q
+ *     keys plus its last L - n_f q keys in pieces of min(q, max(256, q/NIYAMA_TAIL_DIV));
+ *     units = sum over rows of that piece count, times Hkv.
  *  3. grid and prefill CTAs n_p by the planner's CTA split (niyama_plan_info).
  *  4. List scheduling: each tile in queue order goes to the prefill CTA that
  *     frees first; f_1 <= ... <= f_np are the CTAs' finish times in steps.
@@ -236,6 +238,7 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  * columns scaled to unit max); keep the grid point of least squared residual
  * (the first one within 1e-9 relative of the minimum). */
 #define NIYAMA_PRED_SMS 148
+#define NIYAMA_TAIL_DIV 4
 #define NIYAMA_STEP_BYTES 160e3
 #define NIYAMA_TILE_SETUP_STEPS 2
 #define NIYAMA_NUM_PARAMS 9

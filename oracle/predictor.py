@@ -15,9 +15,11 @@ fix the model, written out here step by step:
   1. tile queue: prefill slices (o, c > 0) sorted by o + c descending
      (stable); per slice q tiles qt = nqt-1 .. 0 (nqt = ceil(c/R)), each
      repeated Hkv times, cost = ceil((o + min(c, (qt+1) R)) / 128) + SETUP.
-  2. decode units: split_len = the smallest power of two s >= 64 with
+  2. decode units: split_len q = the smallest power of two s >= 64 with
      s >= ceil(max(1, sumL*Hkv) / (4*NSM*8)) and ceil(max_ctx/s) <= 4095
-     (capped at 2^20); units = sum_j ceil(ctx_j / split_len) * Hkv.
+     (capped at 2^20); a row of ctx L is n_f = ceil(L/q) - 1 pieces of q keys
+     plus its last L - n_f*q keys in pieces of min(q, max(256, q // TAIL_DIV));
+     units = Hkv * sum over rows of the piece count.
   3. grid = max(1, min(NSM, tiles + ceil(units/8))); prefill CTAs n_p = 0
      without tiles, = grid without units, else ceil(grid*wp/(wp+wd)) with
      wp = (sum of tile costs) * STEP_BYTES and wd = sumL*Hkv*d*2*e, raised to
@@ -59,6 +61,7 @@ import numpy as np
 from scipy.optimize import nnls
 
 NSM = 148
+TAIL_DIV = 4
 STEP_BYTES = 160e3
 SETUP = 2
 NFEAT = 6
@@ -93,6 +96,7 @@ class Sched:
     grid: int
     np_: int
     fin: List[int] = field(default_factory=list)
+    units: int = 0
 
 
 def cdiv(a: int, b: int) -> int:
@@ -154,12 +158,15 @@ def schedule(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Se
     L = int(sum(decode_ctx))
     units = 0
     if D:
-        s = split_len(L, int(max(decode_ctx)), shape.num_kv_heads)
-        units = sum(cdiv(int(x), s) for x in decode_ctx) * shape.num_kv_heads
+        q = split_len(L, int(max(decode_ctx)), shape.num_kv_heads)
+        small = min(q, max(256, q // TAIL_DIV))
+        for x in decode_ctx:
+            nf = cdiv(int(x), q) - 1
+            units += (nf + cdiv(int(x) - nf * q, small)) * shape.num_kv_heads
     grid, n_p = cta_split(len(costs), units, sum(costs), L, shape)
     Bd = float(L) * shape.num_kv_heads * shape.head_dim * 2.0 * shape.elt_bytes
     rows = sum(c for _, c in slices if c > 0)
-    return Sched(rows, D, L, Bd, grid, n_p, list_schedule(costs, n_p))
+    return Sched(rows, D, L, Bd, grid, n_p, list_schedule(costs, n_p), units)
 
 
 def phi(s: Sched, tau: float, rc: float, bw: float) -> np.ndarray:

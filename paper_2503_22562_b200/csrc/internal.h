@@ -53,16 +53,19 @@ struct DecodeRow {
 
 // Decode queue entry (a5): one per (row, split), in LPT order; unit id u of the
 // queue is entry u / Hkv, kv head u % Hkv.  Everything a warp needs to start the
-// unit is in this one 32-byte record, including the physical block of its first
-// 16-token stage, so claiming a unit costs one dependent load.
+// unit is in this one 48-byte record, including the physical blocks of its first
+// three 16-token stages, so claiming a unit costs one dependent load.
 struct UnitRec {
   int32_t tbl;     // offset of the sequence's block table
   int32_t row;     // batch row
   int32_t k0, k1;  // key range [k0, k1)
   int32_t nsplit;  // splits of the row (1: write O/LSE directly)
   int32_t pbase;   // partial index of kv head 0: ubase + s * Hkv
-  int32_t phys0;   // physical block of key k0
+  int32_t phys0;   // physical block of key k0 (stage 0)
   int32_t crow;    // sorted row index: completion counter crow * Hkv + kv head
+  int32_t phys1;   // physical blocks of stages 1 and 2 (keys min(k0 + 16 s, k1 - 1)), so a
+  int32_t phys2;   //   warp fills its 3-stage ring without a block-table round trip
+  int32_t pad0, pad1;
 };
 
 // Merge row (a6), in readiness order (by the queue position of the row's last

@@ -529,7 +529,9 @@ struct DecodeLoader {
   int nxt_id, nxt_step;  // 0 nothing, 1 id claimed, 2 record requested
   int reserved;          // this warp's pre-assigned first unit (decode-first CTAs), -1 if none
   int id_base;           // ids [0, id_base) are pre-assigned; the queue counter hands out the rest
-  int4 nxt_a, nxt_b;     // raw UnitRec of the next unit, unpacked only when it starts
+  int4 nxt_a, nxt_b, nxt_c;  // raw UnitRec of the next unit, unpacked only when it starts
+  int ph1, ph2;          // blocks of stages 1 and 2 of cur (from its record)
+  bool warm;             // initial ring fill done: the next-unit claim may proceed
   bool done;
   uint32_t issued;
 
@@ -546,6 +548,7 @@ struct DecodeLoader {
         const int4* rp = reinterpret_cast<const int4*>(p.uq + nxt_id / p.Hkv);
         nxt_a = __ldg(rp);
         nxt_b = __ldg(rp + 1);
+        nxt_c = __ldg(rp + 2);
       }
     } else {
       return;
@@ -565,9 +568,11 @@ struct DecodeLoader {
         *n_desc = k + 1;
         return;
       }
-      const UnitRec rec{nxt_a.x, nxt_a.y, nxt_a.z, nxt_a.w, nxt_b.x, nxt_b.y, nxt_b.z, nxt_b.w};
+      const UnitRec rec{nxt_a.x, nxt_a.y, nxt_a.z, nxt_a.w, nxt_b.x, nxt_b.y, nxt_b.z, nxt_b.w, nxt_c.x, nxt_c.y, 0, 0};
       cur = make_unit(rec, nxt_id % p.Hkv);
       phys = rec.phys0;
+      ph1 = rec.phys1;
+      ph2 = rec.phys2;
       s = 0;
       nst = (cur.k1 - cur.k0 + 15) >> 4;
       nxt_step = 0;
@@ -579,10 +584,16 @@ struct DecodeLoader {
     ++s;
     ++issued;
     if (s < nst) {
-      const int lb_prev = (cur.k0 + 16 * (s - 1)) / p.B, lb = (cur.k0 + 16 * s) / p.B;
-      if (lb != lb_prev) phys = __ldg(p.tables + cur.tbl + lb);  // consumed by the next call
+      if (s <= 2) {
+        phys = s == 1 ? ph1 : ph2;  // from the unit record
+      } else {
+        const int lb_prev = (cur.k0 + 16 * (s - 1)) / p.B, lb = (cur.k0 + 16 * s) / p.B;
+        if (lb != lb_prev) phys = __ldg(p.tables + cur.tbl + lb);  // consumed by the next call
+      }
     }
-    advance(p);
+    // During the initial ring fill only the claim itself (step 0) is issued: its
+    // result is first needed after the fill, so the fill never waits on it.
+    if (warm || nxt_step == 0) advance(p);
   }
 };
 
@@ -649,9 +660,12 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   ld.done = false;
   ld.issued = 0;
   ld.phys = 0;
+  ld.warm = false;
+  ld.ph1 = ld.ph2 = 0;
   if (lane == 0) {
     *n_desc = 0;
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
+    ld.warm = true;
   }
   __syncwarp();
 
@@ -737,6 +751,11 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         publish_split(p, pending, lane);
         pending = -1;
       }
+      if (p.trace != nullptr && dec_iter == 0 && warp == 0 && lane == 0) {  // diagnostics: first stage done
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[8 * blockIdx.x + 7] = static_cast<int64_t>(t);
+      }
       __syncwarp();
       if (lane == 0) ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
       ++dec_iter;
@@ -776,6 +795,11 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
     }
   }
   publish_split(p, pending, lane);  // the last split unit of this warp
+  if (p.trace != nullptr && warp == 0 && lane == 0) {  // diagnostics: warp 0 ran out of units
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.trace[8 * blockIdx.x + 5] = static_cast<int64_t>(t);
+  }
 
 }
 
@@ -816,13 +840,13 @@ __device__ __forceinline__ void merge_tail(const AttnParams& p) {
     };
     const int h = kvh * g + hh;
     __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + rec.row) * fa::kD;
-    if (ns <= 16) {
-      // one round trip: (m, l) of split `lane` and the 16 o~ slices are loaded together
+    if (ns <= 32) {
+      // one round trip: (m, l) of split `lane` and up to 32 o~ slices are loaded together
       float2 ml = make_float2(-INFINITY, 0.f);
       if (lane < ns) ml = __ldcg(reinterpret_cast<const float2*>(p.part_ml + pidx(lane) * 2));
-      float4 v[16];
+      float4 v[32];
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
+      for (int k = 0; k < 32; ++k)
         v[k] = k < ns ? __ldcg(reinterpret_cast<const float4*>(p.part_o + pidx(k) * fa::kD + lane * 4))
                       : make_float4(0.f, 0.f, 0.f, 0.f);
       float M = ml.x;
@@ -834,7 +858,8 @@ __device__ __forceinline__ void merge_tail(const AttnParams& p) {
       for (int off = 16; off > 0; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
+      for (int k = 0; k < 32; ++k) {
+        if (k >= ns) break;
         const float wk = __shfl_sync(0xffffffffu, w, k);
         acc.x += wk * v[k].x;
         acc.y += wk * v[k].y;
@@ -954,7 +979,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     decode_warp_loop(p, sbase, bars, descs, n_desc);
     if (p.n_merge_rows > 0) merge_tail(p);
   }
-  uint64_t t_decode = 0, t_barrier = 0;
+  uint64_t t_decode = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_decode));
   tc_fence_before();
   __syncthreads();
@@ -967,7 +992,6 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     tr[2] = static_cast<int64_t>(t_end);
     tr[3] = n_done_items;
     tr[4] = static_cast<int64_t>(t_decode);
-    tr[5] = static_cast<int64_t>(t_barrier);
     tr[6] = static_cast<int64_t>(t_entry);
   }
   if (any_items && warp == 1) {

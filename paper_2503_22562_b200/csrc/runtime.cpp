@@ -82,6 +82,7 @@ struct niyama_kv {
   int64_t* trace = nullptr;  // niyama_debug_trace
   int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
   int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
+  int32_t tail_div = NIYAMA_TAIL_DIV;  // NIYAMA_TAIL_DIV env (tuning knob): last piece of a row in q/tail_div units
 };
 
 struct niyama_plan {
@@ -162,6 +163,7 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
   if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
+  if (const char* td = std::getenv("NIYAMA_TAIL_DIV")) kv->tail_div = std::max(1, std::min(16, std::atoi(td)));
   if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
     const int v = std::atoi(sl);
     if (v >= 16 && v % 16 == 0) kv->split_override = v;
@@ -539,6 +541,17 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       if (tier_of(P + a) != tier_of(P + b)) return tier_of(P + a) < tier_of(P + b);
       return a < b;
     });
+    // Splits of a row of ctx L (a5): n_full = ceil(L/q) - 1 pieces of q = split_len
+    // tokens, then the last piece (1..q tokens) cut into pieces of
+    // min(q, max(256, q / tail_div)) tokens (measured: 64-token pieces cost more in
+    // partials and merges than they win at the tail; 512-token ones at q = 2048 win
+    // 640 -> 613 us on 256 x 4096 decodes).  The queue (LPT) takes every full piece first (longest rows first), then
+    // the small pieces longest first, so the final phase of the launch is made of
+    // short units and the warps run dry together.  Boundaries depend only on the
+    // row's ctx and batch totals (deterministic results).
+    const int32_t q = pl->split_len;
+    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(256, q / kv->tail_div));
+    auto n_full_of = [&](int32_t L) { return static_cast<int32_t>(ceil_div(L, q)) - 1; };
     int32_t ubase = 0;
     pl->drows.reserve(D);
     for (int j : order) {
@@ -546,42 +559,50 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       r.tbl = tbl_off[P + j];
       r.ctx = desc->decode_ctx[j];
       r.row = pl->prefill_rows + j;
-      r.nsplit = static_cast<int32_t>(ceil_div(r.ctx, pl->split_len));
+      const int32_t nf = n_full_of(r.ctx);
+      r.nsplit = nf + static_cast<int32_t>(ceil_div(r.ctx - nf * q, small));
       r.ubase = ubase;
       ubase += r.nsplit * hkv;
       if (r.nsplit > 1) ++pl->n_merge_rows;
       pl->drows.push_back(r);
     }
-    // Queue order (LPT): every full-length split of every row first (row-major,
-    // longest rows first), then each row's partial last split, longest first, so
-    // the queue ends with the smallest units.  uinfo[(row,split)] = row << 12 | split;
-    // heads of one (row, split) are consecutive queue entries.
+    // heads of one (row, split) are consecutive queue entries
     auto entry = [&](int32_t r, int32_t sp) {
       const DecodeRow& dr = pl->drows[r];
+      const int32_t nf = n_full_of(dr.ctx);
       UnitRec u{};
       u.tbl = dr.tbl;
       u.row = dr.row;
-      u.k0 = sp * pl->split_len;
-      u.k1 = std::min(dr.ctx, u.k0 + pl->split_len);
+      u.k0 = sp < nf ? sp * q : nf * q + (sp - nf) * small;
+      u.k1 = std::min(dr.ctx, sp < nf ? u.k0 + q : u.k0 + small);
       u.nsplit = dr.nsplit;
       u.pbase = dr.ubase + sp * hkv;
       u.phys0 = pl->tables[dr.tbl + u.k0 / B];
+      u.phys1 = pl->tables[dr.tbl + std::min(u.k0 + 16, u.k1 - 1) / B];
+      u.phys2 = pl->tables[dr.tbl + std::min(u.k0 + 32, u.k1 - 1) / B];
       u.crow = r;
       pl->uq.push_back(u);
     };
     pl->uq.reserve(static_cast<size_t>(ubase / std::max(hkv, 1)) + 1);
-    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
-      const int32_t full = pl->drows[r].ctx / pl->split_len;
-      for (int32_t sp = 0; sp < full; ++sp) entry(r, sp);
-    }
-    std::vector<int32_t> tails;
     for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r)
-      if (pl->drows[r].ctx % pl->split_len) tails.push_back(r);
-    std::sort(tails.begin(), tails.end(), [&](int32_t a, int32_t b) {
-      const int32_t ra = pl->drows[a].ctx % pl->split_len, rb = pl->drows[b].ctx % pl->split_len;
-      return ra != rb ? ra > rb : a < b;
+      for (int32_t sp = 0; sp < n_full_of(pl->drows[r].ctx); ++sp) entry(r, sp);
+    struct Piece {
+      int32_t len, r, sp;
+    };
+    std::vector<Piece> pieces;
+    for (int32_t r = 0; r < static_cast<int32_t>(pl->drows.size()); ++r) {
+      const DecodeRow& dr = pl->drows[r];
+      const int32_t nf = n_full_of(dr.ctx);
+      for (int32_t sp = nf; sp < dr.nsplit; ++sp) {
+        const int32_t k0 = nf * q + (sp - nf) * small;
+        pieces.push_back(Piece{std::min(dr.ctx, k0 + small) - k0, r, sp});
+      }
+    }
+    std::sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) {
+      if (a.len != b.len) return a.len > b.len;
+      return a.r != b.r ? a.r < b.r : a.sp < b.sp;
     });
-    for (int32_t r : tails) entry(r, pl->drows[r].ctx / pl->split_len);
+    for (const Piece& pc : pieces) entry(pc.r, pc.sp);
     // merge queue (a6): rows with splits, in the order their last split is queued
     std::vector<int32_t> last(pl->drows.size(), -1);
     for (int32_t e = 0; e < static_cast<int32_t>(pl->uq.size()); ++e) last[pl->uq[e].crow] = e;
@@ -917,8 +938,12 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   }
   int64_t n_units = 0;
   if (D > 0) {
-    const int32_t split = choose_split_len(sum_ctx, max_ctx, p.hkv, NIYAMA_PRED_SMS);
-    for (int64_t j = 0; j < D; ++j) n_units += ceil_div(ctx[j], split) * p.hkv;
+    const int32_t q = choose_split_len(sum_ctx, max_ctx, p.hkv, NIYAMA_PRED_SMS);
+    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(256, q / NIYAMA_TAIL_DIV));
+    for (int64_t j = 0; j < D; ++j) {
+      const int64_t nf = ceil_div(ctx[j], q) - 1;
+      n_units += (nf + ceil_div(ctx[j] - nf * q, small)) * p.hkv;
+    }
   }
   r.D = static_cast<double>(D);
   r.sum_ctx = static_cast<double>(sum_ctx);

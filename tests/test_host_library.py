@@ -139,8 +139,9 @@ def test_device_calls_refuse_without_gpu():
 
 
 def test_work_list_sizing():
-    """a2: tiles = sum ceil(c/R) * Hkv with R = 128/g; units = sum ceil(ctx/split) * Hkv;
-    split is the smallest power of two >= 64 with sum ctx * Hkv / split <= 4 * 148 * 8."""
+    """a2: tiles = sum ceil(c/R) * Hkv with R = 128/g; split q is the smallest power of two
+    >= 64 with sum ctx * Hkv / q <= 4 * 148 * 8; a row is ceil(ctx/q) - 1 pieces of q keys
+    plus its last piece cut into min(q, max(256, q/4))-key units."""
     ctx = W.l8b_decode_ctx()
     wl = W.hybrid(W.L8B, "sizing", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
     kv = host_kv(W.L8B, wl.num_blocks)
@@ -150,7 +151,10 @@ def test_work_list_sizing():
     assert info.rows_per_tile == 32
     assert info.num_prefill_tiles == (512 // 32) * 8
     assert info.split_len == 256                      # 133674*8/4736 = 225.8 -> 256
-    assert info.num_decode_units == sum(-(-int(c) // 256) for c in ctx) * 8
+    def pieces(c):
+        nf = -(-int(c) // 256) - 1
+        return nf + -(-(int(c) - 256 * nf) // 256)
+    assert info.num_decode_units == sum(pieces(c) for c in ctx) * 8
     assert info.sum_ctx == 133674 and info.num_rows == 576
 
 
@@ -213,9 +217,11 @@ def test_predictor_eval_matches_oracle():
 def test_planner_cta_split_matches_oracle_schedule():
     """The planner's (grid, prefill CTAs) is the schedule model's step 3."""
     g = np.random.default_rng(4)
-    for _ in range(12):
+    for it in range(12):
         offs, lens, ctx = _rand_batch(g, max_p=3, max_d=80)
-        kv = host_kv(W.L8B, 40000)
+        if it % 3 == 2:
+            ctx = [int(x) for x in g.integers(2048, 8193, size=int(g.integers(100, 200)))]  # split 1024/2048
+        kv = host_kv(W.L8B, 120000)
         n = len(offs)
         pre = W.BatchDesc(list(range(n)) + list(range(100, 100 + len(ctx))), offs + [c - 1 for c in ctx],
                           [1] * n + [1] * len(ctx))
@@ -227,6 +233,7 @@ def test_planner_cta_split_matches_oracle_schedule():
         sch = OP.schedule(SHAPE, list(zip(offs, lens)), ctx)
         assert info.num_prefill_tiles == len(OP.tile_queue(SHAPE, list(zip(offs, lens))))
         assert info.prefill_ctas == sch.np_
+        assert info.num_decode_units == sch.units
         if ctx:
             assert info.split_len == OP.split_len(sum(ctx), max(ctx), 8)
 

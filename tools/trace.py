@@ -35,8 +35,15 @@ def run(wl):
         print(f"  prefill CTAs {len(pre)}: prefill end {us(pre[:,1].min()):.1f} .. {us(pre[:,1].max()):.1f} us")
     dec = cta[cta[:, 4] > 0]
     if len(dec):
-        print(f"  decode end   {us(dec[:,4].min()):.1f} / {us(np.median(dec[:,4])):.1f} / {us(dec[:,4].max()):.1f} us "
-              f"(min/med/max); barrier passed {us(dec[:,5].min()):.1f} .. {us(dec[:,5].max()):.1f}")
+        def mmm(x):
+            return f"{us(x.min()):.1f} / {us(np.median(x)):.1f} / {us(x.max()):.1f}"
+        f7 = dec[dec[:, 7] > 0]
+        if len(f7):
+            print(f"  warp0 first stage consumed {mmm(f7[:, 7])} us (min/med/max)")
+        f5 = dec[dec[:, 5] > 0]
+        if len(f5):
+            print(f"  warp0 queue exhausted      {mmm(f5[:, 5])} us")
+        print(f"  decode+merge end           {mmm(dec[:, 4])} us")
     print(f"  CTA exit     {us(cta[:,2].min()):.1f} / {us(np.median(cta[:,2])):.1f} / {us(cta[:,2].max()):.1f} us")
     e0 = cta[:, 6].min()
     print(f"  entry -> start: {(cta[:,0]-cta[:,6]).min()/1e3:.2f} .. {(cta[:,0]-cta[:,6]).max()/1e3:.2f} us; "
