@@ -218,8 +218,8 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  *     ceil(c / R), R = 128 / (Hq/Hkv)), each repeated Hkv times, with cost
  *     ceil((o + min(c, (qt+1) R)) / 128) + NIYAMA_TILE_SETUP_STEPS steps.
  *  2. Decode units: split_len q from (sum ctx, max ctx) exactly as the planner
- *     (a power of two >= 64 with about 4 units per resident warp on
- *     NIYAMA_PRED_SMS SMs); a row of ctx L has n_f = ceil(L/q) - 1 pieces of q
+ *     (the power of two >= 128 nearest in log scale to sum ctx * Hkv over 4
+ *     units per resident warp on NIYAMA_PRED_SMS SMs); a row of ctx L has n_f = ceil(L/q) - 1 pieces of q
  *     keys plus its last L - n_f q keys in pieces of min(q, max(256, q/NIYAMA_TAIL_DIV));
  *     units = sum over rows of that piece count, times Hkv.
  *  3. grid and prefill CTAs n_p by the planner's CTA split (niyama_plan_info).

@@ -15,9 +15,10 @@ fix the model, written out here step by step:
   1. tile queue: prefill slices (o, c > 0) sorted by o + c descending
      (stable); per slice q tiles qt = nqt-1 .. 0 (nqt = ceil(c/R)), each
      repeated Hkv times, cost = ceil((o + min(c, (qt+1) R)) / 128) + SETUP.
-  2. decode units: split_len q = the smallest power of two s >= 64 with
-     s >= ceil(max(1, sumL*Hkv) / (4*NSM*8)) and ceil(max_ctx/s) <= 4095
-     (capped at 2^20); a row of ctx L is n_f = ceil(L/q) - 1 pieces of q keys
+  2. decode units: split_len q = the smallest power of two s >= 128 with
+     2 s^2 >= raw^2 (s >= raw / sqrt 2: the power of two nearest raw in log
+     scale), raw = ceil(max(1, sumL*Hkv) / (4*NSM*8)), and ceil(max_ctx/s) <=
+     4095 (capped at 2^20); a row of ctx L is n_f = ceil(L/q) - 1 pieces of q keys
      plus its last L - n_f*q keys in pieces of min(q, max(256, q // TAIL_DIV));
      units = Hkv * sum over rows of the piece count.
   3. grid = max(1, min(NSM, tiles + ceil(units/8))); prefill CTAs n_p = 0
@@ -106,8 +107,8 @@ def cdiv(a: int, b: int) -> int:
 def split_len(sum_ctx: int, max_ctx: int, hkv: int, nsm: int = NSM) -> int:
     """Step 2: decode split length."""
     raw = cdiv(max(1, sum_ctx * hkv), 4 * nsm * 8)
-    s = 64
-    while (s < raw or cdiv(max_ctx, s) > 4095) and s < (1 << 20):
+    s = 128
+    while (2 * s * s < raw * raw or cdiv(max_ctx, s) > 4095) and s < (1 << 20):
         s *= 2
     return s
 

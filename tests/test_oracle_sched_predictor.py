@@ -108,10 +108,11 @@ def test_list_schedule_hand_worked():
 
 
 def test_split_len_and_cta_split_hand_worked():
-    assert P.split_len(133674, 4096, 8) == 256        # ceil(1069392 / 4736) = 226 -> 256
-    assert P.split_len(100, 100, 1) == 64
-    assert P.split_len(10**7, 8192, 8) == 32768       # ceil(8e7 / 4736) = 16892
-    assert P.split_len(10, 300000, 1) == 128          # ceil(300000/64) = 4688 > 4095 -> 128
+    assert P.split_len(133674, 4096, 8) == 256        # ceil(1069392 / 4736) = 226 -> nearest 256
+    assert P.split_len(77000, 4096, 8) == 128         # raw 131: 128 is nearer than 256
+    assert P.split_len(100, 100, 1) == 128            # floor 128
+    assert P.split_len(10**7, 8192, 8) == 16384       # ceil(8e7 / 4736) = 16892 -> nearest 16384
+    assert P.split_len(10, 600000, 1) == 256          # ceil(600000/128) = 4688 > 4095 -> 256
     assert P.cta_split(4, 0, 12, 0, SHAPE) == (4, 4)
     assert P.cta_split(0, 600, 0, 133674, SHAPE) == (75, 0)
     # wp = 2074*160e3, wd = 133674*4096 -> 148 * 0.3768 = 55.8 -> 56 (floor 32)
