@@ -183,6 +183,10 @@ constexpr int kThreads = 256;
 constexpr int kDecWarps = 8;
 constexpr int kDecStages = 3;
 constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
+// Decode math: the 16 tokens of a stage on the MMA M dimension and the g <= 8 heads
+// of the group on N (mma.sync m16n8k16, "swap-AB"): 8 MMAs for S^T = K Q^T and 8 for
+// O^T += V^T P^T per stage (heads on M would pad g to 16 rows and need 16 + 16).
+
 static_assert(kDecWarps * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
 // barrier indices (all [2]: double-buffered resources)
 constexpr int kBarKFull = 0;
@@ -514,6 +518,8 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
   bulk_g2s(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar);  // V^T sub-block [128 d][16 keys]
 }
 
+
+
 // Load side of a decode warp (lane 0 only).  It walks a continuous stream of
 // 16-token stages across unit boundaries, keeping kDecStages in flight.  Every
 // dependent global load is issued one step before its value is needed: the
@@ -641,7 +647,6 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   uint32_t dec_iter = 0;
   const float sl2 = p.scale_log2;
   const int mi = lane >> 3, rr = lane & 7;
-  const int ktok = (mi >> 1) * 8 + rr;  // K (non-trans): matrices (tok 0-7,c),(0-7,c+1),(8-15,c),(8-15,c+1)
 
   DecodeLoader ld;
   ld.s = ld.nst = 0;
@@ -665,8 +670,8 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   if (lane == 0) {
     *n_desc = 0;
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
-    ld.warm = true;
   }
+  ld.warm = true;
   __syncwarp();
 
   uint32_t qn0[8], qn2[8];
@@ -689,61 +694,75 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) qa0[kk] = qa2[kk] = 0u;
     }
-    float o[16][4];
+    float o[8][4];  // O^T m-tiles: (dim 16md + gid (+8), heads 2tig, 2tig+1)
 #pragma unroll
-    for (int n = 0; n < 16; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-    float m = -INFINITY, l = 0.f;
+    for (int n = 0; n < 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m = -INFINITY, l = 0.f;      // head 2*tig
+    float mB = -INFINITY, lB = 0.f;    // head 2*tig + 1
     for (int s = 0; s < nst; ++s) {
       const uint32_t slot = dec_iter % kDecStages;
       const uint32_t ph = (dec_iter / kDecStages) & 1;
       const uint32_t stg = ring + slot * kDecStage;
       mbar_wait(bar0 + 8 * slot, ph);
-      // S = Q K^T over 16 tokens (2 n-tiles of 8)
-      float sc0[4] = {0.f, 0.f, 0.f, 0.f}, sc1[4] = {0.f, 0.f, 0.f, 0.f};
+      // S^T [16 tok x 8 heads] = K [16 tok x 128 d] . Q^T: A = K via ldmatrix (matrices
+      // (tok 0-7, c), (tok 8-15, c), (tok 0-7, c+1), (tok 8-15, c+1)), B = Q fragments.
+      float st[4] = {0.f, 0.f, 0.f, 0.f};
+      const int ttok = (mi & 1) * 8 + rr;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const int chunk = (kk & 3) * 2 + (mi & 1);
-        const uint32_t addr = stg + (kk >> 2) * 2048 + ktok * 128 + ((chunk ^ (ktok & 7)) << 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(addr, b0, b1, b2, b3);
-        mma_bf16_16816(sc0, qa0[kk], 0u, qa2[kk], 0u, b0, b1);
-        mma_bf16_16816(sc1, qa0[kk], 0u, qa2[kk], 0u, b2, b3);
+        const int chunk = (kk & 3) * 2 + (mi >> 1);
+        const uint32_t addr = stg + (kk >> 2) * 2048 + ttok * 128 + ((chunk ^ (ttok & 7)) << 4);
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(addr, a0, a1, a2, a3);
+        mma_bf16_16816(st, a0, a1, a2, a3, qa0[kk], qa2[kk]);
       }
+      // st: (tok gid, head 2tig), (tok gid, head 2tig+1), (tok gid+8, 2tig), (tok gid+8, 2tig+1)
       const int tb = u.k0 + 16 * s;
-      float x0 = sc0[0] * sl2, x1 = sc0[1] * sl2, x2 = sc1[0] * sl2, x3 = sc1[1] * sl2;
+      float x0 = st[0] * sl2, x1 = st[1] * sl2, x2 = st[2] * sl2, x3 = st[3] * sl2;
       if (tb + 16 > u.k1) {
-        const int t0 = tb + 2 * tig;
-        if (t0 >= u.k1) x0 = -INFINITY;
-        if (t0 + 1 >= u.k1) x1 = -INFINITY;
-        if (t0 + 8 >= u.k1) x2 = -INFINITY;
-        if (t0 + 9 >= u.k1) x3 = -INFINITY;
+        if (tb + gid >= u.k1) x0 = x1 = -INFINITY;
+        if (tb + gid + 8 >= u.k1) x2 = x3 = -INFINITY;
       }
-      float mx = fmaxf(fmaxf(x0, x1), fmaxf(x2, x3));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float m_new = fmaxf(m, mx);
-      if (m_new > m) {
-        const float alpha = ex2(m - m_new);
+      float mxA = fmaxf(x0, x2), mxB = fmaxf(x1, x3);  // column (head) max over the 16 tokens
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mxA = fmaxf(mxA, __shfl_xor_sync(0xffffffffu, mxA, off));
+        mxB = fmaxf(mxB, __shfl_xor_sync(0xffffffffu, mxB, off));
+      }
+      const float mnA = fmaxf(m, mxA), mnB = fmaxf(mB, mxB);
+      if (mnA > m) {
+        const float alpha = ex2(m - mnA);
         l *= alpha;
 #pragma unroll
-        for (int n = 0; n < 16; ++n) {
-          o[n][0] *= alpha;
-          o[n][1] *= alpha;
+        for (int md = 0; md < 8; ++md) {
+          o[md][0] *= alpha;
+          o[md][2] *= alpha;
         }
-        m = m_new;
+        m = mnA;
       }
-      const float p0 = ex2(x0 - m), p1 = ex2(x1 - m), p2 = ex2(x2 - m), p3 = ex2(x3 - m);
-      l += (p0 + p1) + (p2 + p3);
-      const uint32_t pa0 = pack_bf16(p0, p1), pa2 = pack_bf16(p2, p3);
-      // O += P V  (16 tokens x 128 dims = 16 n-tiles); V^T sub-block rows = dims (SW32)
+      if (mnB > mB) {
+        const float alpha = ex2(mB - mnB);
+        lB *= alpha;
 #pragma unroll
-      for (int n2 = 0; n2 < 8; ++n2) {
-        const int dr = 16 * n2 + (mi >> 1) * 8 + rr;
-        const uint32_t addr = stg + 4096 + dr * 32 + ((((mi & 1) ^ (dr >> 2)) & 1) << 4);
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(addr, b0, b1, b2, b3);
-        mma_bf16_16816(o[2 * n2], pa0, 0u, pa2, 0u, b0, b1);
-        mma_bf16_16816(o[2 * n2 + 1], pa0, 0u, pa2, 0u, b2, b3);
+        for (int md = 0; md < 8; ++md) {
+          o[md][1] *= alpha;
+          o[md][3] *= alpha;
+        }
+        mB = mnB;
+      }
+      const float p0 = ex2(x0 - m), p1 = ex2(x1 - mB), p2 = ex2(x2 - m), p3 = ex2(x3 - mB);
+      l += p0 + p2;
+      lB += p1 + p3;
+      // P^T as the B operand: transpose the two 8x8 (tok x head) halves in registers
+      const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1)), pb1 = movmatrix_trans(pack_bf16(p2, p3));
+      // O^T [128 d x 8 heads] += V^T [128 d x 16 tok] . P^T: A = V^T m-tile via ldmatrix
+#pragma unroll
+      for (int md = 0; md < 8; ++md) {
+        const int dr = 16 * md + (mi & 1) * 8 + rr;
+        const uint32_t addr = stg + 4096 + dr * 32 + ((((mi >> 1) ^ (dr >> 2)) & 1) << 4);
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(addr, a0, a1, a2, a3);
+        mma_bf16_16816(o[md], a0, a1, a2, a3, pb0, pb1);
       }
       // Publish the previous split unit once two stages of this one have gone by: its
       // partial stores have landed by then, so the fence costs nothing.
@@ -771,26 +790,48 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         }
       }
     }
-    l += __shfl_xor_sync(0xffffffffu, l, 1);
-    l += __shfl_xor_sync(0xffffffffu, l, 2);
     if (u.nsplit > 1) pending = u.crow * p.Hkv + u.kvh;  // published two stages into the next unit
-    if (gid < g) {
-      const float inv = 1.f / l;
-      if (u.nsplit == 1) {
-        const int h = u.kvh * g + gid;
-        __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) + (static_cast<int64_t>(h) * p.T + u.row) * kD;
 #pragma unroll
-        for (int n = 0; n < 16; ++n)
-          *reinterpret_cast<uint32_t*>(orow + n * 8 + 2 * tig) = pack_bf16(o[n][0] * inv, o[n][1] * inv);
-        if (tig == 0 && p.lse != nullptr)
-          p.lse[static_cast<int64_t>(h) * p.T + u.row] = (m + __log2f(l)) * 0.69314718055994530942f;
-      } else {
-        float* po = p.part_o + (static_cast<int64_t>(u.id) * g + gid) * kD;
+    for (int off = 4; off < 32; off <<= 1) {
+      l += __shfl_xor_sync(0xffffffffu, l, off);
+      lB += __shfl_xor_sync(0xffffffffu, lB, off);
+    }
+    const int hA = 2 * tig, hB = 2 * tig + 1;  // this lane's heads (columns of O^T)
+    const float invA = 1.f / l, invB = 1.f / lB;
+    if (u.nsplit == 1) {
+      // transpose (d, head) 8x8 blocks back to (head, d): lane (head gid) gets dims 2tig, 2tig+1
+      __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) +
+                            (static_cast<int64_t>(u.kvh * g + gid) * p.T + u.row) * kD;
 #pragma unroll
-        for (int n = 0; n < 16; ++n)
-          __stcg(reinterpret_cast<float2*>(po + n * 8 + 2 * tig), make_float2(o[n][0] * inv, o[n][1] * inv));
-        if (tig == 0)
-          __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(u.id) * g + gid) * 2), make_float2(m, l));
+      for (int md = 0; md < 8; ++md) {
+        const uint32_t lo = movmatrix_trans(pack_bf16(o[md][0] * invA, o[md][1] * invB));
+        const uint32_t hi = movmatrix_trans(pack_bf16(o[md][2] * invA, o[md][3] * invB));
+        if (gid < g) {
+          *reinterpret_cast<uint32_t*>(orow + 16 * md + 2 * tig) = lo;
+          *reinterpret_cast<uint32_t*>(orow + 16 * md + 8 + 2 * tig) = hi;
+        }
+      }
+      if (gid == 0 && p.lse != nullptr) {
+        if (hA < g) p.lse[static_cast<int64_t>(u.kvh * g + hA) * p.T + u.row] = (m + __log2f(l)) * 0.69314718055994530942f;
+        if (hB < g) p.lse[static_cast<int64_t>(u.kvh * g + hB) * p.T + u.row] = (mB + __log2f(lB)) * 0.69314718055994530942f;
+      }
+    } else {
+      float* poA = p.part_o + (static_cast<int64_t>(u.id) * g + hA) * kD;
+      float* poB = p.part_o + (static_cast<int64_t>(u.id) * g + hB) * kD;
+#pragma unroll
+      for (int md = 0; md < 8; ++md) {
+        if (hA < g) {
+          __stcg(poA + 16 * md + gid, o[md][0] * invA);
+          __stcg(poA + 16 * md + 8 + gid, o[md][2] * invA);
+        }
+        if (hB < g) {
+          __stcg(poB + 16 * md + gid, o[md][1] * invB);
+          __stcg(poB + 16 * md + 8 + gid, o[md][3] * invB);
+        }
+      }
+      if (gid == 0) {
+        if (hA < g) __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(u.id) * g + hA) * 2), make_float2(m, l));
+        if (hB < g) __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(u.id) * g + hB) * 2), make_float2(mB, lB));
       }
     }
   }

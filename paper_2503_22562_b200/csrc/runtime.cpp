@@ -835,8 +835,10 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   if (kv->cfg.dtype == NIYAMA_BF16) {
     if (kv->d != 128 || kv->g > 8)
       return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
-    p.prefill_ctas = kv->prefill_cap > 0 ? std::min(kv->prefill_cap, plan->grid) : plan->prefill_ctas;
-    NY_CUDA(launch_attention_bf16(p, plan->grid, s));
+    static const int grid_cap = std::getenv("NIYAMA_GRID_CAP") ? std::atoi(std::getenv("NIYAMA_GRID_CAP")) : 0;
+    const int grid = grid_cap > 0 ? std::min(grid_cap, plan->grid) : plan->grid;  // diagnostics knob
+    p.prefill_ctas = kv->prefill_cap > 0 ? std::min(kv->prefill_cap, grid) : std::min(plan->prefill_ctas, grid);
+    NY_CUDA(launch_attention_bf16(p, grid, s));
     ++plan->launches;
   } else {
     if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");

@@ -79,6 +79,9 @@ def gap(wl):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "l70b":
+        run(W.config4_l70b())
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "gap":
         gap(W.config2_l8b())
         gap(W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2))
