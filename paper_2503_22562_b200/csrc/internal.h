@@ -102,6 +102,8 @@ struct AttnParams {
   int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] merge queue (self-resetting)
   int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
   int32_t T, Hq, Hkv, d, B, g, R;
+  int32_t b_shift;    // log2(B) (block sizes are powers of two)
+  int32_t hkv_shift;  // log2(Hkv) when Hkv is a power of two, else -1 (divide)
   int32_t n_tiles, n_units, n_slices, n_drows, split_len;
   int32_t n_merge_rows;  // rows with nsplit > 1
   int32_t prefill_ctas;  // CTAs [0, prefill_ctas) serve prefill items first; the rest decode at once

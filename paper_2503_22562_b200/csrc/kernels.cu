@@ -297,9 +297,9 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes;
       }
       const int key = j * kBN + 16 * lane;
-      const int lb = min(key / p.B, t.nblk - 1);
+      const int lb = min(key >> p.b_shift, t.nblk - 1);
       return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes +
-             static_cast<int64_t>((key % p.B) >> 4) * 4096;
+             static_cast<int64_t>((key & (p.B - 1)) >> 4) * 4096;
     };
     int64_t next = piece_off(0);
     for (int j = 0; j < nk; ++j) {
@@ -486,6 +486,12 @@ struct UnitDesc {
   int id, tbl, row, kvh, k0, k1, nsplit, crow;
 };
 
+// x / Hkv and x % Hkv without a runtime integer division (a ~100-cycle dependent
+// sequence) whenever Hkv is a power of two.
+__device__ __forceinline__ int div_hkv(const AttnParams& p, int x) {
+  return p.hkv_shift >= 0 ? x >> p.hkv_shift : x / p.Hkv;
+}
+
 // Unit = (row, split s, kv head h); d.id = its canonical partial index ubase + s*Hkv + h.
 __device__ __forceinline__ UnitDesc make_unit(const UnitRec& r, int h) {
   UnitDesc d;
@@ -505,7 +511,7 @@ __device__ __forceinline__ UnitDesc make_unit(const UnitRec& r, int h) {
 __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc& u, int s, int phys,
                                              uint32_t stage, uint32_t bar) {
   const int tok = u.k0 + 16 * s;
-  const int sub = (tok % p.B) >> 4;  // 16-token sub-block of the block
+  const int sub = (tok & (p.B - 1)) >> 4;  // 16-token sub-block of the block
   const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + u.kvh) * p.chunk_bytes;
   const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
   mbar_expect_tx(bar, fa::kDecStage);
@@ -551,7 +557,7 @@ struct DecodeLoader {
       }
     } else if (nxt_step == 1) {
       if (nxt_id < p.n_units) {
-        const int4* rp = reinterpret_cast<const int4*>(p.uq + nxt_id / p.Hkv);
+        const int4* rp = reinterpret_cast<const int4*>(p.uq + div_hkv(p, nxt_id));
         nxt_a = __ldg(rp);
         nxt_b = __ldg(rp + 1);
         nxt_c = __ldg(rp + 2);
@@ -575,7 +581,7 @@ struct DecodeLoader {
         return;
       }
       const UnitRec rec{nxt_a.x, nxt_a.y, nxt_a.z, nxt_a.w, nxt_b.x, nxt_b.y, nxt_b.z, nxt_b.w, nxt_c.x, nxt_c.y, 0, 0};
-      cur = make_unit(rec, nxt_id % p.Hkv);
+      cur = make_unit(rec, nxt_id - div_hkv(p, nxt_id) * p.Hkv);
       phys = rec.phys0;
       ph1 = rec.phys1;
       ph2 = rec.phys2;
@@ -593,7 +599,7 @@ struct DecodeLoader {
       if (s <= 2) {
         phys = s == 1 ? ph1 : ph2;  // from the unit record
       } else {
-        const int lb_prev = (cur.k0 + 16 * (s - 1)) / p.B, lb = (cur.k0 + 16 * s) / p.B;
+        const int lb_prev = (cur.k0 + 16 * (s - 1)) >> p.b_shift, lb = (cur.k0 + 16 * s) >> p.b_shift;
         if (lb != lb_prev) phys = __ldg(p.tables + cur.tbl + lb);  // consumed by the next call
       }
     }
@@ -703,7 +709,15 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       const uint32_t slot = dec_iter % kDecStages;
       const uint32_t ph = (dec_iter / kDecStages) & 1;
       const uint32_t stg = ring + slot * kDecStage;
+      // diagnostics (p.trace, decode-only launches): warp 0 of CTA 0, first 64 stages
+      int64_t* dev = (p.trace != nullptr && p.n_tiles == 0 && blockIdx.x == 0 && warp == 0 && lane == 0 &&
+                      dec_iter < 64) ? p.trace + 8 * 160 : nullptr;
+      auto dstamp = [&](int role) {
+        if (dev != nullptr) dev[role * 64 + dec_iter] = static_cast<int64_t>(clock64());
+      };
+      dstamp(0);
       mbar_wait(bar0 + 8 * slot, ph);
+      dstamp(1);
       // S^T [16 tok x 8 heads] = K [16 tok x 128 d] . Q^T: A = K via ldmatrix (matrices
       // (tok 0-7, c), (tok 8-15, c), (tok 0-7, c+1), (tok 8-15, c+1)), B = Q fragments.
       float st[4] = {0.f, 0.f, 0.f, 0.f};
@@ -716,6 +730,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         ldsm_x4(addr, a0, a1, a2, a3);
         mma_bf16_16816(st, a0, a1, a2, a3, qa0[kk], qa2[kk]);
       }
+      dstamp(2);
       // st: (tok gid, head 2tig), (tok gid, head 2tig+1), (tok gid+8, 2tig), (tok gid+8, 2tig+1)
       const int tb = u.k0 + 16 * s;
       float x0 = st[0] * sl2, x1 = st[1] * sl2, x2 = st[2] * sl2, x3 = st[3] * sl2;
@@ -753,6 +768,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       const float p0 = ex2(x0 - m), p1 = ex2(x1 - mB), p2 = ex2(x2 - m), p3 = ex2(x3 - mB);
       l += p0 + p2;
       lB += p1 + p3;
+      dstamp(3);
       // P^T as the B operand: transpose the two 8x8 (tok x head) halves in registers
       const uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1)), pb1 = movmatrix_trans(pack_bf16(p2, p3));
       // O^T [128 d x 8 heads] += V^T [128 d x 16 tok] . P^T: A = V^T m-tile via ldmatrix
@@ -776,7 +792,9 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         p.trace[8 * blockIdx.x + 7] = static_cast<int64_t>(t);
       }
       __syncwarp();
+      dstamp(4);
       if (lane == 0) ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
+      dstamp(5);
       ++dec_iter;
       // prefetch the next unit's Q fragments once its descriptor is published
       if (!qn_valid && s + 2 >= nst) {

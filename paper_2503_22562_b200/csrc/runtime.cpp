@@ -818,6 +818,8 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.d = kv->d;
   p.B = kv->B;
   p.g = kv->g;
+  p.b_shift = __builtin_ctz(static_cast<unsigned>(kv->B));
+  p.hkv_shift = (kv->hkv & (kv->hkv - 1)) == 0 ? __builtin_ctz(static_cast<unsigned>(kv->hkv)) : -1;
   p.R = plan->R;
   p.n_tiles = plan->n_tiles;
   p.n_units = plan->n_units;
