@@ -486,6 +486,37 @@ struct UnitDesc {
   int id, tbl, row, kvh, k0, k1, nsplit, crow;
 };
 
+// Per-warp unit-descriptor ring (4 entries) and its published count live in shared
+// memory; lane 0 writes, the warp reads after __syncwarp (which orders shared
+// memory among the warp's lanes), so plain st/ld.shared suffice.
+__device__ __forceinline__ void desc_store(uint32_t ring, int k, const UnitDesc& d) {
+  const uint32_t a = ring + (k & 3) * 32;
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(d.id), "r"(d.tbl), "r"(d.row), "r"(d.kvh)
+               : "memory");
+  asm volatile("st.shared.v4.s32 [%0], {%1, %2, %3, %4};" ::"r"(a + 16), "r"(d.k0), "r"(d.k1), "r"(d.nsplit),
+               "r"(d.crow)
+               : "memory");
+}
+__device__ __forceinline__ UnitDesc desc_load(uint32_t ring, int k) {
+  const uint32_t a = ring + (k & 3) * 32;
+  UnitDesc d;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(d.id), "=r"(d.tbl), "=r"(d.row), "=r"(d.kvh) : "r"(a)
+               : "memory");
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(d.k0), "=r"(d.k1), "=r"(d.nsplit), "=r"(d.crow)
+               : "r"(a + 16)
+               : "memory");
+  return d;
+}
+__device__ __forceinline__ void count_store(uint32_t a, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ int count_load(uint32_t a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+
 // x / Hkv and x % Hkv without a runtime integer division (a ~100-cycle dependent
 // sequence) whenever Hkv is a power of two.
 __device__ __forceinline__ int div_hkv(const AttnParams& p, int x) {
@@ -542,6 +573,7 @@ struct DecodeLoader {
   int reserved;          // this warp's pre-assigned first unit (decode-first CTAs), -1 if none
   int id_base;           // ids [0, id_base) are pre-assigned; the queue counter hands out the rest
   int4 nxt_a, nxt_b, nxt_c;  // raw UnitRec of the next unit, unpacked only when it starts
+  int nd;                // descriptors published so far (lane 0's copy of the shared count)
   int ph1, ph2;          // blocks of stages 1 and 2 of cur (from its record)
   bool warm;             // initial ring fill done: the next-unit claim may proceed
   bool done;
@@ -567,17 +599,19 @@ struct DecodeLoader {
     }
     ++nxt_step;
   }
-  __device__ __forceinline__ void issue_next(const AttnParams& p, uint32_t ring, uint32_t bar0, UnitDesc* descs,
-                                             volatile int* n_desc) {
+  __device__ __forceinline__ void issue_next(const AttnParams& p, uint32_t ring, uint32_t bar0, uint32_t descs,
+                                             uint32_t n_desc) {
     using namespace fa;
     if (done) return;
     if (s == nst) {
       while (nxt_step < 2) advance(p);
-      const int k = *n_desc;
+      const int k = nd;
       if (nxt_id >= p.n_units) {
         done = true;
-        descs[k & 3].id = -1;  // end of stream
-        *n_desc = k + 1;
+        UnitDesc end{};
+        end.id = -1;  // end of stream
+        desc_store(descs, k, end);
+        count_store(n_desc, ++nd);
         return;
       }
       const UnitRec rec{nxt_a.x, nxt_a.y, nxt_a.z, nxt_a.w, nxt_b.x, nxt_b.y, nxt_b.z, nxt_b.w, nxt_c.x, nxt_c.y, 0, 0};
@@ -588,8 +622,8 @@ struct DecodeLoader {
       s = 0;
       nst = (cur.k1 - cur.k0 + 15) >> 4;
       nxt_step = 0;
-      descs[k & 3] = cur;
-      *n_desc = k + 1;
+      desc_store(descs, k, cur);
+      count_store(n_desc, ++nd);
     }
     const uint32_t slot = issued % kDecStages;
     decode_issue(p, cur, s, phys, ring + slot * kDecStage, bar0 + 8 * slot);
@@ -642,7 +676,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
 // Compute side: every lane of the warp.  Split rows write an fp32 partial
 // (m, l, o~) at index `unit id` (fire and forget); unsplit rows write O / LSE.
 __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars,
-                                                 UnitDesc* descs, volatile int* n_desc) {
+                                                 uint32_t descs, uint32_t n_desc) {
   using namespace fa;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -673,8 +707,9 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   ld.phys = 0;
   ld.warm = false;
   ld.ph1 = ld.ph2 = 0;
+  ld.nd = 0;
   if (lane == 0) {
-    *n_desc = 0;
+    count_store(n_desc, 0);
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
   }
   ld.warm = true;
@@ -685,7 +720,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   int pending = -1;  // completion counter of the last split unit, not yet published
   for (int ck = 0;; ++ck) {
     __syncwarp();
-    const UnitDesc u = descs[ck & 3];
+    const UnitDesc u = desc_load(descs, ck);
     if (u.id < 0) break;
     const int nst = (u.k1 - u.k0 + 15) >> 4;
     uint32_t qa0[8], qa2[8];
@@ -799,8 +834,8 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       // prefetch the next unit's Q fragments once its descriptor is published
       if (!qn_valid && s + 2 >= nst) {
         __syncwarp();
-        if (*n_desc > ck + 1) {
-          const UnitDesc nu = descs[(ck + 1) & 3];
+        if (count_load(n_desc) > ck + 1) {
+          const UnitDesc nu = desc_load(descs, ck + 1);
           if (nu.id >= 0) {
             load_q_frags(p, nu, gid, tig, qn0, qn2);
             qn_valid = true;
@@ -1034,8 +1069,8 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   __syncthreads();
   if (p.n_units > 0) {
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
-    volatile int* n_desc = reinterpret_cast<volatile int*>(misc + 64 + 16 * warp);
-    decode_warp_loop(p, sbase, bars, descs, n_desc);
+    const uint32_t n_desc = smem_u32(misc + 64 + 16 * warp);
+    decode_warp_loop(p, sbase, bars, smem_u32(descs), n_desc);
     if (p.n_merge_rows > 0) merge_tail(p);
   }
   uint64_t t_decode = 0;
