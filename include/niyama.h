@@ -253,8 +253,8 @@ typedef struct {
 } niyama_sample;
 typedef struct niyama_predictor niyama_predictor;
 
-/* Fit on the default grid: tau 1.0..2.5 us step 0.1 us, r_cta 30..100 GB/s
- * step 5 GB/s, BW 5.0..7.6 TB/s step 0.2 TB/s. */
+/* Fit on the default grid: tau 0.5..2.5 us step 0.1 us, r_cta 30..120 GB/s
+ * step 5 GB/s, BW 5.0..8.4 TB/s step 0.2 TB/s. */
 niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
                                    niyama_predictor** out);
 /* Fit on an explicit grid {tau_lo, tau_hi, tau_step, r_lo, r_hi, r_step,

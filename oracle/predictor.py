@@ -67,7 +67,7 @@ STEP_BYTES = 160e3
 SETUP = 2
 NFEAT = 6
 NPARAM = 9
-DEFAULT_GRID = (1.0e-6, 2.5e-6, 0.1e-6, 30e9, 100e9, 5e9, 5.0e12, 7.6e12, 0.2e12)
+DEFAULT_GRID = (0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12)
 
 
 @dataclass

@@ -18,7 +18,7 @@ BF16, F32 = 0, 1
 DEVICE_NONE = -1
 NUM_FEATURES = 6
 NUM_PARAMS = 9
-DEFAULT_FIT_GRID = (1.0e-6, 2.5e-6, 0.1e-6, 30e9, 100e9, 5e9, 5.0e12, 7.6e12, 0.2e12)
+DEFAULT_FIT_GRID = (0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12)
 
 
 class NiyamaError(RuntimeError):

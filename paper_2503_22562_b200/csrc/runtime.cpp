@@ -1156,7 +1156,7 @@ std::vector<double> grid_values(double lo, double hi, double step) {
   return v;
 }
 
-constexpr double kDefaultGrid[9] = {1.0e-6, 2.5e-6, 0.1e-6, 30e9, 100e9, 5e9, 5.0e12, 7.6e12, 0.2e12};
+constexpr double kDefaultGrid[9] = {0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12};
 
 }  // namespace
 
