@@ -3,10 +3,10 @@
 //   kv_append_kernel        a3  scatter new K/V rows into the swizzled paged pool
 //   kv_gather_kernel            read-back of a sequence (tests)
 //   hybrid_attn_bf16_kernel a4-a6  ONE persistent launch:
-//        prefill tiles  — TMA-engine bulk copies of paged K/V into SW128 smem,
-//                         S = Q K^T and O += P V on tcgen05 (accumulators in TMEM),
-//                         one softmax thread per TMEM lane (online softmax, lazy
-//                         rescale of O in TMEM);
+//        prefill tiles  — TMA-engine bulk copies of paged K/V (one per block) into
+//                         shared memory, S = Q K^T (SS) and O += P V (TS, P in TMEM)
+//                         on tcgen05, two softmax warp sets on alternate key steps
+//                         (online softmax, lazy rescale of O in TMEM);
 //        decode units   — warp-level split-KV streaming (bulk copies into a per-warp
 //                         3-stage ring, mma.sync m16n8k16 with the GQA group on M),
 //                         partials merged by log-sum-exp by the last split of a row.
@@ -38,6 +38,15 @@ __device__ __forceinline__ int vt_offset(int slot, int e, int head_dim) {
   return (slot >> 4) * (head_dim * 32) + e * 32 + ((((k >> 3) ^ (e >> 2)) & 1) << 4) + ((k & 7) << 1);
 }
 
+// Byte offset, inside a (block, kv head) chunk, of the 16-byte piece j (dims 8j..8j+7)
+// of K row `slot` in the bf16 core-matrix layout: [slot/8][piece j][slot%8][16 B].  A
+// block of B rows is B*row_bytes contiguous bytes, so one bulk copy per block lands a
+// canonical no-swizzle K-major UMMA operand (LBO 128 B between pieces, SBO 8*row_bytes
+// between 8-row groups) and ldmatrix reads 8 contiguous rows of a piece.
+__device__ __forceinline__ int k_core_offset(int slot, int j, int row_bytes) {
+  return (slot >> 3) * (row_bytes * 8) + j * 128 + ((slot & 7) << 4);
+}
+
 // One thread per 16-byte piece of a (row, kv head) vector, 32-bit index math (the
 // launcher guarantees T*Hkv*pieces < 2^31).  Source rows are dense [T][Hkv][row_bytes];
 // piece j of the K row at (block, slot) lands in panel j/8 at chunk position
@@ -61,10 +70,14 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
       const int32_t sm = __ldg(p.slot_map + r);
       const int blk = sm / p.B;
       const int slot = sm - blk * p.B;
-      const int64_t dst_off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + (j >> 3) * p.B * 128 +
-                              slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
-      *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
-      if (!p.v_t) *reinterpret_cast<uint4*>(p.pool_v + dst_off) = __ldg(reinterpret_cast<const uint4*>(p.v_new) + idx);
+      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
+      if (p.v_t) {  // bf16: K in 8x16-byte core matrices (k_core_offset)
+        *reinterpret_cast<uint4*>(p.pool_k + chunk + k_core_offset(slot, j, p.row_bytes)) = kv;
+      } else {      // f32: K and V in swizzled 128-byte panels
+        const int64_t dst_off = chunk + (j >> 3) * p.B * 128 + slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
+        *reinterpret_cast<uint4*>(p.pool_k + dst_off) = kv;
+        *reinterpret_cast<uint4*>(p.pool_v + dst_off) = __ldg(reinterpret_cast<const uint4*>(p.v_new) + idx);
+      }
     } else if (idx < nk + ng) {  // V^T: 8 tokens x one dim -> one 16-byte segment of row e
       const int k = idx - nk;
       const int e = k % d;
@@ -134,7 +147,8 @@ __global__ void kv_gather_kernel(const uint8_t* __restrict__ pool_k, const uint8
     const int64_t chunk = (blk * Hkv + h) * chunk_bytes;
     const int64_t src = chunk + static_cast<int64_t>(j >> 3) * B * 128 + slot * 128 + (((j & 7) ^ (slot & 7)) << 4);
     const int64_t dst = th * row_bytes + (static_cast<int64_t>(j) << 4);
-    *reinterpret_cast<uint4*>(k_out + dst) = *reinterpret_cast<const uint4*>(pool_k + src);
+    *reinterpret_cast<uint4*>(k_out + dst) =
+        *reinterpret_cast<const uint4*>(pool_k + (v_t ? chunk + k_core_offset(slot, j, row_bytes) : src));
     if (v_t) {
       const int d = row_bytes >> 1;
       uint32_t w[4] = {0, 0, 0, 0};
@@ -163,11 +177,12 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 
 // ===================================================== fused bf16 attention
 // CTA = 256 threads (8 warps), 1 CTA/SM, 512 TMEM columns.
-// Shared memory map (32 KB regions from the 1024-aligned base; the two operands of
-// every MMA sit in different regions, which the tensor core needs for full rate):
-//   [0,32K) Q tile | [32K,96K) K stages x2 | [96K,160K) V^T stages x2 | [160K,224K) P x2
-// Q, K, P: 2 panels x 128 rows x 128 B (SW128, K-major).  V^T stage: 8 sub-blocks of
-// [128 d][16 keys] (SW32, K-major).  TMEM: S0 [0,128), S1 [128,256), O [256,384).
+// Shared memory map (32 KB regions from the 1024-aligned base):
+//   [0,32K) Q tile | [32K,128K) K stages x3 | [128K,224K) V^T stages x3
+// Q: 2 panels x 128 rows x 128 B (SW128, K-major).  K stage: 128 rows in 8x16-byte core
+// matrices (no swizzle, K-major: LBO 128 B, SBO 2 KB), one bulk copy per paged block.
+// V^T stage: 8 sub-blocks of [128 d][16 keys] (SW32, K-major).  TMEM: S/P buffers
+// [0,128) [128,256) [256,384) (P, bf16 pairs, overwrites its S), O [384,512).
 // The decode role reuses [0, 192K) as 8 warps x 3 stages x 8 KB.
 namespace fa {
 constexpr int kD = 128;             // head dim (bf16 path)
@@ -175,11 +190,19 @@ constexpr int kBN = 128;            // keys per prefill key tile
 constexpr int kPanel = 128 * 128;   // one 64-column panel of a 128-row tile
 constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 constexpr int kQOff = 0;
-constexpr int kKOff = kTile;        // K stage s at kKOff + s * kTile
-constexpr int kVOff = 3 * kTile;    // V^T stage s at kVOff + s * kTile
-constexpr int kPOff = 5 * kTile;    // P buffer b at kPOff + b * kTile
-constexpr int kDataBytes = 7 * kTile;  // 224 KB
-constexpr int kThreads = 256;
+#ifndef NIYAMA_K_STAGES
+#define NIYAMA_K_STAGES 3
+#endif
+#ifndef NIYAMA_V_STAGES
+#define NIYAMA_V_STAGES 3
+#endif
+constexpr int kKStages = NIYAMA_K_STAGES;  // K tile ring depth
+constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
+constexpr int kSBufs = 3;                  // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
+constexpr int kKOff = kTile;                       // K stage s at kKOff + s * kTile
+constexpr int kVOff = kKOff + kKStages * kTile;    // V^T stage s at kVOff + s * kTile
+constexpr int kDataBytes = kVOff + kVStages * kTile;  // 224 KB
+constexpr int kThreads = 384;  // 12 warps: producers/MMA (0-3), softmax sets (4-7, 8-11)
 constexpr int kDecWarps = 8;
 constexpr int kDecStages = 3;
 constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
@@ -188,23 +211,26 @@ constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
 // O^T += V^T P^T per stage (heads on M would pad g to 16 rows and need 16 + 16).
 
 static_assert(kDecWarps * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
-// barrier indices (all [2]: double-buffered resources)
-constexpr int kBarKFull = 0;
-constexpr int kBarKEmpty = 2;
-constexpr int kBarVFull = 4;
-constexpr int kBarVEmpty = 6;
-constexpr int kBarSFull = 8;    // QK^T committed into S[b]
-constexpr int kBarSFree = 10;   // softmax read S[b] (128 arrivals)
-constexpr int kBarPFull = 12;   // softmax wrote P[b] (128 arrivals)
-constexpr int kBarODone = 14;   // PV from P[b] committed (P[b] free, O includes it)
-constexpr int kBarDec = 16;     // kDecWarps x kDecStages
+static_assert(kDataBytes <= 7 * kTile, "prefill buffers exceed shared memory");
+// barrier indices
+constexpr int kBarKFull = 0;                       // [kKStages]
+constexpr int kBarKEmpty = kBarKFull + kKStages;   // [kKStages]
+constexpr int kBarVFull = kBarKEmpty + kKStages;   // [kVStages]
+constexpr int kBarVEmpty = kBarVFull + kVStages;   // [kVStages]
+constexpr int kBarSFull = kBarVEmpty + kVStages;   // [kSBufs] QK^T committed into S[b]
+constexpr int kBarPFull = kBarSFull + kSBufs;      // [kSBufs] softmax wrote P over S[b] (128 arrivals)
+constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from S[b] committed (S[b] free, O includes it)
+constexpr int kBarDec = kBarODone + kSBufs;        // kDecWarps x kDecStages
 constexpr int kNumBars = kBarDec + kDecWarps * kDecStages;
+constexpr int kBarBytes = (kNumBars * 8 + 63) & ~63;  // keeps the misc area 64-byte aligned (v4 accesses)
 constexpr int kMiscBytes = 64 + kDecWarps * 16;      // tmem slot, item slot, per-warp desc counters
-constexpr int kDescBytes = kDecWarps * 4 * 40;       // per-warp 4-entry UnitDesc rings
-constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kNumBars * 8 + kMiscBytes + kDescBytes;
+constexpr int kDescBytes = kDecWarps * 4 * 40;       // per-warp 4-entry UnitDesc rings (decode);
+                                                     // the prefill softmax chain [2][128] floats (prefill)
+static_assert(kDescBytes >= 2 * 128 * 4, "softmax chain must fit");
+constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kBarBytes + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemO = 256;  // O accumulator columns [256, 384); S buffers at 0 and 128
+constexpr uint32_t kTmemO = 384;  // O accumulator columns [384, 512)
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 0);  // both operands K-major
 }  // namespace fa
@@ -217,6 +243,13 @@ __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     ev[role * 64 + j] = c;
   }
+}
+
+// Causal mask of one 64-column slice of a score row: columns e > last become -inf.
+__device__ __forceinline__ void mask_tail(uint32_t (&sr)[64], int last) {
+#pragma unroll
+  for (int e = 0; e < 64; ++e)
+    if (e > last) sr[e] = 0xff800000u;  // -inf
 }
 
 struct TileDesc {
@@ -242,15 +275,16 @@ __device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
   return d;
 }
 
-// Roles inside the 256-thread CTA: warp 0 lane 0 streams K tiles, warp 2 lane 0 V^T
-// tiles (bulk copies of pre-swizzled paged blocks), warp 1 lane 0 issues tcgen05 MMAs,
-// warps 4-7 run the softmax (thread = TMEM lane = tile row r = hh*R + i, GQA packing).
-// Pipeline per key tile j (global iteration g = it + j; buffers g % 2):
-//   MMA:     QK_{j+1} -> S[(g+1)%2] (once the softmax read S_{j-1}),  PV_j from P[g%2]
-//   softmax: S_g -> max -> exps (P in registers) -> [rare: wait PV_{j-1}, rescale O in
-//            TMEM] -> [wait PV_{j-2} done: P[g%2] free] -> P -> smem -> arrive
+// Roles inside the 384-thread CTA: warp 0 lanes < 8 stream K tiles, warp 2 lanes < 8
+// V^T tiles (bulk copies of the pre-laid-out paged blocks), warp 1 lane 0 issues the
+// tcgen05 MMAs, warps 4-7 and 8-11 run the softmax of even / odd key steps (thread =
+// TMEM lane = tile row r = hh*R + i, GQA packing).
+// Pipeline per key tile j (global iteration g = it + j; S buffer g % 3):
+//   MMA:     QK_{j+1} -> S[(g+1)%3] (once PV_{j-2} has read P from it),  PV_j (P from S[g%3])
+//   softmax: S_g -> row max -> m chain from step j-1 -> [rare: wait PV_{j-1}, rescale O
+//            in TMEM] -> exps -> P over S_g in TMEM -> arrive
 __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc& t, uint32_t sbase, uint32_t bars,
-                                             uint32_t tmem, uint32_t& kv_it, uint32_t& it) {
+                                             uint32_t tmem, float* xch, uint8_t* xch_base, uint32_t& kv_it, uint32_t& it) {
   using namespace fa;
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
@@ -287,7 +321,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     const uint8_t* pool = isK ? p.pool_k : p.pool_v;
     const uint32_t ring = sbase + (isK ? kKOff : kVOff);
     const int bar_full = isK ? kBarKFull : kBarVFull, bar_empty = isK ? kBarKEmpty : kBarVEmpty;
-    const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
+    const uint32_t nstg = isK ? kKStages : kVStages;
     const int bpt = kBN / p.B;                  // K: blocks per key step
     const int npc = isK ? bpt : kBN / 16;       // pieces per step
     auto piece_off = [&](int j) -> int64_t {    // byte offset of this lane's piece of step j
@@ -306,18 +340,19 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       const int64_t cur = next;
       next = piece_off(j + 1);
       const uint32_t k_it = kv_it + j;
-      const int st = k_it & 1;
+      const int st = k_it % nstg;
       const uint32_t full = bars + 8 * (bar_full + st);
       if (lane == 0) {
-        mbar_wait(bars + 8 * (bar_empty + st), ((k_it >> 1) & 1) ^ 1);
+        mbar_wait(bars + 8 * (bar_empty + st), ((k_it / nstg) & 1) ^ 1);
         ev_stamp(ev, isK ? 0 : 1, j);
         mbar_expect_tx(full, kTile);
       }
       __syncwarp();
       const uint32_t dst0 = ring + st * kTile;
       if (lane < npc) {
-        if (isK) {
-          for (int pn = 0; pn < 2; ++pn) bulk_g2s(dst0 + pn * kPanel + lane * seg, pool + cur + pn * seg, seg, full);
+        if (isK) {  // one copy per block: B rows x 256 B, contiguous in pool and tile
+          bulk_g2s(dst0 + lane * static_cast<uint32_t>(p.chunk_bytes), pool + cur, static_cast<uint32_t>(p.chunk_bytes),
+                   full);
         } else {
           bulk_g2s(dst0 + lane * 4096, pool + cur, 4096, full);
         }
@@ -328,103 +363,117 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       // ---------------- tcgen05 issuer (single thread, in order)
       auto qk = [&](int j) {
         const uint32_t k_it = kv_it + j, gj = it + j;
-        const int st = k_it & 1, sb = gj & 1;
-        if (gj >= 2) mbar_wait(bars + 8 * (kBarSFree + sb), ((gj >> 1) & 1) ^ 1);
-        mbar_wait(bars + 8 * (kBarKFull + st), (k_it >> 1) & 1);
+        const int st = k_it % kKStages, sb = gj % kSBufs;
+        if (gj >= kSBufs)  // PV_{j-3} has read its P from S[sb]
+          mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
+        mbar_wait(bars + 8 * (kBarKFull + st), (k_it / kKStages) & 1);
         tc_fence_after();
         ev_stamp(ev, 2, j);
         const uint32_t qa = sbase + kQOff, ka = sbase + kKOff + st * kTile;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t koff = (kk >> 2) * kPanel + (kk & 3) * 32;
-          umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), sw128_desc(ka + koff, 16, 1024), kIdescQK,
+          umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), noswz_desc(ka + kk * 256, 128, 2048), kIdescQK,
                    kk > 0);
         }
         umma_commit(bars + 8 * (kBarSFull + sb));
         umma_commit(bars + 8 * (kBarKEmpty + st));
+        ev_stamp(ev, 9, j);
       };
       qk(0);
       for (int j = 0; j < nk; ++j) {
         if (j + 1 < nk) qk(j + 1);
         const uint32_t k_it = kv_it + j, gj = it + j;
-        const int st = k_it & 1, pb = gj & 1;
-        mbar_wait(bars + 8 * (kBarPFull + pb), (gj >> 1) & 1);
-        mbar_wait(bars + 8 * (kBarVFull + st), (k_it >> 1) & 1);
+        const int st = k_it % kVStages, sb = gj % kSBufs;
+        mbar_wait(bars + 8 * (kBarPFull + sb), (gj / kSBufs) & 1);
+        mbar_wait(bars + 8 * (kBarVFull + st), (k_it / kVStages) & 1);
         tc_fence_after();
         ev_stamp(ev, 3, j);
-        const uint32_t pa = sbase + kPOff + pb * kTile, va = sbase + kVOff + st * kTile;
+        const uint32_t va = sbase + kVOff + st * kTile;
+        // O += P V: A = P (bf16, 128 rows x 16 keys per MMA) from TMEM columns
+        // [S[sb] + 8 kk, +8) (TS form), B = the V^T sub-block kk (SW32 K-major)
 #pragma unroll
-        for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint32_t poff = (kk >> 2) * kPanel + (kk & 3) * 32;
-          umma_f16(tmem + kTmemO, sw128_desc(pa + poff, 16, 1024), sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
-                   (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        umma_commit(bars + 8 * (kBarODone + pb));
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tmem + kTmemO, tmem + sb * 128 + kk * 8, sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(bars + 8 * (kBarODone + sb));
         umma_commit(bars + 8 * (kBarVEmpty + st));
       }
     }
   } else if (warp >= 4) {
-    // ---------------- softmax: this thread owns tile row r (TMEM lane r)
-    const int quarter = warp - 4;
+    // ---------------- softmax: two warp sets take alternate key steps (set = parity
+    // of the global step gj), so one set's exponentials (MUFU-bound) overlap the
+    // other's TMEM loads, row max, P stores and barrier waits.  Thread = tile row r
+    // (TMEM lane r) in both sets.  The running max is a chain: the set on step j
+    // receives m_{j-1} from the other set (shared memory + named barrier) after its
+    // own row max, decides m_j (lazy: raised only when it grows by > 8 in log2
+    // units) and passes it on.  Each set keeps its partial row sum l at the max it
+    // last used; the two are combined in the epilogue.  S is read from TMEM twice
+    // (row max, then exponentials) in 64-column halves to bound registers.
+    const int quarter = warp & 3;
+    const int set = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;
     const int hh = r / R, i = r - hh * R;
     const bool valid = i < vrows;
     const int pos = t.o + t.t0 + (valid ? i : 0);  // last visible key of this row
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-    float m_ref = -INFINITY, l = 0.f;
+    uint8_t* smem_gen = xch_base;
+    volatile float* chain = reinterpret_cast<volatile float*>(xch);  // [set][128]: m passed by that set
+    const int bar_in = 1 + 4 * set + quarter, bar_out = 1 + 4 * (set ^ 1) + quarter;
+    float m_set = -INFINITY, l = 0.f;  // this set's partial sum, expressed at max m_set
+    float m_ref = -INFINITY;           // max of the latest step this set handled
     const float sl2 = p.scale_log2;
+    const bool tracer = quarter == 0 && lane == 0;
     for (int j = 0; j < nk; ++j) {
       const uint32_t gj = it + j;
-      const int sb = gj & 1;
-      mbar_wait(bars + 8 * (kBarSFull + sb), (gj >> 1) & 1);
+      if (static_cast<int>(gj & 1) != set) continue;
+      const int sb = gj % kSBufs;
+      mbar_wait(bars + 8 * (kBarSFull + sb), (gj / kSBufs) & 1);
       tc_fence_after();
-      if (r == 0) ev_stamp(ev, 4, j);
-      uint32_t sr[kBN];
-      tmem_ld128(lane_addr + sb * 128, sr);
+      if (tracer) ev_stamp(ev, 4, j);
+#if NIYAMA_DIAG_SKIP_SOFTMAX  // timing diagnostic only: P = S bits, no softmax work (wrong results)
       tc_fence_before();
-      mbar_arrive(bars + 8 * (kBarSFree + sb));  // S[sb] may be overwritten by QK_{j+2}
-      float s[kBN];
-#pragma unroll
-      for (int e = 0; e < kBN; ++e) s[e] = __uint_as_float(sr[e]);
+      mbar_arrive(bars + 8 * (kBarPFull + sb));
+      continue;
+#endif
       const int kbase = j * kBN;
-      if (kbase + kBN - 1 > pos) {  // diagonal / tail tile: causal mask on raw scores
+      const bool diag = kbase + kBN - 1 > pos;
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t sr[64];
+        tmem_ld64(lane_addr + sb * 128 + hf * 64, sr);
+        if (diag) mask_tail(sr, pos - (kbase + hf * 64));
+        float m8[8];
 #pragma unroll
-        for (int e = 0; e < kBN; ++e)
-          if (kbase + e > pos) s[e] = -INFINITY;
+        for (int k = 0; k < 8; ++k) m8[k] = __uint_as_float(sr[k]);
+#pragma unroll
+        for (int e = 8; e < 64; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(sr[e]));
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                             fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
       }
-      float m8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) m8[k] = s[k];
-#pragma unroll
-      for (int e = 8; e < kBN; ++e) m8[e & 7] = fmaxf(m8[e & 7], s[e]);
-      const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-      const float m_new = fmaxf(m_ref, mx * sl2);
-      const bool need = m_new > m_ref + 8.0f;  // lazy rescale: p <= 2^8 otherwise
-      const float alpha = need ? ex2(m_ref - m_new) : 1.f;  // 0 on the first tile (m_ref = -inf)
-      if (need) {
-        l *= alpha;
-        m_ref = m_new;
+      float m_prev = -INFINITY;
+      if (j > 0) {  // m_{j-1} from the other set
+        named_bar_sync(bar_in, 64);
+        m_prev = chain[(set ^ 1) * 128 + r];
       }
-      if (r == 0) ev_stamp(ev, 5, j);
-      const float nm = -m_ref;
-      uint32_t pk[kBN / 2];
-      float sum0 = 0.f, sum1 = 0.f;
-      // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each.  (Moving a share of
-      // them to a polynomial on the FMA pipe was measured slower: the step is bound
-      // by the MMA pipe and issue, not by MUFU.)
-      {
-#pragma unroll
-        for (int c = 0; c < kBN / 2; ++c) {
-          const float e0 = ex2(fmaf(s[2 * c], sl2, nm)), e1 = ex2(fmaf(s[2 * c + 1], sl2, nm));
-          if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
-          pk[c] = pack_bf16(e0, e1);
-        }
+      const float m_new = fmaxf(m_prev, mx * sl2);
+      const bool need = m_new > m_prev + 8.0f;  // lazy rescale: p <= 2^8 otherwise
+      const float m_use = need ? m_new : m_prev;
+      if (j + 1 < nk) {  // pass m_j on
+        chain[set * 128 + r] = m_use;
+        named_bar_arrive(bar_out, 64);
       }
-      l += sum0 + sum1;
-      if (r == 0) ev_stamp(ev, 8, j);
+      if (m_use != m_set) {
+        l *= ex2(m_set - m_use);  // 0 while this set has no sum yet (m_set = -inf)
+        m_set = m_use;
+      }
+      m_ref = m_use;
+      if (tracer) ev_stamp(ev, 5, j);
       if (j > 0 && __any_sync(0xffffffffu, need)) {
         // rare: rescale O after PV_{j-1} (PV_j waits for our P)
-        mbar_wait(bars + 8 * (kBarODone + ((gj - 1) & 1)), ((gj - 1) >> 1) & 1);
+        const float alpha = ex2(m_prev - m_use);
+        mbar_wait(bars + 8 * (kBarODone + (gj - 1) % kSBufs), ((gj - 1) / kSBufs) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < kD / 32; ++c) {
@@ -436,29 +485,56 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         }
         tmem_wait_st();
       }
-      if (j >= 2) mbar_wait(bars + 8 * (kBarODone + sb), ((gj - 2) >> 1) & 1);  // PV_{j-2} released P[sb]
-      if (r == 0) ev_stamp(ev, 7, j);
-      const uint32_t prow = sbase + kPOff + sb * kTile + r * 128;
+      if (tracer) ev_stamp(ev, 7, j);
+      const float nm = -m_use;
+      float sum0 = 0.f, sum1 = 0.f;
+#pragma unroll 1
+      for (int hf = 0; hf < 2; ++hf) {
+        uint32_t sr[64];
+        tmem_ld64(lane_addr + sb * 128 + hf * 64, sr);
+        if (diag) mask_tail(sr, pos - (kbase + hf * 64));
+        // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each; P (bf16 pairs, even key
+        // in the low half) overwrites the consumed columns [32 hf, 32 hf + 32) of S[sb]
+        uint32_t pk[32];
 #pragma unroll
-      for (int c = 0; c < kBN / 8; ++c)
-        st_shared_v4(prow + (c >> 3) * kPanel + (((c & 7) ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                     pk[4 * c + 3]);
-      fence_proxy_async_smem();
+        for (int c = 0; c < 32; ++c) {
+          const float e0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, nm));
+          const float e1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, nm));
+          if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
+          pk[c] = pack_bf16(e0, e1);
+        }
+        tmem_st32(lane_addr + sb * 128 + hf * 32, pk);
+      }
+      l += sum0 + sum1;
+      if (tracer) ev_stamp(ev, 8, j);
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bars + 8 * (kBarPFull + sb));
-      if (r == 0) ev_stamp(ev, 6, j);
+      if (tracer) ev_stamp(ev, 6, j);
     }
-    // ---------------- epilogue: O / l -> bf16, LSE
-    mbar_wait(bars + 8 * (kBarODone + ((it + nk - 1) & 1)), ((it + nk - 1) >> 1) & 1);
+    // ---------------- epilogue: combine the sets' (l, m); O / l -> bf16 (set s writes
+    // dims [64 s, 64 s + 64)), LSE
+    mbar_wait(bars + 8 * (kBarODone + (it + nk - 1) % kSBufs), ((it + nk - 1) / kSBufs) & 1);
     tc_fence_after();
+    {
+      // every MMA of the tile has completed, so the Q tile's shared memory is free:
+      // exchange (l, m_set) of the two sets through it
+      float2* xq = reinterpret_cast<float2*>(smem_gen + kQOff);
+      xq[set * 128 + r] = make_float2(l, m_set);
+      named_bar_sync(9 + quarter, 64);
+      const float2 other = xq[(set ^ 1) * 128 + r];
+      m_ref = fmaxf(m_set, other.y);  // the max of the last step (the chain never decreases)
+      l = l * ex2(m_set - m_ref) + other.x * ex2(other.y - m_ref);
+    }
     const float inv_l = 1.f / l;
     const int h = t.kvh * g + hh;
     const int64_t trow = t.row0 + t.t0 + i;
-    uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD) * 2;
+    const uint32_t col0 = static_cast<uint32_t>(set * 64);
+    uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD + col0) * 2;
 #pragma unroll 1
-    for (int c = 0; c < kD / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t ov[32];
-      tmem_ld32(lane_addr + kTmemO + c * 32, ov);
+      tmem_ld32(lane_addr + kTmemO + col0 + c * 32, ov);
       if (valid) {
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
@@ -471,7 +547,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         }
       }
     }
-    if (valid && p.lse != nullptr)
+    if (set == 0 && valid && p.lse != nullptr)
       p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
   }
   kv_it += nk;
@@ -544,15 +620,12 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
   const int tok = u.k0 + 16 * s;
   const int sub = (tok & (p.B - 1)) >> 4;  // 16-token sub-block of the block
   const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + u.kvh) * p.chunk_bytes;
-  const uint32_t seg = static_cast<uint32_t>(p.B) * 128;
+  // Streamed once: evict-first keeps the KV stream from displacing reused lines in L2
+  // (measured: config 2 108.6 -> 102.6 us, decode-only 95.7 -> 91.3 us per launch).
+  const uint64_t pol = policy_evict_first();
   mbar_expect_tx(bar, fa::kDecStage);
-  if (seg == 2048) {  // B = 16: the K chunk is one contiguous 4 KB run
-    bulk_g2s(stage, p.pool_k + chunk, 4096, bar);
-  } else {            // 16 rows of each of the two 128-byte K panels
-    bulk_g2s(stage, p.pool_k + chunk + sub * 2048, 2048, bar);
-    bulk_g2s(stage + 2048, p.pool_k + chunk + seg + sub * 2048, 2048, bar);
-  }
-  bulk_g2s(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar);  // V^T sub-block [128 d][16 keys]
+  bulk_g2s_hint(stage, p.pool_k + chunk + sub * 4096, 4096, bar, pol);  // K: 16 rows = two 8-row core groups
+  bulk_g2s_hint(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar, pol);  // V^T sub-block [128 d][16 keys]
 }
 
 
@@ -759,8 +832,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       const int ttok = (mi & 1) * 8 + rr;
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk) {
-        const int chunk = (kk & 3) * 2 + (mi >> 1);
-        const uint32_t addr = stg + (kk >> 2) * 2048 + ttok * 128 + ((chunk ^ (ttok & 7)) << 4);
+        const uint32_t addr = stg + (ttok >> 3) * 2048 + (kk * 2 + (mi >> 1)) * 128 + ((ttok & 7) << 4);
         uint32_t a0, a1, a2, a3;
         ldsm_x4(addr, a0, a1, a2, a3);
         mma_bf16_16816(st, a0, a1, a2, a3, qa0[kk], qa2[kk]);
@@ -1020,7 +1092,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = smem_u32(smem);
   const uint32_t bars = sbase + kDataBytes;
-  uint8_t* misc = smem + kDataBytes + kNumBars * 8;
+  uint8_t* misc = smem + kDataBytes + kBarBytes;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(misc);
   volatile int* item_slot = reinterpret_cast<volatile int*>(misc + 16);
   const int tid = threadIdx.x;
@@ -1030,7 +1102,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
 
   if (tid == 0) {
     for (int b = 0; b < kBarDec; ++b)
-      mbar_init(bars + 8 * b, (b == kBarSFree || b == kBarSFree + 1 || b == kBarPFull || b == kBarPFull + 1) ? 128 : 1);
+      mbar_init(bars + 8 * b, (b >= kBarPFull && b < kBarPFull + kSBufs) ? 128 : 1);
     for (int b = kBarDec; b < kNumBars; ++b) mbar_init(bars + 8 * b, 1);
     fence_mbar_init();
   }
@@ -1058,7 +1130,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     const int item = *item_slot;
     __syncthreads();
     if (item >= p.n_tiles) break;
-    prefill_tile(p, tile_desc(p, item), sbase, bars, tmem, kv_it, it);
+    prefill_tile(p, tile_desc(p, item), sbase, bars, tmem, reinterpret_cast<float*>(misc + kMiscBytes), smem, kv_it, it);
     ++n_done_items;
   }
   uint64_t t_prefill = 0;
@@ -1067,7 +1139,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
   __syncthreads();
-  if (p.n_units > 0) {
+  if (p.n_units > 0 && warp < kDecWarps) {  // warps 8-11 only serve the prefill softmax
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     const uint32_t n_desc = smem_u32(misc + 64 + 16 * warp);
     decode_warp_loop(p, sbase, bars, smem_u32(descs), n_desc);

@@ -10,7 +10,8 @@ import torch  # noqa: E402
 import workloads as W  # noqa: E402
 from kbench import setup  # noqa: E402
 
-ROLES = ["K issue", "V issue", "QK issue", "PV issue", "S ready", "max done", "P wr w0", "P wr w1", "P wr w2", "P wr w3"]
+ROLES = ["K issue", "V issue", "QK issue", "PV issue", "S ready", "max done", "P arrive", "O waited", "exps done",
+         "QK issued"]
 
 
 def run(wl):

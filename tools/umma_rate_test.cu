@@ -26,7 +26,7 @@ __global__ void rate_kernel(long long* out, int n, int only) {
   __shared__ uint32_t tslot;
   __shared__ __align__(8) uint64_t bar;
   const int tid = threadIdx.x, warp = tid >> 5;
-  for (int i = tid; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
+  for (int i = tid; i < 150 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
   fence_proxy_async_smem();
   if (tid == 0) {
     mbar_init(smem_u32(&bar), 1);
@@ -62,6 +62,12 @@ __global__ void rate_kernel(long long* out, int n, int only) {
                    idesc, i > 0);
         else if (variant == 5)  // TS, B K-major
           umma_ts(tmem + 256, tmem + (i & 7) * 8, sw128_desc(b + (i & 3) * 32, 16, 1024), idesc, i > 0);
+        else if (variant == 8)  // SS, A SW128 K-major (P), B SW32 K-major (V^T sub-block, the kernel's PV)
+          umma_f16(tmem + 256, sw128_desc(a + (i & 3) * 32, 16, 1024), sw32_desc(b + (i & 7) * 4096, 16, 256), idesc,
+                   i > 0);
+        else if (variant == 9)  // SS, A SW128 (Q), B SW128 (K), operands 64 KB apart (the kernel's QK)
+          umma_f16(tmem + 256, sw128_desc(a + (i & 3) * 32, 16, 1024), sw128_desc(a + 65536 + (i & 3) * 32, 16, 1024),
+                   idesc, i > 0);
         else  // 7: SS, A K-major, B MN-major with 16 KB panels (128-key V tile)
           umma_f16(tmem + 256, sw128_desc(a + (i & 3) * 32, 16, 1024), sw128_desc(b + (i & 7) * 2048, 16384, 1024),
                    idesc, i > 0);
@@ -83,21 +89,21 @@ __global__ void rate_kernel(long long* out, int n, int only) {
 int main() {
   long long* d;
   cudaMalloc(&d, 128);
-  cudaFuncSetAttribute(rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int n = 1 << 16;
-  const char* names[8] = {"SS N64 B K-major", "SS N128 B K-major", "TS N128 B MN-major", "SS N128 A,B 128 rows",
+  const char* names[10] = {"SS N64 B K-major", "SS N128 B K-major", "TS N128 B MN-major", "SS N128 A,B 128 rows",
                           "SS N128 B MN-major (8K panel)", "TS N128 B K-major", "SS N256 B K-major",
-                          "SS N128 B MN-major (16K panel)"};
+                          "SS N128 B MN-major (16K panel)", "SS N128 B SW32 K-major (PV)", "SS N128 QK 64K apart"};
   const double F = 2.0 * 128 * 16;
-  const double flop[8] = {F * 64, F * 128, F * 128, F * 128, F * 128, F * 128, F * 256, F * 128};
+  const double flop[10] = {F * 64, F * 128, F * 128, F * 128, F * 128, F * 128, F * 256, F * 128, F * 128, F * 128};
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int w = 0; w < 20; ++w) rate_kernel<<<1, 128, 100 * 1024>>>(d, n, 1);  // clock warm-up
+  for (int w = 0; w < 20; ++w) rate_kernel<<<1, 128, 160 * 1024>>>(d, n, 1);  // clock warm-up
   for (int rep = 0; rep < 2; ++rep)
-    for (int v = 0; v < 8; ++v) {
+    for (int v = 0; v < 10; ++v) {
       cudaEventRecord(a);
-      rate_kernel<<<1, 128, 100 * 1024>>>(d, n, v);
+      rate_kernel<<<1, 128, 160 * 1024>>>(d, n, v);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
       float ms;
