@@ -198,7 +198,13 @@ constexpr int kQOff = 0;
 #endif
 constexpr int kKStages = NIYAMA_K_STAGES;  // K tile ring depth
 constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
-constexpr int kSBufs = 3;                  // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
+#ifndef NIYAMA_Q_TMEM
+#define NIYAMA_Q_TMEM 1
+#endif
+// Q in TMEM (QK^T as a TS MMA: only K is read from shared memory) leaves room for two S
+// buffers; Q in shared memory (SS) for three.
+constexpr bool kQTmem = NIYAMA_Q_TMEM != 0;
+constexpr int kSBufs = kQTmem ? 2 : 3;     // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
 constexpr int kKOff = kTile;                       // K stage s at kKOff + s * kTile
 constexpr int kVOff = kKOff + kKStages * kTile;    // V^T stage s at kVOff + s * kTile
 constexpr int kDataBytes = kVOff + kVStages * kTile;  // 224 KB
@@ -230,7 +236,8 @@ static_assert(kDescBytes >= 2 * 128 * 4, "softmax chain must fit");
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kBarBytes + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemO = 384;  // O accumulator columns [384, 512)
+constexpr uint32_t kTmemO = 128 * kSBufs;  // O accumulator: 128 columns after the S buffers
+constexpr uint32_t kTmemQ = kTmemO + 128;   // Q (kQTmem): 64 columns of bf16 pairs
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 0);  // both operands K-major
 }  // namespace fa
@@ -295,7 +302,32 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && it == 0) ? p.trace + 8 * 160 : nullptr;  // [10][64]
 
   // ---- Q tile: rows r = hh*R + i  <-  q[row0 + t0 + i][kvh*g + hh][:]
-  {
+  if (kQTmem) {  // TMEM lane r, columns [kTmemQ, +64): dims (2c, 2c+1) in column c
+    if (warp >= 4 && warp < 8) {
+      const int r = (warp & 3) * 32 + lane;
+      const int hh = r / R, i = r - hh * R;
+      uint32_t w[64];
+      if (i < vrows) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const uint8_t*>(p.q) +
+                                                          (((t.row0 + t.t0 + i) * static_cast<int64_t>(p.Hq) + t.kvh * g + hh) * kD) * 2);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          const uint4 v = __ldg(src + c);
+          w[4 * c] = v.x, w[4 * c + 1] = v.y, w[4 * c + 2] = v.z, w[4 * c + 3] = v.w;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 64; ++c) w[c] = 0u;
+      }
+      const uint32_t qa = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + kTmemQ;
+      tmem_st32(qa, *reinterpret_cast<uint32_t(*)[32]>(w));
+      tmem_st32(qa + 32, *reinterpret_cast<uint32_t(*)[32]>(w + 32));
+      tmem_wait_st();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  } else {
     const uint8_t* q = static_cast<const uint8_t*>(p.q);
     for (int idx = tid; idx < 128 * 16; idx += kThreads) {
       const int r = idx >> 4, j = idx & 15;
@@ -373,8 +405,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t koff = (kk >> 2) * kPanel + (kk & 3) * 32;
-          umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), noswz_desc(ka + kk * 256, 128, 2048), kIdescQK,
-                   kk > 0);
+          if (kQTmem)
+            umma_ts(tmem + sb * 128, tmem + kTmemQ + kk * 8, noswz_desc(ka + kk * 256, 128, 2048), kIdescQK, kk > 0);
+          else
+            umma_f16(tmem + sb * 128, sw128_desc(qa + koff, 16, 1024), noswz_desc(ka + kk * 256, 128, 2048),
+                     kIdescQK, kk > 0);
         }
         umma_commit(bars + 8 * (kBarSFull + sb));
         umma_commit(bars + 8 * (kBarKEmpty + st));
