@@ -8,19 +8,19 @@
 namespace niyama {
 
 // KV pool physical layout:
-//   pool[layer][K=0|V=1][block][kv_head][panel][slot][128 B]
-// A (block, kv head) chunk is block_size * head_dim * elt bytes, contiguous.
-// K: each token row (head_dim * elt bytes) is cut into 128-byte panels; inside a
-// panel the 16-byte chunk c of the row at slot s is stored at chunk position
-// c ^ (s & 7) — the tcgen05 / TMA SWIZZLE_128B pattern.  A bulk copy of any
-// 8-row-aligned run of a panel into 1024-byte aligned shared memory is
-// therefore already a canonical K-major UMMA SW128 operand for S = Q K^T.
+//   bf16: pool[layer][block][kv_head][K | V^T chunk]   (K and V^T of a block adjacent)
+//   f32:  pool[layer][K=0|V=1][block][kv_head][chunk]
+// A chunk is block_size * head_dim * elt bytes, contiguous; chunk_stride is the
+// distance between consecutive (block, kv head) chunks of K (or of V).
+// K (bf16): 8 x 16-byte core matrices — the 16-byte piece j of row s at
+// (s / 8) * 8 * row_bytes + 128 j + 16 (s % 8).  A block is one bulk copy and lands
+// as a canonical no-swizzle K-major UMMA operand (LBO 128 B, SBO 8 * row_bytes).
 // V (bf16): stored TRANSPOSED in 16-key sub-blocks: sub-block u of a chunk is
 // V^T [head_dim rows][16 keys] (32 B per row), 16-byte half c of row e at
 // c ^ ((e >> 2) & 1) — the SWIZZLE_32B pattern.  One 4 KB sub-block is a
-// canonical K-major UMMA SW32 operand (N = head_dim, K = 16 keys) for O += P V:
-// K-major operands run at full tensor rate, MN-major ones at half rate.
-// V (f32 path) keeps the row layout of K.
+// canonical K-major UMMA SW32 operand (N = head_dim, K = 16 keys) for O += P V.
+// K and V (f32 path): each token row is cut into 128-byte panels; inside a panel
+// the 16-byte piece c of the row at slot s is at position c ^ (s & 7).
 
 // Compact work list (a2 -> a4/a5).  The kernel expands item indices itself, so
 // the per-iteration H2D stays small (tables + one record per slice / decode).
@@ -100,7 +100,9 @@ struct AttnParams {
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]
   int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] merge queue (self-resetting)
-  int64_t chunk_bytes;  // bytes of one (block, kv head) chunk
+  int64_t chunk_bytes;   // bytes of one (block, kv head) chunk
+  int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks of pool_k / pool_v
+  int32_t kv_adjacent;   // 1: pool_v = pool_k + chunk_bytes (K and V^T chunks of a block adjacent)
   int32_t T, Hq, Hkv, d, B, g, R;
   int32_t b_shift;    // log2(B) (block sizes are powers of two)
   int32_t hkv_shift;  // log2(Hkv) when Hkv is a power of two, else -1 (divide)
@@ -118,6 +120,7 @@ struct AppendParams {
   const uint8_t* v_new;
   const int32_t* slot_map;  // [T] block * B + slot
   int64_t chunk_bytes;
+  int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks
   int32_t T, Hkv, row_bytes, B;
   int32_t v_t;  // 1: V stored transposed in 16-key SW32 sub-blocks (bf16 path)
   // v_t only: V^T writes are grouped — vgrp[k] = first batch row of 8 consecutive rows

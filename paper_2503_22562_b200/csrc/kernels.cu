@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
       const int32_t sm = __ldg(p.slot_map + r);
       const int blk = sm / p.B;
       const int slot = sm - blk * p.B;
-      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
+      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_stride;
       if (p.v_t) {  // bf16: K in 8x16-byte core matrices (k_core_offset)
         *reinterpret_cast<uint4*>(p.pool_k + chunk + k_core_offset(slot, j, p.row_bytes)) = kv;
       } else {      // f32: K and V in swizzled 128-byte panels
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
       const int32_t sm = __ldg(p.slot_map + r0);
       const int blk = sm / p.B;
       const int slot = sm - blk * p.B;  // 8-aligned
-      const int64_t off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes + vt_offset(slot, e, d);
+      const int64_t off = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_stride + vt_offset(slot, e, d);
       *reinterpret_cast<uint4*>(p.pool_v + off) = make_uint4(w[0], w[1], w[2], w[3]);
     } else {  // V^T element-wise: row r, dims 8j..8j+7
       const int k = idx - nk - ng;
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
       const int32_t sm = __ldg(p.slot_map + r);
       const int blk = sm / p.B;
       const int slot = sm - blk * p.B;
-      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_bytes;
+      const int64_t chunk = (static_cast<int64_t>(blk) * p.Hkv + h) * p.chunk_stride;
       const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
       for (int q = 0; q < 8; ++q)
@@ -360,11 +360,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       if (lane >= npc || j >= nk) return 0;
       if (isK) {
         const int lb = min(j * bpt + lane, t.nblk - 1);  // past the end: finite data, masked (P = 0)
-        return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes;
+        return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_stride;
       }
       const int key = j * kBN + 16 * lane;
       const int lb = min(key >> p.b_shift, t.nblk - 1);
-      return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_bytes +
+      return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_stride +
              static_cast<int64_t>((key & (p.B - 1)) >> 4) * 4096;
     };
     int64_t next = piece_off(0);
@@ -654,13 +654,17 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
                                              uint32_t stage, uint32_t bar) {
   const int tok = u.k0 + 16 * s;
   const int sub = (tok & (p.B - 1)) >> 4;  // 16-token sub-block of the block
-  const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + u.kvh) * p.chunk_bytes;
+  const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + u.kvh) * p.chunk_stride;
   // Streamed once: evict-first keeps the KV stream from displacing reused lines in L2
   // (measured: config 2 108.6 -> 102.6 us, decode-only 95.7 -> 91.3 us per launch).
   const uint64_t pol = policy_evict_first();
   mbar_expect_tx(bar, fa::kDecStage);
-  bulk_g2s_hint(stage, p.pool_k + chunk + sub * 4096, 4096, bar, pol);  // K: 16 rows = two 8-row core groups
-  bulk_g2s_hint(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar, pol);  // V^T sub-block [128 d][16 keys]
+  if (p.kv_adjacent && p.B == 16) {  // the block's K chunk and V^T chunk are one 8 KB run
+    bulk_g2s_hint(stage, p.pool_k + chunk, 8192, bar, pol);
+  } else {
+    bulk_g2s_hint(stage, p.pool_k + chunk + sub * 4096, 4096, bar, pol);  // K: 16 rows = two 8-row core groups
+    bulk_g2s_hint(stage + 4096, p.pool_v + chunk + sub * 4096, 4096, bar, pol);  // V^T sub-block [128 d][16 keys]
+  }
 }
 
 
@@ -1263,7 +1267,7 @@ __global__ void __launch_bounds__(128) hybrid_attn_generic_f32_kernel(const Attn
   for (int t = 0; t < ri.n; ++t) {
     const int64_t blk = p.tables[ri.tbl + t / p.B];
     const int slot = t % p.B;
-    const int64_t base = (blk * p.Hkv + kvh) * p.chunk_bytes + slot * 128;
+    const int64_t base = (blk * p.Hkv + kvh) * p.chunk_stride + slot * 128;
     float kv[kMaxDPerLane], vv[kMaxDPerLane];
 #pragma unroll
     for (int k = 0; k < kMaxDPerLane; ++k) {

@@ -57,6 +57,8 @@ struct niyama_kv {
   niyama_kv_config cfg{};
   int hq = 0, hkv = 0, d = 0, B = 0, elt = 0, g = 0, row_bytes = 0;
   int64_t chunk_bytes = 0;  // one (block, kv head) chunk
+  int64_t chunk_stride = 0;  // between consecutive chunks of one of K / V
+  int64_t v_offset = 0;      // V's chunk of (block, kv head) = K's + v_offset
   int64_t half_bytes = 0;   // K (or V) of one layer
   bool has_device = false;
   int num_sms = 148;
@@ -161,6 +163,11 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->row_bytes = c.head_dim * elt;
   kv->chunk_bytes = static_cast<int64_t>(c.block_size) * kv->row_bytes;
   kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
+  // bf16: a (block, kv head)'s K chunk and V^T chunk are adjacent ([layer][block][kv head][K|V]),
+  // so a decode stage of B = 16 tokens is ONE 8 KB bulk copy.  f32 (config 1): [layer][K|V][block][kv head].
+  const bool adjacent = c.dtype == NIYAMA_BF16 && !(std::getenv("NIYAMA_KV_SPLIT") && std::atoi(std::getenv("NIYAMA_KV_SPLIT")));
+  kv->chunk_stride = adjacent ? 2 * kv->chunk_bytes : kv->chunk_bytes;
+  kv->v_offset = adjacent ? kv->chunk_bytes : kv->half_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
   if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
   if (const char* td = std::getenv("NIYAMA_TAIL_DIV")) kv->tail_div = std::max(1, std::min(16, std::atoi(td)));
@@ -279,7 +286,7 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
   NY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tbl), tbl.size() * sizeof(int32_t), s));
   NY_CUDA(cudaMemcpyAsync(d_tbl, tbl.data(), tbl.size() * sizeof(int32_t), cudaMemcpyHostToDevice, s));
   const uint8_t* pk = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
-  NY_CUDA(launch_gather(pk, pk + kv->half_bytes, d_tbl, len, kv->hkv, kv->row_bytes, kv->B, kv->chunk_bytes,
+  NY_CUDA(launch_gather(pk, pk + kv->v_offset, d_tbl, len, kv->hkv, kv->row_bytes, kv->B, kv->chunk_stride,
                         kv->cfg.dtype == NIYAMA_BF16 ? 1 : 0, static_cast<uint8_t*>(k_out), static_cast<uint8_t*>(v_out),
                         s));
   NY_CUDA(cudaFreeAsync(d_tbl, s));
@@ -770,11 +777,12 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
     return fail(NIYAMA_EINVAL, "k_new/v_new must be 16-byte aligned");
   AppendParams p{};
   p.pool_k = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
-  p.pool_v = p.pool_k + kv->half_bytes;
+  p.pool_v = p.pool_k + kv->v_offset;
   p.k_new = static_cast<const uint8_t*>(k_new);
   p.v_new = static_cast<const uint8_t*>(v_new);
   p.slot_map = plan->d_slot;
   p.chunk_bytes = kv->chunk_bytes;
+  p.chunk_stride = kv->chunk_stride;
   p.T = plan->T;
   p.Hkv = kv->hkv;
   p.row_bytes = kv->row_bytes;
@@ -800,7 +808,7 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   const float scale = softmax_scale > 0.f ? softmax_scale : 1.0f / std::sqrt(static_cast<float>(kv->d));
   AttnParams p{};
   p.pool_k = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
-  p.pool_v = p.pool_k + kv->half_bytes;
+  p.pool_v = p.pool_k + kv->v_offset;
   p.q = q;
   p.o = o;
   p.lse = lse;
@@ -812,6 +820,8 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.part_ml = plan->d_part_ml;
   p.work = plan->d_work;
   p.chunk_bytes = kv->chunk_bytes;
+  p.chunk_stride = kv->chunk_stride;
+  p.kv_adjacent = kv->v_offset == kv->chunk_bytes ? 1 : 0;
   p.T = plan->T;
   p.Hq = kv->hq;
   p.Hkv = kv->hkv;
