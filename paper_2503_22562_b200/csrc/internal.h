@@ -103,6 +103,7 @@ struct AttnParams {
   int64_t chunk_bytes;   // bytes of one (block, kv head) chunk
   int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks of pool_k / pool_v
   int32_t kv_adjacent;   // 1: pool_v = pool_k + chunk_bytes (K and V^T chunks of a block adjacent)
+  int32_t dec_warps;     // bf16 decode warps per CTA: 12 (2-stage rings) or 8 (3-stage rings)
   int32_t T, Hq, Hkv, d, B, g, R;
   int32_t b_shift;    // log2(B) (block sizes are powers of two)
   int32_t hkv_shift;  // log2(Hkv) when Hkv is a power of two, else -1 (divide)

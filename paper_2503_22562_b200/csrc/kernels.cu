@@ -177,19 +177,19 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 
 // ===================================================== fused bf16 attention
 // CTA = 256 threads (8 warps), 1 CTA/SM, 512 TMEM columns.
-// Shared memory map (32 KB regions from the 1024-aligned base):
-//   [0,32K) Q tile | [32K,128K) K stages x3 | [128K,224K) V^T stages x3
-// Q: 2 panels x 128 rows x 128 B (SW128, K-major).  K stage: 128 rows in 8x16-byte core
-// matrices (no swizzle, K-major: LBO 128 B, SBO 2 KB), one bulk copy per paged block.
-// V^T stage: 8 sub-blocks of [128 d][16 keys] (SW32, K-major).  TMEM: S/P buffers
-// [0,128) [128,256) [256,384) (P, bf16 pairs, overwrites its S), O [384,512).
-// The decode role reuses [0, 192K) as 8 warps x 3 stages x 8 KB.
+// Shared memory map (from the 1024-aligned base), Q in TMEM (default):
+//   [0,96K) K stages x3 | [96K,192K) V^T stages x3 | [192K,194K) end-of-tile exchange
+// (Q in shared memory, NIYAMA_Q_TMEM=0: a 32 KB SW128 Q tile first, everything after it.)
+// K stage: 128 rows in 8x16-byte core matrices (no swizzle, K-major: LBO 128 B, SBO
+// 2 KB), one bulk copy per paged block.  V^T stage: 8 sub-blocks of [128 d][16 keys]
+// (SW32, K-major).  TMEM: S/P buffers of 128 columns (P, bf16 pairs, overwrites its
+// S), O (128 columns), Q (64 columns).
+// The decode role reuses [0, 192K) as per-warp rings of 8 KB stages.
 namespace fa {
 constexpr int kD = 128;             // head dim (bf16 path)
 constexpr int kBN = 128;            // keys per prefill key tile
 constexpr int kPanel = 128 * 128;   // one 64-column panel of a 128-row tile
 constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
-constexpr int kQOff = 0;
 #ifndef NIYAMA_K_STAGES
 #define NIYAMA_K_STAGES 3
 #endif
@@ -205,19 +205,26 @@ constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
 // buffers; Q in shared memory (SS) for three.
 constexpr bool kQTmem = NIYAMA_Q_TMEM != 0;
 constexpr int kSBufs = kQTmem ? 2 : 3;     // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
-constexpr int kKOff = kTile;                       // K stage s at kKOff + s * kTile
+// Q staging tile (SS only) | K stages | V^T stages | end-of-tile exchange (2 KB; the Q
+// tile's space when Q is staged in shared memory)
+constexpr int kQOff = 0;
+constexpr int kKOff = kQTmem ? 0 : kTile;          // K stage s at kKOff + s * kTile
 constexpr int kVOff = kKOff + kKStages * kTile;    // V^T stage s at kVOff + s * kTile
-constexpr int kDataBytes = kVOff + kVStages * kTile;  // 224 KB
+constexpr int kXOff = kQTmem ? kVOff + kVStages * kTile : kQOff;
+constexpr int kPrefillBytes = kQTmem ? kXOff + 2048 : kVOff + kVStages * kTile;
 constexpr int kThreads = 384;  // 12 warps: producers/MMA (0-3), softmax sets (4-7, 8-11)
-constexpr int kDecWarps = 8;
-constexpr int kDecStages = 3;
+// Decode: warps [0, p.dec_warps) stream units through per-warp rings of kDecSlots /
+// dec_warps stages: 8 warps x 3 stages (g = 8: more work per byte, deeper rings) or 12 x 2
+// (g <= 4: more warps in flight per SM).
+constexpr int kDecSlots = 24;    // 8 KB stage slots shared by the rings (192 KB)
+constexpr int kDecWarps = 12;    // the most decode warps per CTA
 constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
 // Decode math: the 16 tokens of a stage on the MMA M dimension and the g <= 8 heads
 // of the group on N (mma.sync m16n8k16, "swap-AB"): 8 MMAs for S^T = K Q^T and 8 for
 // O^T += V^T P^T per stage (heads on M would pad g to 16 rows and need 16 + 16).
 
-static_assert(kDecWarps * kDecStages * kDecStage <= kDataBytes, "decode ring must fit");
-static_assert(kDataBytes <= 7 * kTile, "prefill buffers exceed shared memory");
+constexpr int kDataBytes = kPrefillBytes > kDecSlots * kDecStage ? kPrefillBytes : kDecSlots * kDecStage;
+static_assert(kDecWarps <= kThreads / 32, "decode warps");
 // barrier indices
 constexpr int kBarKFull = 0;                       // [kKStages]
 constexpr int kBarKEmpty = kBarKFull + kKStages;   // [kKStages]
@@ -226,11 +233,11 @@ constexpr int kBarVEmpty = kBarVFull + kVStages;   // [kVStages]
 constexpr int kBarSFull = kBarVEmpty + kVStages;   // [kSBufs] QK^T committed into S[b]
 constexpr int kBarPFull = kBarSFull + kSBufs;      // [kSBufs] softmax wrote P over S[b] (128 arrivals)
 constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from S[b] committed (S[b] free, O includes it)
-constexpr int kBarDec = kBarODone + kSBufs;        // kDecWarps x kDecStages
-constexpr int kNumBars = kBarDec + kDecWarps * kDecStages;
+constexpr int kBarDec = kBarODone + kSBufs;        // [kDecSlots] decode ring stages
+constexpr int kNumBars = kBarDec + kDecSlots;
 constexpr int kBarBytes = (kNumBars * 8 + 63) & ~63;  // keeps the misc area 64-byte aligned (v4 accesses)
 constexpr int kMiscBytes = 64 + kDecWarps * 16;      // tmem slot, item slot, per-warp desc counters
-constexpr int kDescBytes = kDecWarps * 4 * 40;       // per-warp 4-entry UnitDesc rings (decode);
+constexpr int kDescBytes = kDecWarps * 4 * 32;       // per-warp 4-entry UnitDesc rings (decode);
                                                      // the prefill softmax chain [2][128] floats (prefill)
 static_assert(kDescBytes >= 2 * 128 * 4, "softmax chain must fit");
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kBarBytes + kMiscBytes + kDescBytes;
@@ -554,7 +561,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     {
       // every MMA of the tile has completed, so the Q tile's shared memory is free:
       // exchange (l, m_set) of the two sets through it
-      float2* xq = reinterpret_cast<float2*>(smem_gen + kQOff);
+      float2* xq = reinterpret_cast<float2*>(smem_gen + kXOff);
       xq[set * 128 + r] = make_float2(l, m_set);
       named_bar_sync(9 + quarter, 64);
       const float2 other = xq[(set ^ 1) * 128 + r];
@@ -677,6 +684,7 @@ __device__ __forceinline__ void decode_issue(const AttnParams& p, const UnitDesc
 // row index -> row record -> descriptor + first block), so lane 0 never waits on
 // memory in the issue path.  Each new unit's descriptor is published to the
 // compute lanes through a 4-entry per-warp ring in shared memory (+ a counter).
+template <int kDecStages>
 struct DecodeLoader {
   UnitDesc cur;
   int s, nst;
@@ -787,6 +795,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
 
 // Compute side: every lane of the warp.  Split rows write an fp32 partial
 // (m, l, o~) at index `unit id` (fire and forget); unsplit rows write O / LSE.
+template <int kDecWarpsT, int kDecStages>
 __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars,
                                                  uint32_t descs, uint32_t n_desc) {
   using namespace fa;
@@ -800,7 +809,7 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   const float sl2 = p.scale_log2;
   const int mi = lane >> 3, rr = lane & 7;
 
-  DecodeLoader ld;
+  DecodeLoader<kDecStages> ld;
   ld.s = ld.nst = 0;
   ld.nxt_step = 0;
   ld.nxt_id = 0;
@@ -809,9 +818,9 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
     // the first claim is a plain load instead of an atomic; prefill-first CTAs and
     // every later claim use the queue counter.
     const int dec_first = p.n_tiles > 0 ? p.prefill_ctas : 0;
-    ld.id_base = (static_cast<int>(gridDim.x) - dec_first) * kDecWarps;
+    ld.id_base = (static_cast<int>(gridDim.x) - dec_first) * kDecWarpsT;
     ld.reserved = static_cast<int>(blockIdx.x) >= dec_first
-                      ? (static_cast<int>(blockIdx.x) - dec_first) * kDecWarps + warp
+                      ? (static_cast<int>(blockIdx.x) - dec_first) * kDecWarpsT + warp
                       : -1;
   }
   ld.done = false;
@@ -1178,10 +1187,13 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
   __syncthreads();
-  if (p.n_units > 0 && warp < kDecWarps) {  // warps 8-11 only serve the prefill softmax
+  if (p.n_units > 0 && warp < p.dec_warps) {  // the other warps only serve the prefill softmax
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     const uint32_t n_desc = smem_u32(misc + 64 + 16 * warp);
-    decode_warp_loop(p, sbase, bars, smem_u32(descs), n_desc);
+    if (p.dec_warps == 12)
+      decode_warp_loop<12, 2>(p, sbase, bars, smem_u32(descs), n_desc);
+    else
+      decode_warp_loop<8, 3>(p, sbase, bars, smem_u32(descs), n_desc);
     if (p.n_merge_rows > 0) merge_tail(p);
   }
   uint64_t t_decode = 0;

@@ -59,6 +59,7 @@ struct niyama_kv {
   int64_t chunk_bytes = 0;  // one (block, kv head) chunk
   int64_t chunk_stride = 0;  // between consecutive chunks of one of K / V
   int64_t v_offset = 0;      // V's chunk of (block, kv head) = K's + v_offset
+  int32_t dec_warps_override = 0;  // NIYAMA_DEC_WARPS (A/B experiments): 8 or 12, 0 = by g
   int64_t half_bytes = 0;   // K (or V) of one layer
   bool has_device = false;
   int num_sms = 148;
@@ -170,6 +171,7 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->v_offset = adjacent ? kv->chunk_bytes : kv->half_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
   if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
+  if (const char* dw = std::getenv("NIYAMA_DEC_WARPS")) kv->dec_warps_override = std::atoi(dw) == 12 ? 12 : 8;
   if (const char* td = std::getenv("NIYAMA_TAIL_DIV")) kv->tail_div = std::max(1, std::min(16, std::atoi(td)));
   if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
     const int v = std::atoi(sl);
@@ -822,6 +824,10 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.chunk_bytes = kv->chunk_bytes;
   p.chunk_stride = kv->chunk_stride;
   p.kv_adjacent = kv->v_offset == kv->chunk_bytes ? 1 : 0;
+  // g <= 4: 12 decode warps x 2-stage rings; g = 8 (twice the MMA work per byte): 8 x 3
+  // (measured: config 2 102.6 -> 99.4 us with 12; config 4 1180 -> 1218 us with 12)
+  p.dec_warps = kv->g <= 4 ? 12 : 8;
+  if (kv->dec_warps_override) p.dec_warps = kv->dec_warps_override;
   p.T = plan->T;
   p.Hq = kv->hq;
   p.Hkv = kv->hkv;
