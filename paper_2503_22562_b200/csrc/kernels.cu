@@ -177,13 +177,15 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 
 // ===================================================== fused bf16 attention
 // CTA = 256 threads (8 warps), 1 CTA/SM, 512 TMEM columns.
-// Shared memory map (from the 1024-aligned base), Q in TMEM (default):
-//   [0,96K) K stages x3 | [96K,192K) V^T stages x3 | [192K,194K) end-of-tile exchange
-// (Q in shared memory, NIYAMA_Q_TMEM=0: a 32 KB SW128 Q tile first, everything after it.)
+// Shared memory map (from the 1024-aligned base), default (Q in shared memory):
+//   [0,32K) Q tile (SW128; also the end-of-tile exchange) | [32K,128K) K stages x3 |
+//   [128K,192K) V^T stages x2
+// (NIYAMA_Q_TMEM=1: Q in TMEM, no Q tile; two S buffers instead of three — measured
+// slower, the S-buffer reuse then sits in every other step's dependency cycle.)
 // K stage: 128 rows in 8x16-byte core matrices (no swizzle, K-major: LBO 128 B, SBO
 // 2 KB), one bulk copy per paged block.  V^T stage: 8 sub-blocks of [128 d][16 keys]
 // (SW32, K-major).  TMEM: S/P buffers of 128 columns (P, bf16 pairs, overwrites its
-// S), O (128 columns), Q (64 columns).
+// S), O (128 columns) [, Q (64 columns)].
 // The decode role reuses [0, 192K) as per-warp rings of 8 KB stages.
 namespace fa {
 constexpr int kD = 128;             // head dim (bf16 path)
@@ -194,15 +196,17 @@ constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 #define NIYAMA_K_STAGES 3
 #endif
 #ifndef NIYAMA_V_STAGES
-#define NIYAMA_V_STAGES 3
+#define NIYAMA_V_STAGES 2
 #endif
 constexpr int kKStages = NIYAMA_K_STAGES;  // K tile ring depth
 constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
 #ifndef NIYAMA_Q_TMEM
-#define NIYAMA_Q_TMEM 1
+#define NIYAMA_Q_TMEM 0
 #endif
 // Q in TMEM (QK^T as a TS MMA: only K is read from shared memory) leaves room for two S
-// buffers; Q in shared memory (SS) for three.
+// buffers; Q in shared memory (SS) for three.  Three win: with two, QK(j+2) waits for
+// PV(j) to complete, putting two MMA-burst latencies (~0.7 K cycles each) and a softmax
+// into every two steps (L70B prefill-only 556 -> 440 us with three).
 constexpr bool kQTmem = NIYAMA_Q_TMEM != 0;
 constexpr int kSBufs = kQTmem ? 2 : 3;     // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
 // Q staging tile (SS only) | K stages | V^T stages | end-of-tile exchange (2 KB; the Q
@@ -210,8 +214,8 @@ constexpr int kSBufs = kQTmem ? 2 : 3;     // S (then P) TMEM buffers: columns [
 constexpr int kQOff = 0;
 constexpr int kKOff = kQTmem ? 0 : kTile;          // K stage s at kKOff + s * kTile
 constexpr int kVOff = kKOff + kKStages * kTile;    // V^T stage s at kVOff + s * kTile
-constexpr int kXOff = kQTmem ? kVOff + kVStages * kTile : kQOff;
-constexpr int kPrefillBytes = kQTmem ? kXOff + 2048 : kVOff + kVStages * kTile;
+constexpr int kXOff = kVOff + kVStages * kTile;  // 2 KB of its own (the Q tile stays intact)
+constexpr int kPrefillBytes = kXOff + 2048;
 constexpr int kThreads = 384;  // 12 warps: producers/MMA (0-3), softmax sets (4-7, 8-11)
 // Decode: warps [0, p.dec_warps) stream units through per-warp rings of kDecSlots /
 // dec_warps stages: 8 warps x 3 stages (g = 8: more work per byte, deeper rings) or 12 x 2
@@ -399,11 +403,14 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- tcgen05 issuer (single thread, in order)
-      auto qk = [&](int j) {
+      // ---------------- QK^T issuer.  Issuing blocks while earlier MMAs execute (the
+      // tensor pipe's queue is a few MMAs deep; a burst of 8 takes ~0.7 K cycles,
+      // tools/umma_issue_test.cu), so QK^T and PV have an issuing thread each: neither
+      // stream's readiness waits behind the other's issue.
+      for (int j = 0; j < nk; ++j) {
         const uint32_t k_it = kv_it + j, gj = it + j;
         const int st = k_it % kKStages, sb = gj % kSBufs;
-        if (gj >= kSBufs)  // PV_{j-3} has read its P from S[sb]
+        if (gj >= kSBufs)  // PV_{j-kSBufs} has read its P from S[sb]
           mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
         mbar_wait(bars + 8 * (kBarKFull + st), (k_it / kKStages) & 1);
         tc_fence_after();
@@ -421,10 +428,12 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         umma_commit(bars + 8 * (kBarSFull + sb));
         umma_commit(bars + 8 * (kBarKEmpty + st));
         ev_stamp(ev, 9, j);
-      };
-      qk(0);
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ---------------- PV issuer
       for (int j = 0; j < nk; ++j) {
-        if (j + 1 < nk) qk(j + 1);
         const uint32_t k_it = kv_it + j, gj = it + j;
         const int st = k_it % kVStages, sb = gj % kSBufs;
         mbar_wait(bars + 8 * (kBarPFull + sb), (gj / kSBufs) & 1);
