@@ -240,6 +240,10 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
 #define NIYAMA_PRED_SMS 148
 #define NIYAMA_TAIL_DIV 4
 #define NIYAMA_STEP_BYTES 160e3
+/* CTA split: decode KV bytes weigh this much more when g = Hq/Hkv > 4 (the launch then
+ * streams decode with 8 warps per CTA instead of 12, so a CTA moves fewer bytes per
+ * unit time; config 4 measured 1,073 us at the unweighted split, 926 us at 80 CTAs). */
+#define NIYAMA_WIDE_GROUP_DECODE_WEIGHT 1.8
 #define NIYAMA_TILE_SETUP_STEPS 2
 #define NIYAMA_NUM_PARAMS 9
 #define NIYAMA_NUM_FEATURES 6

@@ -23,8 +23,10 @@ fix the model, written out here step by step:
      units = Hkv * sum over rows of the piece count.
   3. grid = max(1, min(NSM, tiles + ceil(units/8))); prefill CTAs n_p = 0
      without tiles, = grid without units, else ceil(grid*wp/(wp+wd)) with
-     wp = (sum of tile costs) * STEP_BYTES and wd = sumL*Hkv*d*2*e, raised to
-     ceil(tiles/4), then capped at tiles and at grid, and at least 1.
+     wp = (sum of tile costs) * STEP_BYTES and wd = sumL*Hkv*d*2*e (times
+     WIDE_GROUP_DECODE_WEIGHT when g = Hq/Hkv > 4), raised to
+     min(ceil(tiles/4), ceil(grid/2)), then capped at tiles and at grid, and at
+     least 1.
   4. list scheduling: each tile in queue order goes to the prefill CTA that
      frees first; f_1 <= ... <= f_np the finish times (in steps).
   5. fluid decode: B_d = sumL*Hkv*d*2*e bytes stream at min(BW, k*r_cta),
@@ -64,6 +66,7 @@ from scipy.optimize import nnls
 NSM = 148
 TAIL_DIV = 4
 STEP_BYTES = 160e3
+WIDE_GROUP_DECODE_WEIGHT = 1.8   # include/niyama.h NIYAMA_WIDE_GROUP_DECODE_WEIGHT
 SETUP = 2
 NFEAT = 6
 NPARAM = 9
@@ -136,8 +139,10 @@ def cta_split(n_tiles: int, n_units: int, tile_cost: int, sum_ctx: int, shape: P
         return grid, grid
     wp = float(tile_cost) * STEP_BYTES
     wd = float(sum_ctx) * shape.num_kv_heads * shape.head_dim * 2.0 * shape.elt_bytes
+    if shape.num_q_heads // shape.num_kv_heads > 4:   # 8 decode warps per CTA instead of 12
+        wd *= WIDE_GROUP_DECODE_WEIGHT
     n_p = math.ceil(grid * wp / (wp + wd))
-    n_p = max(n_p, cdiv(n_tiles, 4))
+    n_p = max(n_p, min(cdiv(n_tiles, 4), cdiv(grid, 2)))
     n_p = min(n_p, n_tiles, grid)
     return grid, max(1, n_p)
 

@@ -327,7 +327,7 @@ struct CtaSplit {
   int32_t grid, prefill_ctas;
 };
 CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv, int d, int elt,
-                   int num_sms) {
+                   int g, int num_sms) {
   CtaSplit r{};
   r.grid = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div(n_units, 8))));
   if (n_tiles == 0) return r;
@@ -336,9 +336,12 @@ CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t 
     return r;
   }
   const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
-  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt;
+  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt * (g > 4 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
   int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
-  np = std::max<int64_t>(np, ceil_div(n_tiles, 4));  // a tile-count floor keeps prefill off the tail
+  // a tile-count floor keeps short-tile prefill off the tail (at most 4 tiles per prefill
+  // CTA), itself capped at half the grid: with many long tiles (config 4: 1,024) it would
+  // put every CTA on prefill first (measured 1,073 us vs 926 us at 80 prefill CTAs)
+  np = std::max<int64_t>(np, std::min<int64_t>(ceil_div(n_tiles, 4), ceil_div(r.grid, 2)));
   np = std::min<int64_t>({np, n_tiles, static_cast<int64_t>(r.grid)});
   r.prefill_ctas = static_cast<int32_t>(std::max<int64_t>(1, np));
   return r;
@@ -346,7 +349,7 @@ CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t 
 
 void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
   const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_tiles,
-                               pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->num_sms);
+                               pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->g, kv->num_sms);
   pl->grid = r.grid;
   pl->prefill_ctas = r.prefill_ctas;
 }
@@ -971,7 +974,7 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   r.sum_ctx = static_cast<double>(sum_ctx);
   r.Bd = static_cast<double>(sum_ctx) * p.hkv * p.d * 2.0 * p.elt;
   // 3. CTA split (the planner's rule)
-  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, NIYAMA_PRED_SMS);
+  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, p.hq / p.hkv, NIYAMA_PRED_SMS);
   r.grid = cs.grid;
   r.np = cs.prefill_ctas;
   // 4. list scheduling of the queue on the prefill CTAs.  Each tile goes to a CTA

@@ -118,6 +118,13 @@ def test_split_len_and_cta_split_hand_worked():
     # wp = 2074*160e3, wd = 133674*4096 -> 148 * 0.3768 = 55.8 -> 56 (floor 32)
     assert P.cta_split(128, 600, 2074, 133674, SHAPE) == (148, 56)
     assert P.cta_split(128, 600, 10, 133674, SHAPE) == (148, 32)   # tile-count floor ceil(128/4)
+    # g = 8 (8 decode warps per CTA): wd weighs 1.8x -> wp = 331.84e6, wd = 985.55e6,
+    # 148 * 0.25188 = 37.28 -> 38
+    shape8 = P.PredShape(num_q_heads=64, num_kv_heads=8, head_dim=128, elt_bytes=2)
+    assert P.cta_split(128, 600, 2074, 133674, shape8) == (148, 38)
+    # config 4: wp = 59904*160e3 = 9.585e9, wd = 1048576*4096*1.8 = 7.731e9 -> 148 * 0.5535
+    # = 81.9 -> 82; the floor is min(ceil(1024/4), ceil(148/2)) = 74
+    assert P.cta_split(1024, 7168, 59904, 1048576, shape8) == (148, 82)
 
 
 def test_fluid_decode_closed_forms():
