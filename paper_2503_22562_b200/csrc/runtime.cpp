@@ -86,6 +86,7 @@ struct niyama_kv {
   int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
   int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
   int32_t tail_div = NIYAMA_TAIL_DIV;  // NIYAMA_TAIL_DIV env (tuning knob): last piece of a row in q/tail_div units
+  int32_t tail_min = 256;              // NIYAMA_TAIL_MIN env (tuning knob): floor of those pieces
 };
 
 struct niyama_plan {
@@ -173,6 +174,7 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
   if (const char* dw = std::getenv("NIYAMA_DEC_WARPS")) kv->dec_warps_override = std::atoi(dw) == 12 ? 12 : 8;
   if (const char* td = std::getenv("NIYAMA_TAIL_DIV")) kv->tail_div = std::max(1, std::min(16, std::atoi(td)));
+  if (const char* tm = std::getenv("NIYAMA_TAIL_MIN")) kv->tail_min = std::max(16, (std::atoi(tm) / 16) * 16);
   if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
     const int v = std::atoi(sl);
     if (v >= 16 && v % 16 == 0) kv->split_override = v;
@@ -564,7 +566,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     // short units and the warps run dry together.  Boundaries depend only on the
     // row's ctx and batch totals (deterministic results).
     const int32_t q = pl->split_len;
-    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(256, q / kv->tail_div));
+    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(kv->tail_min, q / kv->tail_div));
     auto n_full_of = [&](int32_t L) { return static_cast<int32_t>(ceil_div(L, q)) - 1; };
     int32_t ubase = 0;
     pl->drows.reserve(D);

@@ -105,6 +105,15 @@ def test_config2_l8b_full_size_sampled():
     run_and_compare(wl, rows=rows)
 
 
+def test_config4_l70b_full_size_sampled():
+    """Config 4 (Llama-3-70B heads, g = 8: 2048-token chunk at o = 6144 + 128 decodes at
+    ctx 8192) at full size in the launch configuration bench.py times (CTA split, 8
+    decode warps, split length 2048); checked on tile-edge prefill rows and decode rows."""
+    wl = W.config4_l70b()
+    rows = [0, 15, 16, 17, 1023, 1024, 2032, 2047, 2048, 2049, 2111, 2175]
+    run_and_compare(wl, rows=rows)
+
+
 def test_deterministic_and_tier_invariant():
     wl = W.random_hybrid(W.L8B, seed=21, num_prefill=2, max_chunk=300, num_decode=12, max_ctx=3000)
     r = Run(wl)
