@@ -20,6 +20,7 @@
  *   a2 niyama_plan_create                                (host planner)
  *   a3 niyama_kv_append                                  (scatter kernel)
  *   a4-a6 niyama_hybrid_attention                        (ONE fused launch)
+ *   a3-a6 niyama_append_attention                        (append + attention, ONE launch)
  *   a7 niyama_comm_init + niyama_allgather_heads         (NCCL over NVLink)
  *   a8 niyama_predictor_fit + niyama_predict_iter_time   (host, fp64)
  *
@@ -186,6 +187,17 @@ niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t l
  * T = 0 is a no-op. */
 niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q,
                                       void* o, float* lse, float softmax_scale, niyama_stream stream);
+
+/* a3 + a4-a6 in ONE launch: the result of niyama_kv_append followed by
+ * niyama_hybrid_attention (same arguments, same layouts, same outputs).  bf16:
+ * the attention launch scatters k_new / v_new into the pool itself before any
+ * tile or decode unit reads it (CTAs claim append pieces from a queue, every
+ * CTA waits for the completion count, which needs no co-residency because all
+ * pieces are claimed by running CTAs) — one launch per layer instead of two.
+ * f32: the two launches.  Errors as the two calls. */
+niyama_status niyama_append_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
+                                      const void* v_new, const void* q, void* o, float* lse, float softmax_scale,
+                                      niyama_stream stream);
 
 /* Diagnostics: when device_buf (DEVICE, int64, >= 160*8 + 10*64 entries,
  * zeroed by the caller) is non-NULL every later niyama_hybrid_attention

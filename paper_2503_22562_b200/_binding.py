@@ -85,6 +85,7 @@ def _load():
         "niyama_plan_slots": ([vp, C.POINTER(i32), C.POINTER(i32), i32], st),
         "niyama_kv_append": ([vp, vp, i32, vp, vp, vp], st),
         "niyama_hybrid_attention": ([vp, vp, i32, vp, vp, vp, C.c_float, vp], st),
+        "niyama_append_attention": ([vp, vp, i32, vp, vp, vp, vp, vp, C.c_float, vp], st),
         "niyama_debug_trace": ([vp, vp], st),
         "niyama_comm_init": ([vp, vp], st),
         "niyama_get_unique_id": ([vp], st),
@@ -257,6 +258,11 @@ class KVCache:
     def attention(self, plan: Plan, layer: int, q, o, lse=None, scale: float = 0.0, stream=None):
         _check(lib.niyama_hybrid_attention(self.handle, plan.handle, layer, _ptr(q), _ptr(o), _ptr(lse),
                                            float(scale), _stream(stream)))
+
+    def append_attention(self, plan: Plan, layer: int, k_new, v_new, q, o, lse=None, scale: float = 0.0,
+                         stream=None):
+        _check(lib.niyama_append_attention(self.handle, plan.handle, layer, _ptr(k_new), _ptr(v_new), _ptr(q),
+                                           _ptr(o), _ptr(lse), float(scale), _stream(stream)))
 
     def gather(self, layer: int, seq: int, n: int, k_out, v_out, stream=None):
         _check(lib.niyama_kv_gather(self.handle, layer, int(seq), n, _ptr(k_out), _ptr(v_out), _stream(stream)))

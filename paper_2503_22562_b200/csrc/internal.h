@@ -83,6 +83,24 @@ struct RowInfo {
   int32_t n;  // visible keys
 };
 
+struct AppendParams {
+  uint8_t* pool_k;
+  uint8_t* pool_v;
+  const uint8_t* k_new;
+  const uint8_t* v_new;
+  const int32_t* slot_map;  // [T] block * B + slot
+  int64_t chunk_bytes;
+  int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks
+  int32_t T, Hkv, row_bytes, B;
+  int32_t v_t;  // 1: V stored transposed in 16-key SW32 sub-blocks (bf16 path)
+  // v_t only: V^T writes are grouped — vgrp[k] = first batch row of 8 consecutive rows
+  // whose positions form one 8-aligned half of a 16-key sub-block (written as one 16-byte
+  // V^T row segment per dim); velem[k] = every other row (element-wise 2-byte writes).
+  const int32_t* vgrp;
+  const int32_t* velem;
+  int32_t n_grp, n_elem;
+};
+
 struct AttnParams {
   const uint8_t* pool_k;  // layer base of K
   const uint8_t* pool_v;  // layer base of V
@@ -112,25 +130,12 @@ struct AttnParams {
   int32_t prefill_ctas;  // CTAs [0, prefill_ctas) serve prefill items first; the rest decode at once
   int64_t* trace;  // optional per-CTA timeline [grid][4] (globaltimer ns), nullptr = off
   float scale_log2;     // softmax scale * log2(e)
+  // niyama_append_attention: the KV append of this batch runs inside the launch
+  // (append_total > 0 pieces, claimed through work[4], completion counted in work[5])
+  AppendParams ap;
+  int32_t append_total;
 };
 
-struct AppendParams {
-  uint8_t* pool_k;
-  uint8_t* pool_v;
-  const uint8_t* k_new;
-  const uint8_t* v_new;
-  const int32_t* slot_map;  // [T] block * B + slot
-  int64_t chunk_bytes;
-  int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks
-  int32_t T, Hkv, row_bytes, B;
-  int32_t v_t;  // 1: V stored transposed in 16-key SW32 sub-blocks (bf16 path)
-  // v_t only: V^T writes are grouped — vgrp[k] = first batch row of 8 consecutive rows
-  // whose positions form one 8-aligned half of a 16-key sub-block (written as one 16-byte
-  // V^T row segment per dim); velem[k] = every other row (element-wise 2-byte writes).
-  const int32_t* vgrp;
-  const int32_t* velem;
-  int32_t n_grp, n_elem;
-};
 
 // Launchers (kernels.cu).  Return cudaSuccess or the launch error.
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s);

@@ -51,16 +51,20 @@ __device__ __forceinline__ int k_core_offset(int slot, int j, int row_bytes) {
 // launcher guarantees T*Hkv*pieces < 2^31).  Source rows are dense [T][Hkv][row_bytes];
 // piece j of the K row at (block, slot) lands in panel j/8 at chunk position
 // (j%8) ^ (slot%8).  V pieces go to the same place (f32) or are scattered element by
-// element into the transposed sub-block (bf16, v_t).
-__global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
-  grid_dep_launch();  // the attention launch that follows may start its prologue
+// element into the transposed sub-block (bf16, v_t).  Piece order: K pieces, then V^T
+// 8-token segments, then element-wise V^T pieces.
+__device__ __forceinline__ int append_total(const AppendParams& p) {
+  const int pieces = p.row_bytes >> 4;
+  const int d = p.row_bytes >> 1;
+  return p.T * p.Hkv * pieces + (p.v_t ? p.n_grp * p.Hkv * d + p.n_elem * p.Hkv * pieces : 0);
+}
+
+__device__ __forceinline__ void append_piece(const AppendParams& p, const int idx) {
   const int pieces = p.row_bytes >> 4;  // 16 at d = 128 bf16
   const int nk = p.T * p.Hkv * pieces;  // K pieces (and V pieces when !v_t)
   const int d = p.row_bytes >> 1;       // head_dim (bf16)
   const int ng = p.v_t ? p.n_grp * p.Hkv * d : 0;
-  const int ne = p.v_t ? p.n_elem * p.Hkv * pieces : 0;
-  const int total = nk + ng + ne;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+  {
     if (idx < nk) {  // K row pieces (and V when stored row-major)
       const int j = idx % pieces;
       const int rh = idx / pieces;
@@ -113,6 +117,13 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
             static_cast<uint16_t>(w[q >> 1] >> ((q & 1) * 16));
     }
   }
+}
+
+__global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
+  grid_dep_launch();  // the attention launch that follows may start its prologue
+  const int total = append_total(p);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x)
+    append_piece(p, idx);
 }
 
 cudaError_t launch_append(const AppendParams& p, cudaStream_t s) {
@@ -1177,6 +1188,41 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // KV append) has completed and its writes are visible.
   grid_dep_wait();
 
+  if (p.append_total > 0) {
+    // niyama_append_attention: this batch's KV append (a3) inside the launch.  CTAs claim
+    // kThreads pieces at a time until the queue is empty and count the pieces they
+    // finished; only then does any CTA wait for the count to reach the total.  Every
+    // piece is therefore claimed by a CTA that is already running, so the wait needs no
+    // co-residency of the grid.  The pool writes (generic proxy) are fenced for the
+    // bulk-copy (async proxy) reads that follow, on both sides of the release/acquire.
+    for (;;) {
+      if (tid == 0) *item_slot = atomicAdd(p.work + 4, kThreads);
+      __syncthreads();
+      const int base = *item_slot;
+      __syncthreads();
+      if (base >= p.append_total) break;
+      const int n = min(kThreads, p.append_total - base);
+      if (tid < n) append_piece(p.ap, base + tid);
+      fence_proxy_async_global();
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(p.work + 5, n);
+      }
+    }
+    if (tid == 0) {
+      uint32_t polls = 0;
+      while (ld_acquire_gpu(p.work + 5) < p.append_total) {
+        __nanosleep(32);
+#ifndef NIYAMA_NO_WATCHDOG
+        if (++polls == (1u << 26)) __trap();
+#endif
+      }
+      fence_proxy_async_global();
+    }
+    __syncthreads();
+  }
+
   uint64_t t_start = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   int n_done_items = 0;
@@ -1232,6 +1278,8 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
       p.work[1] = 0;
       p.work[2] = 0;
       p.work[3] = 0;
+      p.work[4] = 0;
+      p.work[5] = 0;
       __threadfence();
     }
   }

@@ -651,7 +651,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_mq = take(pl->mq.size() * sizeof(MergeRec));
     const size_t o_vgrp = take(pl->vgrp.size() * 4);
     const size_t o_velem = take(pl->velem.size() * 4);
-    const size_t o_work = take(16);  // zero-initialised through the H2D (with the counters)
+    const size_t o_work = take(32);  // [8] zero-initialised through the H2D (with the counters)
     const size_t o_cnt = take(pl->drows.size() * static_cast<size_t>(hkv) * 4);
     const size_t meta_bytes = off;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
@@ -774,15 +774,13 @@ niyama_status check_launch(niyama_kv* kv, const niyama_plan* plan, int32_t layer
 }
 }  // namespace
 
-extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
-                                          const void* v_new, niyama_stream stream) {
-  niyama_status st = check_launch(kv, plan, layer);
-  if (st != NIYAMA_OK) return st;
-  if (plan->T == 0) return NIYAMA_OK;
+namespace {
+niyama_status fill_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new, const void* v_new,
+                          AppendParams& p) {
   if (!k_new || !v_new) return fail(NIYAMA_EINVAL, "k_new/v_new is NULL");
   if ((reinterpret_cast<uintptr_t>(k_new) | reinterpret_cast<uintptr_t>(v_new)) & 15)
     return fail(NIYAMA_EINVAL, "k_new/v_new must be 16-byte aligned");
-  AppendParams p{};
+  p = AppendParams{};
   p.pool_k = kv->pool + static_cast<int64_t>(layer) * 2 * kv->half_bytes;
   p.pool_v = p.pool_k + kv->v_offset;
   p.k_new = static_cast<const uint8_t*>(k_new);
@@ -799,8 +797,47 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
   p.velem = plan->d_velem;
   p.n_grp = static_cast<int32_t>(plan->vgrp.size());
   p.n_elem = static_cast<int32_t>(plan->velem.size());
+  return NIYAMA_OK;
+}
+
+int64_t append_pieces(const AppendParams& p) {
+  const int64_t pieces = p.row_bytes >> 4;
+  return static_cast<int64_t>(p.T) * p.Hkv * pieces +
+         (p.v_t ? static_cast<int64_t>(p.n_grp) * p.Hkv * (p.row_bytes >> 1) + static_cast<int64_t>(p.n_elem) * p.Hkv * pieces
+                : 0);
+}
+
+niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q, void* o, float* lse,
+                             float softmax_scale, niyama_stream stream, const AppendParams* ap);
+}  // namespace
+
+extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
+                                          const void* v_new, niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, layer);
+  if (st != NIYAMA_OK) return st;
+  if (plan->T == 0) return NIYAMA_OK;
+  AppendParams p{};
+  st = fill_append(kv, plan, layer, k_new, v_new, p);
+  if (st != NIYAMA_OK) return st;
   NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
   return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_append_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer,
+                                                 const void* k_new, const void* v_new, const void* q, void* o,
+                                                 float* lse, float softmax_scale, niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, layer);
+  if (st != NIYAMA_OK) return st;
+  if (plan->T == 0) return NIYAMA_OK;
+  if (kv->cfg.dtype != NIYAMA_BF16) {  // f32 (config 1): the two launches
+    st = niyama_kv_append(kv, plan, layer, k_new, v_new, stream);
+    return st != NIYAMA_OK ? st : niyama_hybrid_attention(kv, plan, layer, q, o, lse, softmax_scale, stream);
+  }
+  AppendParams ap{};
+  st = fill_append(kv, plan, layer, k_new, v_new, ap);
+  if (st != NIYAMA_OK) return st;
+  if (append_pieces(ap) >= (int64_t(1) << 31)) return fail(NIYAMA_EINVAL, "append: too many pieces");
+  return attention_impl(kv, plan, layer, q, o, lse, softmax_scale, stream, &ap);
 }
 
 extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_plan* plan, int32_t layer,
@@ -809,6 +846,12 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   niyama_status st = check_launch(kv, plan, layer);
   if (st != NIYAMA_OK) return st;
   if (plan->T == 0) return NIYAMA_OK;
+  return attention_impl(kv, plan, layer, q, o, lse, softmax_scale, stream, nullptr);
+}
+
+namespace {
+niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q, void* o, float* lse,
+                             float softmax_scale, niyama_stream stream, const AppendParams* ap) {
   if (!q || !o) return fail(NIYAMA_EINVAL, "q/o is NULL");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(NIYAMA_EINVAL, "q/o must be 16-byte aligned");
@@ -854,6 +897,10 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   p.n_merge_rows = plan->n_merge_rows;
   p.scale_log2 = scale * 1.4426950408889634f;
   p.trace = kv->trace;
+  if (ap) {
+    p.ap = *ap;
+    p.append_total = static_cast<int32_t>(append_pieces(*ap));
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (kv->cfg.dtype == NIYAMA_BF16) {
     if (kv->d != 128 || kv->g > 8)
@@ -869,6 +916,7 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
   }
   return NIYAMA_OK;
 }
+}  // namespace
 
 extern "C" niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf) {
   if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");

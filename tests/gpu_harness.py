@@ -37,16 +37,21 @@ class Run:
     """Executes every step of a workload through libniyama (append every step,
     attention on the final step)."""
 
-    def __init__(self, wl: W.Workload, layers: int = 1, extra_blocks: int = 0, kv=None, scale: float = 0.0):
+    def __init__(self, wl: W.Workload, layers: int = 1, extra_blocks: int = 0, kv=None, scale: float = 0.0,
+                 fused: bool = False):
+        """fused: the final step's append runs inside the attention launch
+        (niyama_append_attention) instead of its own launch."""
         import paper_2503_22562_b200 as ny
         s = wl.shape
-        self.wl, self.s = wl, s
+        self.wl, self.s, self.fused = wl, s, fused
         self.kv = kv or ny.KVCache(layers, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + extra_blocks,
                                    block_size=s.block_size, dtype=s.dtype, device=0)
         self.plans = []
-        for st in wl.steps:
+        for n, st in enumerate(wl.steps):
             p = self.kv.plan(st.desc)
             self.plans.append(p)
+            if fused and n == len(wl.steps) - 1:
+                continue
             for layer in range(layers):
                 self.kv.append(p, layer, to_dev(st.k, s.dtype), to_dev(st.v, s.dtype))
         self.plan = self.plans[-1]
@@ -60,7 +65,11 @@ class Run:
         tdt = torch.bfloat16 if s.dtype == "bf16" else torch.float32
         o = torch.full((s.num_q_heads, T, s.head_dim), float("nan"), dtype=tdt, device="cuda")
         lse = torch.full((s.num_q_heads, T), float("nan"), dtype=torch.float32, device="cuda")
-        self.kv.attention(self.plan, layer, qd, o, lse, self.scale)
+        if self.fused:
+            self.kv.append_attention(self.plan, layer, to_dev(st.k, s.dtype), to_dev(st.v, s.dtype), qd, o, lse,
+                                     self.scale)
+        else:
+            self.kv.attention(self.plan, layer, qd, o, lse, self.scale)
         torch.cuda.synchronize()
         return o, lse
 

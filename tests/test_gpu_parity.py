@@ -114,6 +114,40 @@ def test_config4_l70b_full_size_sampled():
     run_and_compare(wl, rows=rows)
 
 
+@pytest.mark.parametrize("case", ["ragged", "peaky", "f32", "config2"])
+def test_fused_append_attention(case):
+    """niyama_append_attention (a3 + a4-a6 in one launch) gives bitwise the same
+    output as niyama_kv_append followed by niyama_hybrid_attention, leaves the same
+    pool (gather read-back), and matches the oracle."""
+    if case == "ragged":
+        wl = W.random_hybrid(W.L8B, seed=31, num_prefill=2, max_chunk=300, num_decode=9, max_ctx=900)
+    elif case == "peaky":
+        wl = W.random_hybrid(W.L8B, seed=5, num_prefill=1, max_chunk=256, num_decode=8, max_ctx=2000, q_scale=8.0)
+    elif case == "f32":
+        wl = W.config1_tiny("unaligned")
+    else:
+        wl = W.config2_l8b()
+    r1, r2 = Run(wl), Run(wl, fused=True)
+    o1, l1 = r1.attention()
+    o2, l2 = r2.attention()
+    if wl.shape.dtype == "bf16":
+        assert torch.equal(o1.view(torch.int16), o2.view(torch.int16))
+    else:
+        assert torch.equal(o1, o2)
+    assert torch.equal(l1, l2)
+    if case != "config2":
+        _, _, O, L = oracle_for(wl)
+        assert_close(to_host_f64(o2, wl.shape.dtype), O, l2.cpu().numpy().astype(np.float64), L)
+    seq = wl.final.desc.prefill_seq[0] if wl.final.desc.prefill_seq else wl.final.desc.decode_seq[0]
+    n = r1.kv.seq_len(seq)
+    tdt = torch.bfloat16 if wl.shape.dtype == "bf16" else torch.float32
+    ka, va, kb, vb = (torch.empty((n, wl.shape.num_kv_heads, wl.shape.head_dim), dtype=tdt, device="cuda")
+                      for _ in range(4))
+    r1.kv.gather(0, seq, n, ka, va)
+    r2.kv.gather(0, seq, n, kb, vb)
+    assert torch.equal(ka, kb) and torch.equal(va, vb)
+
+
 def test_deterministic_and_tier_invariant():
     wl = W.random_hybrid(W.L8B, seed=21, num_prefill=2, max_chunk=300, num_decode=12, max_ctx=3000)
     r = Run(wl)
