@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--config", default="l8b", choices=["l8b", "l70b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0, help="untimed GPU work before warm-up (clock settle)")
+    ap.add_argument("--fused-append", action="store_true",
+                    help="a3-a6 in one launch (niyama_append_attention) instead of niyama_kv_append + "
+                         "niyama_hybrid_attention (measured slower on config 2: 113 vs 100 + 10 us)")
     return ap.parse_args()
 
 
@@ -272,6 +275,7 @@ def main():
     s = wl.shape
     hq, hkv = s.num_q_heads // world, s.num_kv_heads // world
     q0, k0 = rank * hq, rank * hkv
+    fused = args.fused_append
     kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
                     dtype=s.dtype, world_size=world, rank=rank, device=local)
     if world > 1:
@@ -344,10 +348,15 @@ def main():
         plan = kv.plan(batch, stream)                   # a2
         if evs is not None:
             evs[0].record(stream)
-        kv.append(plan, 0, k_new, v_new, stream)        # a3
-        if evs is not None:
-            evs[1].record(stream)
-        kv.attention(plan, 0, q, o, lse, 0.0, stream)   # a4-a6
+        if fused:   # a3-a6 in ONE launch (niyama_append_attention)
+            if evs is not None:
+                evs[1].record(stream)
+            kv.append_attention(plan, 0, k_new, v_new, q, o, lse, 0.0, stream)
+        else:
+            kv.append(plan, 0, k_new, v_new, stream)        # a3
+            if evs is not None:
+                evs[1].record(stream)
+            kv.attention(plan, 0, q, o, lse, 0.0, stream)   # a4-a6
         if evs is not None:
             evs[2].record(stream)
         if world > 1:
@@ -423,8 +432,12 @@ def main():
         stream.wait_event(ev_out[b_])
         a1_step()
         plan = kv.plan(batch, stream)
-        kv.append(plan, 0, d_k[b_], d_v[b_], stream)
-        kv.attention(plan, 0, d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0, stream)
+        if fused:
+            kv.append_attention(plan, 0, d_k[b_], d_v[b_], d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0,
+                                stream)
+        else:
+            kv.append(plan, 0, d_k[b_], d_v[b_], stream)
+            kv.attention(plan, 0, d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0, stream)
         if world > 1:
             kv.allgather_heads(plan, e_of[b_], e_lf[b_], stream)
         pred.predict(batch)
@@ -481,11 +494,13 @@ def main():
                    "num_decode": desc.num_decode, "sum_ctx": int(sum(desc.decode_ctx)), "T": T,
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "l2": f"inputs larger than L2 ({B_kv / 1e6:.0f} MB KV read per step per GPU vs 126 MB L2)",
-                   "step": "a1 slack+chunk, a2 plan, a3 append, a4-a6 fused attention" +
+                   "step": ("a1 slack+chunk, a2 plan, a3-a6 ONE launch (append inside the attention)" if fused else
+                            "a1 slack+chunk, a2 plan, a3 append, a4-a6 fused attention") +
                            (", a7 NCCL all-gather" if world > 1 else "") + ", a8 predict; 1 layer"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "hybrid_attn_bf16_kernel", "algorithmic_bytes_per_launch": B_kv,
+                     "kernel": "hybrid_attn_bf16_kernel" + (" (incl. the KV append)" if fused else ""),
+                     "algorithmic_bytes_per_launch": B_kv,
                      "launch_us": attn_avg_ms * 1e3, "peak_source": peak_src,
                      "tensor_frac": F / attn_s / (tf_peak * 1e12),
                      "t_roof_us": max(F / (tf_peak * 1e12), B_kv / (hbm_peak * 1e9)) * 1e6},
@@ -496,7 +511,7 @@ def main():
         "e2e": {"value": T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "output_matches_device_run": ok,
                 "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": (1 if fused else 2) * args.steps,
         "timing_note": f"attention/append launch times from events on every {EV_EVERY}th timed step",
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
