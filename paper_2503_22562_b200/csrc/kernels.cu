@@ -1,15 +1,17 @@
 // sm_100a kernels of the Niyama hybrid-batch paged-attention path.
 //
-//   kv_append_kernel        a3  scatter new K/V rows into the swizzled paged pool
+//   kv_append_kernel        a3  scatter new K/V rows into the paged pool (core-matrix K, V^T)
 //   kv_gather_kernel            read-back of a sequence (tests)
 //   hybrid_attn_bf16_kernel a4-a6  ONE persistent launch:
 //        prefill tiles  — TMA-engine bulk copies of paged K/V (one per block) into
 //                         shared memory, S = Q K^T (SS) and O += P V (TS, P in TMEM)
 //                         on tcgen05, two softmax warp sets on alternate key steps
 //                         (online softmax, lazy rescale of O in TMEM);
-//        decode units   — warp-level split-KV streaming (bulk copies into a per-warp
-//                         3-stage ring, mma.sync m16n8k16 with the GQA group on M),
-//                         partials merged by log-sum-exp by the last split of a row.
+//        decode units   — warp-level split-KV streaming (one 8 KB bulk copy per
+//                         16-token stage into per-warp rings: 12 warps x 2 stages at
+//                         g <= 4, 8 x 3 at g = 8; mma.sync m16n8k16 swap-AB with the
+//                         GQA group on N), partials merged by log-sum-exp in-launch.
+//   (niyama_append_attention: the append pieces run inside this launch first.)
 //   hybrid_attn_generic_kernel  f32 path (config 1): SIMT warp per (row, kv head).
 //
 // Math (PAPER P:319 PagedAttention semantics, R1/R7/R10/R11): for row r
