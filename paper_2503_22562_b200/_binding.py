@@ -225,7 +225,12 @@ class KVCache:
         d = desc if isinstance(desc, _Desc) else _Desc(desc)
         h = C.c_void_p()
         _check(lib.niyama_plan_create(self.handle, C.byref(d.c), _stream(stream), C.byref(h)))
-        return Plan(self, h.value)
+        plan = Plan(self, h.value)
+        if not hasattr(self, "_plans"):
+            import weakref
+            self._plans = weakref.WeakSet()
+        self._plans.add(plan)
+        return plan
 
     def release(self, seq: int):
         _check(lib.niyama_kv_release(self.handle, int(seq)))
@@ -279,6 +284,9 @@ class KVCache:
 
     def close(self):
         if getattr(self, "handle", None):
+            # a plan's buffers come from this cache's memory pool: destroy live plans first
+            for plan in list(getattr(self, "_plans", ())):
+                plan.close()
             lib.niyama_kv_destroy(self.handle)
             self.handle = None
 

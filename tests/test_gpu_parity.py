@@ -196,3 +196,18 @@ def test_empty_batch_noop_and_errors():
         kv.append(p, 0, x[1:].data_ptr(), x.data_ptr())   # misaligned
     with pytest.raises(ny.NiyamaError):
         kv.append(p, 1, x, x)                              # layer out of range
+
+
+def test_close_cache_with_live_plans():
+    """Closing a cache destroys its live plans first (their buffers come from the cache's
+    memory pool): no use after free when the plan objects are collected later."""
+    import gc
+    import paper_2503_22562_b200 as ny
+    for _ in range(2):
+        kv = ny.KVCache(1, 32, 8, 128, 256, dtype="bf16", device=0)
+        plan = kv.plan(W.BatchDesc([0, 1], [0, 0], [100, 37]))
+        kv.close()
+        assert plan.handle is None
+        del plan
+        gc.collect()
+    torch.cuda.synchronize()
