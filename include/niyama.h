@@ -95,7 +95,8 @@ typedef struct niyama_plan niyama_plan;
  * (Hkv/G)*block_size*head_dim elements of device memory (zero-filled) plus
  * the block tables.  Errors: EINVAL (shape), EUNSUPPORTED, ECUDA (OOM). */
 niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv** out);
-void niyama_kv_destroy(niyama_kv* kv); /* synchronises the device; NULL is a no-op */
+void niyama_kv_destroy(niyama_kv* kv); /* synchronises the device; NULL is a no-op.  Destroy every plan of
+                                          * this kv first: their buffers live in its memory pool. */
 
 /* Request finished (P:205 ⑦, §8 a13 feedback): free its blocks (they become
  * the smallest-free-id candidates again, R9).  ENOSEQ if unknown. */
@@ -146,7 +147,8 @@ typedef struct {
  * The plan is reused by every layer's append/attention of the iteration. */
 niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_desc* desc, niyama_stream stream,
                                  niyama_plan** out);
-void niyama_plan_destroy(niyama_plan* plan); /* stream-ordered free on the plan's stream */
+void niyama_plan_destroy(niyama_plan* plan); /* stream-ordered free on the plan's stream; before the plan's
+                                               * niyama_kv is destroyed */
 /* Undo the plan's host bookkeeping: every sequence of the batch returns to its
  * length before niyama_plan_create (sequences the plan created are removed);
  * blocks past the old lengths are freed (R9).  The plan's device buffers stay
