@@ -76,12 +76,24 @@ struct niyama_kv {
     size_t cap = 0;
     cudaEvent_t ev = nullptr;
     bool pending = false;
+    // device buffer uploaded on copy_stream (async_plan): owned by at most one live plan;
+    // `released` is recorded on that plan's stream when it is destroyed, and the next
+    // upload into the buffer waits for it (kStaging plans later: long complete)
+    uint8_t* d = nullptr;
+    size_t dcap = 0;
+    cudaEvent_t released = nullptr;
+    const void* owner = nullptr;
   } stg[kStaging];
   int stg_next = 0;
   // Plan device buffers come from a library-owned stream-ordered pool that never
   // returns memory to the OS (release threshold = max): the per-step
   // allocate/free is then a pointer bump, never a page map.
   cudaMemPool_t mempool = nullptr;
+  // Plans are uploaded on this library-owned stream (their buffers come from `mempool`
+  // allocated on it), so a plan's H2D overlaps the caller's previous kernels; every
+  // use of the plan makes the caller's stream wait for its upload (plan->ready).
+  cudaStream_t copy_stream = nullptr;
+  bool async_plan = true;  // NIYAMA_PLAN_COPY_STREAM=0: upload on the caller's stream
   int64_t* trace = nullptr;  // niyama_debug_trace
   int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
   int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
@@ -92,6 +104,8 @@ struct niyama_kv {
 struct niyama_plan {
   niyama_kv* kv = nullptr;
   cudaStream_t stream = nullptr;
+  cudaEvent_t ready = nullptr;  // upload finished (kv->copy_stream); null: uploaded on `stream`
+  int32_t slot = -1;            // staging slot whose device buffer holds the plan (-1: pool)
   int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0;
   int64_t sum_ctx = 0;
   std::vector<int32_t> slot_map;
@@ -186,8 +200,10 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
     const size_t bytes = static_cast<size_t>(kv->half_bytes) * 2 * c.num_layers;
     if (e == cudaSuccess) e = cudaMalloc(&kv->pool, bytes);
     if (e == cudaSuccess) e = cudaMemset(kv->pool, 0, bytes);  // stale slots stay finite (masked, P = 0)
-    for (int i = 0; i < niyama_kv::kStaging && e == cudaSuccess; ++i)
+    for (int i = 0; i < niyama_kv::kStaging && e == cudaSuccess; ++i) {
       e = cudaEventCreateWithFlags(&kv->stg[i].ev, cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&kv->stg[i].released, cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) {
       cudaMemPoolProps props{};
       props.allocType = cudaMemAllocationTypePinned;
@@ -198,9 +214,14 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
       uint64_t keep = ~uint64_t(0);
       if (e == cudaSuccess) e = cudaMemPoolSetAttribute(kv->mempool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
+    if (const char* pc = std::getenv("NIYAMA_PLAN_COPY_STREAM")) kv->async_plan = std::atoi(pc) != 0;
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&kv->copy_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
-      for (auto& st : kv->stg)
+      for (auto& st : kv->stg) {
         if (st.ev) cudaEventDestroy(st.ev);
+        if (st.released) cudaEventDestroy(st.released);
+      }
+      if (kv->copy_stream) cudaStreamDestroy(kv->copy_stream);
       if (kv->mempool) cudaMemPoolDestroy(kv->mempool);
       if (kv->pool) cudaFree(kv->pool);
       delete kv;
@@ -221,7 +242,10 @@ extern "C" void niyama_kv_destroy(niyama_kv* kv) {
     for (auto& st : kv->stg) {
       if (st.h) cudaFreeHost(st.h);
       if (st.ev) cudaEventDestroy(st.ev);
+      if (st.released) cudaEventDestroy(st.released);
+      if (st.d) cudaFree(st.d);
     }
+    if (kv->copy_stream) cudaStreamDestroy(kv->copy_stream);
     if (kv->mempool) cudaMemPoolDestroy(kv->mempool);
   }
   delete kv;
@@ -657,9 +681,29 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
     const size_t total = off;
-    cudaStream_t s = pl->stream;
+    // upload on the library's copy stream into the staging slot's own device buffer when
+    // no live plan holds it (the common case); otherwise from the pool on the caller's stream
+    const bool use_slot = kv->async_plan && stg->owner == nullptr;
+    cudaStream_t s = use_slot ? kv->copy_stream : pl->stream;  // upload stream
     cudaError_t e = cudaSetDevice(kv->cfg.device);
-    if (e == cudaSuccess) e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pl->dbuf), total, kv->mempool, s);
+    if (use_slot) {
+      if (e == cudaSuccess && stg->dcap < total) {
+        if (stg->d) e = cudaFree(stg->d);  // grows rarely (first plans, larger batches)
+        stg->d = nullptr;
+        stg->dcap = 0;
+        const size_t cap = total + total / 4 + (1 << 20);
+        if (e == cudaSuccess) e = cudaMalloc(&stg->d, cap);
+        if (e == cudaSuccess) stg->dcap = cap;
+      }
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, stg->released, 0);  // its previous plan's kernels
+      if (e == cudaSuccess) {
+        pl->dbuf = stg->d;
+        pl->slot = kv->stg_next;
+        stg->owner = pl;
+      }
+    } else if (e == cudaSuccess) {
+      e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&pl->dbuf), total, kv->mempool, s);
+    }
     if (e == cudaSuccess && stg->cap < meta_bytes) {
       if (stg->h) cudaFreeHost(stg->h);
       stg->h = nullptr;
@@ -684,11 +728,17 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     if (e == cudaSuccess) e = cudaEventRecord(stg->ev, s);
     if (e != cudaSuccess) {
       rollback();  // the error leaves the pool as it was
-      if (pl->dbuf) cudaFreeAsync(pl->dbuf, s);
+      if (pl->slot >= 0)
+        stg->owner = nullptr;
+      else if (pl->dbuf)
+        cudaFreeAsync(pl->dbuf, s);
       delete pl;
       return fail(NIYAMA_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
     }
     stg->pending = true;
+    // (a later plan may re-record this event after kStaging more uploads; waiting on the
+    // later record only waits longer — the upload stream is FIFO and never waits on callers)
+    if (use_slot) pl->ready = stg->ev;
     kv->stg_next = (kv->stg_next + 1) % niyama_kv::kStaging;
     pl->d_slot = reinterpret_cast<int32_t*>(pl->dbuf + o_slot);
     pl->d_tables = reinterpret_cast<int32_t*>(pl->dbuf + o_tbl);
@@ -712,7 +762,13 @@ extern "C" void niyama_plan_destroy(niyama_plan* plan) {
   if (!plan) return;
   if (plan->dbuf) {
     cudaSetDevice(plan->kv->cfg.device);
-    cudaFreeAsync(plan->dbuf, plan->stream);
+    if (plan->slot >= 0) {  // the slot's buffer may be re-uploaded once this plan's kernels are done
+      niyama_kv::Staging& st = plan->kv->stg[plan->slot];
+      cudaEventRecord(st.released, plan->stream);
+      st.owner = nullptr;
+    } else {
+      cudaFreeAsync(plan->dbuf, plan->stream);
+    }
   }
   delete plan;
 }
@@ -772,6 +828,12 @@ niyama_status check_launch(niyama_kv* kv, const niyama_plan* plan, int32_t layer
   if (layer < 0 || layer >= kv->cfg.num_layers) return fail(NIYAMA_EINVAL, "layer out of range");
   return NIYAMA_OK;
 }
+
+// The caller's stream waits for the plan's upload (kv->copy_stream) before using it.
+cudaError_t wait_plan(const niyama_plan* plan, niyama_stream stream) {
+  if (!plan->ready) return cudaSuccess;
+  return cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), plan->ready, 0);
+}
 }  // namespace
 
 namespace {
@@ -819,6 +881,7 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
   AppendParams p{};
   st = fill_append(kv, plan, layer, k_new, v_new, p);
   if (st != NIYAMA_OK) return st;
+  NY_CUDA(wait_plan(plan, stream));
   NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
   return NIYAMA_OK;
 }
@@ -902,6 +965,7 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
     p.append_total = static_cast<int32_t>(append_pieces(*ap));
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  NY_CUDA(wait_plan(plan, stream));
   if (kv->cfg.dtype == NIYAMA_BF16) {
     if (kv->d != 128 || kv->g > 8)
       return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");

@@ -211,3 +211,19 @@ def test_close_cache_with_live_plans():
         del plan
         gc.collect()
     torch.cuda.synchronize()
+
+
+def test_many_live_plans_fallback():
+    """More live plans than upload slots (8): later plans fall back to pool buffers
+    uploaded on the caller's stream; results still match the oracle, and slots are
+    reused once plans are destroyed."""
+    import paper_2503_22562_b200 as ny
+    wl = W.random_hybrid(W.L8B, seed=41, num_prefill=1, max_chunk=200, num_decode=6, max_ctx=700)
+    s = wl.shape
+    kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, dtype="bf16", device=0)
+    hold = [kv.plan(W.BatchDesc([5000 + i], [0], [16])) for i in range(9)]
+    run_and_compare(wl, kv=kv)
+    for p in hold:
+        p.close()
+    wl2 = W.random_hybrid(W.L8B, seed=42, num_prefill=1, max_chunk=150, num_decode=5, max_ctx=500)
+    run_and_compare(wl2)
