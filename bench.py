@@ -512,7 +512,9 @@ def main():
                 "d2h_bytes_per_step": d2h, "output_matches_device_run": ok,
                 "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
         "gpu_launches": (1 if fused else 2) * args.steps,
-        "timing_note": f"attention/append launch times from events on every {EV_EVERY}th timed step",
+        "timing_note": (f"attention/append launch times from events on every {EV_EVERY}th timed step; the append "
+                        "interval includes the wait for the plan's upload (library copy stream), so 'other' = step "
+                        "- append - attention can be negative"),
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
     }
