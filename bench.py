@@ -47,6 +47,10 @@ def parse():
     ap.add_argument("--config", default="l8b", choices=["l8b", "l70b"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0, help="untimed GPU work before warm-up (clock settle)")
+    ap.add_argument("--host-only", action="store_true",
+                    help="CPU check of the N-rank plumbing (gloo, NIYAMA_DEVICE_NONE pools): rank setup, replicated "
+                         "planner, NCCL unique-id broadcast, a1/a2/a8 host steps; prints a line marked "
+                         "impl=host-only (not a bench result)")
     ap.add_argument("--fused-append", action="store_true",
                     help="a3-a6 in one launch (niyama_append_attention) instead of niyama_kv_append + "
                          "niyama_hybrid_attention (measured slower on config 2: 113 vs 100 + 10 us)")
@@ -134,7 +138,21 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup(n):
+def spawn_ranks(n):
+    """`python bench.py --gpus N` without torchrun: re-launch this command under
+    torch.distributed.run with N ranks on 127.0.0.1 (one process per GPU), forwarding
+    its output; returns the exit code."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
+def dist_setup(n, host_only=False):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -144,9 +162,53 @@ def dist_setup(n):
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if os.environ.get("NIYAMA_BENCH_GLOO") is None else "gloo")
+        gloo = host_only or os.environ.get("NIYAMA_BENCH_GLOO") is not None
+        dist.init_process_group("gloo" if gloo else "nccl")
         pg = dist
     return rank, world, local, pg
+
+
+def run_host_only(args, rank, world, dist):
+    """--host-only: the N-rank plumbing of the real run on CPU (tests/test_bench_spawn.py).
+    Every rank owns Hkv/N heads of a DEVICE_NONE pool, plans the config's batch with the
+    replicated planner (no metadata exchange), receives the NCCL unique id broadcast by
+    rank 0, and runs the a1/a2/a8 host steps; rank 0 checks every rank planned the same
+    slots and prints one line."""
+    import paper_2503_22562_b200 as ny
+    wl = workload(args.config)
+    s = wl.shape
+    kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
+                    dtype=s.dtype, world_size=world, rank=rank, device=None)
+    uid = [ny.get_unique_id() if rank == 0 else b""]
+    if dist:
+        dist.broadcast_object_list(uid, src=0)
+    for st in wl.steps[:-1]:
+        kv.plan(st.desc).close()
+    batch = ny.Batch(wl.final.desc)
+    cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
+    pred = ny.Predictor.from_params(cfg, [3e-5, 5e-9, 0.0, 0.0, 1.0, 0.1, 1.3e-6, 70e9, 7.2e12]).bind(kv)
+    slots, t_pred = None, 0.0
+    t0 = time.perf_counter()
+    for i in range(args.warmup + args.steps):
+        plan = kv.plan(batch)
+        if slots is None:
+            slots = plan.slots()
+        t_pred = pred.predict(batch)
+        plan.rollback()
+        plan.close()
+    host_us = (time.perf_counter() - t0) * 1e6 / (args.warmup + args.steps)
+    got = [None] * world
+    if dist:
+        dist.all_gather_object(got, (slots, len(uid[0])))
+    else:
+        got = [(slots, len(uid[0]))]
+    if rank == 0:
+        print(json.dumps({"impl": "host-only", "metric": METRIC, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "value": None, "world_size_seen": world,
+                          "replicated_plans_equal": all(g == got[0] for g in got),
+                          "unique_id_bytes": [g[1] for g in got], "host_step_us": host_us,
+                          "predicted_launch_s": t_pred, "config": {"workload": wl.name,
+                          "parallelism": f"kv-head shard x{world}"}}), flush=True)
 
 
 def cpu_baseline(wl, budget_s=20.0):
@@ -255,7 +317,15 @@ def main():
     args = parse()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
-    rank, world, local, dist = dist_setup(args.gpus)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(spawn_ranks(args.gpus))
+    rank, world, local, dist = dist_setup(args.gpus, args.host_only)
+    if args.host_only:
+        run_host_only(args, rank, world, dist)
+        if dist:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         if dist:
@@ -339,8 +409,8 @@ def main():
     # Per-launch events cost device time (~1-2 us each) and break the programmatic
     # launch overlap of append -> attention, so they bracket every EV_EVERY-th timed
     # step only; the attention roofline uses the mean over those launches.
-    EV_EVERY = 4
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) if i % EV_EVERY == 0 else None
+    EV_EVERY = 2
+    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) if i % EV_EVERY == 0 else None
           for i in range(args.steps)]
 
     def step(evs=None):
@@ -361,6 +431,8 @@ def main():
             evs[2].record(stream)
         if world > 1:
             kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
+        if evs is not None:
+            evs[3].record(stream)
         pred.predict(batch)                             # a8
         plan.rollback()                                 # replay the same batch next step (host only)
         plan.close()
@@ -394,11 +466,19 @@ def main():
     ms = e0.elapsed_time(e1)
     attn_ms = [e[1].elapsed_time(e[2]) for e in ev if e is not None]
     append_ms = [e[0].elapsed_time(e[1]) for e in ev if e is not None]
+    ag_ms = [e[2].elapsed_time(e[3]) for e in ev if e is not None]
     attn_avg_ms = sum(attn_ms) / len(attn_ms)
+    ag_avg_ms = sum(ag_ms) / len(ag_ms)
+    attn_q = [float(x) for x in np.percentile(np.array(attn_ms) * 1e3, [10, 50, 90])]
+    per_rank = {"attention_us": [attn_avg_ms * 1e3], "allgather_us": [ag_avg_ms * 1e3], "step_us": [ms / args.steps * 1e3]}
     if dist:
-        t = torch.tensor([ms, attn_avg_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, attn_avg_ms = float(t[0]), float(t[1])
+        t = torch.tensor([ms, attn_avg_ms, ag_avg_ms], device=dev)
+        allr = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allr, t)
+        per_rank = {"attention_us": [float(x[1]) * 1e3 for x in allr], "allgather_us": [float(x[2]) * 1e3 for x in allr],
+                    "step_us": [float(x[0]) / args.steps * 1e3 for x in allr]}
+        ms = max(float(x[0]) for x in allr)
+        attn_avg_ms = max(float(x[1]) for x in allr)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the
     # timed region.  Two buffer sets: the H2D of step i+1 (copy stream) and the
@@ -506,13 +586,18 @@ def main():
                      "t_roof_us": max(F / (tf_peak * 1e12), B_kv / (hbm_peak * 1e9)) * 1e6},
         "attn_tokens_per_s": T / attn_s,
         "step_breakdown_us": {"append": 1e3 * sum(append_ms) / len(append_ms), "attention": attn_avg_ms * 1e3,
+                              "allgather": ag_avg_ms * 1e3,
                               "other": ms / args.steps * 1e3 - attn_avg_ms * 1e3 - 1e3 * sum(append_ms) / len(append_ms),
                               "host_issue": host_issue_us},
+        "attention_launch_us": {"p10": attn_q[0], "median": attn_q[1], "p90": attn_q[2], "mean": attn_avg_ms * 1e3,
+                                "samples": len(attn_ms)},
+        "per_rank": per_rank,
         "e2e": {"value": T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "output_matches_device_run": ok,
                 "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
         "gpu_launches": (1 if fused else 2) * args.steps,
-        "timing_note": (f"attention/append launch times from events on every {EV_EVERY}th timed step; the append "
+        "timing_note": (f"attention/append/all-gather launch times from events on every {EV_EVERY}nd timed step; "
+                        "the roofline uses their mean (rank max); the append "
                         "interval includes the wait for the plan's upload (library copy stream), so 'other' = step "
                         "- append - attention can be negative"),
         "clocks": clocks.summary(t_settle, t_wall1),

@@ -67,14 +67,28 @@ const char* niyama_version(void);
 
 #define NIYAMA_DEVICE_NONE (-1)
 
+/* Device use: every call that touches the GPU runs on cfg.device and restores the
+ * calling thread's current device before returning.
+ *
+ * Failure and recovery: a kernel that detects a lost completion (a watchdog of ~2^26
+ * polls in the in-launch merge / append wait) executes a trap.  A trap, like any
+ * kernel fault, is a sticky CUDA context error: every later call on the device returns
+ * NIYAMA_ECUDA, and the context (and with it the pool, plans and communicator) cannot
+ * be reused — the process must destroy its objects and restart (the serving layer
+ * re-plans the iteration from its own request state; KV bytes are lost with the
+ * context).  A launch that fails to START (configuration error, returned as ECUDA)
+ * changes nothing: the plan's launch count and queues are untouched and the call may
+ * be retried.  A plan's launches must be ordered on one stream (or explicitly
+ * ordered): they share the plan's work queues and completion counters. */
+
 typedef enum { NIYAMA_BF16 = 0, NIYAMA_F32 = 1 } niyama_dtype;
 
 /* KV-cache configuration.  Heads are GLOBAL counts; with world_size G the
  * library on `rank` owns kv heads [rank*Hkv/G, (rank+1)*Hkv/G) and query
  * heads [rank*Hq/G, (rank+1)*Hq/G) (GQA groups stay whole, §8e
- * tensor parallelism).  Supported: head_dim*elt a multiple of 128 bytes
- * (bf16: 64, 128; f32: 32, 64), Hq/Hkv a power of two <= 128, block_size in
- * {16, 32, 64, 128} (R9: default 16). */
+ * tensor parallelism).  Supported (anything else is EUNSUPPORTED at create):
+ * bf16 head_dim 128; f32 head_dim 32, 64, 96 or 128; Hq/Hkv a power of two
+ * <= 8; block_size in {16, 32, 64, 128} (R9: default 16). */
 typedef struct {
   int32_t num_layers;
   int32_t num_q_heads;
@@ -151,8 +165,12 @@ void niyama_plan_destroy(niyama_plan* plan); /* stream-ordered free on the plan'
                                                * niyama_kv is destroyed */
 /* Undo the plan's host bookkeeping: every sequence of the batch returns to its
  * length before niyama_plan_create (sequences the plan created are removed);
- * blocks past the old lengths are freed (R9).  The plan's device buffers stay
- * valid for launches already enqueued.  Used to abort or replay an iteration. */
+ * blocks past the old lengths are freed (R9).  An entry applies only to the
+ * sequence the plan saw (same id and creation generation): a sequence released
+ * meanwhile — or released and re-created under the same id — is left alone.
+ * Every entry is validated before anything changes (ESTATE if a sequence is now
+ * shorter than before the plan; nothing rolled back).  The plan's device buffers
+ * stay valid for launches already enqueued.  Used to abort or replay an iteration. */
 niyama_status niyama_plan_rollback(niyama_kv* kv, niyama_plan* plan);
 
 typedef struct {
@@ -211,10 +229,34 @@ niyama_status niyama_append_attention(niyama_kv* kv, const niyama_plan* plan, in
  * written).  NULL = off (default). */
 niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
 
+/* Launch tuning (explicit, per kv; default = the planner's own choices).  Used by the
+ * measurement tools; the predictor sees the same values through niyama_predictor_bind.
+ *   prefill_ctas      0 = work-proportional CTA split; n > 0 = at most n CTAs take
+ *                     prefill tiles first
+ *   split_len         0 = decode split length from batch totals; else a multiple of 16
+ *   tail_div, tail_min  a row's last piece is cut into min(q, max(tail_min, q/tail_div))
+ *                     tokens (defaults NIYAMA_TAIL_DIV, NIYAMA_TAIL_MIN)
+ *   grid_cap          0 = grid from the plan; n > 0 = at most n CTAs (diagnostics)
+ *   plan_copy_stream  1 = plans upload on the library's copy stream (default), 0 = on
+ *                     the caller's stream
+ * A changed tuning applies to plans created afterwards (split, CTA split) and to
+ * launches issued afterwards (grid cap). */
+typedef struct {
+  int32_t prefill_ctas;
+  int32_t split_len;
+  int32_t tail_div;
+  int32_t tail_min;
+  int32_t grid_cap;
+  int32_t plan_copy_stream;
+} niyama_tuning;
+niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning* out);
+niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t); /* EINVAL on out-of-range fields */
+
 /* a7 — head sharding across the GPUs of one node (§8e).  comm_init creates
  * the library's own NCCL communicator from a 128-byte ncclUniqueId produced
  * by rank 0 and broadcast by the caller (world/rank from the config).
- * allgather_heads gathers every rank's [Hq/G][T][d] slice into o_full
+ * allgather_heads (ncclAllGather, issued at every world size — at 1 it is NCCL's
+ * in-place copy; EINVAL before comm_init) gathers every rank's [Hq/G][T][d] slice into o_full
  * [Hq][T][d] IN PLACE (this rank's slice must already sit at
  * o_full + rank*(Hq/G)*T*d) and likewise lse_full [Hq][T] if non-NULL. */
 niyama_status niyama_comm_init(niyama_kv* kv, const void* nccl_unique_id);
@@ -253,6 +295,7 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  * (the first one within 1e-9 relative of the minimum). */
 #define NIYAMA_PRED_SMS 148
 #define NIYAMA_TAIL_DIV 4
+#define NIYAMA_TAIL_MIN 256
 #define NIYAMA_STEP_BYTES 160e3
 /* CTA split: decode KV bytes weigh this much more when g = Hq/Hkv > 4 (the launch then
  * streams decode with 8 warps per CTA instead of 12, so a CTA moves fewer bytes per
@@ -296,6 +339,10 @@ niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_
                                         int32_t chunk_offset, int32_t prefill_remaining, double slack_s,
                                         int32_t max_chunk, int32_t* chunk_out, int32_t* infeasible_out);
 void niyama_predictor_destroy(niyama_predictor* p);
+/* Model the launches of this kv: its device's SM count (default NIYAMA_PRED_SMS) and
+ * its current niyama_tuning (default tuning otherwise).  EINVAL if the predictor's
+ * local shape (Hq/G, Hkv/G, head_dim, dtype) differs from the kv's. */
+niyama_status niyama_predictor_bind(niyama_predictor* p, const niyama_kv* kv);
 
 /* a1 — slack of the running decodes (§3.3; Eq. 1-3).
  * Interactive decode: D_n - now with D_n = t_arrival + TTFT + (n-1)*TBT (Eq. 2)

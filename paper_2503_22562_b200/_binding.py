@@ -47,6 +47,11 @@ class PlanInfo(C.Structure):
                 ("rows_per_tile", C.c_int32), ("prefill_ctas", C.c_int32), ("sum_ctx", C.c_int64)]
 
 
+class Tuning(C.Structure):
+    _fields_ = [("prefill_ctas", C.c_int32), ("split_len", C.c_int32), ("tail_div", C.c_int32),
+                ("tail_min", C.c_int32), ("grid_cap", C.c_int32), ("plan_copy_stream", C.c_int32)]
+
+
 class SampleC(C.Structure):
     _fields_ = [("chunk_len", C.c_int32), ("chunk_offset", C.c_int32), ("num_decode", C.c_int32),
                 ("sum_ctx", C.c_int64), ("seconds", C.c_double)]
@@ -87,6 +92,9 @@ def _load():
         "niyama_hybrid_attention": ([vp, vp, i32, vp, vp, vp, C.c_float, vp], st),
         "niyama_append_attention": ([vp, vp, i32, vp, vp, vp, vp, vp, C.c_float, vp], st),
         "niyama_debug_trace": ([vp, vp], st),
+        "niyama_kv_get_tuning": ([vp, C.POINTER(Tuning)], st),
+        "niyama_kv_set_tuning": ([vp, C.POINTER(Tuning)], st),
+        "niyama_predictor_bind": ([vp, vp], st),
         "niyama_comm_init": ([vp, vp], st),
         "niyama_get_unique_id": ([vp], st),
         "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
@@ -275,6 +283,20 @@ class KVCache:
     def debug_trace(self, buf):
         _check(lib.niyama_debug_trace(self.handle, _ptr(buf)))
 
+    def tuning(self) -> Tuning:
+        t = Tuning()
+        _check(lib.niyama_kv_get_tuning(self.handle, C.byref(t)))
+        return t
+
+    def set_tuning(self, **fields):
+        """Change named niyama_tuning fields (include/niyama.h); the others keep their values."""
+        t = self.tuning()
+        for k, v in fields.items():
+            if not hasattr(t, k):
+                raise AttributeError(f"niyama_tuning has no field {k}")
+            setattr(t, k, int(v))
+        _check(lib.niyama_kv_set_tuning(self.handle, C.byref(t)))
+
     def comm_init(self, unique_id: bytes):
         buf = C.create_string_buffer(bytes(unique_id), 128)
         _check(lib.niyama_comm_init(self.handle, buf))
@@ -337,6 +359,11 @@ class Predictor:
         h = C.c_void_p()
         _check(lib.niyama_predictor_from_params(C.byref(cfg), th, C.byref(h)))
         return cls(h.value)
+
+    def bind(self, kv: "KVCache") -> "Predictor":
+        """Model kv's launches: its SM count and tuning (niyama_predictor_bind)."""
+        _check(lib.niyama_predictor_bind(self.handle, kv.handle))
+        return self
 
     def params(self) -> np.ndarray:
         th = (C.c_double * NUM_PARAMS)()

@@ -142,6 +142,7 @@ cudaError_t launch_append(const AppendParams& p, cudaStream_t s);
 cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const int32_t* table, int32_t len,
                           int32_t Hkv, int32_t row_bytes, int32_t B, int64_t chunk_bytes, int32_t v_t, uint8_t* k_out,
                           uint8_t* v_out, cudaStream_t s);
+cudaError_t configure_attention_bf16();  // per-device smem opt-in (current device)
 cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s);
 cudaError_t launch_attention_generic_f32(const AttnParams& p, cudaStream_t s);
 int attention_bf16_smem_bytes();

@@ -1289,14 +1289,13 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
 
 int attention_bf16_smem_bytes() { return fa::kSmemBytes; }
 
+// The dynamic shared-memory opt-in is a per-device attribute: niyama_kv_create sets it
+// on the pool's device (current at that point), so every device that owns a bf16 pool has it.
+cudaError_t configure_attention_bf16() {
+  return cudaFuncSetAttribute(hybrid_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::kSmemBytes);
+}
+
 cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(hybrid_attn_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         fa::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(fa::kThreads);

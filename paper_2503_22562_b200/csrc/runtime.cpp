@@ -49,6 +49,34 @@ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct Seq {
   std::vector<int32_t> blocks;
   int32_t len = 0;
+  uint64_t gen = 0;  // creation generation: a released id reused later is a different sequence
+};
+
+niyama_tuning default_tuning() {
+  niyama_tuning t{};
+  t.prefill_ctas = 0;
+  t.split_len = 0;
+  t.tail_div = NIYAMA_TAIL_DIV;
+  t.tail_min = NIYAMA_TAIL_MIN;
+  t.grid_cap = 0;
+  t.plan_copy_stream = 1;
+  return t;
+}
+
+// Runs the calling thread on `device` for the scope and restores the caller's device
+// (the library never leaves the caller's current device changed).
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int device) {
+    if (device < 0) return;
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != device) err = cudaSetDevice(device);
+    else prev = -1;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
 };
 
 }  // namespace
@@ -59,7 +87,6 @@ struct niyama_kv {
   int64_t chunk_bytes = 0;  // one (block, kv head) chunk
   int64_t chunk_stride = 0;  // between consecutive chunks of one of K / V
   int64_t v_offset = 0;      // V's chunk of (block, kv head) = K's + v_offset
-  int32_t dec_warps_override = 0;  // NIYAMA_DEC_WARPS (A/B experiments): 8 or 12, 0 = by g
   int64_t half_bytes = 0;   // K (or V) of one layer
   bool has_device = false;
   int num_sms = 148;
@@ -93,24 +120,23 @@ struct niyama_kv {
   // allocated on it), so a plan's H2D overlaps the caller's previous kernels; every
   // use of the plan makes the caller's stream wait for its upload (plan->ready).
   cudaStream_t copy_stream = nullptr;
-  bool async_plan = true;  // NIYAMA_PLAN_COPY_STREAM=0: upload on the caller's stream
   int64_t* trace = nullptr;  // niyama_debug_trace
-  int32_t split_override = 0;  // NIYAMA_SPLIT_LEN (tuning knob; 0 = choose from batch totals)
-  int32_t prefill_cap = 0;     // NIYAMA_PREFILL_CTAS (tuning knob; 0 = every CTA may take prefill tiles)
-  int32_t tail_div = NIYAMA_TAIL_DIV;  // NIYAMA_TAIL_DIV env (tuning knob): last piece of a row in q/tail_div units
-  int32_t tail_min = 256;              // NIYAMA_TAIL_MIN env (tuning knob): floor of those pieces
+  niyama_tuning tune = default_tuning();  // niyama_kv_set_tuning (explicit; no environment knobs)
+  // per-plan upload events (each plan records its own; returned here on destroy)
+  std::vector<cudaEvent_t> free_events;
+  uint64_t next_gen = 1;  // sequence generations (rollback identity)
 };
 
 struct niyama_plan {
   niyama_kv* kv = nullptr;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ready = nullptr;  // upload finished (kv->copy_stream); null: uploaded on `stream`
+  cudaEvent_t ready = nullptr;  // this plan's own event, recorded right after its upload (either path)
   int32_t slot = -1;            // staging slot whose device buffer holds the plan (-1: pool)
   int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0;
   int64_t sum_ctx = 0;
   std::vector<int32_t> slot_map;
   std::vector<int32_t> tables;
-  struct Prev { int64_t seq; bool existed; int32_t len; };
+  struct Prev { int64_t seq; bool existed; int32_t len; uint64_t gen; };
   std::vector<Prev> prev;  // bookkeeping before this plan (niyama_plan_rollback)
   std::vector<PrefillSlice> slices;
   std::vector<DecodeRow> drows;
@@ -142,6 +168,8 @@ struct niyama_plan {
 
 struct niyama_predictor {
   int hq = 0, hkv = 0, d = 0, elt = 0;
+  int num_sms = NIYAMA_PRED_SMS;          // niyama_predictor_bind: the kv's device
+  niyama_tuning tune = default_tuning();  // niyama_predictor_bind: the kv's tuning
   double theta[NIYAMA_NUM_PARAMS] = {0, 0, 0, 0, 0, 0, 1e-6, 50e9, 6e12};
 };
 
@@ -168,6 +196,11 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   if (c.num_blocks < 1) return fail(NIYAMA_EINVAL, "num_blocks < 1");
   if (static_cast<int64_t>(c.num_blocks) * c.block_size >= (int64_t(1) << 31))
     return fail(NIYAMA_EINVAL, "num_blocks*block_size must be < 2^31");
+  // shapes the kernels are built for (rejected here, not at the first launch)
+  if (c.dtype == NIYAMA_BF16 && (c.head_dim != 128 || g > 8))
+    return fail(NIYAMA_EUNSUPPORTED, "bf16: the fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
+  if (c.dtype == NIYAMA_F32 && (c.head_dim > 128 || g > 8))
+    return fail(NIYAMA_EUNSUPPORTED, "f32: head_dim <= 128 and Hq/Hkv <= 8");
   auto* kv = new niyama_kv();
   kv->cfg = c;
   kv->hq = c.num_q_heads / c.world_size;
@@ -181,21 +214,14 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
   kv->half_bytes = static_cast<int64_t>(c.num_blocks) * kv->hkv * kv->chunk_bytes;
   // bf16: a (block, kv head)'s K chunk and V^T chunk are adjacent ([layer][block][kv head][K|V]),
   // so a decode stage of B = 16 tokens is ONE 8 KB bulk copy.  f32 (config 1): [layer][K|V][block][kv head].
-  const bool adjacent = c.dtype == NIYAMA_BF16 && !(std::getenv("NIYAMA_KV_SPLIT") && std::atoi(std::getenv("NIYAMA_KV_SPLIT")));
+  const bool adjacent = c.dtype == NIYAMA_BF16;
   kv->chunk_stride = adjacent ? 2 * kv->chunk_bytes : kv->chunk_bytes;
   kv->v_offset = adjacent ? kv->chunk_bytes : kv->half_bytes;
   for (int32_t b = 0; b < c.num_blocks; ++b) kv->free_.insert(kv->free_.end(), b);
-  if (const char* pc = std::getenv("NIYAMA_PREFILL_CTAS")) kv->prefill_cap = std::max(0, std::atoi(pc));
-  if (const char* dw = std::getenv("NIYAMA_DEC_WARPS")) kv->dec_warps_override = std::atoi(dw) == 12 ? 12 : 8;
-  if (const char* td = std::getenv("NIYAMA_TAIL_DIV")) kv->tail_div = std::max(1, std::min(16, std::atoi(td)));
-  if (const char* tm = std::getenv("NIYAMA_TAIL_MIN")) kv->tail_min = std::max(16, (std::atoi(tm) / 16) * 16);
-  if (const char* sl = std::getenv("NIYAMA_SPLIT_LEN")) {
-    const int v = std::atoi(sl);
-    if (v >= 16 && v % 16 == 0) kv->split_override = v;
-  }
   if (c.device != NIYAMA_DEVICE_NONE) {
     kv->has_device = true;
-    cudaError_t e = cudaSetDevice(c.device);
+    DeviceGuard dg(c.device);
+    cudaError_t e = dg.err;
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&kv->num_sms, cudaDevAttrMultiProcessorCount, c.device);
     const size_t bytes = static_cast<size_t>(kv->half_bytes) * 2 * c.num_layers;
     if (e == cudaSuccess) e = cudaMalloc(&kv->pool, bytes);
@@ -214,8 +240,8 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
       uint64_t keep = ~uint64_t(0);
       if (e == cudaSuccess) e = cudaMemPoolSetAttribute(kv->mempool, cudaMemPoolAttrReleaseThreshold, &keep);
     }
-    if (const char* pc = std::getenv("NIYAMA_PLAN_COPY_STREAM")) kv->async_plan = std::atoi(pc) != 0;
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&kv->copy_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess && c.dtype == NIYAMA_BF16) e = configure_attention_bf16();  // per device (this one)
     if (e != cudaSuccess) {
       for (auto& st : kv->stg) {
         if (st.ev) cudaEventDestroy(st.ev);
@@ -235,9 +261,10 @@ extern "C" niyama_status niyama_kv_create(const niyama_kv_config* cfg, niyama_kv
 extern "C" void niyama_kv_destroy(niyama_kv* kv) {
   if (!kv) return;
   if (kv->has_device) {
-    cudaSetDevice(kv->cfg.device);
+    DeviceGuard dg(kv->cfg.device);
     cudaDeviceSynchronize();
     if (kv->comm) ncclCommDestroy(kv->comm);
+    for (cudaEvent_t ev : kv->free_events) cudaEventDestroy(ev);
     if (kv->pool) cudaFree(kv->pool);
     for (auto& st : kv->stg) {
       if (st.h) cudaFreeHost(st.h);
@@ -309,6 +336,8 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
   if (len == 0) return NIYAMA_OK;
   if (!k_out || !v_out) return fail(NIYAMA_EINVAL, "k_out/v_out is NULL");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
   const auto& tbl = it->second.blocks;
   int32_t* d_tbl = nullptr;
   NY_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_tbl), tbl.size() * sizeof(int32_t), s));
@@ -378,6 +407,7 @@ void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
                                pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->g, kv->num_sms);
   pl->grid = r.grid;
   pl->prefill_ctas = r.prefill_ctas;
+  if (kv->tune.prefill_ctas > 0 && pl->n_tiles > 0) pl->prefill_ctas = std::min(kv->tune.prefill_ctas, pl->grid);
 }
 
 }  // namespace
@@ -448,12 +478,13 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     }
   }
   // ---- commit: smallest free ids, descriptor order (R9); remember how to undo it
-  struct Undo { int64_t seq; bool existed; size_t nblocks; int32_t len; };
+  struct Undo { int64_t seq; bool existed; size_t nblocks; int32_t len; uint64_t gen; };
   std::vector<Undo> undo;
   undo.reserve(new_len.size());
   for (auto& [s, n] : new_len) {
     auto it = kv->seqs.find(s);
-    undo.push_back(it == kv->seqs.end() ? Undo{s, false, 0, 0} : Undo{s, true, it->second.blocks.size(), it->second.len});
+    undo.push_back(it == kv->seqs.end() ? Undo{s, false, 0, 0, 0}
+                                        : Undo{s, true, it->second.blocks.size(), it->second.len, it->second.gen});
   }
   auto rollback = [&]() {
     for (auto it = undo.rbegin(); it != undo.rend(); ++it) {
@@ -469,6 +500,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   };
   for (auto& [s, n] : new_len) {
     Seq& q = kv->seqs[s];
+    if (q.gen == 0) q.gen = kv->next_gen++;  // created by this plan
     const int64_t need = std::max<int64_t>(0, ceil_div(n, kv->B) - static_cast<int64_t>(q.blocks.size()));
     for (int64_t k = 0; k < need; ++k) {
       auto fit = kv->free_.begin();
@@ -480,7 +512,8 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   // ---- host metadata
   auto* pl = new niyama_plan();
   pl->kv = kv;
-  for (const auto& u : undo) pl->prev.push_back(niyama_plan::Prev{u.seq, u.existed, u.len});
+  for (const auto& u : undo)
+    pl->prev.push_back(niyama_plan::Prev{u.seq, u.existed, u.len, u.existed ? u.gen : kv->seqs[u.seq].gen});
   pl->stream = reinterpret_cast<cudaStream_t>(stream);
   pl->T = static_cast<int32_t>(T);
   pl->D = D;
@@ -572,7 +605,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
   int32_t max_ctx = 0;
   for (int j = 0; j < D; ++j) max_ctx = std::max(max_ctx, desc->decode_ctx[j]);
   pl->split_len = choose_split_len(pl->sum_ctx, max_ctx, hkv, kv->num_sms);
-  if (kv->split_override > 0 && ceil_div(max_ctx, kv->split_override) <= 4095) pl->split_len = kv->split_override;
+  if (kv->tune.split_len > 0 && ceil_div(max_ctx, kv->tune.split_len) <= 4095) pl->split_len = kv->tune.split_len;
   {
     std::vector<int> order(D);
     for (int j = 0; j < D; ++j) order[j] = j;
@@ -590,7 +623,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     // short units and the warps run dry together.  Boundaries depend only on the
     // row's ctx and batch totals (deterministic results).
     const int32_t q = pl->split_len;
-    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(kv->tail_min, q / kv->tail_div));
+    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(kv->tune.tail_min, q / kv->tune.tail_div));
     auto n_full_of = [&](int32_t L) { return static_cast<int32_t>(ceil_div(L, q)) - 1; };
     int32_t ubase = 0;
     pl->drows.reserve(D);
@@ -683,10 +716,19 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t total = off;
     // upload on the library's copy stream into the staging slot's own device buffer when
     // no live plan holds it (the common case); otherwise from the pool on the caller's stream
-    const bool use_slot = kv->async_plan && stg->owner == nullptr;
+    const bool use_slot = kv->tune.plan_copy_stream && stg->owner == nullptr;
     cudaStream_t s = use_slot ? kv->copy_stream : pl->stream;  // upload stream
-    cudaError_t e = cudaSetDevice(kv->cfg.device);
-    if (use_slot) {
+    DeviceGuard dg(kv->cfg.device);
+    cudaError_t e = dg.err;
+    if (e == cudaSuccess) {  // this plan's own upload event (pooled)
+      if (kv->free_events.empty()) {
+        e = cudaEventCreateWithFlags(&pl->ready, cudaEventDisableTiming);
+      } else {
+        pl->ready = kv->free_events.back();
+        kv->free_events.pop_back();
+      }
+    }
+    if (e == cudaSuccess && use_slot) {
       if (e == cudaSuccess && stg->dcap < total) {
         if (stg->d) e = cudaFree(stg->d);  // grows rarely (first plans, larger batches)
         stg->d = nullptr;
@@ -725,9 +767,11 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       std::memset(h + o_work, 0, meta_bytes - o_work);
       e = cudaMemcpyAsync(pl->dbuf, h, meta_bytes, cudaMemcpyHostToDevice, s);
     }
-    if (e == cudaSuccess) e = cudaEventRecord(stg->ev, s);
+    if (e == cudaSuccess) e = cudaEventRecord(stg->ev, s);  // staging buffer reusable after this
+    if (e == cudaSuccess) e = cudaEventRecord(pl->ready, s);  // every use of the plan waits for this
     if (e != cudaSuccess) {
       rollback();  // the error leaves the pool as it was
+      if (pl->ready) kv->free_events.push_back(pl->ready);
       if (pl->slot >= 0)
         stg->owner = nullptr;
       else if (pl->dbuf)
@@ -736,9 +780,6 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       return fail(NIYAMA_ECUDA, std::string("plan_create: ") + cudaGetErrorString(e));
     }
     stg->pending = true;
-    // (a later plan may re-record this event after kStaging more uploads; waiting on the
-    // later record only waits longer — the upload stream is FIFO and never waits on callers)
-    if (use_slot) pl->ready = stg->ev;
     kv->stg_next = (kv->stg_next + 1) % niyama_kv::kStaging;
     pl->d_slot = reinterpret_cast<int32_t*>(pl->dbuf + o_slot);
     pl->d_tables = reinterpret_cast<int32_t*>(pl->dbuf + o_tbl);
@@ -760,8 +801,9 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
 
 extern "C" void niyama_plan_destroy(niyama_plan* plan) {
   if (!plan) return;
+  if (plan->ready) plan->kv->free_events.push_back(plan->ready);  // re-recorded by a later plan
   if (plan->dbuf) {
-    cudaSetDevice(plan->kv->cfg.device);
+    DeviceGuard dg(plan->kv->cfg.device);
     if (plan->slot >= 0) {  // the slot's buffer may be re-uploaded once this plan's kernels are done
       niyama_kv::Staging& st = plan->kv->stg[plan->slot];
       cudaEventRecord(st.released, plan->stream);
@@ -775,20 +817,29 @@ extern "C" void niyama_plan_destroy(niyama_plan* plan) {
 
 extern "C" niyama_status niyama_plan_rollback(niyama_kv* kv, niyama_plan* plan) {
   if (!kv || !plan || plan->kv != kv) return fail(NIYAMA_EINVAL, "kv/plan mismatch");
+  // An entry applies only to the sequence the plan saw: same id AND same generation (a
+  // released id reused by a later plan is another sequence and is left alone).
+  auto target = [&](const niyama_plan::Prev& pv) -> Seq* {
+    auto sit = kv->seqs.find(pv.seq);
+    return sit == kv->seqs.end() || sit->second.gen != pv.gen ? nullptr : &sit->second;
+  };
+  for (const auto& pv : plan->prev) {  // validate everything before any change
+    const Seq* q = target(pv);
+    if (q && pv.existed && pv.len > q->len)
+      return fail(NIYAMA_ESTATE, "rollback: seq " + std::to_string(pv.seq) + " is shorter than before the plan");
+  }
   for (auto it = plan->prev.rbegin(); it != plan->prev.rend(); ++it) {
-    auto sit = kv->seqs.find(it->seq);
-    if (sit == kv->seqs.end()) continue;  // released meanwhile
+    Seq* q = target(*it);
+    if (!q) continue;  // released (or released and re-created) meanwhile
     if (!it->existed) {
-      for (int32_t b : sit->second.blocks) kv->free_.insert(b);
-      kv->seqs.erase(sit);
+      for (int32_t b : q->blocks) kv->free_.insert(b);
+      kv->seqs.erase(it->seq);
       continue;
     }
-    Seq& q = sit->second;
-    if (it->len > q.len) return fail(NIYAMA_ESTATE, "rollback: sequence shorter than before the plan");
     const size_t keep = static_cast<size_t>(ceil_div(it->len, kv->B));
-    for (size_t k = keep; k < q.blocks.size(); ++k) kv->free_.insert(q.blocks[k]);
-    q.blocks.resize(keep);
-    q.len = it->len;
+    for (size_t k = keep; k < q->blocks.size(); ++k) kv->free_.insert(q->blocks[k]);
+    q->blocks.resize(keep);
+    q->len = it->len;
   }
   plan->prev.clear();
   return NIYAMA_OK;
@@ -881,6 +932,8 @@ extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan
   AppendParams p{};
   st = fill_append(kv, plan, layer, k_new, v_new, p);
   if (st != NIYAMA_OK) return st;
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
   NY_CUDA(wait_plan(plan, stream));
   NY_CUDA(launch_append(p, reinterpret_cast<cudaStream_t>(stream)));
   return NIYAMA_OK;
@@ -938,7 +991,6 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   // g <= 4: 12 decode warps x 2-stage rings; g = 8 (twice the MMA work per byte): 8 x 3
   // (measured: config 2 102.6 -> 99.4 us with 12; config 4 1180 -> 1218 us with 12)
   p.dec_warps = kv->g <= 4 ? 12 : 8;
-  if (kv->dec_warps_override) p.dec_warps = kv->dec_warps_override;
   p.T = plan->T;
   p.Hq = kv->hq;
   p.Hkv = kv->hkv;
@@ -965,17 +1017,15 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
     p.append_total = static_cast<int32_t>(append_pieces(*ap));
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
   NY_CUDA(wait_plan(plan, stream));
-  if (kv->cfg.dtype == NIYAMA_BF16) {
-    if (kv->d != 128 || kv->g > 8)
-      return fail(NIYAMA_EUNSUPPORTED, "bf16 fused kernel is built for head_dim 128 and Hq/Hkv <= 8");
-    static const int grid_cap = std::getenv("NIYAMA_GRID_CAP") ? std::atoi(std::getenv("NIYAMA_GRID_CAP")) : 0;
-    const int grid = grid_cap > 0 ? std::min(grid_cap, plan->grid) : plan->grid;  // diagnostics knob
-    p.prefill_ctas = kv->prefill_cap > 0 ? std::min(kv->prefill_cap, grid) : std::min(plan->prefill_ctas, grid);
+  if (kv->cfg.dtype == NIYAMA_BF16) {  // shapes checked at niyama_kv_create
+    const int grid = kv->tune.grid_cap > 0 ? std::min(kv->tune.grid_cap, plan->grid) : plan->grid;
+    p.prefill_ctas = std::min(plan->prefill_ctas, grid);
     NY_CUDA(launch_attention_bf16(p, grid, s));
     ++plan->launches;
   } else {
-    if (kv->d > 128 || kv->g > 8) return fail(NIYAMA_EUNSUPPORTED, "f32 kernel: head_dim <= 128 and Hq/Hkv <= 8");
     NY_CUDA(launch_attention_generic_f32(p, s));
   }
   return NIYAMA_OK;
@@ -985,6 +1035,23 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
 extern "C" niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf) {
   if (!kv) return fail(NIYAMA_EINVAL, "kv is NULL");
   kv->trace = device_buf;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning* out) {
+  if (!kv || !out) return fail(NIYAMA_EINVAL, "kv/out is NULL");
+  *out = kv->tune;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t) {
+  if (!kv || !t) return fail(NIYAMA_EINVAL, "kv/tuning is NULL");
+  if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
+  if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
+  if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");
+  if (t->tail_min < 16 || t->tail_min % 16) return fail(NIYAMA_EINVAL, "tuning: tail_min must be a multiple of 16");
+  if (t->plan_copy_stream != 0 && t->plan_copy_stream != 1) return fail(NIYAMA_EINVAL, "tuning: plan_copy_stream");
+  kv->tune = *t;
   return NIYAMA_OK;
 }
 
@@ -1004,7 +1071,8 @@ extern "C" niyama_status niyama_comm_init(niyama_kv* kv, const void* nccl_unique
   if (kv->comm) return fail(NIYAMA_EINVAL, "communicator already initialised");
   ncclUniqueId id;
   std::memcpy(&id, nccl_unique_id, sizeof(id));
-  NY_CUDA(cudaSetDevice(kv->cfg.device));
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
   NY_NCCL(ncclCommInitRank(&kv->comm, kv->cfg.world_size, id, kv->cfg.rank));
   return NIYAMA_OK;
 }
@@ -1014,19 +1082,29 @@ extern "C" niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan
   niyama_status st = check_launch(kv, plan, 0);
   if (st != NIYAMA_OK) return st;
   if (!o_full) return fail(NIYAMA_EINVAL, "o_full is NULL");
-  if (kv->cfg.world_size == 1 || plan->T == 0) return NIYAMA_OK;
   if (!kv->comm) return fail(NIYAMA_EINVAL, "niyama_comm_init was not called");
+  if (plan->T == 0) return NIYAMA_OK;
+  // The collective runs at every world size (at 1 it is NCCL's in-place copy), so the
+  // single-GPU path exercises the same call a sharded job makes.
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
   const size_t count = static_cast<size_t>(kv->hq) * plan->T * kv->d;
   uint8_t* base = static_cast<uint8_t*>(o_full);
   const ncclDataType_t ty = kv->cfg.dtype == NIYAMA_BF16 ? ncclBfloat16 : ncclFloat32;
-  NY_NCCL(ncclGroupStart());
-  NY_NCCL(ncclAllGather(base + count * kv->elt * kv->cfg.rank, base, count, ty, kv->comm, s));
+  // Every grouped call is issued and the group always closed, even after an error (an
+  // open group would capture the thread's later NCCL calls, torch's included).
+  ncclResult_t r = ncclGroupStart();
+  if (r != ncclSuccess) return fail(NIYAMA_ENCCL, std::string("ncclGroupStart: ") + ncclGetErrorString(r));
+  ncclResult_t first = ncclAllGather(base + count * kv->elt * kv->cfg.rank, base, count, ty, kv->comm, s);
   if (lse_full) {
     const size_t lc = static_cast<size_t>(kv->hq) * plan->T;
-    NY_NCCL(ncclAllGather(lse_full + lc * kv->cfg.rank, lse_full, lc, ncclFloat32, kv->comm, s));
+    const ncclResult_t r2 = ncclAllGather(lse_full + lc * kv->cfg.rank, lse_full, lc, ncclFloat32, kv->comm, s);
+    if (first == ncclSuccess) first = r2;
   }
-  NY_NCCL(ncclGroupEnd());
+  r = ncclGroupEnd();
+  if (first == ncclSuccess) first = r;
+  if (first != ncclSuccess) return fail(NIYAMA_ENCCL, std::string("all-gather: ") + ncclGetErrorString(first));
   return NIYAMA_OK;
 }
 
@@ -1077,8 +1155,9 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   }
   int64_t n_units = 0;
   if (D > 0) {
-    const int32_t q = choose_split_len(sum_ctx, max_ctx, p.hkv, NIYAMA_PRED_SMS);
-    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(256, q / NIYAMA_TAIL_DIV));
+    int32_t q = choose_split_len(sum_ctx, max_ctx, p.hkv, p.num_sms);
+    if (p.tune.split_len > 0 && ceil_div(max_ctx, p.tune.split_len) <= 4095) q = p.tune.split_len;
+    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(p.tune.tail_min, q / p.tune.tail_div));
     for (int64_t j = 0; j < D; ++j) {
       const int64_t nf = ceil_div(ctx[j], q) - 1;
       n_units += (nf + ceil_div(ctx[j] - nf * q, small)) * p.hkv;
@@ -1088,9 +1167,14 @@ Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int
   r.sum_ctx = static_cast<double>(sum_ctx);
   r.Bd = static_cast<double>(sum_ctx) * p.hkv * p.d * 2.0 * p.elt;
   // 3. CTA split (the planner's rule)
-  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, p.hq / p.hkv, NIYAMA_PRED_SMS);
+  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, p.hq / p.hkv, p.num_sms);
   r.grid = cs.grid;
   r.np = cs.prefill_ctas;
+  if (p.tune.prefill_ctas > 0 && n_tiles > 0) r.np = std::min(p.tune.prefill_ctas, r.grid);
+  if (p.tune.grid_cap > 0 && r.grid > p.tune.grid_cap) {
+    r.grid = p.tune.grid_cap;
+    r.np = std::min(r.np, r.grid);
+  }
   // 4. list scheduling of the queue on the prefill CTAs.  Each tile goes to a CTA
   //    that frees first; CTAs with equal loads are interchangeable, so the loads are
   //    kept as an ascending (load, count) list and up to `count` tiles of a group go
@@ -1453,6 +1537,15 @@ extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, co
 }
 
 extern "C" void niyama_predictor_destroy(niyama_predictor* p) { delete p; }
+
+extern "C" niyama_status niyama_predictor_bind(niyama_predictor* p, const niyama_kv* kv) {
+  if (!p || !kv) return fail(NIYAMA_EINVAL, "predictor/kv is NULL");
+  if (p->hq != kv->hq || p->hkv != kv->hkv || p->d != kv->d || p->elt != kv->elt)
+    return fail(NIYAMA_EINVAL, "predictor shape differs from the kv's local shape");
+  p->num_sms = kv->num_sms;
+  p->tune = kv->tune;
+  return NIYAMA_OK;
+}
 
 // ================================================================ slack (a1)
 extern "C" niyama_status niyama_min_slack(const niyama_decode_qos* decodes, int32_t n, double now, double* slack_out) {

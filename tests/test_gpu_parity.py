@@ -14,7 +14,7 @@ torch = pytest.importorskip("torch")
 if not torch.cuda.is_available():  # pragma: no cover
     pytest.skip("needs a GPU", allow_module_level=True)
 
-from tests.gpu_harness import Run, assert_close, oracle_for, stored_bits, to_host_f64  # noqa: E402
+from tests.gpu_harness import Run, assert_close, oracle_for, stored_bits, to_dev, to_host_f64  # noqa: E402
 
 
 def run_and_compare(wl, rows=None, **kw):
@@ -33,9 +33,19 @@ def run_and_compare(wl, rows=None, **kw):
     return r, assert_close(og, O, lg, L)
 
 
+F32_TOL = 1e-5   # fp32 storage and fp32 SIMT math: rounding ~1e-7 relative, so 1e-5 leaves margin
+
+
 @pytest.mark.parametrize("variant,peaky", [("aligned", False), ("unaligned", False), ("aligned", True)])
 def test_config1_tiny_f32(variant, peaky):
-    run_and_compare(W.config1_tiny(variant, peaky))
+    """Config 1 (fp32) at fp32 tolerance (not the bf16 bar); the achieved error is printed."""
+    wl = W.config1_tiny(variant, peaky)
+    r = Run(wl)
+    o, lse = r.attention()
+    _, _, O, L = oracle_for(wl)
+    ma, rl = assert_close(to_host_f64(o, "f32"), O, lse.cpu().numpy().astype(np.float64), L, max_abs=F32_TOL,
+                          rel_l2=F32_TOL, lse_tol=F32_TOL)
+    print(f"config1 {variant}{' peaky' if peaky else ''}: max_abs={ma:.2e} rel_l2={rl:.2e}")
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "f32"])
@@ -176,12 +186,45 @@ def test_block_permutation_invariant():
     assert torch.equal(o1.view(torch.int16), o2.view(torch.int16)) and torch.equal(l1, l2)
 
 
-def test_multilayer_independent():
-    wl = W.random_hybrid(W.L8B, seed=23, num_prefill=1, max_chunk=100, num_decode=4, max_ctx=300)
-    r = Run(wl, layers=3)
-    o0, _ = r.attention(0)
-    o2, _ = r.attention(2)
-    assert torch.equal(o0.view(torch.int16), o2.view(torch.int16))
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_multilayer_distinct_kv_one_plan(dtype):
+    """32 layers, each with its OWN K/V/Q values (W.revalue), appended and attended with
+    ONE plan per iteration reused by every layer — the real per-iteration pattern (the
+    plan's split-completion counters advance one epoch per launch).  Every layer must
+    match the oracle run on that layer's values; a kernel that ignored the layer offset
+    or mis-counted epochs fails."""
+    import paper_2503_22562_b200 as ny
+    shape = W.L8B if dtype == "bf16" else W.TINY
+    base = W.random_hybrid(shape, seed=23, num_prefill=2, max_chunk=200, num_decode=10, max_ctx=2500)
+    layers = [W.revalue(base, 500 + l) for l in range(32)]
+    s = shape
+    kv = ny.KVCache(32, s.num_q_heads, s.num_kv_heads, s.head_dim, base.num_blocks, block_size=s.block_size,
+                    dtype=s.dtype, device=0)
+    for n, st in enumerate(base.steps):
+        plan = kv.plan(st.desc)          # one plan per iteration ...
+        for l in range(32):              # ... used by every layer
+            kv.append(plan, l, to_dev(layers[l].steps[n].k, s.dtype), to_dev(layers[l].steps[n].v, s.dtype))
+    info = plan.info()
+    if dtype == "bf16":
+        assert info.num_decode_units > info.num_decode * s.num_kv_heads   # rows are split (a6 merges run)
+    T = base.final.desc.num_rows
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    outs = []
+    for l in range(32):
+        o = torch.full((s.num_q_heads, T, s.head_dim), float("nan"), dtype=tdt, device="cuda")
+        lse = torch.full((s.num_q_heads, T), float("nan"), dtype=torch.float32, device="cuda")
+        kv.attention(plan, l, to_dev(layers[l].final.q, s.dtype), o, lse)
+        outs.append((o, lse))
+    torch.cuda.synchronize()
+    tol = {} if dtype == "bf16" else dict(max_abs=F32_TOL, rel_l2=F32_TOL, lse_tol=F32_TOL)
+    prev = None
+    for l in range(32):
+        _, _, O, L = oracle_for(layers[l])
+        og = to_host_f64(outs[l][0], dtype)
+        assert_close(og, O, outs[l][1].cpu().numpy().astype(np.float64), L, **tol)
+        if prev is not None:
+            assert not np.array_equal(og, prev)   # the layers really differ
+        prev = og
 
 
 def test_empty_batch_noop_and_errors():

@@ -4,7 +4,8 @@ Every rank of a head-sharded job runs the same planner and its own kernels over 
 kv heads; only the all-gather exchanges data.  With one GPU available the ranks are
 run as separate library instances (world_size G, rank r) on cuda:0 writing their
 head slices of one head-major output, which must equal the full fp64 oracle; the
-NCCL all-gather itself is exercised at world size 1 (an in-place no-op copy)."""
+NCCL all-gather itself runs at world size 1 (ncclAllGather is issued at every world
+size; at 1 it is NCCL's in-place copy)."""
 import numpy as np
 import pytest
 import torch
@@ -36,6 +37,16 @@ def test_head_sharded_ranks_match_full_oracle(world):
         torch.cuda.synchronize()
     _, _, O, L = oracle_for(wl)
     assert_close(to_host_f64(o_full, "bf16"), O, lse_full.double().cpu().numpy(), L)
+
+
+def test_allgather_needs_comm_init():
+    import paper_2503_22562_b200 as ny
+    kv = ny.KVCache(1, 8, 2, 128, 16, dtype="bf16", device=0)
+    p = kv.plan(W.BatchDesc([0], [0], [5]))
+    o = torch.zeros((8, 5, 128), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ny.NiyamaError) as e:
+        kv.allgather_heads(p, o)
+    assert e.value.status == 1   # EINVAL
 
 
 def test_nccl_allgather_world1_inplace():

@@ -42,7 +42,7 @@ def test_golden_tables_through_c_abi():
     p = fx["pool"]
     # the library needs block_size >= 16: scale the fixture's block size 4 -> 16 by
     # scaling every length by 4 (ceil(4n/16) == ceil(n/4)); slots scale the same way.
-    kv = ny.KVCache(1, 1, 1, 64, p["num_blocks"], block_size=16, dtype="bf16", device=None)
+    kv = ny.KVCache(1, 1, 1, 128, p["num_blocks"], block_size=16, dtype="bf16", device=None)
     codes = {"EINVAL": NB.EINVAL, "ENOBLOCKS": NB.ENOBLOCKS, "ENOSEQ": NB.ENOSEQ, "ESTATE": NB.ESTATE}
     for st in fx["steps"]:
         if st["op"] == "release":
@@ -176,6 +176,115 @@ def test_plan_rollback_matches_oracle_truncate():
         kv.seq_len(777)
     # replaying the same plan lands in the same blocks and slots
     assert kv.plan(nxt).slots() == [tuple(x) for x in pool.plan(nxt).slots]
+
+
+def test_plan_rollback_equals_oracle_truncate_and_release():
+    """niyama_plan_rollback == the oracle's truncate of every sequence the plan extended back
+    to its old length plus release of every sequence it created (R9), compared on block
+    tables, lengths and the free list (the next allocation's ids)."""
+    shape = W.Shape(num_q_heads=8, num_kv_heads=2, head_dim=128, block_size=16, dtype="bf16")
+    for seed in range(4):
+        wl = W.random_hybrid(shape, seed=50 + seed, num_prefill=3, max_chunk=150, num_decode=7, max_ctx=400,
+                             extra_blocks=96)
+        kv, pool, _ = replay_both(wl)
+        d = wl.final.desc
+        old = dict(pool.length)
+        nxt = W.BatchDesc(prefill_seq=list(d.prefill_seq) + [900 + seed], prefill_offset=[o + c for o, c in zip(
+            d.prefill_offset, d.prefill_len)] + [0], prefill_len=[17 + 9 * seed] * len(d.prefill_seq) + [45],
+            decode_seq=list(d.decode_seq), decode_ctx=[c + 1 for c in d.decode_ctx])
+        p = kv.plan(nxt)
+        pool.plan(nxt)
+        p.rollback()
+        for s_, n in old.items():
+            pool.truncate(s_, n)
+        pool.release(900 + seed)
+        assert kv.num_free() == len(pool.free)
+        for s_ in pool.table:
+            assert kv.block_table(s_) == pool.table[s_] and kv.seq_len(s_) == pool.length[s_]
+        probe = W.BatchDesc([5000], [0], [16 * 20 + 3])
+        assert kv.plan(probe).slots() == [tuple(x) for x in pool.plan(probe).slots]
+
+
+def test_kv_truncate_matches_oracle():
+    shape = W.Shape(num_q_heads=8, num_kv_heads=2, head_dim=128, block_size=16, dtype="bf16")
+    wl = W.random_hybrid(shape, seed=77, num_prefill=3, max_chunk=200, num_decode=6, max_ctx=600)
+    kv, pool, _ = replay_both(wl)
+    g = np.random.default_rng(5)
+    for s_ in list(pool.table):
+        n = int(g.integers(0, pool.length[s_] + 1))
+        kv.truncate(s_, n)
+        pool.truncate(s_, n)
+        assert kv.block_table(s_) == pool.table[s_] and kv.num_free() == len(pool.free)
+    with pytest.raises(ny.NiyamaError):
+        kv.truncate(list(pool.table)[0], 10 ** 6)
+
+
+def test_rollback_validates_before_any_change():
+    """an ESTATE rollback must not have rolled back earlier entries."""
+    kv = host_kv(W.L8B, 64)
+    kv.plan(W.BatchDesc([1, 2], [0, 0], [40, 40]))
+    p = kv.plan(W.BatchDesc([1, 2], [40, 40], [30, 30]))   # both -> 70
+    kv.truncate(2, 10)                                     # seq 2 now shorter than before the plan
+    t1 = kv.block_table(1)
+    with pytest.raises(ny.NiyamaError) as e:
+        p.rollback()
+    assert e.value.status == NB.ESTATE
+    assert kv.seq_len(1) == 70 and kv.block_table(1) == t1  # untouched
+
+
+def test_rollback_skips_reused_seq_id():
+    """a late rollback must not free the blocks of a later sequence that reuses
+    a released id (identity = id + creation generation)."""
+    kv = host_kv(W.L8B, 64)
+    p = kv.plan(W.BatchDesc([7], [0], [50]))     # creates seq 7
+    kv.release(7)
+    kv.plan(W.BatchDesc([7], [0], [20]))         # a new seq 7
+    t = kv.block_table(7)
+    free = kv.num_free()
+    p.rollback()
+    assert kv.seq_len(7) == 20 and kv.block_table(7) == t and kv.num_free() == free
+
+
+def test_unsupported_shapes_rejected_at_create():
+    for args, dt in [((1, 8, 8, 64), "bf16"), ((1, 32, 2, 128), "bf16"), ((1, 8, 8, 256), "f32"),
+                     ((1, 32, 2, 64), "f32")]:
+        with pytest.raises(ny.NiyamaError) as e:
+            ny.KVCache(*args, 64, dtype=dt, device=None)
+        assert e.value.status == NB.EUNSUPPORTED
+    ny.KVCache(1, 64, 8, 128, 64, dtype="bf16", device=None)   # g = 8 supported
+    ny.KVCache(1, 4, 2, 64, 64, dtype="f32", device=None)      # config 1
+
+
+def test_tuning_roundtrip_validation_and_effect():
+    kv = host_kv(W.L8B, 4096)
+    t = kv.tuning()
+    assert (t.prefill_ctas, t.split_len, t.tail_div, t.tail_min, t.grid_cap, t.plan_copy_stream) == \
+        (0, 0, 4, 256, 0, 1)
+    for bad in ({"split_len": 24}, {"tail_div": 0}, {"tail_min": 8}, {"prefill_ctas": -1}, {"plan_copy_stream": 2}):
+        with pytest.raises(ny.NiyamaError) as e:
+            kv.set_tuning(**bad)
+        assert e.value.status == NB.EINVAL
+    assert kv.tuning().split_len == 0          # a rejected call changes nothing
+    ctx = W.l8b_decode_ctx()
+    wl = W.hybrid(W.L8B, "tune", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
+    kv = host_kv(W.L8B, wl.num_blocks)
+    kv.set_tuning(split_len=512, prefill_ctas=7)
+    for st in wl.steps:
+        p = kv.plan(st.desc)
+    assert p.info().split_len == 512 and p.info().prefill_ctas == 7
+
+
+def test_predictor_bind_uses_kv_tuning():
+    kv = host_kv(W.L8B, 64)
+    pr = ny.Predictor.from_params(CFG, THETA)
+    b = W.BatchDesc([0], [1536], [512], decode_seq=list(range(1, 65)), decode_ctx=W.l8b_decode_ctx().tolist())
+    t0 = pr.predict(b)
+    kv.set_tuning(prefill_ctas=2)
+    pr.bind(kv)
+    assert pr.predict(b) != t0                 # the CTA split it models changed
+    kv70 = ny.KVCache(1, 64, 8, 128, 64, dtype="bf16", device=None)
+    with pytest.raises(ny.NiyamaError):
+        pr.bind(kv70)                          # another local shape
 
 
 def test_head_shard_config():

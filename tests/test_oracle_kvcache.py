@@ -85,3 +85,36 @@ def test_zero_length_slice_registers_seq():
     assert plan.rows == [] and pool.length[5] == 0 and pool.table[5] == []
     plan = pool.plan(W.BatchDesc(decode_seq=[5], decode_ctx=[1]))
     assert plan.rows == [(5, 0, 1)] and plan.slots == [(0, 0)]
+
+
+def test_truncate_hand_worked():
+    """KVPool.truncate (R9: a sequence of n tokens owns ceil(n/B) blocks; freed blocks are
+    the smallest-free candidates again), hand-worked at B = 4 with 8 blocks:
+      seq 1 gets 10 tokens -> blocks [0, 1, 2]; seq 2 gets 6 -> [3, 4]; free [5, 6, 7]
+      truncate(1, 5): keeps ceil(5/4) = 2 blocks [0, 1]; block 2 freed -> free [2, 5, 6, 7]
+      truncate(1, 4): keeps 1 block [0]; free [1, 2, 5, 6, 7]
+      truncate(2, 0): keeps 0 blocks; free [1, 2, 3, 4, 5, 6, 7]
+      seq 3 gets 9 tokens -> the 3 smallest free ids [1, 2, 3]
+      truncate(1, 4) again is a no-op; truncate(1, 5) (> cached 4) is EINVAL, unknown seq ENOSEQ."""
+    pool = K.KVPool(1, 1, 2, 4, 8, "f32")
+    pool.plan(W.BatchDesc([1, 2], [0, 0], [10, 6]))
+    assert pool.table == {1: [0, 1, 2], 2: [3, 4]} and pool.free == [5, 6, 7]
+    pool.truncate(1, 5)
+    assert pool.table[1] == [0, 1] and pool.length[1] == 5 and pool.free == [2, 5, 6, 7]
+    pool.truncate(1, 4)
+    assert pool.table[1] == [0] and pool.free == [1, 2, 5, 6, 7]
+    pool.truncate(2, 0)
+    assert pool.table[2] == [] and pool.length[2] == 0 and pool.free == [1, 2, 3, 4, 5, 6, 7]
+    plan = pool.plan(W.BatchDesc([3], [0], [9]))
+    assert pool.table[3] == [1, 2, 3] and [tuple(s) for s in plan.slots][:5] == [(1, 0), (1, 1), (1, 2), (1, 3), (2, 0)]
+    pool.truncate(1, 4)
+    assert pool.table[1] == [0]
+    with pytest.raises(K.OracleError) as e:
+        pool.truncate(1, 5)
+    assert e.value.code == K.EINVAL
+    with pytest.raises(K.OracleError) as e:
+        pool.truncate(99, 0)
+    assert e.value.code == K.ENOSEQ
+    # a truncated sequence resumes at its new length (prefill offset = cached length, R4)
+    pool.plan(W.BatchDesc([1], [4], [3]))
+    assert pool.table[1] == [0, 4] and pool.length[1] == 7

@@ -1,4 +1,4 @@
-"""Prefill-CTA share sweep: attention launch time vs NIYAMA_PREFILL_CTAS for several
+"""Prefill-CTA share sweep: attention launch time vs the niyama_tuning prefill_ctas cap for several
 batch shapes (diagnostic for the runtime's prefill/decode CTA split policy)."""
 import json
 import os
@@ -24,11 +24,8 @@ def main():
     caps = [int(x) for x in sys.argv[2].split(",")] if len(sys.argv) > 2 else CAPS
     res = {}
     for cap in caps:
-        if cap:
-            os.environ["NIYAMA_PREFILL_CTAS"] = str(cap)
-        else:
-            os.environ.pop("NIYAMA_PREFILL_CTAS", None)
         rig = Rig(W.L8B, num_blocks=256 * 4096 // 16 + 8192)
+        rig.kv.set_tuning(prefill_ctas=cap)
         for (c, o, D) in SHAPES:
             ctx = W.l8b_decode_ctx(D).tolist() if D else []
             t, T = rig.measure(c, o, ctx, 9)

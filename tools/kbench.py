@@ -16,10 +16,12 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).cuda().view(torch.bfloat16)
 
 
-def setup(wl):
+def setup(wl, tuning=None):
     s = wl.shape
     kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 16, block_size=s.block_size,
                     dtype=s.dtype, device=0)
+    if tuning:
+        kv.set_tuning(**tuning)   # niyama_tuning fields (include/niyama.h)
     plan = None
     for st in wl.steps:
         plan = kv.plan(st.desc)
@@ -32,8 +34,8 @@ def setup(wl):
     return kv, plan, q, o, lse
 
 
-def time_it(wl, reps=50, trace=False):
-    kv, plan, q, o, lse = setup(wl)
+def time_it(wl, reps=50, trace=False, tuning=None):
+    kv, plan, q, o, lse = setup(wl, tuning)
     for _ in range(5):
         kv.attention(plan, 0, q, o, lse)
     # back-to-back launches (no host sync in between, so host launch latency is hidden)

@@ -265,6 +265,15 @@ def sweep_point(chunk: int, num_decode: int, seed: int, shape: Shape = L8B, max_
                   decode_ctx=ctx, seed=seed + 77)
 
 
+def revalue(wl: Workload, seed: int, q_scale: float = 1.0) -> Workload:
+    """The same batches (descriptors, shapes) with fresh Q/K/V values from PCG64(seed):
+    another layer of the same iterations (a model's layers see the same batch
+    composition with different activations)."""
+    g = rng(seed)
+    steps = [make_step(g, wl.shape, st.desc, with_q=st.q is not None, q_scale=q_scale) for st in wl.steps]
+    return Workload(name=f"{wl.name}-v{seed}", shape=wl.shape, steps=steps, num_blocks=wl.num_blocks)
+
+
 def random_hybrid(shape: Shape, seed: int, *, num_prefill: int = 1, max_chunk: int = 300,
                   num_decode: int = 8, max_ctx: int = 700, q_scale: float = 1.0,
                   extra_blocks: int = 0) -> Workload:
