@@ -1,13 +1,13 @@
-"""Config 3 — dynamic-chunking sweep: measure the hybrid attention launch on B200 over
-chunk {256, 512, 1024, 2048} x decodes {16, 32, 64, 128, 256} x 3 seeds (ShareGPT-like
-lengths, workloads.sweep_point), fit niyama_predict_iter_time (a8) on two seeds, and
-report its error on the held-out seed plus off-grid points.  Also the fig:chunk-perf
-analogue ("28% lower" throughput at small chunk): attention tokens/s at chunk
-256 vs 2048.  Timing: CUDA events around each launch, median of N reps, L2 flushed
-(512 MB scratch write) before every rep.  K/V values are drawn on the device (timing
-only; parity is covered by tests/).  Writes profiles/predictor_fit.json.
+"""Config 3 — dynamic-chunking sweep (a8 training and held-out data): measure the hybrid
+attention launch on B200 over chunk {256, 512, 1024, 2048} x decodes {16, 32, 64, 128,
+256} x 3 seeds (ShareGPT-like lengths, workloads.sweep_point), 40 off-grid points and
+--train-random random points over the whole (c, D) space (incl. prefill-only and
+decode-only batches).  Timing: CUDA events around ONE launch, median (and p10/p90) of
+--reps reps, L2 flushed before every rep by reading a 512 MB buffer.  K/V values are
+drawn on the device (timing only; parity is covered by tests/).  Writes the raw points;
+tools/fit_predictor.py fits and evaluates (CPU, no GPU needed).
 
-    python tools/sweep_predictor.py [--reps 15] [--out profiles/predictor_fit.json]
+    python tools/sweep_predictor.py [--reps 50] [--raw profiles/r02/predictor_sweep_l8b.json]
 """
 import argparse
 import json
@@ -41,11 +41,16 @@ def point_desc(chunk, D, seed, max_ctx=8192):
 
 
 class Rig:
-    def __init__(self, shape, num_blocks):
+    def __init__(self, shape, num_blocks, flush="read"):
         self.s = shape
         self.kv = ny.KVCache(1, shape.num_q_heads, shape.num_kv_heads, shape.head_dim, num_blocks,
                              block_size=shape.block_size, dtype="bf16", device=0)
-        self.scratch = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        # L2 flush by READING 512 MB (a write flush leaves ~126 MB of dirty lines whose
+        # write-back lands inside the next timed launch: +~20 us and noise)
+        self.scratch = torch.ones(256 << 20, dtype=torch.float16, device="cuda")
+        self.sink = torch.empty((), dtype=torch.float32, device="cuda")
+        self.flush = flush
+        self.want_trace = False
         self.gen = torch.Generator(device="cuda")
         self.gen.manual_seed(0)
 
@@ -78,13 +83,32 @@ class Rig:
             kv.attention(plan, 0, q, out)
         ts = []
         for _ in range(reps):
-            self.scratch.fill_(1)
+            if self.flush == "read":
+                torch.sum(self.scratch, dtype=torch.float32, out=self.sink)
+            else:
+                self.scratch.fill_(1)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             kv.attention(plan, 0, q, out)
             b.record()
             b.synchronize()
             ts.append(a.elapsed_time(b) * 1e-3)
+        self.last_trace = None
+        if self.want_trace:
+            # one more flushed launch with the per-CTA timeline on (niyama_debug_trace):
+            # entry, start, prefill end, decode end, exit (ns from the first entry), tiles done
+            buf = torch.zeros(160 * 8 + 10 * 64, dtype=torch.int64, device="cuda")
+            kv.debug_trace(buf)
+            torch.sum(self.scratch, dtype=torch.float32, out=self.sink)
+            kv.attention(plan, 0, q, out)
+            torch.cuda.synchronize()
+            kv.debug_trace(None)
+            tr = buf.cpu().numpy()[:160 * 8].reshape(160, 8)
+            tr = tr[tr[:, 0] > 0]
+            e0 = int(tr[:, 6].min())
+            self.last_trace = {"entry_ns": (tr[:, 6] - e0).tolist(), "start_ns": (tr[:, 0] - e0).tolist(),
+                               "prefill_end_ns": (tr[:, 1] - e0).tolist(), "decode_end_ns": (tr[:, 4] - e0).tolist(),
+                               "exit_ns": (tr[:, 2] - e0).tolist(), "tiles": tr[:, 3].tolist()}
         plan.close()
         p.close()
         for sq in [0] + seqs:
@@ -100,78 +124,61 @@ def plan_fields(rig):
                 p90=float(np.percentile(rig.last_ts, 90)))
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--reps", type=int, default=15)
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "predictor_fit.json"))
-    ap.add_argument("--offgrid", type=int, default=20)
-    args = ap.parse_args()
-    s = W.L8B
-    rig = Rig(s, num_blocks=256 * 8192 // 16 + 8192)
-    cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, "bf16")
+def sweep(args):
+    s = W.L8B if args.config == "l8b" else W.L70B
+    rig = Rig(s, num_blocks=args.max_decode * 8192 // 16 + 8192, flush=args.flush)
     rows = []
     t0 = time.time()
+
+    def run(kind, seed, chunk, D):
+        o, ctx = point_desc(max(chunk, 1), D, seed)
+        if chunk == 0:
+            o = 0
+        rig.want_trace = args.trace_every > 0 and len(rows) % args.trace_every == 0
+        t, T = rig.measure(chunk, o, ctx, args.reps)
+        rows.append(dict(kind=kind, seed=seed, chunk=chunk, offset=o, D=D, sum_ctx=int(sum(ctx)),
+                         seconds=t, T=T, ctx=ctx, **plan_fields(rig)))
+        if rig.last_trace is not None:
+            rows[-1]["trace"] = rig.last_trace
+        print(f"{kind:8s} seed={seed:4d} c={chunk:5d} o={o:5d} D={D:3d} sumctx={sum(ctx):8d} t={t*1e6:8.1f}us", flush=True)
+
     for seed in range(3):
         for chunk in (256, 512, 1024, 2048):
             for D in (16, 32, 64, 128, 256):
-                o, ctx = point_desc(chunk, D, seed)
-                t, T = rig.measure(chunk, o, ctx, args.reps)
-                rows.append(dict(kind="grid", seed=seed, chunk=chunk, offset=o, D=D, sum_ctx=int(sum(ctx)),
-                                 seconds=t, T=T, ctx=ctx, **plan_fields(rig)))
-                print(f"seed={seed} c={chunk:5d} o={o:5d} D={D:3d} sumctx={sum(ctx):8d} t={t*1e6:8.1f}us", flush=True)
+                run("grid", seed, chunk, min(D, args.max_decode))
     g = np.random.default_rng(123)
     for i in range(args.offgrid):
-        chunk = int(g.integers(1, 2049))
-        D = int(g.integers(1, 257))
-        o, ctx = point_desc(chunk, D, 100 + i)
-        t, T = rig.measure(chunk, o, ctx, args.reps)
-        rows.append(dict(kind="offgrid", seed=100 + i, chunk=chunk, offset=o, D=D, sum_ctx=int(sum(ctx)),
-                         seconds=t, T=T, ctx=ctx, **plan_fields(rig)))
-        print(f"offgrid c={chunk:5d} o={o:5d} D={D:3d} t={t*1e6:8.1f}us", flush=True)
+        run("offgrid", 100 + i, int(g.integers(1, 2049)), int(g.integers(1, args.max_decode + 1)))
+    g = np.random.default_rng(456)
+    for i in range(args.train_random):
+        # random training points over the whole space, including prefill-only (D = 0)
+        # and decode-only (c = 0) batches
+        u = g.random()
+        chunk = 0 if u < 0.08 else int(g.integers(1, 2049))
+        D = 0 if 0.08 <= u < 0.16 else int(g.integers(1, args.max_decode + 1))
+        run("random", 1000 + i, chunk, D)
+    return rows, time.time() - t0
 
-    def sample(r):
-        class S:
-            pass
-        x = S()
-        x.chunk_len, x.chunk_offset, x.num_decode, x.sum_ctx, x.seconds = r["chunk"], r["offset"], r["D"], r["sum_ctx"], r["seconds"]
-        return x
 
-    train = [r for r in rows if r["kind"] == "grid" and r["seed"] != 2]
-    held = [r for r in rows if r["kind"] == "offgrid" or (r["kind"] == "grid" and r["seed"] == 2)]
-    pred = ny.Predictor.fit(cfg, [sample(r) for r in train])
-    theta = pred.params().tolist()
-
-    def err(r):
-        # held-out and training points are evaluated on their real decode contexts
-        d = W.BatchDesc(prefill_seq=[0] if r["chunk"] else [], prefill_offset=[r["offset"]] if r["chunk"] else [],
-                        prefill_len=[r["chunk"]] if r["chunk"] else [], decode_seq=list(range(1, r["D"] + 1)),
-                        decode_ctx=list(r["ctx"]))
-        return pred.predict(d) / r["seconds"] - 1.0
-
-    e_train = np.abs([err(r) for r in train])
-    e_held = np.abs([err(r) for r in held])
-    # fig:chunk-perf analogue: attention tokens/s per chunk size (mean over D, seeds)
-    perf = {}
-    for c in (256, 512, 1024, 2048):
-        rs = [r for r in rows if r["kind"] == "grid" and r["chunk"] == c]
-        perf[c] = float(np.mean([r["T"] / r["seconds"] for r in rs]))
-    out = {"config": "l8b", "world": 1, "theta": theta,
-           "params": ["c0", "per row (c+D)", "per decode", "per ctx token", "max(T_d,T_p)", "min(T_d,T_p)",
-                      "tau s/step", "r_cta B/s", "BW B/s"],
-           "model": "a8 schedule model (include/niyama.h, DESIGN.md)",
-           "train_points": len(train), "heldout_points": len(held),
-           "train_rel_err": {"p50": float(np.median(e_train)), "p95": float(np.percentile(e_train, 95)),
-                             "max": float(e_train.max())},
-           "heldout_rel_err": {"p50": float(np.median(e_held)), "p95": float(np.percentile(e_held, 95)),
-                               "max": float(e_held.max())},
-           "chunk_perf_tokens_per_s": perf,
-           "chunk256_vs_2048_throughput_ratio": perf[256] / perf[2048],
-           "paper_context": "P:71 reports 28% lower full-model throughput at small chunk on A100 (ratio ~0.72)",
-           "reps": args.reps, "timing": "median of reps, CUDA events, L2 flushed (512 MB write) before each rep",
-           "points": rows, "wall_s": time.time() - t0}
-    os.makedirs(os.path.dirname(args.out), exist_ok=True)
-    json.dump(out, open(args.out, "w"), indent=1)
-    print(json.dumps({k: v for k, v in out.items() if k != "points"}, indent=1))
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="l8b", choices=["l8b", "l70b"])
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--flush", default="read", choices=["read", "write"])
+    ap.add_argument("--offgrid", type=int, default=40)
+    ap.add_argument("--train-random", type=int, default=120)
+    ap.add_argument("--max-decode", type=int, default=256)
+    ap.add_argument("--trace-every", type=int, default=3, help="per-CTA timeline of every k-th point (0 = none)")
+    ap.add_argument("--raw", default=os.path.join(ROOT, "profiles", "r02", "predictor_sweep_l8b.json"))
+    args = ap.parse_args()
+    rows, wall = sweep(args)
+    out = {"config": args.config, "world": 1, "device": torch.cuda.get_device_name(0), "reps": args.reps,
+           "timing": f"median of {args.reps} reps, CUDA events around one launch, L2 flushed before every rep "
+                     f"({'512 MB read' if args.flush == 'read' else '512 MB write'})",
+           "points": rows, "wall_s": wall}
+    os.makedirs(os.path.dirname(args.raw), exist_ok=True)
+    json.dump(out, open(args.raw, "w"), indent=1)
+    print(f"{len(rows)} points in {wall:.0f} s -> {args.raw}")
 
 
 if __name__ == "__main__":
