@@ -23,6 +23,7 @@
  *   a3-a6 niyama_append_attention                        (append + attention, ONE launch)
  *   a7 niyama_comm_init + niyama_allgather_heads         (NCCL over NVLink)
  *   a8 niyama_predictor_fit + niyama_predict_iter_time   (host, fp64)
+ *   §8(f)1 niyama_sched_*: QoS scheduler core            (host)
  *
  * Conventions (all calls):
  *  - Every call returns niyama_status unless noted; on error the message is
@@ -357,6 +358,89 @@ typedef struct {
   double t_arrival, slo_ttft, slo_tbt, slo_ttlt; /* seconds */
 } niyama_decode_qos;
 niyama_status niyama_min_slack(const niyama_decode_qos* decodes, int32_t n, double now, double* slack_out);
+
+
+/* ===================================================================== §8(f)1
+ * QoS scheduler core (per replica; P:205 pipeline ①-⑦).  Each iteration:
+ * ① order the prefill queue by the policy's key (NIYAMA: hybrid priority Eq. 4
+ * P:264 interactive P = t_arrival + TTFT + alpha*Prefill_rem, Eq. 5
+ * non-interactive P = t_arrival + TTLT + alpha*(Prefill_rem + Decode_rem), the
+ * decode estimate being mean + 2 std of the app's completed decode lengths,
+ * P:276; FCFS / EDF / SJF / SRPF baselines; ties by arrival
+ * then id); ② check violations (Violated: deadline < now; WillViolate:
+ * deadline < now + Prefill_rem (+ Decode_rem for TTLT), R23); ③ eager
+ * relegation (Low-priority violators first, High ones only in an
+ * iteration that relegated no Low one, R22); the relegated queue is served
+ * (earliest original deadline first) only when no primary candidate is left
+ * (R28); selective preemption (R26); ④ dynamic chunking: the largest
+ * chunk whose predicted batch latency fits the min slack of the running
+ * decodes (bisection as niyama_max_feasible_chunk; relegated decodes do
+ * not bind, R29), or fixed_chunk; ⑤ greedy multi-fill (R27; the last
+ * slice is shrunk if the filled batch predicts above the slack); ⑦ complete():
+ * each running decode emitted one token; finished ones leave (their length
+ * feeds the history); completed prefills enter the decode queue (R21).
+ * Prefill_rem = the cost model's prefill-only time of the remaining prompt in
+ * max_chunk pieces (R24); Decode_rem = estimated tokens x decode_token_s (R25).
+ * Request ids are the KV cache's sequence ids.  Single-threaded. */
+typedef enum {
+  NIYAMA_POLICY_NIYAMA = 0, NIYAMA_POLICY_FCFS = 1, NIYAMA_POLICY_EDF = 2, NIYAMA_POLICY_SJF = 3,
+  NIYAMA_POLICY_SRPF = 4
+} niyama_policy;
+typedef enum { NIYAMA_PREEMPT_NEVER = 0, NIYAMA_PREEMPT_SELECTIVE = 1, NIYAMA_PREEMPT_ALWAYS = 2 } niyama_preemption;
+typedef enum { NIYAMA_QOS_OK = 0, NIYAMA_VIOLATED = 1, NIYAMA_WILL_VIOLATE = 2 } niyama_qos_status;
+typedef struct {
+  int32_t policy;               /* niyama_policy */
+  int32_t preemption;           /* niyama_preemption (ALWAYS = priority order alone) */
+  int32_t dynamic_chunk;        /* 1 = slack-driven chunk; 0 = fixed_chunk (Sarathi baselines) */
+  int32_t fixed_chunk;          /* tokens, >= 0 */
+  int32_t max_chunk;            /* tokens, >= 1 (2K) */
+  int32_t relegation;           /* eager relegation on/off */
+  int32_t multi_fill;           /* several prefill slices per batch */
+  int32_t history_min_samples;  /* completions per app before the history replaces the prior */
+  double alpha;                 /* Eq. 4-5 weight, >= 0 (s of deadline per s of remaining work) */
+  double prior_mean, prior_std; /* decode-length prior (tokens) */
+  double decode_token_s;        /* seconds per decode iteration in Decode_rem (R25) */
+} niyama_sched_config;
+typedef struct {
+  int32_t interactive;          /* 1: TTFT + TBT (Eq. 1-2); 0: TTLT (Eq. 3) */
+  int32_t reserved;
+  double slo_ttft, slo_tbt, slo_ttlt; /* seconds */
+} niyama_qos_spec;
+typedef struct niyama_sched niyama_sched;
+typedef struct {
+  niyama_batch_desc desc;       /* ready for niyama_plan_create; arrays owned by the scheduler, valid until the
+                                   next next_batch / destroy.  Slices in fill order, decodes by (arrival, id);
+                                   tier = the request's submit tier. */
+  int32_t chunk_budget;         /* ④ budget (before the fill) */
+  int32_t infeasible;           /* 1: even a decode-only batch predicts above the slack (budget 0) */
+  double predicted_s;           /* the cost model on desc */
+  double min_slack_s;           /* +INF without binding decodes */
+  int32_t num_relegated;        /* ids relegated by this call */
+  const int64_t* relegated;
+} niyama_sched_batch;
+typedef struct {
+  int32_t state;                /* 0 prefill queue, 1 decode queue, 2 relegated queue, 3 done */
+  int32_t relegated, prefill_done, decoded, prompt, low;
+} niyama_request_info;
+
+void niyama_sched_config_default(niyama_sched_config* cfg); /* NIYAMA, selective, dynamic, 256/2048, relegation,
+                                                               multi-fill, 30, alpha 0, prior 415 +- 300, 50 ms */
+/* model: borrowed (must outlive the scheduler).  EINVAL on a bad config. */
+niyama_status niyama_sched_create(const niyama_sched_config* cfg, const niyama_predictor* model, niyama_sched** out);
+void niyama_sched_destroy(niyama_sched* s);
+/* ① a request arrives (prompt >= 1, new id).  tier 0..255 is copied to the batch desc. */
+niyama_status niyama_sched_submit(niyama_sched* s, int64_t id, double t_arrival, int32_t prompt_tokens,
+                                  const niyama_qos_spec* qos, int32_t low_priority, int32_t app_id, int32_t tier);
+/* ①-⑤ build the iteration's batch at time `now` (ESTATE if the previous non-empty batch was not completed).
+ * An empty batch (no slices, no decodes) needs no complete(). */
+niyama_status niyama_sched_next_batch(niyama_sched* s, double now, niyama_sched_batch* out);
+/* ⑦ the outstanding batch ran and ended at `now`; finished = its decodes that emitted their last token
+ * (EINVAL for any other id; validated before any change). */
+niyama_status niyama_sched_complete(niyama_sched* s, double now, const int64_t* finished, int32_t n_finished);
+niyama_status niyama_sched_request(const niyama_sched* s, int64_t id, niyama_request_info* out);
+niyama_status niyama_sched_counts(const niyama_sched* s, int32_t* counts4); /* requests per state */
+/* The request's policy key at its current state and its violation status at `now` (tests, tools). */
+niyama_status niyama_sched_priority(niyama_sched* s, int64_t id, double now, double* key_out, int32_t* status_out);
 
 #ifdef __cplusplus
 }

@@ -6,7 +6,7 @@ with the same names; PyTorch is used by callers only for device memory,
 streams and process groups.
 """
 from ._binding import (BF16, DEVICE_NONE, F32, Batch, DecodeQoS, KVCache, NiyamaError, Plan, PlanInfo, Predictor, QoSArray,
-                       get_unique_id, lib, min_slack)
+                       SchedBatch, Scheduler, get_unique_id, lib, min_slack)
 
 __all__ = ["BF16", "DEVICE_NONE", "F32", "Batch", "DecodeQoS", "KVCache", "NiyamaError", "Plan", "PlanInfo", "Predictor",
-           "QoSArray", "get_unique_id", "lib", "min_slack"]
+           "QoSArray", "SchedBatch", "Scheduler", "get_unique_id", "lib", "min_slack"]

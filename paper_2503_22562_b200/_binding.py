@@ -63,6 +63,29 @@ class DecodeQoSC(C.Structure):
                 ("slo_tbt", C.c_double), ("slo_ttlt", C.c_double)]
 
 
+class SchedConfigC(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("preemption", C.c_int32), ("dynamic_chunk", C.c_int32),
+                ("fixed_chunk", C.c_int32), ("max_chunk", C.c_int32), ("relegation", C.c_int32),
+                ("multi_fill", C.c_int32), ("history_min_samples", C.c_int32), ("alpha", C.c_double),
+                ("prior_mean", C.c_double), ("prior_std", C.c_double), ("decode_token_s", C.c_double)]
+
+
+class QoSSpecC(C.Structure):
+    _fields_ = [("interactive", C.c_int32), ("reserved", C.c_int32), ("slo_ttft", C.c_double),
+                ("slo_tbt", C.c_double), ("slo_ttlt", C.c_double)]
+
+
+class SchedBatchC(C.Structure):
+    _fields_ = [("desc", BatchDescC), ("chunk_budget", C.c_int32), ("infeasible", C.c_int32),
+                ("predicted_s", C.c_double), ("min_slack_s", C.c_double), ("num_relegated", C.c_int32),
+                ("relegated", C.POINTER(C.c_int64))]
+
+
+class RequestInfoC(C.Structure):
+    _fields_ = [("state", C.c_int32), ("relegated", C.c_int32), ("prefill_done", C.c_int32),
+                ("decoded", C.c_int32), ("prompt", C.c_int32), ("low", C.c_int32)]
+
+
 def _load():
     # NIYAMA_LIB_PATH: load an alternate build of the same library (A/B experiments
     # with tools/build_variant.py); the default is the in-tree libniyama.so.
@@ -108,6 +131,15 @@ def _load():
                                        C.POINTER(i32)], st),
         "niyama_predictor_destroy": ([vp], None),
         "niyama_min_slack": ([C.POINTER(DecodeQoSC), i32, C.c_double, C.POINTER(C.c_double)], st),
+        "niyama_sched_config_default": ([C.POINTER(SchedConfigC)], None),
+        "niyama_sched_create": ([C.POINTER(SchedConfigC), vp, C.POINTER(vp)], st),
+        "niyama_sched_destroy": ([vp], None),
+        "niyama_sched_submit": ([vp, i64, C.c_double, i32, C.POINTER(QoSSpecC), i32, i32, i32], st),
+        "niyama_sched_next_batch": ([vp, C.c_double, C.POINTER(SchedBatchC)], st),
+        "niyama_sched_complete": ([vp, C.c_double, C.POINTER(i64), i32], st),
+        "niyama_sched_request": ([vp, i64, C.POINTER(RequestInfoC)], st),
+        "niyama_sched_counts": ([vp, C.POINTER(i32)], st),
+        "niyama_sched_priority": ([vp, i64, C.c_double, C.POINTER(C.c_double), C.POINTER(i32)], st),
     }
     for name, (args, res) in sigs.items():
         f = getattr(lib, name)
@@ -437,3 +469,106 @@ def min_slack(decodes, now: float) -> float:
     out = C.c_double()
     _check(lib.niyama_min_slack(arr, len(decodes), float(now), C.byref(out)))
     return out.value
+
+
+# ---------------------------------------------------------------- §8(f)1 scheduler
+POLICY = {"niyama": 0, "fcfs": 1, "edf": 2, "sjf": 3, "srpf": 4}
+PREEMPT = {"never": 0, "selective": 1, "always": 2}
+STATE_NAMES = ["prefill", "decode", "relegated", "done"]
+
+
+class SchedBatch:
+    """One iteration's batch from niyama_sched_next_batch (copied out of the scheduler's arrays)."""
+
+    __slots__ = ("slices", "decodes", "tier", "budget", "infeasible", "predicted", "min_slack", "relegated", "raw")
+
+    def __init__(self, c: SchedBatchC):
+        d = c.desc
+        self.slices = [(int(d.prefill_seq[i]), int(d.prefill_offset[i]), int(d.prefill_len[i]))
+                       for i in range(d.num_prefill)]
+        self.decodes = [(int(d.decode_seq[j]), int(d.decode_ctx[j])) for j in range(d.num_decode)]
+        self.tier = [int(d.tier[i]) for i in range(d.num_prefill + d.num_decode)]
+        self.budget, self.infeasible = int(c.chunk_budget), bool(c.infeasible)
+        self.predicted, self.min_slack = float(c.predicted_s), float(c.min_slack_s)
+        self.relegated = [int(c.relegated[i]) for i in range(c.num_relegated)]
+        self.raw = c
+
+    @property
+    def empty(self) -> bool:
+        return not self.slices and not self.decodes
+
+    def desc(self):
+        """A niyama_batch_desc for KVCache.plan (marshalled once)."""
+        class _D:
+            pass
+        x = _D()
+        x.prefill_seq = [s for s, _, _ in self.slices]
+        x.prefill_offset = [o for _, o, _ in self.slices]
+        x.prefill_len = [n for _, _, n in self.slices]
+        x.decode_seq = [s for s, _ in self.decodes]
+        x.decode_ctx = [c for _, c in self.decodes]
+        x.tier = list(self.tier)
+        return _Desc(x)
+
+
+class Scheduler:
+    """niyama_sched: the per-replica QoS scheduler core (include/niyama.h §8(f)1)."""
+
+    def __init__(self, model: "Predictor", policy="niyama", preemption="selective", dynamic_chunk=True,
+                 fixed_chunk=256, max_chunk=2048, relegation=True, multi_fill=True, history_min_samples=30,
+                 alpha=0.0, prior_mean=415.0, prior_std=300.0, decode_token_s=0.05):
+        cfg = SchedConfigC()
+        lib.niyama_sched_config_default(C.byref(cfg))
+        cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
+        cfg.preemption = PREEMPT[preemption] if isinstance(preemption, str) else int(preemption)
+        cfg.dynamic_chunk, cfg.fixed_chunk, cfg.max_chunk = int(bool(dynamic_chunk)), int(fixed_chunk), int(max_chunk)
+        cfg.relegation, cfg.multi_fill = int(bool(relegation)), int(bool(multi_fill))
+        cfg.history_min_samples = int(history_min_samples)
+        cfg.alpha, cfg.prior_mean, cfg.prior_std = float(alpha), float(prior_mean), float(prior_std)
+        cfg.decode_token_s = float(decode_token_s)
+        self.model = model           # keep the borrowed predictor alive
+        h = C.c_void_p()
+        _check(lib.niyama_sched_create(C.byref(cfg), model.handle, C.byref(h)))
+        self.handle = h.value
+
+    def submit(self, rid, t_arrival, prompt, interactive, slo_ttft=0.0, slo_tbt=0.0, slo_ttlt=0.0, low=False,
+               app=0, tier=0):
+        q = QoSSpecC(int(bool(interactive)), 0, float(slo_ttft), float(slo_tbt), float(slo_ttlt))
+        _check(lib.niyama_sched_submit(self.handle, int(rid), float(t_arrival), int(prompt), C.byref(q),
+                                       int(bool(low)), int(app), int(tier)))
+
+    def next_batch(self, now: float) -> SchedBatch:
+        out = SchedBatchC()
+        _check(lib.niyama_sched_next_batch(self.handle, float(now), C.byref(out)))
+        return SchedBatch(out)
+
+    def complete(self, now: float, finished: Sequence[int] = ()):
+        arr = (C.c_int64 * max(1, len(finished)))(*[int(x) for x in finished])
+        _check(lib.niyama_sched_complete(self.handle, float(now), arr, len(finished)))
+
+    def request(self, rid) -> dict:
+        out = RequestInfoC()
+        _check(lib.niyama_sched_request(self.handle, int(rid), C.byref(out)))
+        return dict(state=STATE_NAMES[out.state], relegated=bool(out.relegated), prefill_done=out.prefill_done,
+                    decoded=out.decoded, prompt=out.prompt, low=bool(out.low))
+
+    def counts(self) -> dict:
+        arr = (C.c_int32 * 4)()
+        _check(lib.niyama_sched_counts(self.handle, arr))
+        return dict(zip(STATE_NAMES, list(arr)))
+
+    def priority(self, rid, now: float):
+        k, s = C.c_double(), C.c_int32()
+        _check(lib.niyama_sched_priority(self.handle, int(rid), float(now), C.byref(k), C.byref(s)))
+        return k.value, s.value
+
+    def close(self):
+        if self.handle:
+            lib.niyama_sched_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -5,7 +5,12 @@
 
 #include <cuda_runtime.h>
 
+#include "niyama.h"
+
 namespace niyama {
+
+// Sets niyama_last_error() for this thread and returns s (host translation units).
+niyama_status set_error(niyama_status s, const char* msg);
 
 // KV pool physical layout:
 //   bf16: pool[layer][block][kv_head][K | V^T chunk]   (K and V^T of a block adjacent)

@@ -31,6 +31,12 @@ niyama_status fail(niyama_status s, const std::string& msg) {
   return s;
 }
 
+}  // namespace
+
+niyama_status niyama::set_error(niyama_status s, const char* msg) { return fail(s, msg); }
+
+namespace {
+
 #define NY_CUDA(x)                                                                         \
   do {                                                                                     \
     cudaError_t e_ = (x);                                                                  \

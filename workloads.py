@@ -295,3 +295,68 @@ def random_hybrid(shape: Shape, seed: int, *, num_prefill: int = 1, max_chunk: i
     steps.append(make_step(g, shape, desc, with_q=True, q_scale=q_scale))
     nb = blocks_needed([o + c for o, c in zip(offs, lens)] + ctx, shape.block_size) + extra_blocks
     return Workload(name=f"random-s{seed}", shape=shape, steps=steps, num_blocks=nb)
+
+
+# ---------------------------------------------------------------------------
+# config 5: QoS-tiered arrival traces (inputs of the scheduler; no method arithmetic)
+# ---------------------------------------------------------------------------
+
+# Table 3: three equal buckets; Q1 interactive TTFT 6 s / TBT 50 ms,
+# Q2 / Q3 non-interactive TTLT 600 s / 1800 s.
+TABLE3 = [dict(interactive=True, slo_ttft=6.0, slo_tbt=0.050, slo_ttlt=0.0, share=1 / 3),
+          dict(interactive=False, slo_ttft=0.0, slo_tbt=0.0, slo_ttlt=600.0, share=1 / 3),
+          dict(interactive=False, slo_ttft=0.0, slo_tbt=0.0, slo_ttlt=1800.0, share=1 / 3)]
+
+
+@dataclass
+class TraceRequest:
+    id: int
+    t_arrival: float
+    prompt: int
+    decode: int          # ground truth (the engine's EOS), hidden from the scheduler
+    bucket: int          # index into the trace's bucket list
+    low: bool            # application hint "low priority" (20% per bucket)
+    app: int             # decode-length history key = bucket (one application per bucket)
+
+
+def qos_trace(duration_s: float, qps_schedule, seed: int, dataset=SHAREGPT, low_fraction: float = 0.2,
+              buckets=TABLE3, max_prompt: Optional[int] = None, max_decode: Optional[int] = None) -> List[TraceRequest]:
+    """Poisson arrivals with a piecewise-constant rate: qps_schedule = [(t_start,
+    qps), ...] (inclusive start; P:534's diurnal low/high steps), or a single qps.  Token
+    counts from the dataset's two-percentile lognormals (Table 1), rounded, >= 1
+    (optionally capped); bucket by the shares; Low priority with probability
+    low_fraction within each bucket.  Deterministic given seed (PCG64)."""
+    if not isinstance(qps_schedule, (list, tuple)):
+        qps_schedule = [(0.0, float(qps_schedule))]
+    g = rng(seed)
+    mu_p, sd_p = lognormal_fit(*dataset["prompt"])
+    mu_d, sd_d = lognormal_fit(*dataset["decode"])
+    shares = np.cumsum([b["share"] for b in buckets])
+    out: List[TraceRequest] = []
+    steps = list(qps_schedule) + [(duration_s, 0.0)]
+    for (t0, qps), (t1, _) in zip(steps[:-1], steps[1:]):
+        t = t0
+        while qps > 0:
+            t += g.exponential(1.0 / qps)
+            if t >= min(t1, duration_s):
+                break
+            p = max(1, int(round(g.lognormal(mu_p, sd_p))))
+            d = max(1, int(round(g.lognormal(mu_d, sd_d))))
+            if max_prompt:
+                p = min(p, max_prompt)
+            if max_decode:
+                d = min(d, max_decode)
+            b = int(np.searchsorted(shares, g.random() * shares[-1], side="right"))
+            low = bool(g.random() < low_fraction)
+            out.append(TraceRequest(len(out), float(t), p, d, min(b, len(buckets) - 1), low, min(b, len(buckets) - 1)))
+    return out
+
+
+def diurnal_schedule(duration_s: float, low_qps: float, high_qps: float, period_s: float = 900.0):
+    """load alternates between low and high every 15 minutes."""
+    sched, t, hi = [], 0.0, False
+    while t < duration_s:
+        sched.append((t, high_qps if hi else low_qps))
+        t += period_s
+        hi = not hi
+    return sched
