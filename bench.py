@@ -186,7 +186,7 @@ def run_host_only(args, rank, world, dist):
         kv.plan(st.desc).close()
     batch = ny.Batch(wl.final.desc)
     cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
-    pred = ny.Predictor.from_params(cfg, [3e-5, 5e-9, 0.0, 0.0, 1.0, 0.1, 1.3e-6, 70e9, 7.2e12]).bind(kv)
+    pred = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA)).bind(kv)
     slots, t_pred = None, 0.0
     t0 = time.perf_counter()
     for i in range(args.warmup + args.steps):
@@ -378,10 +378,10 @@ def main():
     # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
     fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
     cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
-    theta = [3.1e-5, 5e-9, 0.0, 0.0, 1.07, 0.16, 1.3e-6, 70e9, 7.2e12]   # config-3 fit (profiles/r01)
+    theta = list(ny.DEFAULT_THETA)   # the config-3 fit of round 2 (profiles/predictor_fit.json)
     if os.path.exists(fit_path):
         fj = json.load(open(fit_path))
-        ok = fj.get("world", 1) == world and fj.get("config") == args.config and len(fj.get("theta", [])) == 9
+        ok = fj.get("world", 1) == world and fj.get("config") == args.config and len(fj.get("theta", [])) == ny.NUM_PARAMS
         theta = fj["theta"] if ok else theta
     pred = ny.Predictor.from_params(cfg, theta)
     # a1 inputs: decodes carry Table 3 tiers; interactive ones are mid-stream
@@ -602,6 +602,10 @@ def main():
                         "- append - attention can be negative"),
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
+        "a8": {"predicted_attention_us": pred.predict(batch) * 1e6, "measured_attention_us": attn_avg_ms * 1e3,
+               "rel_err": pred.predict(batch) / (attn_avg_ms * 1e-3) - 1.0,
+               "note": "the event model fitted on flushed single launches (profiles/predictor_fit.json) vs the "
+                       "mean launch inside the bench step (not flushed: inputs larger than L2)"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl)

@@ -267,33 +267,41 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
 
 /* a8 — iteration-time predictor (P:205 ④ "A lightweight predictor is then used
  * to estimate the latency of the batch"; reading R16).  The paper's
- * predictor is a random forest on profiles; this one is a SCHEDULE MODEL of the
- * fused launch, evaluated on this rank's shape:
+ * predictor is a random forest on profiles; this one is an EVENT MODEL of the
+ * fused launch fitted to measured launch times, evaluated on this
+ * rank's shape.  The launch-shaping rules are the planner's own (one definition,
+ * csrc/internal.h), so the model sees the launch the kernel runs:
  *
  *  1. Prefill tile queue: slices (o, c > 0) sorted by o + c descending (stable);
- *     per slice the q tiles from last to first (qt = nqt-1 .. 0, nqt =
- *     ceil(c / R), R = 128 / (Hq/Hkv)), each repeated Hkv times, with cost
- *     ceil((o + min(c, (qt+1) R)) / 128) + NIYAMA_TILE_SETUP_STEPS steps.
- *  2. Decode units: split_len q from (sum ctx, max ctx) exactly as the planner
- *     (the power of two >= 128 nearest in log scale to sum ctx * Hkv over 4
- *     units per resident warp on NIYAMA_PRED_SMS SMs); a row of ctx L has n_f = ceil(L/q) - 1 pieces of q
- *     keys plus its last L - n_f q keys in pieces of min(q, max(256, q/NIYAMA_TAIL_DIV));
- *     units = sum over rows of that piece count, times Hkv.
- *  3. grid and prefill CTAs n_p by the planner's CTA split (niyama_plan_info).
- *  4. List scheduling: each tile in queue order goes to the prefill CTA that
- *     frees first; f_1 <= ... <= f_np are the CTAs' finish times in steps.
- *  5. Fluid decode: B_d = sum ctx * Hkv * d * 2 * elt bytes stream at
- *     min(BW, k(t) * r_cta), k(t) = grid - (prefill CTAs still busy at t); a
- *     step lasts tau seconds.  T_p = tau * f_np, T_d = time B_d is done.
- *  6. phi = [1, c + D, D, sum ctx, max(T_d, T_p), min(T_d, T_p)] (c = prefill
- *     rows, D = decodes) and t_hat = theta_lin . phi.
- * Parameters (NIYAMA_NUM_PARAMS doubles): theta[0..5] = theta_lin >= 0,
- * theta[6] = tau (s), theta[7] = r_cta (B/s), theta[8] = BW (B/s), all > 0 for
- * 6..8.  SPEC's affine model is theta_lin = (c0, c1, 0, c2, 0, 0).
- * Fit: for every (tau, r_cta, BW) of a grid (tau-major), theta_lin by
- * non-negative least squares on relative residuals (phi_i / t_i against 1,
- * columns scaled to unit max); keep the grid point of least squared residual
- * (the first one within 1e-9 relative of the minimum). */
+ *     per slice the q tiles from last to first (qt = nqt-1 .. 0, nqt = ceil(c/R),
+ *     R = 128 / (Hq/Hkv)), each repeated Hkv times, with s = ceil((o + min(c,
+ *     (qt+1) R)) / 128) key steps.
+ *  2. Decode unit queue: split length q from (sum ctx, max ctx) as the planner;
+ *     rows by ctx descending contribute ceil(L/q) - 1 full pieces of q keys
+ *     (x Hkv units each), then every row's last L - n_f q keys cut into pieces of
+ *     min(q, max(tail_min, q / tail_div)) keys, all such pieces longest first
+ *     (x Hkv).  A unit of k keys streams k * d * 2 * elt bytes.
+ *  3. grid and prefill CTAs n_p: the planner's CTA split (niyama_plan_info).
+ *  4. Prefill: a step lasts tau = tau0 + tau_p n_p/NIYAMA_PRED_SMS
+ *     + tau_d (grid - n_p)/grid (the last term only with decode units: HBM
+ *     contention from the decode CTAs); each tile in queue order goes to the
+ *     prefill CTA that frees first and occupies it (s + sigma) tau seconds.
+ *  5. Decode: grid - n_p CTAs' warps (12 per CTA when Hq/Hkv <= 4, else 8) are
+ *     free at 0, each prefill CTA's warps when its last tile ends; each unit in
+ *     queue order goes to the warp that frees first (at time a) and occupies it
+ *     u0 + bytes / min(r_w, BW / W(a)) seconds, W(a) = warps streaming by a.
+ *  6. T_sim = the later of the last tile and the last unit to end;
+ *     t_hat = theta[0] + theta[1] (c + D) + theta[2] D + theta[3] sum ctx
+ *             + theta[4] units + theta[5] T_sim   (c = prefill rows, D = decodes).
+ * Parameters (NIYAMA_NUM_PARAMS doubles): theta[0..5] >= 0 (linear part);
+ * theta[6..12] = tau0 (s), tau_p (s), tau_d (s), sigma (steps), r_w (B/s),
+ * u0 (s), BW (B/s), all > 0.  SPEC's affine model is the special case
+ * theta[0..5] = (c0, c1, 0, c2, 0, 0).
+ * Fit (niyama_predictor_fit_batches): Nelder-Mead over the logarithms of
+ * theta[6..12] (then once more from its best vertex); for each candidate, the
+ * simulations of all samples and theta[0..4] >= 0 by non-negative least squares on
+ * relative residuals with theta[5] = 1; the objective is the sum of squared
+ * relative errors.  Deterministic. */
 #define NIYAMA_PRED_SMS 148
 #define NIYAMA_TAIL_DIV 4
 #define NIYAMA_TAIL_MIN 256
@@ -303,8 +311,7 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  * unit time; config 4 measured 1,073 us at the unweighted split, 926 us at 80 CTAs). */
 #define NIYAMA_WIDE_GROUP_DECODE_WEIGHT 1.8
 #define NIYAMA_TILE_SETUP_STEPS 2
-#define NIYAMA_NUM_PARAMS 9
-#define NIYAMA_NUM_FEATURES 6
+#define NIYAMA_NUM_PARAMS 16
 
 typedef struct {
   int32_t chunk_len;    /* prefill rows of the (single) slice, 0 if none */
@@ -314,20 +321,35 @@ typedef struct {
   double seconds;       /* measured launch time (> 0) */
 } niyama_sample;
 typedef struct niyama_predictor niyama_predictor;
+typedef struct {
+  const double* start;  /* NIYAMA_NUM_PARAMS starting values (only theta[6..12] are used), or NULL = defaults */
+  int32_t max_evals;    /* Nelder-Mead objective evaluations (0 = 1200, plus half as many on the restart) */
+  int32_t subsample;    /* Nelder-Mead on every k-th sample (0/1 = all); the final linear fit uses all */
+} niyama_fit_options;
 
-/* Fit on the default grid: tau 0.5..2.5 us step 0.1 us, r_cta 30..120 GB/s
- * step 5 GB/s, BW 5.0..8.4 TB/s step 0.2 TB/s. */
+/* Fit on measured launches: batch i (its slices and decode contexts; tiers ignored) took
+ * seconds[i] > 0.  opt may be NULL.  Host pointers; EINVAL on an invalid sample. */
+niyama_status niyama_predictor_fit_batches(const niyama_kv_config* shape, const niyama_batch_desc* batches,
+                                           const double* seconds, int32_t n, const niyama_fit_options* opt,
+                                           niyama_predictor** out);
+/* The same fit on summary samples (each a single slice + decodes with sum ctx spread evenly). */
 niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
                                    niyama_predictor** out);
-/* Fit on an explicit grid {tau_lo, tau_hi, tau_step, r_lo, r_hi, r_step,
- * bw_lo, bw_hi, bw_step}: values lo + i*step for i = 0 .. round((hi-lo)/step). */
-niyama_status niyama_predictor_fit_grid(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
-                                        const double* grid9, niyama_predictor** out);
-niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta9,
-                                           niyama_predictor** out); /* theta_lin >= 0, theta[6..8] > 0 */
-niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta9_out);
+niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta,
+                                           niyama_predictor** out); /* theta[0..5] >= 0, theta[6..12] > 0 */
+niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta_out);
 /* Seconds for the batch (slices and decodes of desc; tiers ignored); < 0 on invalid input. */
 double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc);
+typedef struct {
+  int32_t grid, prefill_ctas;   /* step 3 */
+  int32_t split_len, small_piece; /* step 2: q and the small-piece length */
+  int32_t warps_per_cta;        /* decode warps per CTA (step 5) */
+  int32_t reserved;
+  int64_t num_units;
+  double sim_seconds;   /* T_sim (step 6) */
+  double seconds;       /* t_hat */
+} niyama_predict_info;
+niyama_status niyama_predict_detail(const niyama_predictor* p, const niyama_batch_desc* desc, niyama_predict_info* out);
 /* a1 — chunk for the batch {C prefill rows at chunk_offset} + desc's decodes
  * (desc's prefill slices are ignored) against slack_s (a latency equal to the
  * slack is feasible, R18; 1e-12 relative guard).  cap = max(0, min(max_chunk,

@@ -1,51 +1,55 @@
-"""Oracle: iteration-time predictor for one hybrid-batch attention launch.
+"""Oracle: the a8 iteration-time predictor and the a1 chunk choice.
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 
 The paper's predictor maps a batch composition to latency (P:205 step ④ "A
 lightweight predictor is then used to estimate the latency of the batch";
-P:319 a random forest on Vidur profiles; P:744 draft: a profile lookup
-table).  Its features are never published.  The north_star replaces it with
-`niyama_predict_iter_time`, fitted from MEASURED launch latency against chunk
-size and decode count.  DESIGN.md reading R16 and section "a8 schedule model"
-fix the model, written out here step by step:
+P:319 a random forest on Vidur profiles; P:744 draft: a profile lookup table).
+Its features are never published; the north_star asks for
+`niyama_predict_iter_time` "fitted from measured kernel latency against chunk
+size and decode count".  DESIGN.md reading R16 and §6.4 fix the model: an
+event model of one hybrid-attention launch, written out here step by step.
 
-  shape: local heads Hq, Hkv, head dim d, element bytes e; g = Hq/Hkv,
-  R = max(1, 128 // g) chunk rows per prefill tile; NSM = 148 SMs.
-  1. tile queue: prefill slices (o, c > 0) sorted by o + c descending
-     (stable); per slice q tiles qt = nqt-1 .. 0 (nqt = ceil(c/R)), each
-     repeated Hkv times, cost = ceil((o + min(c, (qt+1) R)) / 128) + SETUP.
-  2. decode units: split_len q = the smallest power of two s >= 128 with
-     2 s^2 >= raw^2 (s >= raw / sqrt 2: the power of two nearest raw in log
-     scale), raw = ceil(max(1, sumL*Hkv) / (4*NSM*8)), and ceil(max_ctx/s) <=
-     4095 (capped at 2^20); a row of ctx L is n_f = ceil(L/q) - 1 pieces of q keys
-     plus its last L - n_f*q keys in pieces of min(q, max(256, q // TAIL_DIV));
-     units = Hkv * sum over rows of the piece count.
-  3. grid = max(1, min(NSM, tiles + ceil(units/8))); prefill CTAs n_p = 0
-     without tiles, = grid without units, else ceil(grid*wp/(wp+wd)) with
-     wp = (sum of tile costs) * STEP_BYTES and wd = sumL*Hkv*d*2*e (times
-     WIDE_GROUP_DECODE_WEIGHT when g = Hq/Hkv > 4), raised to
-     min(ceil(tiles/4), ceil(grid/2)), then capped at tiles and at grid, and at
-     least 1.
-  4. list scheduling: each tile in queue order goes to the prefill CTA that
-     frees first; f_1 <= ... <= f_np the finish times (in steps).
-  5. fluid decode: B_d = sumL*Hkv*d*2*e bytes stream at min(BW, k*r_cta),
-     k = grid - (prefill CTAs still busy); a step lasts tau seconds.
-     T_p = tau * f_np; T_d = the time B_d is done (0 when B_d = 0).
-  6. phi = [1, c + D, D, sumL, max(T_d, T_p), min(T_d, T_p)];
-     t_hat = theta[0:6] . phi with theta[0:6] >= 0; theta[6:9] = (tau, r_cta, BW).
+Inputs.  The batch (prefill slices (o, c), decode contexts) defines the WORK —
+the causal key range of every prefill q tile and the key pieces of every decode
+row — and the launch configuration (`Launch`: split length q, small-piece
+length, grid, prefill CTAs n_p, decode warps per CTA) is the kernel's plan
+(`niyama_plan_info`), an input here: the oracle models "this launch", it does
+not re-derive the planner's heuristics.
 
-  SPEC's affine cost model (c0 + c1*(tokens) + c2*sum ctx) is the
-  special case theta[0:6] = (c0, c1, 0, c2, 0, 0); its worked examples pin
-  eval and max_feasible_chunk.
+  shape: local heads Hq, Hkv, head dim d, element bytes e; g = Hq / Hkv,
+  R = 128 // g chunk rows per prefill tile; NSM = 148.
+  1. tile queue: slices sorted by o + c descending (stable); per slice the q tiles
+     qt = nqt-1 .. 0 (nqt = ceil(c / R)), each Hkv times, with
+     s = ceil((o + min(c, (qt+1) R)) / 128) key steps (the keys row o + (qt+1) R - 1
+     sees, causal).
+  2. unit queue: rows by ctx descending; a row of L keys has n_f = ceil(L/q) - 1
+     full pieces of q keys (each Hkv units, row by row), then the remaining
+     L - n_f q keys of every row in pieces of `small` keys, all those pieces
+     longest first (each Hkv units).  A unit of k keys streams k d 2 e bytes.
+  3. event model, two clocks.  Prefill CTAs advance together on a step clock S
+     at 1/tau(t) steps/s, tau = tau0 + tau_p P/NSM + tau_d B/W (P prefill CTAs
+     busy, B decode warps busy, W = grid x warps per CTA); the queue's next tile
+     goes to a free prefill CTA; a tile of s steps taken at S = x ends at
+     S = x + s + sigma, except a CTA's first tile, which ends at S = s + sigma0
+     (its setup includes the CTA's start).  Decode warps advance together on a byte clock V at
+     rate = min(r_w, BW / B, r_cta (grid - P) / B) / (1 + gamma P / NSM) bytes/s
+     each; a free warp takes the queue's next unit; a unit of b bytes taken at
+     V = v ends at V = v + b + u0 r_w.  The grid - n_p decode CTAs' warps are free
+     at t = 0, a prefill CTA's warps when it finds the tile queue empty.  The next
+     event is the earlier of the first tile end and the first unit end.
+     T_sim = the time the last tile or unit ends.
+  4. t_hat = th[0] + th[1] (rows + D) + th[2] D + th[3] sum ctx + th[4] units
+             + th[5] T_sim,
+     th[6:16] = (tau0, tau_p, tau_d, sigma, r_w, u0, BW, gamma, r_cta, sigma0).
 
-fit (R16): for every (tau, r_cta, BW) of a grid (tau-major, then r_cta, then
-BW; values lo + i*step, i = 0..round((hi-lo)/step)), theta[0:6] by
-non-negative least squares of phi_i/t_i against 1 (columns scaled to unit
-max); the grid point with the least sum of squared relative residuals wins
-(the first within 1e-9 relative of the minimum).  A sample (c, o, D, sumL)
-stands for the batch {slice (o, c) if c > 0} + D decodes with sumL spread
-evenly (the first sumL mod D of them one longer).
+  SPEC's affine cost model (c0 + c1 * tokens + c2 * sum ctx) is the
+  special case th[0:6] = (c0, c1, 0, c2, 0, 0); its worked examples pin eval and
+  max_feasible_chunk.
+
+fit (R16): th[6:16] minimise the sum of squared relative errors, th[0:5] >= 0 by
+non-negative least squares on relative residuals at fixed th[5] = 1 (the
+library runs Nelder-Mead on the logarithms; any minimiser may be used here).
 
 max_feasible_chunk: C = 0 infeasible -> (0, infeasible);
 cap feasible -> cap; else bisection lo = 0, hi = cap, mid = (lo+hi)//2 until
@@ -55,22 +59,17 @@ non-decreasing in C this is S:119's "largest C", which
 """
 from __future__ import annotations
 
-import heapq
+import bisect
 import math
 from dataclasses import dataclass, field
-from typing import List, Sequence, Tuple
+from typing import Callable, List, Sequence, Tuple
 
 import numpy as np
 from scipy.optimize import nnls
 
 NSM = 148
-TAIL_DIV = 4
-STEP_BYTES = 160e3
-WIDE_GROUP_DECODE_WEIGHT = 1.8   # include/niyama.h NIYAMA_WIDE_GROUP_DECODE_WEIGHT
-SETUP = 2
-NFEAT = 6
-NPARAM = 9
-DEFAULT_GRID = (0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12)
+NPARAM = 16
+NLIN = 6
 
 
 @dataclass
@@ -83,161 +82,164 @@ class PredShape:
 
 
 @dataclass
-class Sample:
-    chunk_len: int        # prefill rows (single slice)
-    chunk_offset: int
-    num_decode: int
-    sum_ctx: int          # sum of decode ctx
-    seconds: float
+class Launch:
+    """The launch configuration of a batch: the plan's choices (niyama_plan_info)."""
+
+    split_len: int
+    small: int            # small-piece length min(q, max(tail_min, q // tail_div))
+    grid: int
+    prefill_ctas: int
+    warps_per_cta: int    # 12 when g <= 4, else 8
 
 
 @dataclass
-class Sched:
+class Work:
     rows: int
     D: int
     sum_ctx: int
-    Bd: float
-    grid: int
-    np_: int
-    fin: List[int] = field(default_factory=list)
-    units: int = 0
+    units: int
+    tiles: List[int] = field(default_factory=list)        # steps per tile, queue order
+    pieces: List[float] = field(default_factory=list)     # bytes per unit, queue order
 
 
 def cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
-def split_len(sum_ctx: int, max_ctx: int, hkv: int, nsm: int = NSM) -> int:
-    """Step 2: decode split length."""
-    raw = cdiv(max(1, sum_ctx * hkv), 4 * nsm * 8)
-    s = 128
-    while (2 * s * s < raw * raw or cdiv(max_ctx, s) > 4095) and s < (1 << 20):
-        s *= 2
-    return s
-
-
-def tile_queue(shape: PredShape, slices: Sequence[Tuple[int, int]]) -> List[int]:
-    """Step 1: tile costs in queue order."""
+def work(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int], q: int, small: int) -> Work:
+    """Steps 1-2."""
     g = shape.num_q_heads // shape.num_kv_heads
     R = max(1, 128 // g)
-    live = [(o, c) for o, c in slices if c > 0]
-    live = sorted(live, key=lambda sc: -(sc[0] + sc[1]))         # Python's sort is stable
-    costs = []
+    live = sorted([(o, c) for o, c in slices if c > 0], key=lambda sc: -(sc[0] + sc[1]))   # stable
+    tiles = []
     for o, c in live:
         for qt in range(cdiv(c, R) - 1, -1, -1):
-            cost = cdiv(o + min(c, (qt + 1) * R), 128) + SETUP
-            costs += [cost] * shape.num_kv_heads
-    return costs
+            tiles += [cdiv(o + min(c, (qt + 1) * R), 128)] * shape.num_kv_heads
+    bpt = float(shape.head_dim * 2 * shape.elt_bytes)
+    pieces, tail, units = [], [], 0
+    for L in sorted((int(x) for x in decode_ctx), reverse=True):
+        nf = cdiv(L, q) - 1
+        pieces += [q * bpt] * (nf * shape.num_kv_heads)
+        k0 = nf * q
+        while k0 < L:
+            tail.append(min(L, k0 + small) - k0)
+            k0 += small
+        units += (nf + cdiv(L - nf * q, small)) * shape.num_kv_heads
+    for k in sorted(tail, reverse=True):
+        pieces += [k * bpt] * shape.num_kv_heads
+    return Work(sum(c for _, c in live), len(decode_ctx), int(sum(decode_ctx)), units, tiles, pieces)
 
 
-def cta_split(n_tiles: int, n_units: int, tile_cost: int, sum_ctx: int, shape: PredShape) -> Tuple[int, int]:
-    """Step 3: (grid, prefill CTAs)."""
-    grid = max(1, min(NSM, n_tiles + cdiv(n_units, 8)))
-    if n_tiles == 0:
-        return grid, 0
-    if n_units == 0:
-        return grid, grid
-    wp = float(tile_cost) * STEP_BYTES
-    wd = float(sum_ctx) * shape.num_kv_heads * shape.head_dim * 2.0 * shape.elt_bytes
-    if shape.num_q_heads // shape.num_kv_heads > 4:   # 8 decode warps per CTA instead of 12
-        wd *= WIDE_GROUP_DECODE_WEIGHT
-    n_p = math.ceil(grid * wp / (wp + wd))
-    n_p = max(n_p, min(cdiv(n_tiles, 4), cdiv(grid, 2)))
-    n_p = min(n_p, n_tiles, grid)
-    return grid, max(1, n_p)
+class _Clock:
+    """Ascending multiset of end coordinates (one entry per machine)."""
+
+    def __init__(self):
+        self.v: List[float] = []
+
+    def add(self, x: float):
+        bisect.insort(self.v, x)
 
 
-def list_schedule(costs: Sequence[int], m: int) -> List[int]:
-    """Step 4: finish times of m machines when each job in order goes to the earliest-free one."""
-    if not costs:
-        return []
-    heap = [0] * m
-    for c in costs:
-        t = heapq.heappop(heap)
-        heapq.heappush(heap, t + c)
-    return sorted(heap)
+def simulate(w: Work, ln: Launch, nl: Sequence[float]) -> float:
+    """Step 3: the two-clock event model; returns T_sim."""
+    tau0, tau_p, tau_d, sigma, r_w, u0, bw, gamma, r_cta, sigma0 = [float(x) for x in nl]
+    has_tiles = len(w.tiles) > 0 and ln.prefill_ctas > 0
+    W = float(ln.grid * ln.warps_per_cta)
+    cta, busy = _Clock(), _Clock()
+    tq, uq = list(w.tiles), list(w.pieces)
+    ti = ui = 0
+    t = S = V = 0.0
 
+    def take_units(n):
+        nonlocal ui
+        while n > 0 and ui < len(uq):
+            busy.add(V + uq[ui] + u0 * r_w)
+            ui += 1
+            n -= 1
 
-def schedule(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int]) -> Sched:
-    costs = tile_queue(shape, slices)
-    D = len(decode_ctx)
-    L = int(sum(decode_ctx))
-    units = 0
-    if D:
-        q = split_len(L, int(max(decode_ctx)), shape.num_kv_heads)
-        small = min(q, max(256, q // TAIL_DIV))
-        for x in decode_ctx:
-            nf = cdiv(int(x), q) - 1
-            units += (nf + cdiv(int(x) - nf * q, small)) * shape.num_kv_heads
-    grid, n_p = cta_split(len(costs), units, sum(costs), L, shape)
-    Bd = float(L) * shape.num_kv_heads * shape.head_dim * 2.0 * shape.elt_bytes
-    rows = sum(c for _, c in slices if c > 0)
-    return Sched(rows, D, L, Bd, grid, n_p, list_schedule(costs, n_p), units)
+    def take_tiles(n):          # returns the CTAs that found the queue empty
+        nonlocal ti
+        while n > 0 and ti < len(tq):
+            cta.add(S + tq[ti] + sigma)
+            ti += 1
+            n -= 1
+        return n
 
-
-def phi(s: Sched, tau: float, rc: float, bw: float) -> np.ndarray:
-    """Step 5-6."""
-    Tp = tau * float(s.fin[-1]) if s.fin else 0.0
-    Td = 0.0
-    if s.Bd > 0:
-        t, done, busy = 0.0, 0.0, s.np_
-        for f in s.fin:
-            tf = tau * float(f)
-            rate = min(bw, (s.grid - busy) * rc)
-            if rate > 0 and done + rate * (tf - t) >= s.Bd:
-                Td = t + (s.Bd - done) / rate
-                break
-            done += rate * (tf - t)
-            t = tf
-            busy -= 1
+    if has_tiles:
+        S = sigma0 - sigma
+        take_units((ln.grid - ln.prefill_ctas) * ln.warps_per_cta)
+        take_units(take_tiles(ln.prefill_ctas) * ln.warps_per_cta)
+        S = 0.0
+    else:
+        take_units(ln.grid * ln.warps_per_cta)
+    while cta.v or busy.v:
+        P, B = len(cta.v), len(busy.v)
+        tau = tau0 + tau_p * P / NSM + tau_d * B / W
+        rate = 0.0
+        if B:
+            rate = min(r_w, bw / B, r_cta * max(1.0, float(ln.grid - P)) / B) / (1.0 + gamma * P / NSM)
+        dt_p = (cta.v[0] - S) * tau if P else math.inf
+        dt_d = (busy.v[0] - V) / rate if B else math.inf
+        if dt_p <= dt_d:
+            t += dt_p
+            if B:
+                V += dt_p * rate
+            S = cta.v.pop(0)
+            take_units(take_tiles(1) * ln.warps_per_cta)
         else:
-            Td = t + (s.Bd - done) / min(bw, s.grid * rc)
-    return np.array([1.0, float(s.rows + s.D), float(s.D), float(s.sum_ctx), max(Td, Tp), min(Td, Tp)])
+            t += dt_d
+            if P:
+                S += dt_d / tau
+            V = busy.v.pop(0)
+            take_units(1)
+    return t
 
 
-def predict(theta, shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int]) -> float:
-    theta = np.asarray(theta, dtype=float)
-    return float(np.dot(theta[:NFEAT], phi(schedule(shape, slices, decode_ctx), *theta[NFEAT:])))
+def features(w: Work, t_sim: float) -> np.ndarray:
+    return np.array([1.0, float(w.rows + w.D), float(w.D), float(w.sum_ctx), float(w.units), t_sim])
 
 
-def sample_batch(s: Sample) -> Tuple[List[Tuple[int, int]], List[int]]:
-    slices = [(s.chunk_offset, s.chunk_len)] if s.chunk_len > 0 else []
-    ctx = []
-    if s.num_decode:
-        base, rem = divmod(s.sum_ctx, s.num_decode)
-        ctx = [base + (1 if j < rem else 0) for j in range(s.num_decode)]
-    return slices, ctx
+def predict(theta, w: Work, ln: Launch) -> float:
+    th = np.asarray(theta, dtype=float)
+    return float(np.dot(th[:NLIN], features(w, simulate(w, ln, th[NLIN:]))))
 
 
-def grid_values(lo: float, hi: float, step: float) -> List[float]:
-    n = int(math.floor((hi - lo) / step + 0.5)) + 1
-    return [lo + float(i) * step for i in range(n)]
+def tiles_per_cta(w: Work, ln: Launch) -> List[int]:
+    """Tiles each prefill CTA runs under step 3's list schedule (all prefill CTAs share the
+    step clock, so the assignment is the list schedule of (s + sigma) costs; sigma and
+    sigma0 shift every CTA alike and do not change it)."""
+    if not w.tiles or ln.prefill_ctas == 0:
+        return []
+    free = [(0.0, c) for c in range(ln.prefill_ctas)]
+    count = [0] * ln.prefill_ctas
+    for s in w.tiles:
+        free.sort()
+        t, c = free.pop(0)
+        count[c] += 1
+        free.append((t + s, c))
+    return count
 
 
-def fit(shape: PredShape, samples: List[Sample], grid=DEFAULT_GRID) -> np.ndarray:
-    if len(samples) == 0:
-        raise ValueError("no samples")
-    t = np.array([s.seconds for s in samples], dtype=float)
-    if np.any(t <= 0):
-        raise ValueError("non-positive sample time")
-    scheds = [schedule(shape, *sample_batch(s)) for s in samples]
-    cands = []
-    for tau in grid_values(*grid[0:3]):
-        for rc in grid_values(*grid[3:6]):
-            for bw in grid_values(*grid[6:9]):
-                Phi = np.stack([phi(sc, tau, rc, bw) for sc in scheds])
-                A = Phi / t[:, None]
-                colmax = np.abs(A).max(axis=0)
-                colmax[colmax == 0] = 1.0
-                z, _ = nnls(A / colmax, np.ones_like(t))
-                lin = z / colmax
-                score = float(np.sum((Phi @ lin / t - 1.0) ** 2))
-                cands.append((score, np.concatenate([lin, [tau, rc, bw]])))
-    best = min(c[0] for c in cands)
-    for score, theta in cands:
-        if score <= best * (1.0 + 1e-9):
-            return theta
-    raise AssertionError("unreachable")
+def fit_linear(ws: Sequence[Work], lns: Sequence[Launch], t: np.ndarray, nl) -> Tuple[np.ndarray, float]:
+    """th[0:5] >= 0 by NNLS on relative residuals with th[5] = 1 (module docstring)."""
+    Ts = np.array([simulate(w, ln, nl) for w, ln in zip(ws, lns)])
+    F = np.array([features(w, x)[:5] for w, x in zip(ws, Ts)])
+    A = F / t[:, None]
+    cm = np.abs(A).max(axis=0)
+    cm[cm == 0] = 1.0
+    z, _ = nnls(A / cm, 1.0 - Ts / t)
+    lin = np.concatenate([z / cm, [1.0]])
+    err = (F @ lin[:5] + Ts) / t - 1.0
+    return lin, float(np.sum(err ** 2))
+
+
+def fit(ws, lns, t, minimiser: Callable, start) -> np.ndarray:
+    """Step 'fit': minimiser(objective, x0) -> x over log(th[6:16])."""
+    t = np.asarray(t, dtype=float)
+    x = minimiser(lambda x: fit_linear(ws, lns, t, np.exp(x))[1], np.log(np.asarray(start, dtype=float)))
+    nl = np.exp(x)
+    lin, _ = fit_linear(ws, lns, t, nl)
+    return np.concatenate([lin, nl])
 
 
 def feasible(t: float, slack: float) -> bool:
@@ -245,11 +247,8 @@ def feasible(t: float, slack: float) -> bool:
     return t <= slack + 1e-12 * max(1.0, abs(slack))
 
 
-def max_feasible_chunk(theta, shape: PredShape, decode_ctx: Sequence[int], offset: int, remaining: int,
-                       slack: float, max_chunk: int) -> Tuple[int, bool]:
-    """S:137 boundary by bisection (module docstring)."""
-    def t_of(C):
-        return predict(theta, shape, [(offset, C)], decode_ctx)
+def max_feasible_chunk(t_of: Callable[[int], float], remaining: int, slack: float, max_chunk: int) -> Tuple[int, bool]:
+    """S:137 boundary by bisection (module docstring); t_of(C) = t_hat of the batch with C rows."""
     cap = max(0, min(max_chunk, remaining))
     if not feasible(t_of(0), slack):
         return 0, True
@@ -265,14 +264,19 @@ def max_feasible_chunk(theta, shape: PredShape, decode_ctx: Sequence[int], offse
     return lo, False
 
 
-def largest_feasible_chunk(theta, shape: PredShape, decode_ctx: Sequence[int], offset: int, remaining: int,
-                           slack: float, max_chunk: int) -> Tuple[int, bool]:
+def largest_feasible_chunk(t_of: Callable[[int], float], remaining: int, slack: float,
+                           max_chunk: int) -> Tuple[int, bool]:
     """S:119 literally: the largest C in [0, cap] whose batch is feasible (scan)."""
     cap = max(0, min(max_chunk, remaining))
-    if not feasible(predict(theta, shape, [(offset, 0)], decode_ctx), slack):
+    if not feasible(t_of(0), slack):
         return 0, True
     best = 0
     for C in range(1, cap + 1):
-        if feasible(predict(theta, shape, [(offset, C)], decode_ctx), slack):
+        if feasible(t_of(C), slack):
             best = C
     return best, False
+
+
+def affine(c0: float, c1: float, c2: float, slices, decode_ctx) -> float:
+    """SPEC S:107-115 written out: c0 + c1 * (prefill tokens + decodes) + c2 * sum ctx."""
+    return c0 + c1 * (sum(c for _, c in slices) + len(decode_ctx)) + c2 * float(sum(decode_ctx))

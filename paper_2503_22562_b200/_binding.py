@@ -16,9 +16,15 @@ OK, EINVAL, ENOBLOCKS, ENOSEQ, ESTATE, ECUDA, ENCCL, EUNSUPPORTED = range(8)
 STATUS_NAMES = ["OK", "EINVAL", "ENOBLOCKS", "ENOSEQ", "ESTATE", "ECUDA", "ENCCL", "EUNSUPPORTED"]
 BF16, F32 = 0, 1
 DEVICE_NONE = -1
-NUM_FEATURES = 6
-NUM_PARAMS = 9
-DEFAULT_FIT_GRID = (0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12)
+NUM_PARAMS = 16
+# the config-3 fit of round 2 (L8B shapes, profiles/predictor_fit.json; tools/fit_predictor.py)
+DEFAULT_THETA = (1.710823245208704e-05, 2.5323525874149684e-09, 0.0, 9.681221389473926e-11, 6.504072682583826e-10, 1.0,
+                 8.932967366439305e-07, 4.151486954445609e-08, 2.155656173143665e-07, 9.643396000471798,
+                 73020918185.57639, 1.0000000000000007e-09, 8762510192472.427, 0.14203956201505377,
+                 95980040060.6872, 1.133949902397201)
+PARAM_NAMES = ["c0 (s)", "per row c+D (s)", "per decode (s)", "per ctx token (s)", "per unit (s)", "kappa (T_sim)",
+               "tau0 (s/step)", "tau_p (s/step)", "tau_d (s/step)", "sigma (steps/tile)", "r_w (B/s per warp)",
+               "u0 (s/unit)", "BW (B/s)", "gamma", "r_cta (B/s)", "sigma0 (steps/CTA)"]
 
 
 class NiyamaError(RuntimeError):
@@ -55,6 +61,16 @@ class Tuning(C.Structure):
 class SampleC(C.Structure):
     _fields_ = [("chunk_len", C.c_int32), ("chunk_offset", C.c_int32), ("num_decode", C.c_int32),
                 ("sum_ctx", C.c_int64), ("seconds", C.c_double)]
+
+
+class FitOptionsC(C.Structure):
+    _fields_ = [("start", C.POINTER(C.c_double)), ("max_evals", C.c_int32), ("subsample", C.c_int32)]
+
+
+class PredictInfoC(C.Structure):
+    _fields_ = [("grid", C.c_int32), ("prefill_ctas", C.c_int32), ("split_len", C.c_int32),
+                ("small_piece", C.c_int32), ("warps_per_cta", C.c_int32), ("reserved", C.c_int32),
+                ("num_units", C.c_int64), ("sim_seconds", C.c_double), ("seconds", C.c_double)]
 
 
 class DecodeQoSC(C.Structure):
@@ -122,8 +138,9 @@ def _load():
         "niyama_get_unique_id": ([vp], st),
         "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
         "niyama_predictor_fit": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(vp)], st),
-        "niyama_predictor_fit_grid": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(C.c_double),
-                                       C.POINTER(vp)], st),
+        "niyama_predictor_fit_batches": ([C.POINTER(KVConfig), C.POINTER(BatchDescC), C.POINTER(C.c_double), i32,
+                                          C.POINTER(FitOptionsC), C.POINTER(vp)], st),
+        "niyama_predict_detail": ([vp, C.POINTER(BatchDescC), C.POINTER(PredictInfoC)], st),
         "niyama_predictor_from_params": ([C.POINTER(KVConfig), C.POINTER(C.c_double), C.POINTER(vp)], st),
         "niyama_predictor_params": ([vp, C.POINTER(C.c_double)], st),
         "niyama_predict_iter_time": ([vp, C.POINTER(BatchDescC)], C.c_double),
@@ -358,10 +375,10 @@ def get_unique_id() -> bytes:
 
 
 class Predictor:
-    """Iteration-time predictor (niyama_predictor): the a8 schedule model of include/niyama.h.
+    """Iteration-time predictor (niyama_predictor): the a8 event model of include/niyama.h.
 
-    Parameters: theta[0:6] linear weights of phi = [1, c+D, D, sum ctx, max(T_d,T_p), min(T_d,T_p)],
-    theta[6] = tau (s per prefill step), theta[7] = r_cta (B/s), theta[8] = BW (B/s)."""
+    Parameters (PARAM_NAMES): theta[0:6] linear weights of [1, c+D, D, sum ctx, units, T_sim];
+    theta[6:13] the event model's tau0, tau_p, tau_d, sigma, r_w, u0, BW."""
 
     def __init__(self, handle: int):
         self.handle = handle
@@ -371,17 +388,36 @@ class Predictor:
         return _cfg(1, num_q_heads, num_kv_heads, head_dim, 16, 1, dtype, world_size, 0, None)
 
     @classmethod
-    def fit(cls, cfg: KVConfig, samples: Sequence, grid=None) -> "Predictor":
-        """grid: (tau_lo, tau_hi, tau_step, r_lo, r_hi, r_step, bw_lo, bw_hi, bw_step); None = library default."""
+    def fit(cls, cfg: KVConfig, samples: Sequence) -> "Predictor":
+        """Summary samples (chunk_len, chunk_offset, num_decode, sum_ctx, seconds)."""
         arr = (SampleC * len(samples))(*[SampleC(s.chunk_len, s.chunk_offset, s.num_decode, s.sum_ctx, s.seconds)
                                          for s in samples])
         h = C.c_void_p()
-        if grid is None:
-            _check(lib.niyama_predictor_fit(C.byref(cfg), arr, len(samples), C.byref(h)))
-        else:
-            g = (C.c_double * 9)(*[float(x) for x in grid])
-            _check(lib.niyama_predictor_fit_grid(C.byref(cfg), arr, len(samples), g, C.byref(h)))
+        _check(lib.niyama_predictor_fit(C.byref(cfg), arr, len(samples), C.byref(h)))
         return cls(h.value)
+
+    @classmethod
+    def fit_batches(cls, cfg: KVConfig, batches: Sequence, seconds: Sequence[float], start=None, max_evals=0,
+                    subsample=0) -> "Predictor":
+        """Measured launches: batches (descriptor objects or `Batch`) and their seconds."""
+        ds = [b if isinstance(b, _Desc) else _Desc(b) for b in batches]
+        arr = (BatchDescC * len(ds))(*[d.c for d in ds])
+        sec = (C.c_double * len(ds))(*[float(x) for x in seconds])
+        opt = FitOptionsC(None, int(max_evals), int(subsample))
+        if start is not None:
+            st = (C.c_double * NUM_PARAMS)(*[float(x) for x in start])
+            opt.start = st
+        h = C.c_void_p()
+        _check(lib.niyama_predictor_fit_batches(C.byref(cfg), arr, sec, len(ds), C.byref(opt), C.byref(h)))
+        return cls(h.value)
+
+    def detail(self, desc) -> dict:
+        d = desc if isinstance(desc, _Desc) else _Desc(desc)
+        out = PredictInfoC()
+        _check(lib.niyama_predict_detail(self.handle, C.byref(d.c), C.byref(out)))
+        return dict(grid=out.grid, prefill_ctas=out.prefill_ctas, split_len=out.split_len,
+                    small_piece=out.small_piece, warps_per_cta=out.warps_per_cta, units=out.num_units,
+                    sim=out.sim_seconds, seconds=out.seconds)
 
     @classmethod
     def from_params(cls, cfg: KVConfig, theta) -> "Predictor":

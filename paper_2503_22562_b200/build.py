@@ -53,15 +53,17 @@ def build(force: bool = False) -> str:
     r_obj = os.path.join(BUILD, "runtime.o")
     s_src = os.path.join(CSRC, "sched.cpp")
     s_obj = os.path.join(BUILD, "sched.o")
+    p_src = os.path.join(CSRC, "predictor.cpp")
+    p_obj = os.path.join(BUILD, "predictor.o")
     common = ["-O3", "-std=c++17", "-I", INCLUDE, "-I", CSRC]
     if force or _stale(k_obj, [k_src] + headers):
         _run([NVCC, *ARCH, *common, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC", "-c", k_src, "-o", k_obj])
-    for src, obj in ((r_src, r_obj), (s_src, s_obj)):
+    for src, obj in ((r_src, r_obj), (s_src, s_obj), (p_src, p_obj)):
         if force or _stale(obj, [src] + headers):
             _run([os.environ.get("CXX", "g++"), *common, "-I", os.path.join(CUDA, "include"), "-I", nccl_inc, "-fPIC",
                   "-Wall", "-Wextra", "-Wno-unused-parameter", "-c", src, "-o", obj])
-    if force or _stale(LIB, [k_obj, r_obj, s_obj]):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, k_obj, r_obj, s_obj, "-L", nccl_lib,
+    if force or _stale(LIB, [k_obj, r_obj, s_obj, p_obj]):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, k_obj, r_obj, s_obj, p_obj, "-lpthread", "-L", nccl_lib,
               "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "--no-undefined"])
     return LIB
 

@@ -1,6 +1,8 @@
 // Internal structures shared by the host runtime (runtime.cpp) and the
 // sm_100a kernels (kernels.cu).  Not part of the public C ABI (include/niyama.h).
 #pragma once
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -11,6 +13,82 @@ namespace niyama {
 
 // Sets niyama_last_error() for this thread and returns s (host translation units).
 niyama_status set_error(niyama_status s, const char* msg);
+
+// ---- shared by the planner (runtime.cpp) and the predictor (predictor.cpp, a8), which
+// models the same launch: one definition of every launch-shaping rule.
+inline int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline niyama_tuning default_tuning() {
+  niyama_tuning t{};
+  t.prefill_ctas = 0;
+  t.split_len = 0;
+  t.tail_div = NIYAMA_TAIL_DIV;
+  t.tail_min = NIYAMA_TAIL_MIN;
+  t.grid_cap = 0;
+  t.plan_copy_stream = 1;
+  return t;
+}
+
+// Decode split length (a5), from batch totals only (split boundaries never depend
+// on scheduling, so results stay bitwise deterministic): the power of two nearest
+// (in log scale) to raw = sum ctx * Hkv / (4 units per resident warp), at least 128
+// (measured: 64-key splits lose to 128 on small batches; rounding 131 up to 256 lost
+// to 128), with at most 4095 splits per row.
+inline int32_t choose_split_len(int64_t sum_ctx, int32_t max_ctx, int hkv, int num_sms) {
+  const int64_t target = 4LL * num_sms * 8;
+  const int64_t raw = ceil_div64(std::max<int64_t>(1, sum_ctx * hkv), target);
+  int32_t s = 128;
+  while ((2LL * s * s < raw * raw || ceil_div64(max_ctx, s) > 4095) && s < (1 << 20)) s *= 2;
+  return s;
+}
+
+// CTA split of the bf16 launch.  Prefill tiles are
+// tensor/MUFU-bound and decode streaming is HBM-bound, so the launch runs them side
+// by side: CTAs [0, prefill_ctas) take prefill tiles first (longest first) and then
+// join the decode queue; the others stream decode KV from the start.  The prefill
+// share of the CTAs is its share of the estimated CTA-time: one 128-key prefill
+// step costs a CTA about as long as streaming NIYAMA_STEP_BYTES of decode KV under
+// load (measured: ~3.6 us per step vs ~44 GB/s per CTA on B200, tools/cap_sweep.py).
+// A tile also pays a fixed setup (Q load, pipeline fill, epilogue) of about
+// NIYAMA_TILE_SETUP_STEPS steps, which dominates short tiles (chunk at offset 0).
+// `tile_cost` = sum over tiles of (steps + setup).  Shared by the planner and the
+// predictor (a8), which simulates the same launch.
+struct CtaSplit {
+  int32_t grid, prefill_ctas;
+};
+inline CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv, int d, int elt,
+                   int g, int num_sms) {
+  CtaSplit r{};
+  r.grid = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div64(n_units, 8))));
+  if (n_tiles == 0) return r;
+  if (n_units == 0) {
+    r.prefill_ctas = r.grid;
+    return r;
+  }
+  const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
+  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt * (g > 4 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
+  int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
+  // a tile-count floor keeps short-tile prefill off the tail (at most 4 tiles per prefill
+  // CTA), itself capped at half the grid: with many long tiles (config 4: 1,024) it would
+  // put every CTA on prefill first (measured 1,073 us vs 926 us at 80 prefill CTAs)
+  np = std::max<int64_t>(np, std::min<int64_t>(ceil_div64(n_tiles, 4), ceil_div64(r.grid, 2)));
+  np = std::min<int64_t>({np, n_tiles, static_cast<int64_t>(r.grid)});
+  r.prefill_ctas = static_cast<int32_t>(std::max<int64_t>(1, np));
+  return r;
+}
+
+
+// Prefill work items: with GQA packing a 128-row tile holds R = 128 / g chunk rows of
+// the g query heads of one kv head (a4).
+inline int32_t rows_per_tile(int g) { return 128 / (g > 0 ? g : 1); }
+// Decode warps per CTA of the bf16 launch (12 when g <= 4, else 8)
+inline int decode_warps(int g) { return g <= 4 ? 12 : 8; }
+
+struct KvModel {
+  int hq, hkv, d, elt, num_sms;
+  niyama_tuning tune;
+};
+void kv_model(const niyama_kv* kv, KvModel* m);
 
 // KV pool physical layout:
 //   bf16: pool[layer][block][kv_head][K | V^T chunk]   (K and V^T of a block adjacent)

@@ -22,6 +22,7 @@
 
 using namespace niyama;
 
+
 namespace {
 
 thread_local std::string g_err;
@@ -58,16 +59,6 @@ struct Seq {
   uint64_t gen = 0;  // creation generation: a released id reused later is a different sequence
 };
 
-niyama_tuning default_tuning() {
-  niyama_tuning t{};
-  t.prefill_ctas = 0;
-  t.split_len = 0;
-  t.tail_div = NIYAMA_TAIL_DIV;
-  t.tail_min = NIYAMA_TAIL_MIN;
-  t.grid_cap = 0;
-  t.plan_copy_stream = 1;
-  return t;
-}
 
 // Runs the calling thread on `device` for the scope and restores the caller's device
 // (the library never leaves the caller's current device changed).
@@ -133,6 +124,16 @@ struct niyama_kv {
   uint64_t next_gen = 1;  // sequence generations (rollback identity)
 };
 
+// Model inputs of a kv for the predictor (predictor.cpp)
+void niyama::kv_model(const niyama_kv* kv, KvModel* m) {
+  m->hq = kv->hq;
+  m->hkv = kv->hkv;
+  m->d = kv->d;
+  m->elt = kv->elt;
+  m->num_sms = kv->num_sms;
+  m->tune = kv->tune;
+}
+
 struct niyama_plan {
   niyama_kv* kv = nullptr;
   cudaStream_t stream = nullptr;
@@ -170,13 +171,6 @@ struct niyama_plan {
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   int32_t* d_work = nullptr;
-};
-
-struct niyama_predictor {
-  int hq = 0, hkv = 0, d = 0, elt = 0;
-  int num_sms = NIYAMA_PRED_SMS;          // niyama_predictor_bind: the kv's device
-  niyama_tuning tune = default_tuning();  // niyama_predictor_bind: the kv's tuning
-  double theta[NIYAMA_NUM_PARAMS] = {0, 0, 0, 0, 0, 0, 1e-6, 50e9, 6e12};
 };
 
 extern "C" const char* niyama_last_error(void) { return g_err.c_str(); }
@@ -359,54 +353,6 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
 
 // ================================================================ planner
 namespace {
-
-// Decode split length (a5), from batch totals only (split boundaries never depend
-// on scheduling, so results stay bitwise deterministic): the power of two nearest
-// (in log scale) to raw = sum ctx * Hkv / (4 units per resident warp), at least 128
-// (measured: 64-key splits lose to 128 on small batches; rounding 131 up to 256 lost
-// to 128), with at most 4095 splits per row.
-int32_t choose_split_len(int64_t sum_ctx, int32_t max_ctx, int hkv, int num_sms) {
-  const int64_t target = 4LL * num_sms * 8;
-  const int64_t raw = ceil_div(std::max<int64_t>(1, sum_ctx * hkv), target);
-  int32_t s = 128;
-  while ((2LL * s * s < raw * raw || ceil_div(max_ctx, s) > 4095) && s < (1 << 20)) s *= 2;
-  return s;
-}
-
-// CTA split of the bf16 launch.  Prefill tiles are
-// tensor/MUFU-bound and decode streaming is HBM-bound, so the launch runs them side
-// by side: CTAs [0, prefill_ctas) take prefill tiles first (longest first) and then
-// join the decode queue; the others stream decode KV from the start.  The prefill
-// share of the CTAs is its share of the estimated CTA-time: one 128-key prefill
-// step costs a CTA about as long as streaming NIYAMA_STEP_BYTES of decode KV under
-// load (measured: ~3.6 us per step vs ~44 GB/s per CTA on B200, tools/cap_sweep.py).
-// A tile also pays a fixed setup (Q load, pipeline fill, epilogue) of about
-// NIYAMA_TILE_SETUP_STEPS steps, which dominates short tiles (chunk at offset 0).
-// `tile_cost` = sum over tiles of (steps + setup).  Shared by the planner and the
-// predictor (a8), which simulates the same launch.
-struct CtaSplit {
-  int32_t grid, prefill_ctas;
-};
-CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv, int d, int elt,
-                   int g, int num_sms) {
-  CtaSplit r{};
-  r.grid = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div(n_units, 8))));
-  if (n_tiles == 0) return r;
-  if (n_units == 0) {
-    r.prefill_ctas = r.grid;
-    return r;
-  }
-  const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
-  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt * (g > 4 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
-  int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
-  // a tile-count floor keeps short-tile prefill off the tail (at most 4 tiles per prefill
-  // CTA), itself capped at half the grid: with many long tiles (config 4: 1,024) it would
-  // put every CTA on prefill first (measured 1,073 us vs 926 us at 80 prefill CTAs)
-  np = std::max<int64_t>(np, std::min<int64_t>(ceil_div(n_tiles, 4), ceil_div(r.grid, 2)));
-  np = std::min<int64_t>({np, n_tiles, static_cast<int64_t>(r.grid)});
-  r.prefill_ctas = static_cast<int32_t>(std::max<int64_t>(1, np));
-  return r;
-}
 
 void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
   const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_tiles,
@@ -1111,445 +1057,6 @@ extern "C" niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan
   r = ncclGroupEnd();
   if (first == ncclSuccess) first = r;
   if (first != ncclSuccess) return fail(NIYAMA_ENCCL, std::string("all-gather: ") + ncclGetErrorString(first));
-  return NIYAMA_OK;
-}
-
-// ================================================================ predictor (a8)
-// Schedule model of the fused launch; every step is spelled out in include/niyama.h
-// and DESIGN.md "a8 schedule model" (the oracle re-implements it from there).
-namespace {
-
-// The launch's schedule in step units: independent of (tau, r_cta, BW).
-struct Sched {
-  double rows = 0, D = 0, sum_ctx = 0, Bd = 0;
-  int32_t grid = 1, np = 0;
-  // prefill CTAs' finish times (steps), ascending, as (time, number of CTAs)
-  std::vector<std::pair<int64_t, int32_t>> fin;
-};
-
-struct SliceOC {
-  int32_t o, c;
-};
-
-Sched schedule(const niyama_predictor& p, std::vector<SliceOC> slices, const int32_t* ctx, int64_t D) {
-  Sched r;
-  const int g = p.hq / p.hkv;
-  const int64_t R = std::max(1, 128 / g);
-  // 1. tile queue: slices by o + c descending (stable), q tiles last to first, x Hkv.
-  //    Kept as (cost, Hkv) groups.
-  std::stable_sort(slices.begin(), slices.end(), [](const SliceOC& a, const SliceOC& b) {
-    return static_cast<int64_t>(a.o) + a.c > static_cast<int64_t>(b.o) + b.c;
-  });
-  std::vector<int64_t> costs;  // one entry per group of Hkv equal tiles
-  int64_t tile_cost = 0, n_tiles = 0;
-  for (const SliceOC& sl : slices) {
-    r.rows += sl.c;
-    const int64_t nqt = ceil_div(sl.c, R);
-    for (int64_t qt = nqt - 1; qt >= 0; --qt) {
-      const int64_t cost = ceil_div(sl.o + std::min<int64_t>(sl.c, (qt + 1) * R), 128) + NIYAMA_TILE_SETUP_STEPS;
-      costs.push_back(cost);
-      tile_cost += cost * p.hkv;
-      n_tiles += p.hkv;
-    }
-  }
-  // 2. decode units
-  int64_t sum_ctx = 0;
-  int32_t max_ctx = 0;
-  for (int64_t j = 0; j < D; ++j) {
-    sum_ctx += ctx[j];
-    max_ctx = std::max(max_ctx, ctx[j]);
-  }
-  int64_t n_units = 0;
-  if (D > 0) {
-    int32_t q = choose_split_len(sum_ctx, max_ctx, p.hkv, p.num_sms);
-    if (p.tune.split_len > 0 && ceil_div(max_ctx, p.tune.split_len) <= 4095) q = p.tune.split_len;
-    const int32_t small = std::min<int32_t>(q, std::max<int32_t>(p.tune.tail_min, q / p.tune.tail_div));
-    for (int64_t j = 0; j < D; ++j) {
-      const int64_t nf = ceil_div(ctx[j], q) - 1;
-      n_units += (nf + ceil_div(ctx[j] - nf * q, small)) * p.hkv;
-    }
-  }
-  r.D = static_cast<double>(D);
-  r.sum_ctx = static_cast<double>(sum_ctx);
-  r.Bd = static_cast<double>(sum_ctx) * p.hkv * p.d * 2.0 * p.elt;
-  // 3. CTA split (the planner's rule)
-  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, p.hq / p.hkv, p.num_sms);
-  r.grid = cs.grid;
-  r.np = cs.prefill_ctas;
-  if (p.tune.prefill_ctas > 0 && n_tiles > 0) r.np = std::min(p.tune.prefill_ctas, r.grid);
-  if (p.tune.grid_cap > 0 && r.grid > p.tune.grid_cap) {
-    r.grid = p.tune.grid_cap;
-    r.np = std::min(r.np, r.grid);
-  }
-  // 4. list scheduling of the queue on the prefill CTAs.  Each tile goes to a CTA
-  //    that frees first; CTAs with equal loads are interchangeable, so the loads are
-  //    kept as an ascending (load, count) list and up to `count` tiles of a group go
-  //    to the CTAs at the minimum load at once — the same finish-time multiset as
-  //    one-by-one list scheduling.
-  if (!costs.empty()) {
-    auto& L = r.fin;
-    L.assign(1, {0, r.np});
-    for (int64_t c : costs) {
-      int64_t left = p.hkv;
-      while (left > 0) {
-        const int64_t load = L.front().first;
-        const int32_t take = static_cast<int32_t>(std::min<int64_t>(left, L.front().second));
-        if ((L.front().second -= take) == 0) L.erase(L.begin());
-        left -= take;
-        const int64_t nl = load + c;
-        auto it = std::lower_bound(L.begin(), L.end(), nl,
-                                   [](const std::pair<int64_t, int32_t>& e, int64_t v) { return e.first < v; });
-        if (it != L.end() && it->first == nl)
-          it->second += take;
-        else
-          L.insert(it, {nl, take});
-      }
-    }
-  }
-  return r;
-}
-
-// 5.-6. fluid decode and the feature vector
-void phi_of(const Sched& s, double tau, double rc, double bw, double* phi) {
-  const double Tp = s.fin.empty() ? 0.0 : tau * static_cast<double>(s.fin.back().first);
-  double Td = 0.0;
-  if (s.Bd > 0) {
-    double t = 0.0, done = 0.0;
-    int32_t busy = s.np;
-    bool finished = false;
-    for (const auto& f : s.fin) {  // CTAs with equal finish times leave together
-      const double tf = tau * static_cast<double>(f.first);
-      const double rate = std::min(bw, (s.grid - busy) * rc);
-      if (rate > 0 && done + rate * (tf - t) >= s.Bd) {
-        Td = t + (s.Bd - done) / rate;
-        finished = true;
-        break;
-      }
-      done += rate * (tf - t);
-      t = tf;
-      busy -= f.second;
-    }
-    if (!finished) Td = t + (s.Bd - done) / std::min(bw, s.grid * rc);
-  }
-  phi[0] = 1.0;
-  phi[1] = s.rows + s.D;
-  phi[2] = s.D;
-  phi[3] = s.sum_ctx;
-  phi[4] = std::max(Td, Tp);
-  phi[5] = std::min(Td, Tp);
-}
-
-double lin(const double* theta, const double* phi) {
-  double t = 0;
-  for (int k = 0; k < NIYAMA_NUM_FEATURES; ++k) t += theta[k] * phi[k];
-  return t;
-}
-
-// A sample as a batch: one slice (o, c) if c > 0, D decodes with sum ctx spread evenly.
-Sched schedule_sample(const niyama_predictor& p, const niyama_sample& s) {
-  std::vector<SliceOC> sl;
-  if (s.chunk_len > 0) sl.push_back(SliceOC{s.chunk_offset, s.chunk_len});
-  std::vector<int32_t> ctx(s.num_decode);
-  if (s.num_decode > 0) {
-    const int64_t base = s.sum_ctx / s.num_decode, rem = s.sum_ctx % s.num_decode;
-    for (int32_t j = 0; j < s.num_decode; ++j) ctx[j] = static_cast<int32_t>(base + (j < rem ? 1 : 0));
-  }
-  return schedule(p, sl, ctx.data(), s.num_decode);
-}
-
-// Least squares on the columns `cols` of A (m x n, row-major) by Householder QR.
-bool lsq_subset(const std::vector<double>& A, int m, int n, const std::vector<double>& b, const std::vector<int>& cols,
-                std::vector<double>& z) {
-  const int k = static_cast<int>(cols.size());
-  std::vector<double> M(static_cast<size_t>(m) * k), y(b);
-  for (int i = 0; i < m; ++i)
-    for (int j = 0; j < k; ++j) M[static_cast<size_t>(i) * k + j] = A[static_cast<size_t>(i) * n + cols[j]];
-  for (int j = 0; j < k; ++j) {
-    double norm = 0;
-    for (int i = j; i < m; ++i) norm += M[static_cast<size_t>(i) * k + j] * M[static_cast<size_t>(i) * k + j];
-    norm = std::sqrt(norm);
-    if (norm == 0) return false;
-    const double alpha = M[static_cast<size_t>(j) * k + j] > 0 ? -norm : norm;
-    std::vector<double> v(m, 0.0);
-    for (int i = j; i < m; ++i) v[i] = M[static_cast<size_t>(i) * k + j];
-    v[j] -= alpha;
-    double vn = 0;
-    for (int i = j; i < m; ++i) vn += v[i] * v[i];
-    if (vn == 0) continue;
-    for (int jj = j; jj < k; ++jj) {
-      double s = 0;
-      for (int i = j; i < m; ++i) s += v[i] * M[static_cast<size_t>(i) * k + jj];
-      s = 2 * s / vn;
-      for (int i = j; i < m; ++i) M[static_cast<size_t>(i) * k + jj] -= s * v[i];
-    }
-    double s = 0;
-    for (int i = j; i < m; ++i) s += v[i] * y[i];
-    s = 2 * s / vn;
-    for (int i = j; i < m; ++i) y[i] -= s * v[i];
-  }
-  z.assign(k, 0.0);
-  for (int j = k - 1; j >= 0; --j) {
-    double s = y[j];
-    for (int jj = j + 1; jj < k; ++jj) s -= M[static_cast<size_t>(j) * k + jj] * z[jj];
-    const double diag = M[static_cast<size_t>(j) * k + j];
-    if (std::fabs(diag) < 1e-300) return false;
-    z[j] = s / diag;
-  }
-  return true;
-}
-
-// Lawson-Hanson active-set NNLS: min ||A x - b||, x >= 0.
-std::vector<double> nnls(const std::vector<double>& A, int m, int n, const std::vector<double>& b) {
-  std::vector<double> x(n, 0.0);
-  std::vector<bool> inP(n, false);
-  double norm1 = 0;
-  for (int j = 0; j < n; ++j) {
-    double s = 0;
-    for (int i = 0; i < m; ++i) s += std::fabs(A[static_cast<size_t>(i) * n + j]);
-    norm1 = std::max(norm1, s);
-  }
-  const double tol = 10.0 * std::max(m, n) * norm1 * std::numeric_limits<double>::epsilon();
-  auto gradient = [&](std::vector<double>& w) {
-    std::vector<double> r(b);
-    for (int i = 0; i < m; ++i)
-      for (int j = 0; j < n; ++j) r[i] -= A[static_cast<size_t>(i) * n + j] * x[j];
-    w.assign(n, 0.0);
-    for (int j = 0; j < n; ++j)
-      for (int i = 0; i < m; ++i) w[j] += A[static_cast<size_t>(i) * n + j] * r[i];
-  };
-  std::vector<double> w;
-  for (int outer = 0; outer < 3 * n + 10; ++outer) {
-    gradient(w);
-    int t = -1;
-    double best = tol;
-    for (int j = 0; j < n; ++j)
-      if (!inP[j] && w[j] > best) best = w[j], t = j;
-    if (t < 0) break;
-    inP[t] = true;
-    for (int inner = 0; inner < 3 * n + 10; ++inner) {
-      std::vector<int> cols;
-      for (int j = 0; j < n; ++j)
-        if (inP[j]) cols.push_back(j);
-      std::vector<double> zc;
-      if (!lsq_subset(A, m, n, b, cols, zc)) {
-        inP[cols.back()] = false;
-        break;
-      }
-      std::vector<double> z(n, 0.0);
-      for (size_t k = 0; k < cols.size(); ++k) z[cols[k]] = zc[k];
-      bool allpos = true;
-      for (int j : cols)
-        if (z[j] <= 0) allpos = false;
-      if (allpos) {
-        x = z;
-        break;
-      }
-      double alpha = 2.0;
-      for (int j : cols)
-        if (z[j] <= 0) alpha = std::min(alpha, x[j] / (x[j] - z[j]));
-      for (int j = 0; j < n; ++j) x[j] += alpha * (z[j] - x[j]);
-      for (int j : cols)
-        if (x[j] <= tol) {
-          x[j] = 0;
-          inP[j] = false;
-        }
-    }
-  }
-  return x;
-}
-
-niyama_status pred_shape(const niyama_kv_config* s, niyama_predictor* p) {
-  if (!s) return fail(NIYAMA_EINVAL, "shape is NULL");
-  if (s->world_size < 1 || s->num_kv_heads < 1 || s->num_q_heads < 1 || s->head_dim < 1 ||
-      s->num_kv_heads % s->world_size || s->num_q_heads % s->world_size || s->num_q_heads % s->num_kv_heads)
-    return fail(NIYAMA_EINVAL, "predictor shape");
-  p->hq = s->num_q_heads / s->world_size;
-  p->hkv = s->num_kv_heads / s->world_size;
-  p->d = s->head_dim;
-  p->elt = s->dtype == NIYAMA_BF16 ? 2 : 4;
-  return NIYAMA_OK;
-}
-
-bool feasible(double t, double slack) { return t <= slack + 1e-12 * std::max(1.0, std::fabs(slack)); }
-
-std::vector<double> grid_values(double lo, double hi, double step) {
-  std::vector<double> v;
-  const int64_t n = static_cast<int64_t>(std::floor((hi - lo) / step + 0.5)) + 1;
-  for (int64_t i = 0; i < n; ++i) v.push_back(lo + static_cast<double>(i) * step);
-  return v;
-}
-
-constexpr double kDefaultGrid[9] = {0.5e-6, 2.5e-6, 0.1e-6, 30e9, 120e9, 5e9, 5.0e12, 8.4e12, 0.2e12};
-
-}  // namespace
-
-extern "C" niyama_status niyama_predictor_fit_grid(const niyama_kv_config* shape, const niyama_sample* samples,
-                                                   int32_t n, const double* grid9, niyama_predictor** out) {
-  if (!out) return fail(NIYAMA_EINVAL, "out is NULL");
-  *out = nullptr;
-  if (!samples || n < 1) return fail(NIYAMA_EINVAL, "no samples");
-  if (!grid9) return fail(NIYAMA_EINVAL, "grid is NULL");
-  for (int k = 0; k < 9; k += 3)
-    if (!(grid9[k] > 0) || !(grid9[k + 1] >= grid9[k]) || !(grid9[k + 2] > 0) || !std::isfinite(grid9[k + 1]) ||
-        (grid9[k + 1] - grid9[k]) / grid9[k + 2] > 1e6)
-      return fail(NIYAMA_EINVAL, "grid: need 0 < lo <= hi, step > 0");
-  niyama_predictor p;
-  niyama_status st = pred_shape(shape, &p);
-  if (st != NIYAMA_OK) return st;
-  std::vector<Sched> sch;
-  sch.reserve(n);
-  for (int i = 0; i < n; ++i) {
-    const niyama_sample& s = samples[i];
-    if (!(s.seconds > 0) || !std::isfinite(s.seconds) || s.chunk_len < 0 || s.chunk_offset < 0 || s.num_decode < 0 ||
-        s.sum_ctx < s.num_decode || (s.num_decode == 0 && s.sum_ctx != 0) ||
-        s.sum_ctx / std::max(1, s.num_decode) >= (int64_t(1) << 30))
-      return fail(NIYAMA_EINVAL, "sample " + std::to_string(i) + " is invalid");
-    sch.push_back(schedule_sample(p, s));
-  }
-  const std::vector<double> taus = grid_values(grid9[0], grid9[1], grid9[2]);
-  const std::vector<double> rcs = grid_values(grid9[3], grid9[4], grid9[5]);
-  const std::vector<double> bws = grid_values(grid9[6], grid9[7], grid9[8]);
-  const int F = NIYAMA_NUM_FEATURES;
-  struct Cand {
-    double score;
-    double theta[NIYAMA_NUM_PARAMS];
-  };
-  std::vector<Cand> cands;
-  cands.reserve(taus.size() * rcs.size() * bws.size());
-  std::vector<double> A(static_cast<size_t>(n) * F), b(n, 1.0), phi_all(static_cast<size_t>(n) * F);
-  for (double tau : taus)
-    for (double rc : rcs)
-      for (double bw : bws) {
-        for (int i = 0; i < n; ++i) {
-          phi_of(sch[i], tau, rc, bw, &phi_all[static_cast<size_t>(i) * F]);
-          for (int k = 0; k < F; ++k) A[static_cast<size_t>(i) * F + k] = phi_all[static_cast<size_t>(i) * F + k] / samples[i].seconds;
-        }
-        double colmax[NIYAMA_NUM_FEATURES];
-        for (int k = 0; k < F; ++k) {
-          colmax[k] = 0;
-          for (int i = 0; i < n; ++i) colmax[k] = std::max(colmax[k], std::fabs(A[static_cast<size_t>(i) * F + k]));
-          if (colmax[k] == 0) colmax[k] = 1;
-          for (int i = 0; i < n; ++i) A[static_cast<size_t>(i) * F + k] /= colmax[k];
-        }
-        const std::vector<double> z = nnls(A, n, F, b);
-        Cand c{};
-        for (int k = 0; k < F; ++k) c.theta[k] = z[k] / colmax[k];
-        c.theta[6] = tau;
-        c.theta[7] = rc;
-        c.theta[8] = bw;
-        c.score = 0;
-        for (int i = 0; i < n; ++i) {
-          const double e = lin(c.theta, &phi_all[static_cast<size_t>(i) * F]) / samples[i].seconds - 1.0;
-          c.score += e * e;
-        }
-        cands.push_back(c);
-      }
-  double best = std::numeric_limits<double>::infinity();
-  for (const Cand& c : cands) best = std::min(best, c.score);
-  const Cand* pick = &cands[0];
-  for (const Cand& c : cands)
-    if (c.score <= best * (1.0 + 1e-9)) {
-      pick = &c;
-      break;
-    }
-  auto* res = new niyama_predictor(p);
-  std::memcpy(res->theta, pick->theta, sizeof(res->theta));
-  *out = res;
-  return NIYAMA_OK;
-}
-
-extern "C" niyama_status niyama_predictor_fit(const niyama_kv_config* shape, const niyama_sample* samples, int32_t n,
-                                              niyama_predictor** out) {
-  return niyama_predictor_fit_grid(shape, samples, n, kDefaultGrid, out);
-}
-
-extern "C" niyama_status niyama_predictor_from_params(const niyama_kv_config* shape, const double* theta9,
-                                                      niyama_predictor** out) {
-  if (!out || !theta9) return fail(NIYAMA_EINVAL, "out/theta is NULL");
-  *out = nullptr;
-  niyama_predictor p;
-  niyama_status st = pred_shape(shape, &p);
-  if (st != NIYAMA_OK) return st;
-  for (int k = 0; k < NIYAMA_NUM_PARAMS; ++k) {
-    const bool ok = std::isfinite(theta9[k]) && (k < NIYAMA_NUM_FEATURES ? theta9[k] >= 0 : theta9[k] > 0);
-    if (!ok) return fail(NIYAMA_EINVAL, "theta: linear part finite and >= 0, tau/r_cta/BW finite and > 0");
-    p.theta[k] = theta9[k];
-  }
-  *out = new niyama_predictor(p);
-  return NIYAMA_OK;
-}
-
-extern "C" niyama_status niyama_predictor_params(const niyama_predictor* p, double* theta9_out) {
-  if (!p || !theta9_out) return fail(NIYAMA_EINVAL, "p/out is NULL");
-  std::memcpy(theta9_out, p->theta, sizeof(p->theta));
-  return NIYAMA_OK;
-}
-
-extern "C" double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc) {
-  if (!p || !desc || desc->num_prefill < 0 || desc->num_decode < 0) return -1.0;
-  if (desc->num_prefill > 0 && (!desc->prefill_offset || !desc->prefill_len)) return -1.0;
-  if (desc->num_decode > 0 && !desc->decode_ctx) return -1.0;
-  for (int j = 0; j < desc->num_decode; ++j)
-    if (desc->decode_ctx[j] < 1) return -1.0;
-  std::vector<SliceOC> sl;
-  for (int i = 0; i < desc->num_prefill; ++i) {
-    if (desc->prefill_offset[i] < 0 || desc->prefill_len[i] < 0) return -1.0;
-    if (desc->prefill_len[i] > 0) sl.push_back(SliceOC{desc->prefill_offset[i], desc->prefill_len[i]});
-  }
-  const Sched s = schedule(*p, std::move(sl), desc->decode_ctx, desc->num_decode);
-  double phi[NIYAMA_NUM_FEATURES];
-  phi_of(s, p->theta[6], p->theta[7], p->theta[8], phi);
-  return lin(p->theta, phi);
-}
-
-extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, const niyama_batch_desc* decodes_only,
-                                                   int32_t chunk_offset, int32_t prefill_remaining, double slack_s,
-                                                   int32_t max_chunk, int32_t* chunk_out, int32_t* infeasible_out) {
-  if (!p || !decodes_only || !chunk_out || !infeasible_out) return fail(NIYAMA_EINVAL, "NULL argument");
-  if (chunk_offset < 0 || max_chunk < 0 || std::isnan(slack_s)) return fail(NIYAMA_EINVAL, "chunk_offset/max_chunk/slack");
-  if (decodes_only->num_decode < 0 || (decodes_only->num_decode > 0 && !decodes_only->decode_ctx))
-    return fail(NIYAMA_EINVAL, "decode arrays");
-  for (int j = 0; j < decodes_only->num_decode; ++j)
-    if (decodes_only->decode_ctx[j] < 1) return fail(NIYAMA_EINVAL, "decode_ctx < 1");
-  auto t_of = [&](int32_t C) {
-    std::vector<SliceOC> sl;
-    if (C > 0) sl.push_back(SliceOC{chunk_offset, C});
-    const Sched s = schedule(*p, std::move(sl), decodes_only->decode_ctx, decodes_only->num_decode);
-    double phi[NIYAMA_NUM_FEATURES];
-    phi_of(s, p->theta[6], p->theta[7], p->theta[8], phi);
-    return lin(p->theta, phi);
-  };
-  const int32_t cap = std::max(0, std::min(max_chunk, prefill_remaining));
-  *infeasible_out = 0;
-  if (!feasible(t_of(0), slack_s)) {
-    *chunk_out = 0;
-    *infeasible_out = 1;
-    return NIYAMA_OK;
-  }
-  if (feasible(t_of(cap), slack_s)) {
-    *chunk_out = cap;
-    return NIYAMA_OK;
-  }
-  int32_t lo = 0, hi = cap;  // t_of(lo) feasible, t_of(hi) not
-  while (hi - lo > 1) {
-    const int32_t mid = lo + (hi - lo) / 2;
-    if (feasible(t_of(mid), slack_s))
-      lo = mid;
-    else
-      hi = mid;
-  }
-  *chunk_out = lo;
-  return NIYAMA_OK;
-}
-
-extern "C" void niyama_predictor_destroy(niyama_predictor* p) { delete p; }
-
-extern "C" niyama_status niyama_predictor_bind(niyama_predictor* p, const niyama_kv* kv) {
-  if (!p || !kv) return fail(NIYAMA_EINVAL, "predictor/kv is NULL");
-  if (p->hq != kv->hq || p->hkv != kv->hkv || p->d != kv->d || p->elt != kv->elt)
-    return fail(NIYAMA_EINVAL, "predictor shape differs from the kv's local shape");
-  p->num_sms = kv->num_sms;
-  p->tune = kv->tune;
   return NIYAMA_OK;
 }
 

@@ -21,7 +21,7 @@ TBL3 = [Q.QoS(True, 6.0, 0.050), Q.QoS(False, slo_ttlt=600.0), Q.QoS(False, slo_
 
 def affine_predictor():
     cfg = ny.Predictor.shape_cfg(32, 8, 128, "bf16")
-    return ny.Predictor.from_params(cfg, [C0, C1, 0.0, C2, 0.0, 0.0, 1e-6, 8e10, 7e12])
+    return ny.Predictor.from_params(cfg, [C0, C1, 0.0, C2, 0.0, 0.0] + list(ny.DEFAULT_THETA[6:]))
 
 
 def scale_qos(q, s):

@@ -32,7 +32,7 @@ def main():
     stream = torch.cuda.current_stream()
     batch = ny.Batch(desc)
     cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, 1)
-    pred = ny.Predictor.from_params(cfg, [3.1e-5, 5e-9, 0, 0, 1.07, 0.16, 1.3e-6, 70e9, 7.2e12])
+    pred = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA))
     mode = sys.argv[1] if len(sys.argv) > 1 else "full"
     names = ["plan", "append", "attention", "predict", "rollback", "close"]
     acc = np.zeros(len(names))

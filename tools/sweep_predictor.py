@@ -84,7 +84,7 @@ class Rig:
         ts = []
         for _ in range(reps):
             if self.flush == "read":
-                torch.sum(self.scratch, dtype=torch.float32, out=self.sink)
+                self.sink = self.scratch.sum(dtype=torch.float32)
             else:
                 self.scratch.fill_(1)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -99,7 +99,7 @@ class Rig:
             # entry, start, prefill end, decode end, exit (ns from the first entry), tiles done
             buf = torch.zeros(160 * 8 + 10 * 64, dtype=torch.int64, device="cuda")
             kv.debug_trace(buf)
-            torch.sum(self.scratch, dtype=torch.float32, out=self.sink)
+            self.sink = self.scratch.sum(dtype=torch.float32)
             kv.attention(plan, 0, q, out)
             torch.cuda.synchronize()
             kv.debug_trace(None)
