@@ -390,14 +390,16 @@ niyama_status niyama_min_slack(const niyama_decode_qos* decodes, int32_t n, doub
  * decode estimate being mean + 2 std of the app's completed decode lengths,
  * P:276; FCFS / EDF / SJF / SRPF baselines; ties by arrival
  * then id); ② check violations (Violated: deadline < now; WillViolate:
- * deadline < now + Prefill_rem (+ Decode_rem for TTLT), R23); ③ eager
+ * deadline < now + Prefill_rem + decode_token_s (TTFT; + Decode_rem instead for
+ * TTLT), R23); ③ eager
  * relegation (Low-priority violators first, High ones only in an
  * iteration that relegated no Low one, R22); the relegated queue is served
  * (earliest original deadline first) only when no primary candidate is left
  * (R28); selective preemption (R26); ④ dynamic chunking: the largest
  * chunk whose predicted batch latency fits the min slack of the running
  * decodes (bisection as niyama_max_feasible_chunk; relegated decodes do
- * not bind, R29), or fixed_chunk; ⑤ greedy multi-fill (R27; the last
+ * not bind, R29; an interactive decode already past its token deadline binds at
+ * its TBT, R31), or fixed_chunk; ⑤ greedy multi-fill (R27; the last
  * slice is shrunk if the filled batch predicts above the slack); ⑦ complete():
  * each running decode emitted one token; finished ones leave (their length
  * feeds the history); completed prefills enter the decode queue (R21).
@@ -422,6 +424,8 @@ typedef struct {
   double alpha;                 /* Eq. 4-5 weight, >= 0 (s of deadline per s of remaining work) */
   double prior_mean, prior_std; /* decode-length prior (tokens) */
   double decode_token_s;        /* seconds per decode iteration in Decode_rem (R25) */
+  double layers;                /* an iteration = fixed_s + layers x the predictor's batch time (R30), > 0 */
+  double fixed_s;               /* >= 0 */
 } niyama_sched_config;
 typedef struct {
   int32_t interactive;          /* 1: TTFT + TBT (Eq. 1-2); 0: TTLT (Eq. 3) */
@@ -446,7 +450,8 @@ typedef struct {
 } niyama_request_info;
 
 void niyama_sched_config_default(niyama_sched_config* cfg); /* NIYAMA, selective, dynamic, 256/2048, relegation,
-                                                               multi-fill, 30, alpha 0, prior 415 +- 300, 50 ms */
+                                                               multi-fill, 30, alpha 0, prior 415 +- 300, 50 ms,
+                                                               layers 1, fixed 0 */
 /* model: borrowed (must outlive the scheduler).  EINVAL on a bad config. */
 niyama_status niyama_sched_create(const niyama_sched_config* cfg, const niyama_predictor* model, niyama_sched** out);
 void niyama_sched_destroy(niyama_sched* s);

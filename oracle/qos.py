@@ -18,7 +18,8 @@ operational rules where the paper is silent.  Readings (DESIGN.md
       requests whose status != OK are relegated; High-priority ones with
       status != OK only in an iteration that relegated no Low one.
   R23 "about to violate" horizon (S:291): TTFT case deadline < now +
-      Prefill_rem; TTLT case deadline < now + Prefill_rem + Decode_rem.
+      Prefill_rem + decode_token_s (the first token comes from the first decode
+      iteration, R21); TTLT case deadline < now + Prefill_rem + Decode_rem.
   R24 Prefill_rem (Eq. 4-5; "time to process remaining prefill tokens of
       this request alone"): sum over max_chunk-sized chunks, from the request's
       current prefill offset, of the cost model's prefill-only batch time.
@@ -41,6 +42,12 @@ operational rules where the paper is silent.  Readings (DESIGN.md
       deadline, then arrival, then id) is the candidate; never re-promoted.
   R29 decodes of relegated requests do not bind the slack (they are counted
       violated already, "may finish late").
+  R31 an interactive decode whose next-token deadline has already passed (the
+      token is late whatever the chunk) binds the slack at its SLO_TBT: it is
+      paced, not chased, so one late request does not starve every prefill
+      (measured in the config-5 replay: chasing collapsed at 1.5x load).
+  R30 an iteration's time = fixed_s + layers x the cost model's time of the
+      batch (the model predicts one layer's launch, a8; defaults 0 and 1).
 
 Policies (S:262-268, P:434 baselines): NIYAMA (Eq. 4-5 key), FCFS (arrival),
 EDF (TTFT / TTLT deadline), SJF (prompt tokens), SRPF (remaining prompt
@@ -84,6 +91,8 @@ class Config:
     prior_mean: float = 415.0      # ShareGPT decode p50 (Table 1)
     prior_std: float = 300.0
     decode_token_s: float = 0.05
+    layers: float = 1.0            # an iteration = fixed_s + layers x the cost model's batch time (R30)
+    fixed_s: float = 0.0
 
 
 @dataclass
@@ -146,6 +155,10 @@ class Scheduler:
         self.inflight: Optional[int] = None
         self.last: Optional[Batch] = None
 
+    def iter_time(self, slices, ctx) -> float:
+        """R30: one iteration runs the batch through every layer."""
+        return self.cfg.fixed_s + self.cfg.layers * self.model.iter_time(slices, ctx)
+
     # ---- requests ----
     def submit(self, r: Req):
         if r.prompt < 1 or r.id in self.reqs:
@@ -158,7 +171,7 @@ class Scheduler:
         t, off = 0.0, r.prefill_done
         while off < r.prompt:
             c = min(self.cfg.max_chunk, r.prompt - off)
-            t += self.model.iter_time([(off, c)], [])
+            t += self.iter_time([(off, c)], [])
             off += c
         return t
 
@@ -197,12 +210,15 @@ class Scheduler:
         horizon = self.prefill_rem(r)
         if not r.qos.interactive:
             horizon += self.decode_rem(r)
+        else:
+            horizon += self.cfg.decode_token_s      # R23: the first token needs one decode iteration (R21)
         return WILL_VIOLATE if d < now + horizon else OK
 
     # ---- slack (oracle.sched) ----
     def decode_slack(self, r: Req, now: float) -> float:
         if r.qos.interactive:
-            return deadline_token(r.t_arrival, r.qos.slo_ttft, r.qos.slo_tbt, r.decoded + 1) - now   # R21
+            s = deadline_token(r.t_arrival, r.qos.slo_ttft, r.qos.slo_tbt, r.decoded + 1) - now      # R21
+            return s if s >= 0.0 else r.qos.slo_tbt                                                   # R31
         est = max(1.0, self.hist.estimate(r.app, self.cfg) - r.decoded)
         return (deadline_total(r.t_arrival, r.qos.slo_ttlt) - now) / est                        # R17
 
@@ -242,7 +258,7 @@ class Scheduler:
                 keep = True
                 if c.preemption == SELECTIVE:
                     head = queue[0]
-                    delay = self.model.iter_time([(head.prefill_done, min(c.max_chunk, head.prompt - head.prefill_done))], ctx)
+                    delay = self.iter_time([(head.prefill_done, min(c.max_chunk, head.prompt - head.prefill_done))], ctx)
                     keep = self.status(cur, now + delay) != OK
                 if keep:
                     queue = [cur] + [r for r in queue if r is not cur]
@@ -268,19 +284,19 @@ class Scheduler:
             left -= n
             if not c.multi_fill:
                 break
-        pred = self.model.iter_time([(o, n) for _, o, n in slices], ctx)
+        pred = self.iter_time([(o, n) for _, o, n in slices], ctx)
         if c.dynamic_chunk and slices and pred > slack + 1e-12 * max(1.0, abs(slack)):
             rid, o, n = slices[-1]
             lo, hi = 0, n
             while hi - lo > 1:
                 mid = (lo + hi) // 2
-                t = self.model.iter_time([(a, b) for _, a, b in slices[:-1]] + [(o, mid)], ctx)
+                t = self.iter_time([(a, b) for _, a, b in slices[:-1]] + [(o, mid)], ctx)
                 if t <= slack + 1e-12 * max(1.0, abs(slack)):
                     lo = mid
                 else:
                     hi = mid
             slices = slices[:-1] + ([(rid, o, lo)] if lo > 0 else [])
-            pred = self.model.iter_time([(a, b) for _, a, b in slices], ctx)
+            pred = self.iter_time([(a, b) for _, a, b in slices], ctx)
         b = Batch(slices, dec, budget, pred, slack, infeasible, relegated)
         self.last = b
         return b
@@ -288,7 +304,7 @@ class Scheduler:
     def max_chunk(self, ctx: Sequence[int], offset: int, slack: float, cap: int) -> Tuple[int, bool]:
         """S:116-124 by bisection (oracle.predictor.max_feasible_chunk's rule)."""
         def ok(C):
-            return self.model.iter_time([(offset, C)] if C else [], ctx) <= slack + 1e-12 * max(1.0, abs(slack))
+            return self.iter_time([(offset, C)] if C else [], ctx) <= slack + 1e-12 * max(1.0, abs(slack))
         if not ok(0):
             return 0, True
         if ok(cap):

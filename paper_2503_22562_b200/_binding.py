@@ -83,7 +83,8 @@ class SchedConfigC(C.Structure):
     _fields_ = [("policy", C.c_int32), ("preemption", C.c_int32), ("dynamic_chunk", C.c_int32),
                 ("fixed_chunk", C.c_int32), ("max_chunk", C.c_int32), ("relegation", C.c_int32),
                 ("multi_fill", C.c_int32), ("history_min_samples", C.c_int32), ("alpha", C.c_double),
-                ("prior_mean", C.c_double), ("prior_std", C.c_double), ("decode_token_s", C.c_double)]
+                ("prior_mean", C.c_double), ("prior_std", C.c_double), ("decode_token_s", C.c_double),
+                ("layers", C.c_double), ("fixed_s", C.c_double)]
 
 
 class QoSSpecC(C.Structure):
@@ -552,7 +553,7 @@ class Scheduler:
 
     def __init__(self, model: "Predictor", policy="niyama", preemption="selective", dynamic_chunk=True,
                  fixed_chunk=256, max_chunk=2048, relegation=True, multi_fill=True, history_min_samples=30,
-                 alpha=0.0, prior_mean=415.0, prior_std=300.0, decode_token_s=0.05):
+                 alpha=0.0, prior_mean=415.0, prior_std=300.0, decode_token_s=0.05, layers=1.0, fixed_s=0.0):
         cfg = SchedConfigC()
         lib.niyama_sched_config_default(C.byref(cfg))
         cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
@@ -562,6 +563,7 @@ class Scheduler:
         cfg.history_min_samples = int(history_min_samples)
         cfg.alpha, cfg.prior_mean, cfg.prior_std = float(alpha), float(prior_mean), float(prior_std)
         cfg.decode_token_s = float(decode_token_s)
+        cfg.layers, cfg.fixed_s = float(layers), float(fixed_s)
         self.model = model           # keep the borrowed predictor alive
         h = C.c_void_p()
         _check(lib.niyama_sched_create(C.byref(cfg), model.handle, C.byref(h)))

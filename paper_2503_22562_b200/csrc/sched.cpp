@@ -70,7 +70,7 @@ struct niyama_sched {
     d.num_decode = nctx;
     d.decode_seq = nullptr;
     d.decode_ctx = ctx;
-    return niyama_predict_iter_time(model, &d);
+    return cfg.fixed_s + cfg.layers * niyama_predict_iter_time(model, &d);  // R30
   }
   double one_slice(int32_t off, int32_t len, const int32_t* ctx, int32_t nctx) const {
     s_off.assign(1, off);
@@ -127,12 +127,17 @@ struct niyama_sched {
     const double d = deadline(r);
     if (d < now) return NIYAMA_VIOLATED;
     double horizon = prefill_rem(r);
-    if (!r.qos.interactive) horizon += decode_rem(r);
+    if (!r.qos.interactive)
+      horizon += decode_rem(r);
+    else
+      horizon += cfg.decode_token_s;  // R23: the first token needs one decode iteration
     return d < now + horizon ? NIYAMA_WILL_VIOLATE : NIYAMA_QOS_OK;
   }
   double decode_slack(const Req& r, double now) const {
-    if (r.qos.interactive)  // Eq. 2 at n = decoded + 1 (R21)
-      return r.t_arrival + r.qos.slo_ttft + static_cast<double>(r.decoded) * r.qos.slo_tbt - now;
+    if (r.qos.interactive) {  // Eq. 2 at n = decoded + 1 (R21); a late token is paced at TBT (R31)
+      const double s = r.t_arrival + r.qos.slo_ttft + static_cast<double>(r.decoded) * r.qos.slo_tbt - now;
+      return s >= 0.0 ? s : r.qos.slo_tbt;
+    }
     const double est = std::max(1.0, estimate(r.app) - r.decoded);
     return (r.t_arrival + r.qos.slo_ttlt - now) / est;  // R17
   }
@@ -161,6 +166,8 @@ niyama_status check_cfg(const niyama_sched_config* c) {
   if (!(c->decode_token_s >= 0.0) || !(c->prior_mean >= 0.0) || !(c->prior_std >= 0.0) ||
       c->history_min_samples < 0)
     return niyama::set_error(NIYAMA_EINVAL, "sched config: history / decode_token_s");
+  if (!(c->layers > 0.0) || !(c->fixed_s >= 0.0) || std::isinf(c->layers) || std::isinf(c->fixed_s))
+    return niyama::set_error(NIYAMA_EINVAL, "sched config: layers > 0, fixed_s >= 0");
   return NIYAMA_OK;
 }
 
@@ -181,6 +188,8 @@ extern "C" void niyama_sched_config_default(niyama_sched_config* c) {
   c->prior_mean = 415.0;
   c->prior_std = 300.0;
   c->decode_token_s = 0.05;
+  c->layers = 1.0;
+  c->fixed_s = 0.0;
 }
 
 extern "C" niyama_status niyama_sched_create(const niyama_sched_config* cfg, const niyama_predictor* model,
