@@ -240,6 +240,9 @@ niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
  *   grid_cap          0 = grid from the plan; n > 0 = at most n CTAs (diagnostics)
  *   plan_copy_stream  1 = plans upload on the library's copy stream (default), 0 = on
  *                     the caller's stream
+ *   decode_path       bf16 decode units: 0 = per-warp mma.sync streams (default), 1 = one
+ *                     tensor-core (tcgen05) pipeline per CTA over 128-token steps (same
+ *                     results within bf16 rounding; measured slower: DESIGN.md 6.1)
  * A changed tuning applies to plans created afterwards (split, CTA split) and to
  * launches issued afterwards (grid cap). */
 typedef struct {
@@ -249,6 +252,7 @@ typedef struct {
   int32_t tail_min;
   int32_t grid_cap;
   int32_t plan_copy_stream;
+  int32_t decode_path;
 } niyama_tuning;
 niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning* out);
 niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t); /* EINVAL on out-of-range fields */

@@ -22,6 +22,7 @@ inline niyama_tuning default_tuning() {
   niyama_tuning t{};
   t.prefill_ctas = 0;
   t.split_len = 0;
+  t.decode_path = 0;
   t.tail_div = NIYAMA_TAIL_DIV;
   t.tail_min = NIYAMA_TAIL_MIN;
   t.grid_cap = 0;
@@ -57,16 +58,20 @@ struct CtaSplit {
   int32_t grid, prefill_ctas;
 };
 inline CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv, int d, int elt,
-                   int g, int num_sms) {
+                   int g, int num_sms, int decode_path = 0) {
   CtaSplit r{};
-  r.grid = static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div64(n_units, 8))));
+  // a decode CTA runs one unit at a time (tensor-core pipeline) or one per warp (8+ warps)
+  const int64_t units_per_cta = decode_path == 1 ? 1 : 8;
+  r.grid = static_cast<int32_t>(
+      std::max<int64_t>(1, std::min<int64_t>(num_sms, n_tiles + ceil_div64(n_units, units_per_cta))));
   if (n_tiles == 0) return r;
   if (n_units == 0) {
     r.prefill_ctas = r.grid;
     return r;
   }
   const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
-  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt * (g > 4 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
+  const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt *
+                    (g > 4 && decode_path == 0 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
   int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
   // a tile-count floor keeps short-tile prefill off the tail (at most 4 tiles per prefill
   // CTA), itself capped at half the grid: with many long tiles (config 4: 1,024) it would
@@ -83,6 +88,9 @@ inline CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, i
 inline int32_t rows_per_tile(int g) { return 128 / (g > 0 ? g : 1); }
 // Decode warps per CTA of the bf16 launch (12 when g <= 4, else 8)
 inline int decode_warps(int g) { return g <= 4 ? 12 : 8; }
+// Decode streams per CTA as the predictor models them: one pipeline (tensor-core path) or
+// one per decode warp (mma.sync path).
+inline int decode_streams(int g, int decode_path) { return decode_path == 1 ? 1 : decode_warps(g); }
 
 struct KvModel {
   int hq, hkv, d, elt, num_sms;
@@ -205,6 +213,7 @@ struct AttnParams {
   int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks of pool_k / pool_v
   int32_t kv_adjacent;   // 1: pool_v = pool_k + chunk_bytes (K and V^T chunks of a block adjacent)
   int32_t dec_warps;     // bf16 decode warps per CTA: 12 (2-stage rings) or 8 (3-stage rings)
+  int32_t dec_mode;      // bf16 decode path: 0 = warp mma.sync streams, 1 = tensor-core CTA pipeline (128-token steps)
   int32_t T, Hq, Hkv, d, B, g, R;
   int32_t b_shift;    // log2(B) (block sizes are powers of two)
   int32_t hkv_shift;  // log2(Hkv) when Hkv is a power of two, else -1 (divide)

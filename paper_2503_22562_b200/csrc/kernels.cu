@@ -240,7 +240,22 @@ constexpr int kDecStage = 8192;  // 16 tokens of K (4 KB) + V^T (4 KB)
 // of the group on N (mma.sync m16n8k16, "swap-AB"): 8 MMAs for S^T = K Q^T and 8 for
 // O^T += V^T P^T per stage (heads on M would pad g to 16 rows and need 16 + 16).
 
-constexpr int kDataBytes = kPrefillBytes > kDecSlots * kDecStage ? kPrefillBytes : kDecSlots * kDecStage;
+// Decode, tensor-core CTA pipeline (p.dec_mode == 1, DESIGN.md 6.1 "decode unit"): one
+// pipeline per CTA over 128-token steps of one (row, kv head) unit at a time.  Swap-AB on
+// tcgen05: S^T [128 tokens x 16] = K [128 x 128 d] . Q^T (the g <= 8 heads of the group,
+// zero-padded to N = 16), softmax over the tokens per head (thread = TMEM lane = token),
+// O^T [128 d x 16] += V^T [128 d x 128 tokens] . P^T (P^T bf16 in shared memory).
+// Shared memory: 3 stages of 64 KB (K 128 rows core-matrix | V^T 8 SW32 sub-blocks) |
+// 4 Q^T tiles (4 KB) | 2 P^T tiles (4 KB).  TMEM: S^T [2][16 cols] at 0, O^T [2][16] at 32.
+constexpr int kD2Stages = 3;
+constexpr int kD2Stage = 65536;
+constexpr int kD2QOff = kD2Stages * kD2Stage;
+constexpr int kD2QBufs = 4;
+constexpr int kD2POff = kD2QOff + kD2QBufs * 4096;
+constexpr int kD2Bytes = kD2POff + 2 * 4096;
+constexpr uint32_t kIdescD2 = idesc_bf16_f32(128, 16, 0, 0);
+constexpr int kDataBytes0 = kPrefillBytes > kDecSlots * kDecStage ? kPrefillBytes : kDecSlots * kDecStage;
+constexpr int kDataBytes = kDataBytes0 > kD2Bytes ? kDataBytes0 : kD2Bytes;
 static_assert(kDecWarps <= kThreads / 32, "decode warps");
 // barrier indices
 constexpr int kBarKFull = 0;                       // [kKStages]
@@ -251,12 +266,30 @@ constexpr int kBarSFull = kBarVEmpty + kVStages;   // [kSBufs] QK^T committed in
 constexpr int kBarPFull = kBarSFull + kSBufs;      // [kSBufs] softmax wrote P over S[b] (128 arrivals)
 constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from S[b] committed (S[b] free, O includes it)
 constexpr int kBarDec = kBarODone + kSBufs;        // [kDecSlots] decode ring stages
-constexpr int kNumBars = kBarDec + kDecSlots;
+constexpr int kB2Full = kBarDec + kDecSlots;  // [kD2Stages] K/V step landed (tx)
+constexpr int kB2Empty = kB2Full + kD2Stages;  // [kD2Stages] PV of the step done (commit)
+constexpr int kB2SFull = kB2Empty + kD2Stages;  // [2] QK^T committed into S^T[b]
+constexpr int kB2SFree = kB2SFull + 2;          // [2] softmax loaded S^T[b] (128)
+constexpr int kB2PFull = kB2SFree + 2;          // [2] P^T[b] written (128)
+constexpr int kB2PFree = kB2PFull + 2;          // [2] PV from P^T[b] done (commit)
+constexpr int kB2OFull = kB2PFree + 2;          // [2] unit's last PV into O^T[u%2] done (commit)
+constexpr int kB2OFree = kB2OFull + 2;          // [2] epilogue loaded O^T[u%2] (128)
+constexpr int kB2MLFull = kB2OFree + 2;         // [2] (m, l) of unit u written (128)
+constexpr int kB2MLFree = kB2MLFull + 2;        // [2] epilogue read them (128)
+constexpr int kB2QFull = kB2MLFree + 2;         // [kD2QBufs] Q^T tile written (1, after the producer warp)
+constexpr int kB2QFree = kB2QFull + kD2QBufs;   // [kD2QBufs] unit's last QK^T done (commit)
+constexpr int kB2DFull = kB2QFree + kD2QBufs;   // [4] unit descriptor published (1)
+constexpr int kB2DFree = kB2DFull + 4;          // [4] producer, MMA, softmax, epilogue done with it (4)
+constexpr int kNumBars = kB2DFree + 4;
 constexpr int kBarBytes = (kNumBars * 8 + 63) & ~63;  // keeps the misc area 64-byte aligned (v4 accesses)
 constexpr int kMiscBytes = 64 + kDecWarps * 16;      // tmem slot, item slot, per-warp desc counters
 constexpr int kDescBytes = kDecWarps * 4 * 32;       // per-warp 4-entry UnitDesc rings (decode);
                                                      // the prefill softmax chain [2][128] floats (prefill)
 static_assert(kDescBytes >= 2 * 128 * 4, "softmax chain must fit");
+// decode-v2 scratch in the desc area: 4 descriptors (128 B) | first-step blocks [4][8] (128 B) | max [2][4][16] f32 (512 B) |
+// l [2][4][16] f32 (512 B) | (m, l) [2][16] f32x2 (256 B)
+constexpr int kD2Desc = 0, kD2Red = 256, kD2LRed = kD2Red + 512, kD2ML = kD2LRed + 512;
+static_assert(kD2ML + 256 <= kDescBytes, "decode-v2 scratch must fit");
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kBarBytes + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
@@ -1156,6 +1189,367 @@ __device__ __forceinline__ void merge_tail(const AttnParams& p) {
   }
 }
 
+// ------------------------------------------------- decode, tensor-core CTA pipeline
+// (p.dec_mode == 1; constants and barriers in fa::kD2* / kB2*).  Roles:
+//   warp 0        producer: claims units (pre-assigned first unit per decode-first CTA,
+//                 then the queue counter), publishes their descriptors, writes each
+//                 unit's Q^T tile, and streams its 128-token steps: per paged block one
+//                 bulk copy of its K rows and one of its V^T sub-blocks (evict-first).
+//   warp 1 lane 0 MMA issuer: QK^T of step j+1 is issued before PV of step j, so the
+//                 softmax of j overlaps the tensor core.
+//   warps 4-7     softmax: thread = TMEM lane = token of the step; per-head max over the
+//                 step's 128 tokens (shuffles + 4-warp exchange), lazy O rescale (max
+//                 grows by > 8 in log2 units), P^T (bf16) into shared memory; per-thread
+//                 partial sums l, reduced once per unit.
+//   warps 8-11    epilogue: thread = TMEM lane = head dim; O^T / l -> O (bf16, unsplit
+//                 rows) or the fp32 partial (split rows) + the completion count (a6).
+__device__ __forceinline__ uint32_t d2_pt_off(int h, int t) {  // P^T [K = 128 tokens][N = 16 heads], K-major
+  return (h >> 3) * 2048 + (t >> 3) * 128 + (h & 7) * 16 + (t & 7) * 2;
+}
+
+__device__ __forceinline__ void decode_cta_v2(const AttnParams& p, uint32_t sbase, uint32_t bars, uint32_t tmem,
+                                              uint32_t scratch) {
+  using namespace fa;
+  // diagnostics (p.trace): CTA 0, steps < 64: clock64 per role (0 copies issued, 1 QK issued,
+  // 2 S ready (softmax), 3 P written, 4 PV issued, 5 stage full seen by the MMA, 6 stage empty
+  // seen by the producer)
+  int64_t* tr2 = (p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * 160 : nullptr;
+  auto stamp = [&](int role, uint32_t j) {
+    if (tr2 != nullptr && j < 64) tr2[role * 64 + j] = static_cast<int64_t>(clock64());
+  };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = p.g;
+  const uint32_t descs = scratch + kD2Desc;
+  auto bar = [&](int b) { return bars + 8 * b; };
+  const int tb = p.B < 128 ? p.B : 128;  // tokens of one block inside a step
+  if (warp == 2) {
+    // ---------------------------------------------------------- unit warp
+    // Claims units up to 4 ahead of the pipeline (ring of 4 descriptors + 4 Q^T tiles), so
+    // the claim -> record -> Q round trips never stall the K/V stream.  Each descriptor
+    // also carries the physical blocks of the unit's first step.
+    const int dec_first = p.n_tiles > 0 ? p.prefill_ctas : 0;
+    const int id_base = static_cast<int>(gridDim.x) - dec_first;
+    int reserved = static_cast<int>(blockIdx.x) >= dec_first ? static_cast<int>(blockIdx.x) - dec_first : -1;
+    int next = 0;
+    if (lane == 0) next = reserved >= 0 ? reserved : id_base + atomicAdd(p.work + 1, 1);
+    for (uint32_t u = 0;; ++u) {
+      const int id = __shfl_sync(0xffffffffu, next, 0);
+      // claim the unit after this one now: its round trip overlaps this one's preparation
+      if (lane == 0 && id < p.n_units) next = id_base + atomicAdd(p.work + 1, 1);
+      UnitDesc d{};
+      d.id = -1;
+      int phys0 = 0;
+      if (id < p.n_units) {
+        const int hkv_id = div_hkv(p, id);
+        const int4* rp = reinterpret_cast<const int4*>(p.uq + hkv_id);
+        const int4 a = __ldg(rp), b = __ldg(rp + 1);
+        d.kvh = id - hkv_id * p.Hkv;
+        d.id = b.y + d.kvh;  // pbase + kv head
+        d.tbl = a.x;
+        d.row = a.y;
+        d.k0 = a.z;
+        d.k1 = a.w;
+        d.nsplit = b.x;
+        d.crow = b.w;
+        const int nblk_tbl = (d.k1 + p.B - 1) >> p.b_shift;
+        if (lane * tb < 128) phys0 = __ldg(p.tables + d.tbl + min((d.k0 + lane * tb) >> p.b_shift, nblk_tbl - 1));
+      }
+      const int ds = u & 3;
+      mbar_wait(bar(kB2DFree + ds), ((u >> 2) & 1) ^ 1);
+      if (d.id >= 0) {
+        const int qb = u % kD2QBufs;  // == ds: the Q^T tile is freed with the descriptor (last QK^T)
+        const uint32_t qt = sbase + kD2QOff + qb * 4096;
+        const uint8_t* qsrc = static_cast<const uint8_t*>(p.q) +
+                              (static_cast<int64_t>(d.row) * p.Hq + d.kvh * g) * (kD * 2);
+        for (int pc = lane; pc < g * 16; pc += 32) {
+          const int h = pc >> 4, j = pc & 15;
+          const uint4 v = __ldg(reinterpret_cast<const uint4*>(qsrc + pc * 16));
+          st_shared_v4(qt + (h >> 3) * 2048 + j * 128 + (h & 7) * 16, v.x, v.y, v.z, v.w);
+        }
+        fence_proxy_async_smem();
+        if (lane < 8) asm volatile("st.shared.s32 [%0], %1;" ::"r"(descs + 128 + ds * 32 + lane * 4), "r"(phys0) : "memory");
+      }
+      __syncwarp();
+      if (lane == 0) {
+        desc_store(descs, ds, d);
+        mbar_arrive(bar(kB2DFull + ds));
+      }
+      if (d.id < 0) break;
+    }
+  } else if (warp == 0) {
+    // ------------------------------------------------------------- producer
+    const uint64_t pol = policy_evict_first();
+    const uint32_t bytes_blk = static_cast<uint32_t>(tb) * 512u;  // K rows + V^T sub-blocks
+    uint32_t st = 0;
+    for (uint32_t u = 0;; ++u) {
+      const int ds = u & 3;
+      mbar_wait(bar(kB2DFull + ds), (u >> 2) & 1);
+      const UnitDesc d = desc_load(descs, ds);
+      if (d.id < 0) break;
+      const int nsteps = (d.k1 - d.k0 + 127) >> 7;
+      const int nblk_tbl = (d.k1 + p.B - 1) >> p.b_shift;
+      int phys_next = 0;
+      if (lane < 8) asm volatile("ld.shared.s32 %0, [%1];" : "=r"(phys_next) : "r"(descs + 128 + ds * 32 + lane * 4) : "memory");
+      auto lookup = [&](int s) {
+        const int k = d.k0 + 128 * s + lane * tb;
+        return (lane * tb < 128 && s < nsteps) ? __ldg(p.tables + d.tbl + min(k >> p.b_shift, nblk_tbl - 1)) : 0;
+      };
+      for (int s = 0; s < nsteps; ++s, ++st) {
+        const int phys = phys_next;
+        phys_next = lookup(s + 1);
+        const int k = d.k0 + 128 * s;
+        const int valid = min(128, d.k1 - k);
+        const int nb = (valid + tb - 1) / tb;
+        const int slot = st % kD2Stages;
+        const uint32_t stg = sbase + slot * kD2Stage;
+        if (lane == 0) {
+          mbar_wait(bar(kB2Empty + slot), ((st / kD2Stages) & 1) ^ 1);
+          stamp(6, st);
+          mbar_expect_tx(bar(kB2Full + slot), nb * bytes_blk);
+        }
+        __syncwarp();
+        if (lane < nb) {
+          const int64_t chunk = (static_cast<int64_t>(phys) * p.Hkv + d.kvh) * p.chunk_stride;
+          bulk_g2s_hint(stg + lane * tb * 256, p.pool_k + chunk, tb * 256, bar(kB2Full + slot), pol);
+          bulk_g2s_hint(stg + 32768 + lane * tb * 256, p.pool_v + chunk, tb * 256, bar(kB2Full + slot), pol);
+        }
+        if (lane == 0) stamp(0, st);
+      }
+      if (lane == 0) mbar_arrive(bar(kB2DFree + ds));
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      struct Pend {
+        int slot, b, u, first, last;
+      } pd{0, 0, 0, 0, 0};
+      bool pending = false;
+      uint32_t st = 0;
+      auto issue_pv = [&](const Pend& q, uint32_t qst) {
+        mbar_wait(bar(kB2PFull + q.b), (qst >> 1) & 1);
+        if (q.first) mbar_wait(bar(kB2OFree + (q.u & 1)), ((q.u >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t va = sbase + q.slot * kD2Stage + 32768, pa = sbase + kD2POff + q.b * 4096;
+        // descriptors built once; the start-address field (bits 0-13, 16-byte units) advances per k-step
+        const uint64_t vd = sw32_desc(va, 16, 256), pdsc = noswz_desc(pa, 128, 2048);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          umma_f16(tmem + 32 + 16 * (q.u & 1), vd + static_cast<uint64_t>(kk * (4096 >> 4)),
+                   pdsc + static_cast<uint64_t>(kk * (256 >> 4)), kIdescD2, (q.first && kk == 0) ? 0u : 1u);
+        stamp(4, qst);
+        umma_commit(bar(kB2Empty + q.slot));
+        umma_commit(bar(kB2PFree + q.b));
+        if (q.last) umma_commit(bar(kB2OFull + (q.u & 1)));
+      };
+      for (uint32_t u = 0;; ++u) {
+        mbar_wait(bar(kB2DFull + (u & 3)), (u >> 2) & 1);
+        const UnitDesc d = desc_load(descs, u & 3);
+        if (d.id < 0) break;
+        const int qb = u % kD2QBufs;
+        const int nsteps = (d.k1 - d.k0 + 127) >> 7;
+        const uint32_t qa = sbase + kD2QOff + qb * 4096;
+        for (int s = 0; s < nsteps; ++s, ++st) {
+          const int slot = st % kD2Stages, b = st & 1;
+          mbar_wait(bar(kB2Full + slot), (st / kD2Stages) & 1);
+          stamp(5, st);
+          mbar_wait(bar(kB2SFree + b), ((st >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t ka = sbase + slot * kD2Stage;
+          const uint64_t kd = noswz_desc(ka, 128, 2048), qd = noswz_desc(qa, 128, 2048);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            umma_f16(tmem + 16 * b, kd + static_cast<uint64_t>(kk * (256 >> 4)), qd + static_cast<uint64_t>(kk * (256 >> 4)),
+                     kIdescD2, kk > 0 ? 1u : 0u);
+          umma_commit(bar(kB2SFull + b));
+          stamp(1, st);
+          if (s == nsteps - 1) umma_commit(bar(kB2DFree + (u & 3)));  // Q^T tile read: the slot may be refilled
+          if (pending) issue_pv(pd, st - 1);
+          pd = Pend{slot, static_cast<int>(b), static_cast<int>(u), s == 0, s == nsteps - 1};
+          pending = true;
+        }
+      }
+      if (pending) issue_pv(pd, st - 1);
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------- softmax
+    const int r = tid - 128;  // token of the step (TMEM lane)
+    const int w4 = warp - 4;
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(w4 * 32) << 16);
+    const float sl2 = p.scale_log2;
+    uint32_t st = 0;
+    for (uint32_t u = 0;; ++u) {
+      mbar_wait(bar(kB2DFull + (u & 3)), (u >> 2) & 1);
+      const UnitDesc d = desc_load(descs, u & 3);
+      if (d.id < 0) break;
+      const int nsteps = (d.k1 - d.k0 + 127) >> 7;
+      float m[8], lt[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) m[h] = -INFINITY, lt[h] = 0.f;
+      for (int s = 0; s < nsteps; ++s, ++st) {
+        const int b = st & 1;
+        mbar_wait(bar(kB2SFull + b), (st >> 1) & 1);
+        tc_fence_after();
+        if (r == 0) stamp(2, st);
+        uint32_t sr[16];
+        tmem_ld16(lane_addr + 16 * b, sr);
+        tc_fence_before();
+        mbar_arrive(bar(kB2SFree + b));
+        if (r == 0) stamp(7, st);
+        const bool valid = d.k0 + 128 * s + r < d.k1;
+        float x[8], mx[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          x[h] = (valid && h < g) ? __uint_as_float(sr[h]) * sl2 : -INFINITY;
+          mx[h] = x[h];
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+          for (int h = 0; h < 8; ++h)
+            if (h < g) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], off));
+        const uint32_t red = scratch + kD2Red + b * 256;
+        if (lane < g) {  // mx[lane] without a dynamic register index
+          float v = mx[0];
+#pragma unroll
+          for (int h = 1; h < 8; ++h)
+            if (lane == h) v = mx[h];
+          st_shared_f32(red + w4 * 64 + lane * 4, v);
+        }
+        named_bar_sync(1, 128);
+        if (r == 0) stamp(8, st);
+        bool rescale = false;
+        float alpha[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          alpha[h] = 1.f;
+          if (h < g) {
+            float v = ld_shared_f32(red + h * 4);
+#pragma unroll
+            for (int w = 1; w < 4; ++w) v = fmaxf(v, ld_shared_f32(red + w * 64 + h * 4));
+            if (s == 0) {
+              m[h] = v;
+            } else if (v > m[h] + 8.0f) {  // lazy rescale (P <= 2^8 otherwise)
+              alpha[h] = ex2(m[h] - v);
+              m[h] = v;
+              rescale = true;
+            }
+          }
+        }
+        if (rescale) {  // uniform across the 128 threads: O^T *= alpha per head column, after PV(st-1)
+          mbar_wait(bar(kB2PFree + ((st - 1) & 1)), ((st - 1) >> 1) & 1);
+          tc_fence_after();
+          uint32_t ov[16];
+          tmem_ld16(lane_addr + 32 + 16 * (u & 1), ov);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            ov[h] = __float_as_uint(__uint_as_float(ov[h]) * alpha[h]);
+            lt[h] *= alpha[h];
+          }
+          tmem_st16(lane_addr + 32 + 16 * (u & 1), ov);
+          tmem_wait_st();
+          tc_fence_before();
+        }
+        mbar_wait(bar(kB2PFree + b), ((st >> 1) & 1) ^ 1);  // PV(st-2) has read P^T[b]
+        const uint32_t pt = sbase + kD2POff + b * 4096;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          if (h < g) {
+            const float pv = ex2(x[h] - m[h]);
+            lt[h] += pv;
+            st_shared_u16(pt + d2_pt_off(h, r), __bfloat16_as_ushort(__float2bfloat16_rn(pv)));
+          }
+        }
+        if (r == 0) stamp(9, st);
+        fence_proxy_async_smem();
+        mbar_arrive(bar(kB2PFull + b));
+        if (r == 0) stamp(3, st);
+      }
+      // per-head l over the 128 threads, then (m, l) to the epilogue
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int h = 0; h < 8; ++h)
+          if (h < g) lt[h] += __shfl_xor_sync(0xffffffffu, lt[h], off);
+      const uint32_t lred = scratch + kD2LRed + (u & 1) * 256;
+      if (lane < g) {
+        float v = lt[0];
+#pragma unroll
+        for (int h = 1; h < 8; ++h)
+          if (lane == h) v = lt[h];
+        st_shared_f32(lred + w4 * 64 + lane * 4, v);
+      }
+      named_bar_sync(1, 128);
+      mbar_wait(bar(kB2MLFree + (u & 1)), ((u >> 1) & 1) ^ 1);
+      if (r < g) {
+        float l = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) l += ld_shared_f32(lred + w * 64 + r * 4);
+        float mm = m[0];
+#pragma unroll
+        for (int h = 1; h < 8; ++h)
+          if (r == h) mm = m[h];
+        st_shared_v2f(scratch + kD2ML + (u & 1) * 128 + r * 8, mm, l);
+      }
+      mbar_arrive(bar(kB2MLFull + (u & 1)));
+      if (r == 0) mbar_arrive(bar(kB2DFree + (u & 3)));
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue
+    const int r = tid - 256;  // head dim (TMEM lane)
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>((warp - 8) * 32) << 16);
+    for (uint32_t u = 0;; ++u) {
+      mbar_wait(bar(kB2DFull + (u & 3)), (u >> 2) & 1);
+      const UnitDesc d = desc_load(descs, u & 3);
+      if (d.id < 0) break;
+      mbar_wait(bar(kB2OFull + (u & 1)), (u >> 1) & 1);
+      mbar_wait(bar(kB2MLFull + (u & 1)), (u >> 1) & 1);
+      tc_fence_after();
+      uint32_t ov[16];
+      tmem_ld16(lane_addr + 32 + 16 * (u & 1), ov);
+      tc_fence_before();
+      mbar_arrive(bar(kB2OFree + (u & 1)));
+      float mh[8], lh[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        if (h < g) {
+          const float2 ml = ld_shared_v2f(scratch + kD2ML + (u & 1) * 128 + h * 8);
+          mh[h] = ml.x;
+          lh[h] = ml.y;
+        } else {
+          mh[h] = 0.f;
+          lh[h] = 1.f;
+        }
+      }
+      mbar_arrive(bar(kB2MLFree + (u & 1)));
+      if (d.nsplit == 1) {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          if (h < g) {
+            __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) +
+                                  (static_cast<int64_t>(d.kvh * g + h) * p.T + d.row) * kD;
+            orow[r] = __float2bfloat16_rn(__uint_as_float(ov[h]) / lh[h]);
+            if (r == 0 && p.lse != nullptr)
+              p.lse[static_cast<int64_t>(d.kvh * g + h) * p.T + d.row] = (mh[h] + __log2f(lh[h])) * 0.69314718055994530942f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          if (h < g) {
+            __stcg(p.part_o + (static_cast<int64_t>(d.id) * g + h) * kD + r, __uint_as_float(ov[h]) / lh[h]);
+            if (r == 0) __stcg(reinterpret_cast<float2*>(p.part_ml + (static_cast<int64_t>(d.id) * g + h) * 2),
+                               make_float2(mh[h], lh[h]));
+          }
+        }
+        __threadfence();
+        named_bar_sync(2, 128);
+        if (r == 0) atomicAdd(p.counters + d.crow * p.Hkv + d.kvh, 1);
+      }
+      if (r == 0) mbar_arrive(bar(kB2DFree + (u & 3)));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const AttnParams p) {
   using namespace fa;
   extern __shared__ uint8_t smem_raw[];
@@ -1171,20 +1565,26 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
 
   if (tid == 0) {
-    for (int b = 0; b < kBarDec; ++b)
-      mbar_init(bars + 8 * b, (b >= kBarPFull && b < kBarPFull + kSBufs) ? 128 : 1);
-    for (int b = kBarDec; b < kNumBars; ++b) mbar_init(bars + 8 * b, 1);
+    for (int b = 0; b < kNumBars; ++b) {
+      uint32_t cnt = 1;
+      if (b >= kBarPFull && b < kBarPFull + kSBufs) cnt = 128;
+      if ((b >= kB2SFree && b < kB2PFull + 2) || (b >= kB2OFree && b < kB2MLFree + 2)) cnt = 128;
+      if (b >= kB2DFree && b < kB2DFree + 4) cnt = 4;  // producer, MMA (after the last QK^T), softmax, epilogue
+      mbar_init(bars + 8 * b, cnt);
+    }
     fence_mbar_init();
   }
   const bool any_items = p.n_tiles > 0 && static_cast<int>(blockIdx.x) < p.prefill_ctas;
-  if (any_items && warp == 1) {
+  const bool dec_v2 = p.dec_mode == 1 && p.n_units > 0;
+  const bool need_tmem = any_items || dec_v2;
+  if (need_tmem && warp == 1) {
     tmem_alloc(smem_u32(tmem_slot), kTmemCols);
     tmem_relinquish();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = any_items ? *tmem_slot : 0u;
+  const uint32_t tmem = need_tmem ? *tmem_slot : 0u;
   // Launched with programmatic stream serialization: everything above touched only
   // on-chip state; every global access below comes after the preceding grid (the
   // KV append) has completed and its writes are visible.
@@ -1244,7 +1644,17 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
   __syncthreads();
-  if (p.n_units > 0 && warp < p.dec_warps) {  // the other warps only serve the prefill softmax
+  if (dec_v2) {
+    // tensor-core decode pipeline; its shared memory starts zeroed (padding rows of the
+    // Q^T / P^T tiles, and V^T columns of partial steps must be finite: they meet P = 0)
+    for (int i = tid * 16; i < kD2Bytes; i += kThreads * 16) st_shared_v4(sbase + i, 0u, 0u, 0u, 0u);
+    fence_proxy_async_smem();
+    __syncthreads();
+    decode_cta_v2(p, sbase, bars, tmem, smem_u32(misc + kMiscBytes));
+    tc_fence_before();
+    __syncthreads();
+    if (p.n_merge_rows > 0) merge_tail(p);
+  } else if (p.n_units > 0 && warp < p.dec_warps) {  // the other warps only serve the prefill softmax
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;
     const uint32_t n_desc = smem_u32(misc + 64 + 16 * warp);
     if (p.dec_warps == 12)
@@ -1268,7 +1678,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     tr[4] = static_cast<int64_t>(t_decode);
     tr[6] = static_cast<int64_t>(t_entry);
   }
-  if (any_items && warp == 1) {
+  if (need_tmem && warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }

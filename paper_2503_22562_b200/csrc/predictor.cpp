@@ -59,7 +59,7 @@ Launch build(const niyama_predictor& p, std::vector<SliceOC> slices, const int32
   Launch L;
   const int g = p.hq / p.hkv;
   const int64_t R = rows_per_tile(g);
-  L.wpc = decode_warps(g);
+  L.wpc = decode_streams(g, p.tune.decode_path);
   L.bytes_per_token = static_cast<double>(p.d) * 2.0 * p.elt;
   std::stable_sort(slices.begin(), slices.end(), [](const SliceOC& a, const SliceOC& b) {
     return static_cast<int64_t>(a.o) + a.c > static_cast<int64_t>(b.o) + b.c;
@@ -103,7 +103,7 @@ Launch build(const niyama_predictor& p, std::vector<SliceOC> slices, const int32
   L.D = static_cast<double>(D);
   L.sum_ctx = static_cast<double>(sum_ctx);
   L.units = static_cast<double>(n_units);
-  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, g, p.num_sms);
+  const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, g, p.num_sms, p.tune.decode_path);
   L.grid = cs.grid;
   L.np = cs.prefill_ctas;
   if (p.tune.prefill_ctas > 0 && n_tiles > 0) L.np = std::min(p.tune.prefill_ctas, L.grid);

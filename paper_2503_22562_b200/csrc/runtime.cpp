@@ -356,7 +356,7 @@ namespace {
 
 void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
   const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_tiles,
-                               pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->g, kv->num_sms);
+                               pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->g, kv->num_sms, kv->tune.decode_path);
   pl->grid = r.grid;
   pl->prefill_ctas = r.prefill_ctas;
   if (kv->tune.prefill_ctas > 0 && pl->n_tiles > 0) pl->prefill_ctas = std::min(kv->tune.prefill_ctas, pl->grid);
@@ -943,6 +943,7 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   // g <= 4: 12 decode warps x 2-stage rings; g = 8 (twice the MMA work per byte): 8 x 3
   // (measured: config 2 102.6 -> 99.4 us with 12; config 4 1180 -> 1218 us with 12)
   p.dec_warps = kv->g <= 4 ? 12 : 8;
+  p.dec_mode = kv->tune.decode_path;
   p.T = plan->T;
   p.Hq = kv->hq;
   p.Hkv = kv->hkv;
@@ -999,6 +1000,7 @@ extern "C" niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning
 extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t) {
   if (!kv || !t) return fail(NIYAMA_EINVAL, "kv/tuning is NULL");
   if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
+  if (t->decode_path != 0 && t->decode_path != 1) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0 or 1");
   if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
   if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");
   if (t->tail_min < 16 || t->tail_min % 16) return fail(NIYAMA_EINVAL, "tuning: tail_min must be a multiple of 16");

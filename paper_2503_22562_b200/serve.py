@@ -89,7 +89,8 @@ class GpuExecutor:
         self.q = mk(max_rows, shape.num_q_heads, shape.head_dim)
         self.k = mk(max_rows, shape.num_kv_heads, shape.head_dim)
         self.v = mk(max_rows, shape.num_kv_heads, shape.head_dim)
-        self.o = torch.empty(shape.num_q_heads, max_rows, shape.head_dim, dtype=torch.bfloat16, device=dev)
+        self.obuf = torch.empty(shape.num_q_heads * max_rows * shape.head_dim, dtype=torch.bfloat16, device=dev)
+        self.hq, self.d = shape.num_q_heads, shape.head_dim
         self.stream = torch.cuda.current_stream(device)
         self.e0 = torch.cuda.Event(enable_timing=True)
         self.e1 = torch.cuda.Event(enable_timing=True)
@@ -104,7 +105,7 @@ class GpuExecutor:
             raise ValueError(f"batch of {T} rows exceeds the engine's buffers ({self.max_rows})")
         plan = self.kv.plan(batch.desc(), self.stream)
         q, k, v = self.q[:T], self.k[:T], self.v[:T]
-        o = self.o[:, :T]
+        o = self.obuf[:self.hq * T * self.d].view(self.hq, T, self.d)
         self.e0.record(self.stream)
         for layer in range(self.n_layers):
             self.kv.append(plan, layer, k, v, self.stream)

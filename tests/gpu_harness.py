@@ -38,7 +38,7 @@ class Run:
     attention on the final step)."""
 
     def __init__(self, wl: W.Workload, layers: int = 1, extra_blocks: int = 0, kv=None, scale: float = 0.0,
-                 fused: bool = False):
+                 fused: bool = False, tuning=None):
         """fused: the final step's append runs inside the attention launch
         (niyama_append_attention) instead of its own launch."""
         import paper_2503_22562_b200 as ny
@@ -46,6 +46,8 @@ class Run:
         self.wl, self.s, self.fused = wl, s, fused
         self.kv = kv or ny.KVCache(layers, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + extra_blocks,
                                    block_size=s.block_size, dtype=s.dtype, device=0)
+        if tuning:
+            self.kv.set_tuning(**tuning)
         self.plans = []
         for n, st in enumerate(wl.steps):
             p = self.kv.plan(st.desc)

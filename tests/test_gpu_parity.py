@@ -270,3 +270,19 @@ def test_many_live_plans_fallback():
         p.close()
     wl2 = W.random_hybrid(W.L8B, seed=42, num_prefill=1, max_chunk=150, num_decode=5, max_ctx=500)
     run_and_compare(wl2)
+
+
+@pytest.mark.parametrize("case", ["ragged", "g8", "long-split", "blocks64"])
+def test_tensor_core_decode_path(case):
+    """niyama_tuning.decode_path = 1 (the tcgen05 CTA decode pipeline) against the oracle."""
+    if case == "ragged":
+        wl = W.random_hybrid(W.L8B, seed=21, num_prefill=2, max_chunk=300, num_decode=20, max_ctx=3000)
+    elif case == "g8":
+        wl = W.random_hybrid(W.Shape(64, 8, 128, 16, "bf16"), seed=22, num_prefill=1, max_chunk=200, num_decode=9,
+                             max_ctx=2500)
+    elif case == "long-split":
+        wl = W.hybrid(W.L8B, "long", prefill_offset=0, chunk=0, decode_ctx=[8192, 17, 4095, 1], seed=23)
+    else:
+        wl = W.random_hybrid(W.Shape(32, 8, 128, 64, "bf16"), seed=24, num_prefill=1, max_chunk=300, num_decode=12,
+                             max_ctx=3000)
+    run_and_compare(wl, tuning=dict(decode_path=1))
