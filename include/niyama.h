@@ -354,6 +354,20 @@ typedef struct {
   double seconds;       /* t_hat */
 } niyama_predict_info;
 niyama_status niyama_predict_detail(const niyama_predictor* p, const niyama_batch_desc* desc, niyama_predict_info* out);
+/* Full iteration (§8(f) rank 4; the paper's predictor covers the whole iteration, P:319,
+ * P:672): with layers > 0, niyama_predict_iter_time (and everything built on it: the
+ * chunk choice, the scheduler) returns
+ *     t_iter = c0 + c1 * T + lin(T) + layers * t_hat(batch)
+ * where T = rows of the batch, t_hat the attention model above, and lin the MEASURED time of
+ * one iteration's linear layers at T tokens (a profile lookup table: n >= 2 points
+ * (tokens ascending, > 0), piecewise linear, extrapolated linearly beyond the ends).
+ * layers = 0 restores the single attention launch.  EINVAL on a malformed table. */
+niyama_status niyama_predictor_set_iteration(niyama_predictor* p, int32_t layers, const int32_t* tokens,
+                                             const double* seconds, int32_t n, double c0, double c1);
+/* (c0, c1) by least squares on relative residuals of measured full iterations (host arrays;
+ * the table and layers must be set first); writes them into the predictor. */
+niyama_status niyama_predictor_fit_iteration(niyama_predictor* p, const niyama_batch_desc* batches,
+                                             const double* seconds, int32_t n);
 /* a1 — chunk for the batch {C prefill rows at chunk_offset} + desc's decodes
  * (desc's prefill slices are ignored) against slack_s (a latency equal to the
  * slack is feasible, R18; 1e-12 relative guard).  cap = max(0, min(max_chunk,
@@ -430,6 +444,8 @@ typedef struct {
   double decode_token_s;        /* seconds per decode iteration in Decode_rem (R25) */
   double layers;                /* an iteration = fixed_s + layers x the predictor's batch time (R30), > 0 */
   double fixed_s;               /* >= 0 */
+  int64_t kv_token_budget;      /* KV admission (R32): 0 = unlimited; else prefill slices are cut so that the
+                                   tokens held by unfinished requests plus the batch's new tokens stay <= this */
 } niyama_sched_config;
 typedef struct {
   int32_t interactive;          /* 1: TTFT + TBT (Eq. 1-2); 0: TTLT (Eq. 3) */

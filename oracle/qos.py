@@ -46,6 +46,9 @@ operational rules where the paper is silent.  Readings (DESIGN.md
       token is late whatever the chunk) binds the slack at its SLO_TBT: it is
       paced, not chased, so one late request does not starve every prefill
       (measured in the config-5 replay: chasing collapsed at 1.5x load).
+  R32 KV admission (not in the paper; SPEC lists memory as a non-goal):
+      with a token budget, the fill stops where the tokens held by unfinished
+      requests (prefill done + decoded) plus the batch's new tokens reach it.
   R30 an iteration's time = fixed_s + layers x the cost model's time of the
       batch (the model predicts one layer's launch, a8; defaults 0 and 1).
 
@@ -93,6 +96,7 @@ class Config:
     decode_token_s: float = 0.05
     layers: float = 1.0            # an iteration = fixed_s + layers x the cost model's batch time (R30)
     fixed_s: float = 0.0
+    kv_token_budget: int = 0       # R32: 0 = unlimited
 
 
 @dataclass
@@ -273,9 +277,12 @@ class Scheduler:
             head = queue[0]
             budget, infeasible = self.max_chunk(ctx, head.prefill_done, slack, c.max_chunk)
 
-        # ⑤ fill (R27)
+        # ⑤ fill (R27), within the KV token budget (R32)
         slices: List[Tuple[int, int, int]] = []
         left = budget
+        if c.kv_token_budget > 0:
+            held = len(dec) + sum(r.prefill_done + r.decoded for r in self.reqs.values() if r.state != "done")
+            left = max(0, min(left, c.kv_token_budget - held))
         for r in queue:
             if left <= 0:
                 break

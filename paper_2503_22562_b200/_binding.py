@@ -85,7 +85,7 @@ class SchedConfigC(C.Structure):
                 ("fixed_chunk", C.c_int32), ("max_chunk", C.c_int32), ("relegation", C.c_int32),
                 ("multi_fill", C.c_int32), ("history_min_samples", C.c_int32), ("alpha", C.c_double),
                 ("prior_mean", C.c_double), ("prior_std", C.c_double), ("decode_token_s", C.c_double),
-                ("layers", C.c_double), ("fixed_s", C.c_double)]
+                ("layers", C.c_double), ("fixed_s", C.c_double), ("kv_token_budget", C.c_int64)]
 
 
 class QoSSpecC(C.Structure):
@@ -143,6 +143,9 @@ def _load():
         "niyama_predictor_fit_batches": ([C.POINTER(KVConfig), C.POINTER(BatchDescC), C.POINTER(C.c_double), i32,
                                           C.POINTER(FitOptionsC), C.POINTER(vp)], st),
         "niyama_predict_detail": ([vp, C.POINTER(BatchDescC), C.POINTER(PredictInfoC)], st),
+        "niyama_predictor_set_iteration": ([vp, i32, C.POINTER(i32), C.POINTER(C.c_double), i32, C.c_double,
+                                            C.c_double], st),
+        "niyama_predictor_fit_iteration": ([vp, C.POINTER(BatchDescC), C.POINTER(C.c_double), i32], st),
         "niyama_predictor_from_params": ([C.POINTER(KVConfig), C.POINTER(C.c_double), C.POINTER(vp)], st),
         "niyama_predictor_params": ([vp, C.POINTER(C.c_double)], st),
         "niyama_predict_iter_time": ([vp, C.POINTER(BatchDescC)], C.c_double),
@@ -413,6 +416,21 @@ class Predictor:
         _check(lib.niyama_predictor_fit_batches(C.byref(cfg), arr, sec, len(ds), C.byref(opt), C.byref(h)))
         return cls(h.value)
 
+    def set_iteration(self, layers: int, tokens=(), seconds=(), c0: float = 0.0, c1: float = 0.0) -> "Predictor":
+        """Full-iteration mode (niyama_predictor_set_iteration); layers = 0 switches it off."""
+        n = len(tokens)
+        tk = (C.c_int32 * max(1, n))(*[int(x) for x in tokens])
+        sc = (C.c_double * max(1, n))(*[float(x) for x in seconds])
+        _check(lib.niyama_predictor_set_iteration(self.handle, int(layers), tk, sc, n, float(c0), float(c1)))
+        return self
+
+    def fit_iteration(self, batches, seconds) -> "Predictor":
+        ds = [b if isinstance(b, _Desc) else _Desc(b) for b in batches]
+        arr = (BatchDescC * len(ds))(*[d.c for d in ds])
+        sec = (C.c_double * len(ds))(*[float(x) for x in seconds])
+        _check(lib.niyama_predictor_fit_iteration(self.handle, arr, sec, len(ds)))
+        return self
+
     def detail(self, desc) -> dict:
         d = desc if isinstance(desc, _Desc) else _Desc(desc)
         out = PredictInfoC()
@@ -554,7 +572,8 @@ class Scheduler:
 
     def __init__(self, model: "Predictor", policy="niyama", preemption="selective", dynamic_chunk=True,
                  fixed_chunk=256, max_chunk=2048, relegation=True, multi_fill=True, history_min_samples=30,
-                 alpha=0.0, prior_mean=415.0, prior_std=300.0, decode_token_s=0.05, layers=1.0, fixed_s=0.0):
+                 alpha=0.0, prior_mean=415.0, prior_std=300.0, decode_token_s=0.05, layers=1.0, fixed_s=0.0,
+                 kv_token_budget=0):
         cfg = SchedConfigC()
         lib.niyama_sched_config_default(C.byref(cfg))
         cfg.policy = POLICY[policy] if isinstance(policy, str) else int(policy)
@@ -565,6 +584,7 @@ class Scheduler:
         cfg.alpha, cfg.prior_mean, cfg.prior_std = float(alpha), float(prior_mean), float(prior_std)
         cfg.decode_token_s = float(decode_token_s)
         cfg.layers, cfg.fixed_s = float(layers), float(fixed_s)
+        cfg.kv_token_budget = int(kv_token_budget)
         self.model = model           # keep the borrowed predictor alive
         h = C.c_void_p()
         _check(lib.niyama_sched_create(C.byref(cfg), model.handle, C.byref(h)))

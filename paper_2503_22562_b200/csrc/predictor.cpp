@@ -22,6 +22,10 @@ struct niyama_predictor {
   int num_sms = NIYAMA_PRED_SMS;          // niyama_predictor_bind: the kv's device
   niyama_tuning tune = default_tuning();  // niyama_predictor_bind: the kv's tuning
   double theta[NIYAMA_NUM_PARAMS] = {0, 0, 0, 0, 0, 1, 1e-6, 0, 0, 2, 8e9, 1e-6, 7e12, 0, 1e11, 1};
+  // full iteration (niyama_predictor_set_iteration): layers = 0 -> one attention launch
+  int32_t layers = 0;
+  std::vector<double> lin_t, lin_s;
+  double it_c0 = 0, it_c1 = 0;
 };
 
 namespace {
@@ -567,10 +571,74 @@ extern "C" niyama_status niyama_predictor_params(const niyama_predictor* p, doub
   return NIYAMA_OK;
 }
 
+namespace {
+double lin_table(const niyama_predictor& p, double T) {
+  const std::vector<double>& x = p.lin_t;
+  const std::vector<double>& y = p.lin_s;
+  const size_t n = x.size();
+  size_t i = 1;
+  while (i + 1 < n && x[i] < T) ++i;  // segment [i-1, i] (the first / last one extrapolates)
+  return y[i - 1] + (y[i] - y[i - 1]) * (T - x[i - 1]) / (x[i] - x[i - 1]);
+}
+// One attention launch or, with layers > 0, the full iteration.
+double total(const niyama_predictor& p, const Launch& L) {
+  const double a = eval(p.theta, L);
+  if (p.layers <= 0) return a;
+  const double T = L.rows + L.D;
+  return p.it_c0 + p.it_c1 * T + lin_table(p, T) + p.layers * a;
+}
+}  // namespace
+
 extern "C" double niyama_predict_iter_time(const niyama_predictor* p, const niyama_batch_desc* desc) {
   std::vector<SliceOC> sl;
   if (!p || !parse_batch(desc, sl)) return -1.0;
-  return eval(p->theta, build(*p, std::move(sl), desc->decode_ctx, desc->num_decode));
+  return total(*p, build(*p, std::move(sl), desc->decode_ctx, desc->num_decode));
+}
+
+extern "C" niyama_status niyama_predictor_set_iteration(niyama_predictor* p, int32_t layers, const int32_t* tokens,
+                                                        const double* seconds, int32_t n, double c0, double c1) {
+  if (!p) return fail(NIYAMA_EINVAL, "predictor is NULL");
+  if (layers < 0) return fail(NIYAMA_EINVAL, "layers < 0");
+  if (layers == 0) {
+    p->layers = 0;
+    p->lin_t.clear();
+    p->lin_s.clear();
+    p->it_c0 = p->it_c1 = 0;
+    return NIYAMA_OK;
+  }
+  if (!tokens || !seconds || n < 2) return fail(NIYAMA_EINVAL, "linear table needs >= 2 points");
+  for (int i = 0; i < n; ++i)
+    if (tokens[i] <= 0 || (i > 0 && tokens[i] <= tokens[i - 1]) || !(seconds[i] >= 0) || !std::isfinite(seconds[i]))
+      return fail(NIYAMA_EINVAL, "linear table: tokens ascending and > 0, seconds >= 0");
+  if (!std::isfinite(c0) || !std::isfinite(c1)) return fail(NIYAMA_EINVAL, "c0/c1");
+  p->layers = layers;
+  p->lin_t.assign(tokens, tokens + n);
+  p->lin_s.assign(seconds, seconds + n);
+  p->it_c0 = c0;
+  p->it_c1 = c1;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_predictor_fit_iteration(niyama_predictor* p, const niyama_batch_desc* batches,
+                                                        const double* seconds, int32_t n) {
+  if (!p || !batches || !seconds || n < 2) return fail(NIYAMA_EINVAL, "NULL argument or n < 2");
+  if (p->layers <= 0) return fail(NIYAMA_ESTATE, "set the iteration table first");
+  // min sum ((c0 + c1 T + r_i) / t_i - 1)^2 over (c0, c1), r_i = lin(T_i) + layers * t_hat_i
+  double a11 = 0, a12 = 0, a22 = 0, b1 = 0, b2 = 0;
+  for (int i = 0; i < n; ++i) {
+    std::vector<SliceOC> sl;
+    if (!(seconds[i] > 0) || !parse_batch(&batches[i], sl)) return fail(NIYAMA_EINVAL, "sample " + std::to_string(i));
+    const Launch L = build(*p, std::move(sl), batches[i].decode_ctx, batches[i].num_decode);
+    const double T = L.rows + L.D, t = seconds[i];
+    const double r = lin_table(*p, T) + p->layers * eval(p->theta, L);
+    const double u = 1.0 / t, v = T / t, y = 1.0 - r / t;
+    a11 += u * u, a12 += u * v, a22 += v * v, b1 += u * y, b2 += v * y;
+  }
+  const double det = a11 * a22 - a12 * a12;
+  if (!(std::fabs(det) > 0)) return fail(NIYAMA_EINVAL, "degenerate samples (all T equal)");
+  p->it_c0 = (b1 * a22 - b2 * a12) / det;
+  p->it_c1 = (a11 * b2 - a12 * b1) / det;
+  return NIYAMA_OK;
 }
 
 extern "C" niyama_status niyama_predict_detail(const niyama_predictor* p, const niyama_batch_desc* desc,
@@ -587,7 +655,7 @@ extern "C" niyama_status niyama_predict_detail(const niyama_predictor* p, const 
   out->reserved = 0;
   out->num_units = static_cast<int64_t>(L.units);
   out->sim_seconds = simulate(L, p->theta + kLin);
-  out->seconds = eval(p->theta, L);
+  out->seconds = total(*p, L);
   return NIYAMA_OK;
 }
 
@@ -603,7 +671,7 @@ extern "C" niyama_status niyama_max_feasible_chunk(const niyama_predictor* p, co
   auto t_of = [&](int32_t C) {
     std::vector<SliceOC> sl;
     if (C > 0) sl.push_back(SliceOC{chunk_offset, C});
-    return eval(p->theta, build(*p, std::move(sl), decodes_only->decode_ctx, decodes_only->num_decode));
+    return total(*p, build(*p, std::move(sl), decodes_only->decode_ctx, decodes_only->num_decode));
   };
   const int32_t cap = std::max(0, std::min(max_chunk, prefill_remaining));
   *infeasible_out = 0;

@@ -168,6 +168,7 @@ niyama_status check_cfg(const niyama_sched_config* c) {
     return niyama::set_error(NIYAMA_EINVAL, "sched config: history / decode_token_s");
   if (!(c->layers > 0.0) || !(c->fixed_s >= 0.0) || std::isinf(c->layers) || std::isinf(c->fixed_s))
     return niyama::set_error(NIYAMA_EINVAL, "sched config: layers > 0, fixed_s >= 0");
+  if (c->kv_token_budget < 0) return niyama::set_error(NIYAMA_EINVAL, "sched config: kv_token_budget < 0");
   return NIYAMA_OK;
 }
 
@@ -190,6 +191,7 @@ extern "C" void niyama_sched_config_default(niyama_sched_config* c) {
   c->decode_token_s = 0.05;
   c->layers = 1.0;
   c->fixed_s = 0.0;
+  c->kv_token_budget = 0;
 }
 
 extern "C" niyama_status niyama_sched_create(const niyama_sched_config* cfg, const niyama_predictor* model,
@@ -341,11 +343,19 @@ extern "C" niyama_status niyama_sched_next_batch(niyama_sched* s, double now, ni
     }
   }
 
-  // ⑤ greedy fill (R27)
+  // ⑤ greedy fill (R27), within the KV token budget (R32)
   s->slice_id.clear();
   s->slice_off.clear();
   s->slice_len.clear();
   int32_t left = budget;
+  if (c.kv_token_budget > 0) {
+    int64_t held = nd;  // the decodes' new tokens
+    for (const auto& kvp : s->reqs) {
+      const Req& r = kvp.second;
+      if (r.state != kDone) held += r.prefill_done + r.decoded;
+    }
+    left = static_cast<int32_t>(std::max<int64_t>(0, std::min<int64_t>(left, c.kv_token_budget - held)));
+  }
   for (Req* r : queue) {
     if (left <= 0) break;
     const int32_t n = std::min(r->prompt - r->prefill_done, left);

@@ -35,7 +35,7 @@ def run_both(trace, qos, cfg: Q.Config, max_iters=200000):
                       fixed_chunk=cfg.fixed_chunk, max_chunk=cfg.max_chunk, relegation=cfg.relegation,
                       multi_fill=cfg.multi_fill, history_min_samples=cfg.min_samples, alpha=cfg.alpha,
                       prior_mean=cfg.prior_mean, prior_std=cfg.prior_std, decode_token_s=cfg.decode_token_s,
-                      layers=cfg.layers, fixed_s=cfg.fixed_s)
+                      layers=cfg.layers, fixed_s=cfg.fixed_s, kv_token_budget=cfg.kv_token_budget)
     os_ = Q.Scheduler(cfg, Q.AffineModel(C0, C1, C2))
     reqs = sorted(trace, key=lambda r: (r.t_arrival, r.id))
     truth = {r.id: r.decode for r in reqs}
@@ -84,6 +84,7 @@ def run_both(trace, qos, cfg: Q.Config, max_iters=200000):
     ("srpf", Q.Config(policy=Q.SRPF, relegation=False, preemption=Q.ALWAYS), 12.0, 0.05),
     ("sjf-never", Q.Config(policy=Q.SJF, relegation=True, preemption=Q.NEVER), 12.0, 0.05),
     ("niyama-layers", Q.Config(alpha=0.5, layers=4.0, fixed_s=1e-4), 3.0, 0.1),
+    ("niyama-kvbudget", Q.Config(alpha=0.5, kv_token_budget=60000), 12.0, 0.05),
 ])
 def test_sched_matches_oracle(name, cfg, qps, scale):
     cfg.min_samples = 5

@@ -77,6 +77,7 @@ def main():
     ap.add_argument("--policies", default="niyama,edf")
     ap.add_argument("--seed", type=int, default=5)
     ap.add_argument("--capacity-only", action="store_true")
+    ap.add_argument("--capacity", type=float, default=0.0, help="skip the search: use this capacity (QPS)")
     ap.add_argument("--model-only", action="store_true", help="replay on the predictor (no GPU)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "replay_config5.json"))
     args = ap.parse_args()
@@ -93,8 +94,11 @@ def main():
     out = {"layers": args.layers, "scale": s, "strict_tbt_s": 0.050 * s, "ttft_s": 6.0 * s,
            "ttlt_s": [600.0 * s, 1800.0 * s], "fixed_s_per_iteration": fixed_s, "reference_iteration_s": t_ref}
     t0 = time.time()
-    cap, probes = capacity(pred, args.layers, fixed_s, s, buckets, duration=3600.0 * s, seed=args.seed,
-                           lo=0.5 / s, hi=20.0 / s, tol=0.05 / s, tdec=tdec)
+    if args.capacity > 0:
+        cap, probes = args.capacity, "given (--capacity)"
+    else:
+        cap, probes = capacity(pred, args.layers, fixed_s, s, buckets, duration=3600.0 * s, seed=args.seed,
+                               lo=0.5 / s, hi=20.0 / s, tol=0.05 / s, tdec=tdec)
     out["capacity_qps"] = cap
     out["capacity_probes"] = probes
     out["capacity_search_s"] = time.time() - t0
@@ -122,7 +126,8 @@ def main():
             ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048)
             pred_b = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA)).bind(ex.kv)
             sched = ny.Scheduler(pred_b, max_chunk=2048, layers=args.layers, fixed_s=fixed_s, decode_token_s=tdec,
-                                 history_min_samples=30, **POLICIES[name])
+                                 history_min_samples=30, kv_token_budget=int(gpu["blocks"] * 16 * 0.9),
+                                 **POLICIES[name])
         it, recs = serve.replay(sched, ex, trace, buckets, until=duration * 1.25)
         summ = serve.summarize(it, recs, buckets, fixed_s=fixed_s)
         summ["wall_s"] = time.time() - t1
