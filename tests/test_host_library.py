@@ -455,3 +455,39 @@ def test_min_slack_random_matches_oracle():
                                          est_remaining=int(g.integers(0, 900))))
         now = float(g.uniform(0, 200))
         assert ny.min_slack(decs, now) == pytest.approx(OS.min_slack(decs, now), rel=1e-15, abs=1e-15)
+
+
+def test_iteration_predictor_closed_form_and_committed_fit():
+    """Full-iteration mode (niyama_predictor_set_iteration): t = c0 + c1 T + lin(T) + layers * t_attn with
+    lin piecewise linear (hand-computed), and profiles/iteration_fit.json reproduces through the C ABI
+    with held-out max <= 5 % (the paper's predictor scope)."""
+    pr = ny.Predictor.from_params(CFG, THETA)
+    d = W.BatchDesc([0], [1536], [512], list(range(1, 65)), [2048] * 64)
+    a = pr.predict(d)
+    pr.set_iteration(32, [16, 1024, 4096], [0.002, 0.010, 0.040], c0=1e-4, c1=2e-7)
+    T = 576
+    lin = 0.002 + (0.010 - 0.002) * (T - 16) / (1024 - 16)
+    assert pr.predict(d) == pytest.approx(1e-4 + 2e-7 * T + lin + 32 * a, rel=1e-12)
+    big = W.BatchDesc([0], [0], [2048], list(range(1, 2150)), [5] * 2149)   # T = 4197 > 4096: extrapolated
+    assert pr.predict(big) > 0
+    with pytest.raises(ny.NiyamaError):
+        pr.set_iteration(32, [16, 16], [0.1, 0.2])              # tokens must ascend
+    pr.set_iteration(0)
+    assert pr.predict(d) == a
+    fj = json.load(open(os.path.join(ROOT, "profiles", "iteration_fit.json")))
+    sw = json.load(open(os.path.join(ROOT, fj["sweep"])))
+    pf = json.load(open(os.path.join(ROOT, "profiles", "predictor_fit.json")))
+    p2 = ny.Predictor.from_params(CFG, pf["theta"])
+    lin = sorted(sw["linear"], key=lambda x: x["T"])
+    p2.set_iteration(sw["layers"], [x["T"] for x in lin], [x["seconds"] for x in lin])
+
+    def desc(r):
+        c = r["chunk"]
+        return W.BatchDesc([0] if c else [], [r["offset"]] if c else [], [c] if c else [], list(range(1, r["D"] + 1)),
+                           list(r["ctx"]))
+    train = [r for r in sw["points"] if (r["kind"] == "grid" and r["seed"] != 2) or r["kind"] == "random"]
+    held = [r for r in sw["points"] if r["kind"] == "offgrid" or (r["kind"] == "grid" and r["seed"] == 2)]
+    p2.fit_iteration([desc(r) for r in train], [r["seconds"] for r in train])
+    err = np.abs([p2.predict(desc(r)) / r["seconds"] - 1 for r in held])
+    assert float(err.max()) == pytest.approx(fj["errors"]["analytic"]["heldout"]["max"], rel=1e-9)
+    assert float(err.max()) <= 0.05 and len(held) >= 30
