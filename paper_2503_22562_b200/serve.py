@@ -75,7 +75,9 @@ class GpuExecutor:
     """n_layers x (append + attention) of the batch on cuda:device, timed with CUDA events."""
 
     def __init__(self, shape, n_layers: int, num_blocks: int, max_rows: int = 2048 + 512, device: int = 0,
-                 seed: int = 0):
+                 seed: int = 0, linear=None):
+        """linear: optional callable object with pre(h) -> (q, k, v) and post(h, o, T) -> h (a model's
+        linear layers, e.g. cuBLAS GEMMs) run around every layer's append + attention."""
         import torch
         self.torch = torch
         self.n_layers = n_layers
@@ -98,6 +100,7 @@ class GpuExecutor:
                         for _ in range(n_layers)]
         self.last_attention_s = 0.0
         self.launches = 0
+        self.linear = linear
 
     def run(self, batch) -> float:
         T = sum(n for _, _, n in batch.slices) + len(batch.decodes)
@@ -106,13 +109,18 @@ class GpuExecutor:
         plan = self.kv.plan(batch.desc(), self.stream)
         q, k, v = self.q[:T], self.k[:T], self.v[:T]
         o = self.obuf[:self.hq * T * self.d].view(self.hq, T, self.d)
+        h = self.linear.x[:T] if self.linear is not None else None
         self.e0.record(self.stream)
         for layer in range(self.n_layers):
+            if self.linear is not None:
+                q, k, v = self.linear.pre(h)
             self.kv.append(plan, layer, k, v, self.stream)
             a, b = self.ev_attn[layer]
             a.record(self.stream)
             self.kv.attention(plan, layer, q, o, None, 0.0, self.stream)
             b.record(self.stream)
+            if self.linear is not None:
+                h = self.linear.post(h, o, T)
         self.e1.record(self.stream)
         plan.close()
         self.e1.synchronize()
@@ -169,13 +177,15 @@ def replay(sched: Scheduler, executor, trace: Sequence, buckets: Sequence[QoSBuc
     return iters, recs
 
 
-def verdicts(recs: Dict[int, ReqRecord], buckets: Sequence[QoSBucket]):
+def verdicts(recs: Dict[int, ReqRecord], buckets: Sequence[QoSBucket], t_end: float = math.inf):
     """Per request: violated? (Eq. 1-3, R18 "<=" passes; relegated counts as violated; an unfinished
-    request is judged on what it has produced so far and flagged unfinished)."""
+    request is violated if the deadline of its next token (interactive) or its completion deadline
+    (non-interactive) has passed by t_end)."""
     out = {}
     for r in recs.values():
         b = buckets[r.bucket]
         tbt_miss = 0
+        done = len(r.tokens) == r.decode
         if b.interactive:
             bad = False
             for n, t in enumerate(r.tokens, start=1):
@@ -183,8 +193,12 @@ def verdicts(recs: Dict[int, ReqRecord], buckets: Sequence[QoSBucket]):
                 if t > d + 1e-12 * max(1.0, t):
                     bad = True
                     tbt_miss += n > 1
+            if not done and r.t_arrival + b.slo_ttft + len(r.tokens) * b.slo_tbt < t_end:
+                bad = True
         else:
             bad = bool(r.tokens) and r.tokens[-1] > r.t_arrival + b.slo_ttlt + 1e-12 * max(1.0, r.tokens[-1])
+            if not done and r.t_arrival + b.slo_ttlt < t_end:
+                bad = True
         out[r.id] = dict(violated=bad or r.relegated, relegated=r.relegated, finished=len(r.tokens) == r.decode,
                          tbt_miss=tbt_miss)
     return out
@@ -192,7 +206,8 @@ def verdicts(recs: Dict[int, ReqRecord], buckets: Sequence[QoSBucket]):
 
 def summarize(iters: List[IterRecord], recs: Dict[int, ReqRecord], buckets: Sequence[QoSBucket],
               t_end: Optional[float] = None, fixed_s: float = 0.0) -> dict:
-    v = verdicts(recs, buckets)
+    span = (t_end if t_end is not None else (iters[-1].t_start + iters[-1].seconds if iters else 0.0))
+    v = verdicts(recs, buckets, span)
     done = [r for r in recs.values() if v[r.id]["finished"]]
     judged = [r for r in recs.values() if v[r.id]["finished"] or v[r.id]["violated"]]
     def pct(xs):
@@ -209,7 +224,6 @@ def summarize(iters: List[IterRecord], recs: Dict[int, ReqRecord], buckets: Sequ
     hist = {f"{a}-{b - 1}": int(np.sum((chunks >= a) & (chunks < b))) for a, b in zip(edges[:-1], edges[1:])}
     tokens = sum(len(r.tokens) for r in recs.values() if buckets[r.bucket].interactive)
     ttft = [r.tokens[0] - r.t_arrival for r in recs.values() if r.tokens]
-    span = (t_end if t_end is not None else (iters[-1].t_start + iters[-1].seconds if iters else 0.0))
     good = sum(1 for r in done if not v[r.id]["violated"])
     return {
         "requests": len(recs), "finished": len(done), "judged": len(judged),

@@ -56,7 +56,7 @@ def capacity(pred, layers, fixed_s, s, buckets, duration, seed, lo, hi, tol, tde
         tr = W.qos_trace(duration, qps, seed=seed, max_prompt=8192, max_decode=2048)
         sched = make_sched(pred, "niyama", layers, fixed_s, tdec)
         it, recs = serve.replay(sched, serve.ModelExecutor(pred, layers, fixed_s), tr, buckets, until=duration * 1.5)
-        v = serve.summarize(it, recs, buckets)["violations_pct"]
+        v = serve.summarize(it, recs, buckets, t_end=duration * 1.5)["violations_pct"]
         probes.append((qps, v))
         return v
     if viol(lo) > 1.0:
@@ -79,25 +79,44 @@ def main():
     ap.add_argument("--capacity-only", action="store_true")
     ap.add_argument("--capacity", type=float, default=0.0, help="skip the search: use this capacity (QPS)")
     ap.add_argument("--model-only", action="store_true", help="replay on the predictor (no GPU)")
+    ap.add_argument("--full", action="store_true",
+                    help="full Llama-3-8B iterations: cuBLAS linear layers around every layer's append + attention, "
+                         "scheduled with the full-iteration predictor (profiles/iteration_fit.json's sweep)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "replay_config5.json"))
     args = ap.parse_args()
     shape = W.L8B
     cfg = ny.Predictor.shape_cfg(shape.num_q_heads, shape.num_kv_heads, shape.head_dim, "bf16")
-    pred = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA))
-    append_s = 9e-6                                    # per-layer KV append launch (profiles/r01 launch list)
-    fixed_s = args.layers * append_s
+    def make_pred(kv=None):
+        p = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA))
+        if kv is not None:
+            p.bind(kv)
+        if args.full:
+            sw = json.load(open(os.path.join(ROOT, json.load(open(os.path.join(ROOT, "profiles", "iteration_fit.json")))["sweep"])))
+            lin = sorted(sw["linear"], key=lambda x: x["T"])
+            p.set_iteration(args.layers, [x["T"] for x in lin], [x["seconds"] for x in lin])
+            tr = [x for x in sw["points"] if (x["kind"] == "grid" and x["seed"] != 2) or x["kind"] == "random"]
+            dd = [W.BatchDesc([0] if x["chunk"] else [], [x["offset"]] if x["chunk"] else [],
+                              [x["chunk"]] if x["chunk"] else [], list(range(1, x["D"] + 1)), list(x["ctx"])) for x in tr]
+            p.fit_iteration(dd, [x["seconds"] for x in tr])
+        return p
+    pred = make_pred()
+    if args.full:   # the predictor returns whole iterations
+        layers_s, fixed_s = 1, 0.0
+    else:
+        layers_s, fixed_s = args.layers, args.layers * 9e-6   # + per-layer KV append launch (profiles/r01)
     ref = W.BatchDesc([0], [1536], [256], list(range(1, 65)), [2048] * 64)
-    t_ref = fixed_s + args.layers * pred.predict(ref)
+    t_ref = fixed_s + layers_s * pred.predict(ref)
     s = t_ref / 0.050
     buckets = buckets_scaled(s)
     tdec = t_ref                                        # R25: a decode iteration ~ the reference iteration
-    out = {"layers": args.layers, "scale": s, "strict_tbt_s": 0.050 * s, "ttft_s": 6.0 * s,
+    out = {"layers": args.layers, "engine": "full iteration (cuBLAS linear layers + attention)" if args.full
+           else "attention-only (append + attention per layer)", "scale": s, "strict_tbt_s": 0.050 * s, "ttft_s": 6.0 * s,
            "ttlt_s": [600.0 * s, 1800.0 * s], "fixed_s_per_iteration": fixed_s, "reference_iteration_s": t_ref}
     t0 = time.time()
     if args.capacity > 0:
         cap, probes = args.capacity, "given (--capacity)"
     else:
-        cap, probes = capacity(pred, args.layers, fixed_s, s, buckets, duration=3600.0 * s, seed=args.seed,
+        cap, probes = capacity(pred, layers_s, fixed_s, s, buckets, duration=3600.0 * s, seed=args.seed,
                                lo=0.5 / s, hi=20.0 / s, tol=0.05 / s, tdec=tdec)
     out["capacity_qps"] = cap
     out["capacity_probes"] = probes
@@ -119,17 +138,22 @@ def main():
         gpu = dict(blocks=blocks)
     for name in args.policies.split(","):
         t1 = time.time()
-        sched = make_sched(pred, name, args.layers, fixed_s, tdec)
+        sched = make_sched(pred, name, layers_s, fixed_s, tdec)
         if args.model_only:
-            ex = serve.ModelExecutor(pred, args.layers, fixed_s)
+            ex = serve.ModelExecutor(pred, layers_s, fixed_s)
         else:
-            ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048)
-            pred_b = ny.Predictor.from_params(cfg, list(ny.DEFAULT_THETA)).bind(ex.kv)
-            sched = ny.Scheduler(pred_b, max_chunk=2048, layers=args.layers, fixed_s=fixed_s, decode_token_s=tdec,
+            linear = None
+            if args.full:
+                sys.path.insert(0, os.path.join(ROOT, "tools"))
+                from sweep_iteration import LinearLayers
+                linear = LinearLayers(max_t=2048 + 2048)
+            ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048, linear=linear)
+            pred_b = make_pred(ex.kv)
+            sched = ny.Scheduler(pred_b, max_chunk=2048, layers=layers_s, fixed_s=fixed_s, decode_token_s=tdec,
                                  history_min_samples=30, kv_token_budget=int(gpu["blocks"] * 16 * 0.9),
                                  **POLICIES[name])
         it, recs = serve.replay(sched, ex, trace, buckets, until=duration * 1.25)
-        summ = serve.summarize(it, recs, buckets, fixed_s=fixed_s)
+        summ = serve.summarize(it, recs, buckets, t_end=duration * 1.25, fixed_s=fixed_s)
         summ["wall_s"] = time.time() - t1
         if not args.model_only:
             summ["gpu_launches"] = ex.launches

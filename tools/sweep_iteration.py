@@ -34,8 +34,11 @@ from sweep_predictor import point_desc  # noqa: E402
 HID, INTER, HQ, HKV, D = 4096, 14336, 32, 8, 128
 
 
-class Model:
-    def __init__(self, layers, num_blocks, max_t=4096 + 256):
+class LinearLayers:
+    """One Llama-3-8B layer's linear part (weights shared by every layer); the serve.GpuExecutor
+    `linear` protocol: x (activations buffer), pre(h) -> (q, k, v), post(h, o, T) -> h."""
+
+    def __init__(self, max_t=4096 + 256):
         g = torch.Generator(device="cuda")
         g.manual_seed(0)
         mk = lambda *s, sc=0.02: (torch.randn(*s, generator=g, device="cuda") * sc).to(torch.bfloat16)  # noqa: E731
@@ -44,29 +47,41 @@ class Model:
         self.w_gu = mk(HID, 2 * INTER)
         self.w_d = mk(INTER, HID)
         self.ln = torch.ones(HID, device="cuda", dtype=torch.bfloat16)
-        self.layers = layers
-        self.kv = ny.KVCache(layers, HQ, HKV, D, num_blocks, block_size=16, dtype="bf16", device=0)
         self.x = mk(max_t, HID, sc=1.0)
-        self.obuf = torch.zeros(HQ * max_t * D, device="cuda", dtype=torch.bfloat16)
 
     @staticmethod
     def rms(x, w):
         v = x.float().pow(2).mean(-1, keepdim=True)
         return (x.float() * torch.rsqrt(v + 1e-5)).to(torch.bfloat16) * w
 
-    def linear_pre(self, h):
+    def pre(self, h):
         qkv = self.rms(h, self.ln) @ self.w_qkv
         q = qkv[:, :HQ * D].reshape(-1, HQ, D)
         k = qkv[:, HQ * D:(HQ + HKV) * D].reshape(-1, HKV, D)
         v = qkv[:, (HQ + HKV) * D:].reshape(-1, HKV, D)
         return q.contiguous(), k.contiguous(), v.contiguous()
 
-    def linear_post(self, h, o, T):
+    def post(self, h, o, T):
         a = o.reshape(HQ, T, D).permute(1, 0, 2).reshape(T, HQ * D)   # head-major O -> token-major
         h = h + a @ self.w_o
         gu = self.rms(h, self.ln) @ self.w_gu
         act = torch.nn.functional.silu(gu[:, :INTER]) * gu[:, INTER:]
         return h + act @ self.w_d
+
+
+class Model:
+    def __init__(self, layers, num_blocks, max_t=4096 + 256):
+        self.lin = LinearLayers(max_t)
+        self.layers = layers
+        self.kv = ny.KVCache(layers, HQ, HKV, D, num_blocks, block_size=16, dtype="bf16", device=0)
+        self.x = self.lin.x
+        self.obuf = torch.zeros(HQ * max_t * D, device="cuda", dtype=torch.bfloat16)
+
+    def linear_pre(self, h):
+        return self.lin.pre(h)
+
+    def linear_post(self, h, o, T):
+        return self.lin.post(h, o, T)
 
     def iteration(self, plan, T, attention=True):
         h = self.x[:T]
