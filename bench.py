@@ -211,62 +211,86 @@ def run_host_only(args, rank, world, dist):
                           "parallelism": f"kv-head shard x{world}"}}), flush=True)
 
 
-def cpu_baseline(wl, budget_s=20.0):
-    """The fp64 oracle as it stands, on this host's cores, over a bounded row sample."""
-    import numpy as np
-    from oracle import attention as OA
-    from oracle.kvcache import KVPool
+def cpu_model():
     try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:  # pragma: no cover
-        threads = 1
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:  # pragma: no cover
+        pass
+    return "unknown"
+
+
+def oracle_rows(wl, T, D):
+    """The row sample both oracle legs time (cpu_baseline and --impl reference): 32 evenly
+    spaced prefill rows and every decode row."""
+    return list(range(0, T - D, max(1, (T - D) // 32))) + list(range(T - D, T))
+
+
+def _oracle_pool(wl):
+    from oracle.kvcache import KVPool
     s = wl.shape
     pool = KVPool(1, s.num_kv_heads, s.head_dim, s.block_size, wl.num_blocks, s.dtype)
     plan = None
     for st in wl.steps:
         plan = pool.plan(st.desc)
         pool.append(0, plan, st.k, st.v)
+    return pool, plan
+
+
+def cpu_baseline(wl, budget_s=20.0):
+    """The fp64 oracle as it stands, on this host's cores, over a bounded row sample; timed
+    with the BLAS pool at its default size and again at 1 thread."""
+    from oracle import attention as OA
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # pragma: no cover
+        threadpool_limits, threads = None, 1
+    s = wl.shape
+    pool, plan = _oracle_pool(wl)
     T = len(plan.rows)
     D = wl.final.desc.num_decode
-    prefill_rows = list(range(0, T - D, max(1, (T - D) // 32)))
-    rows = prefill_rows + list(range(T - D, T))
-    t0 = time.perf_counter()
-    done = 0
-    for r in rows:
-        OA.hybrid_attention(pool, 0, plan, wl.final.q, s.num_q_heads, rows=[r])
-        done += 1
-        if time.perf_counter() - t0 > budget_s:
-            break
-    dt = time.perf_counter() - t0
+    rows = oracle_rows(wl, T, D)
+
+    def timed(budget):
+        t0 = time.perf_counter()
+        done = 0
+        for r in rows:
+            OA.hybrid_attention(pool, 0, plan, wl.final.q, s.num_q_heads, rows=[r])
+            done += 1
+            if time.perf_counter() - t0 > budget:
+                break
+        return done, time.perf_counter() - t0
+    done, dt = timed(budget_s * 0.6)
+    one = None
+    if threadpool_limits is not None:
+        with threadpool_limits(limits=1):
+            d1, t1 = timed(budget_s * 0.4)
+        one = {"value": d1 / t1, "unit": "tokens/s", "cores": 1, "rows": d1}
     return {"value": done / dt, "unit": "tokens/s", "cores": threads, "kind": "oracle",
-            "host_cpus": os.cpu_count(),
-            "sample": f"{done} of {T} batch rows ({len(prefill_rows)} evenly spaced prefill rows + all {D} decode "
-                      f"rows, all {s.num_q_heads} heads), fp64 numpy, {dt:.1f} s"}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model(), "one_thread": one,
+            "sample": f"{done} of {T} batch rows ({len(rows) - D} evenly spaced prefill rows + all {D} decode "
+                      f"rows, all {s.num_q_heads} heads), fp64 numpy, {dt:.1f} s (the reference arm's sample)"}
 
 
 def run_reference(args, rank, world):
     """--impl reference: the oracle (this tier's reference arm), rank 0 only."""
     if rank != 0:
         return
-    import numpy as np
     from oracle import attention as OA
-    from oracle.kvcache import KVPool
     wl = workload(args.config)
     s = wl.shape
-    pool = KVPool(1, s.num_kv_heads, s.head_dim, s.block_size, wl.num_blocks, s.dtype)
-    plan = None
-    for st in wl.steps:
-        plan = pool.plan(st.desc)
-        pool.append(0, plan, st.k, st.v)
+    pool, plan = _oracle_pool(wl)
     T = len(plan.rows)
     D = wl.final.desc.num_decode
-    g = np.random.default_rng(0)
+    sample = oracle_rows(wl, T, D)   # the cpu_baseline leg's sample, 8 rows per step, cycling
     per_step = 8
-    cand = list(range(T))
+    pos = [0]
 
     def one():
-        rows = sorted(g.choice(cand, size=per_step, replace=False).tolist())
+        rows = sorted(sample[(pos[0] + i) % len(sample)] for i in range(per_step))
+        pos[0] = (pos[0] + per_step) % len(sample)
         OA.hybrid_attention(pool, 0, plan, wl.final.q, s.num_q_heads, rows=rows)
         return len(rows)
 
@@ -284,7 +308,8 @@ def run_reference(args, rank, world):
     out = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-           "config": {"workload": wl.name, "step": f"fp64 oracle on {per_step} random rows of the batch"},
+           "config": {"workload": wl.name, "step": f"fp64 oracle on {per_step} rows of the batch per step "
+                      f"(cycling through the cpu_baseline sample: {len(sample)} rows)"},
            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": threads, "kind": "oracle",
                             "sample": f"{per_step} random batch rows per step of {T}"},
            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -579,6 +604,8 @@ def main():
                            (", a7 NCCL all-gather" if world > 1 else "") + ", a8 predict; 1 layer"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
+                     "traffic_source": "stored: dram__bytes_read.sum + dram__bytes_write.sum of this launch from one "
+                                       "ncu --set full capture (profiles/ncu_traffic.json), not measured in this run",
                      "kernel": "hybrid_attn_bf16_kernel" + (" (incl. the KV append)" if fused else ""),
                      "algorithmic_bytes_per_launch": B_kv,
                      "launch_us": attn_avg_ms * 1e3, "peak_source": peak_src,

@@ -240,6 +240,9 @@ niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
  *   grid_cap          0 = grid from the plan; n > 0 = at most n CTAs (diagnostics)
  *   plan_copy_stream  1 = plans upload on the library's copy stream (default), 0 = on
  *                     the caller's stream
+ *   prefill_split     1 = split-K of prefill q tiles when they are fewer than their CTAs (key
+ *                     parts on different CTAs, merged by the last part; parity-tested, measured
+ *                     slower: DESIGN.md 6.1), 0 = never split (default)
  *   decode_path       bf16 decode units: 0 = per-warp mma.sync streams (default), 1 = one
  *                     tensor-core (tcgen05) pipeline per CTA over 128-token steps (same
  *                     results within bf16 rounding; measured slower: DESIGN.md 6.1)
@@ -253,6 +256,7 @@ typedef struct {
   int32_t grid_cap;
   int32_t plan_copy_stream;
   int32_t decode_path;
+  int32_t prefill_split;
 } niyama_tuning;
 niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning* out);
 niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t); /* EINVAL on out-of-range fields */
@@ -276,10 +280,12 @@ niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, voi
  * rank's shape.  The launch-shaping rules are the planner's own (one definition,
  * csrc/internal.h), so the model sees the launch the kernel runs:
  *
- *  1. Prefill tile queue: slices (o, c > 0) sorted by o + c descending (stable);
+ *  1. Prefill work queue: slices (o, c > 0) sorted by o + c descending (stable);
  *     per slice the q tiles from last to first (qt = nqt-1 .. 0, nqt = ceil(c/R),
- *     R = 128 / (Hq/Hkv)), each repeated Hkv times, with s = ceil((o + min(c,
- *     (qt+1) R)) / 128) key steps.
+ *     R = 128 / (Hq/Hkv)), each repeated Hkv times, with nk = ceil((o + min(c,
+ *     (qt+1) R)) / 128) key steps, cut into the planner's split-K parts P (the
+ *     target floor(prefill CTAs / q tiles) <= 16, per slice at most its shortest
+ *     tile's steps / 4): part i has floor((i+1) nk / P) - floor(i nk / P) steps.
  *  2. Decode unit queue: split length q from (sum ctx, max ctx) as the planner;
  *     rows by ctx descending contribute ceil(L/q) - 1 full pieces of q keys
  *     (x Hkv units each), then every row's last L - n_f q keys cut into pieces of
@@ -348,7 +354,7 @@ typedef struct {
   int32_t grid, prefill_ctas;   /* step 3 */
   int32_t split_len, small_piece; /* step 2: q and the small-piece length */
   int32_t warps_per_cta;        /* decode warps per CTA (step 5) */
-  int32_t reserved;
+  int32_t prefill_parts_target; /* split-K target parts per q tile (step 1; 1 = no split) */
   int64_t num_units;
   double sim_seconds;   /* T_sim (step 6) */
   double seconds;       /* t_hat */

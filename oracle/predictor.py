@@ -21,8 +21,9 @@ not re-derive the planner's heuristics.
   R = 128 // g chunk rows per prefill tile; NSM = 148.
   1. tile queue: slices sorted by o + c descending (stable); per slice the q tiles
      qt = nqt-1 .. 0 (nqt = ceil(c / R)), each Hkv times, with
-     s = ceil((o + min(c, (qt+1) R)) / 128) key steps (the keys row o + (qt+1) R - 1
-     sees, causal, P:118).
+     nk = ceil((o + min(c, (qt+1) R)) / 128) key steps (the keys row o + (qt+1) R - 1
+     sees, causal), cut into P split-K parts of floor((i+1) nk/P) - floor(i nk/P)
+     steps (P from the plan's target, a launch input).
   2. unit queue: rows by ctx descending; a row of L keys has n_f = ceil(L/q) - 1
      full pieces of q keys (each Hkv units, row by row), then the remaining
      L - n_f q keys of every row in pieces of `small` keys, all those pieces
@@ -106,15 +107,20 @@ def cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
-def work(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int], q: int, small: int) -> Work:
-    """Steps 1-2."""
+def work(shape: PredShape, slices: Sequence[Tuple[int, int]], decode_ctx: Sequence[int], q: int, small: int,
+         parts_target: int = 1) -> Work:
+    """Steps 1-2.  parts_target: the plan's split-K target (a launch input); a slice's q tiles
+    are cut into P = min(target, its shortest tile's steps // 4) (>= 1) key parts."""
     g = shape.num_q_heads // shape.num_kv_heads
     R = max(1, 128 // g)
     live = sorted([(o, c) for o, c in slices if c > 0], key=lambda sc: -(sc[0] + sc[1]))   # stable
     tiles = []
     for o, c in live:
-        for qt in range(cdiv(c, R) - 1, -1, -1):
-            tiles += [cdiv(o + min(c, (qt + 1) * R), 128)] * shape.num_kv_heads
+        nks = [cdiv(o + min(c, (qt + 1) * R), 128) for qt in range(cdiv(c, R) - 1, -1, -1)]
+        P = max(1, min(parts_target, nks[-1] // 4)) if parts_target > 1 else 1
+        for nk in nks:
+            for _ in range(shape.num_kv_heads):
+                tiles += [(i + 1) * nk // P - i * nk // P for i in range(P)]
     bpt = float(shape.head_dim * 2 * shape.elt_bytes)
     pieces, tail, units = [], [], 0
     for L in sorted((int(x) for x in decode_ctx), reverse=True):

@@ -56,7 +56,7 @@ class PlanInfo(C.Structure):
 class Tuning(C.Structure):
     _fields_ = [("prefill_ctas", C.c_int32), ("split_len", C.c_int32), ("tail_div", C.c_int32),
                 ("tail_min", C.c_int32), ("grid_cap", C.c_int32), ("plan_copy_stream", C.c_int32),
-                ("decode_path", C.c_int32)]
+                ("decode_path", C.c_int32), ("prefill_split", C.c_int32)]
 
 
 class SampleC(C.Structure):
@@ -70,7 +70,7 @@ class FitOptionsC(C.Structure):
 
 class PredictInfoC(C.Structure):
     _fields_ = [("grid", C.c_int32), ("prefill_ctas", C.c_int32), ("split_len", C.c_int32),
-                ("small_piece", C.c_int32), ("warps_per_cta", C.c_int32), ("reserved", C.c_int32),
+                ("small_piece", C.c_int32), ("warps_per_cta", C.c_int32), ("prefill_parts_target", C.c_int32),
                 ("num_units", C.c_int64), ("sim_seconds", C.c_double), ("seconds", C.c_double)]
 
 
@@ -436,7 +436,8 @@ class Predictor:
         out = PredictInfoC()
         _check(lib.niyama_predict_detail(self.handle, C.byref(d.c), C.byref(out)))
         return dict(grid=out.grid, prefill_ctas=out.prefill_ctas, split_len=out.split_len,
-                    small_piece=out.small_piece, warps_per_cta=out.warps_per_cta, units=out.num_units,
+                    small_piece=out.small_piece, warps_per_cta=out.warps_per_cta,
+                    parts_target=out.prefill_parts_target, units=out.num_units,
                     sim=out.sim_seconds, seconds=out.seconds)
 
     @classmethod

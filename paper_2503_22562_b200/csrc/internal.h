@@ -23,6 +23,7 @@ inline niyama_tuning default_tuning() {
   t.prefill_ctas = 0;
   t.split_len = 0;
   t.decode_path = 0;
+  t.prefill_split = 0;
   t.tail_div = NIYAMA_TAIL_DIV;
   t.tail_min = NIYAMA_TAIL_MIN;
   t.grid_cap = 0;
@@ -83,6 +84,27 @@ inline CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, i
 }
 
 
+// Prefill split-K (a4): when there are fewer q tiles than the CTAs the work split would
+// give to prefill, each q tile's key range is cut into P contiguous parts run by different
+// CTAs; the last part to finish merges the tile (log-sum-exp, part order: deterministic).
+// P = floor(target prefill CTAs / q tiles), at most 16; per slice at most (its shortest
+// tile's steps) / 4, so a part has >= 4 key steps.  `tile_cost` = sum of (steps + setup).
+inline int32_t prefill_parts_target(int64_t q_tiles, int64_t n_units, int64_t tile_cost, int64_t sum_ctx, int hkv,
+                                    int d, int elt, int g, int num_sms, int decode_path = 0, int prefill_split = 0) {
+  if (q_tiles <= 0 || prefill_split == 0) return 1;
+  double target = num_sms;
+  if (n_units > 0) {
+    const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
+    const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt *
+                      (g > 4 && decode_path == 0 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
+    target = std::ceil(num_sms * wp / (wp + wd));
+  }
+  return static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(16, static_cast<int64_t>(target) / q_tiles)));
+}
+inline int32_t prefill_parts_of_slice(int32_t target, int64_t min_steps) {
+  return static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(target, min_steps / 4)));
+}
+
 // Prefill work items: with GQA packing a 128-row tile holds R = 128 / g chunk rows of
 // the g query heads of one kv head (a4).
 inline int32_t rows_per_tile(int g) { return 128 / (g > 0 ? g : 1); }
@@ -126,8 +148,9 @@ struct PrefillSlice {
   int32_t c;      // slice length
   int32_t row0;   // batch row of slice row 0
   int32_t nqt;    // q tiles = ceil(c / R)
-  int32_t tbase;  // first tile index
-  int32_t pad0, pad1;
+  int32_t tbase;  // first work item: q tile (nqt-1 - (t-tbase)/(Hkv*parts)), kv head, key part
+  int32_t parts;  // split-K: each q tile's key steps cut into `parts` contiguous ranges (1 = none)
+  int32_t pbase;  // split tiles only: index of this slice's first q tile among all split tiles
 };
 
 // Decode row (sorted by ctx, longest first): unit (row, split s, kv head h) covers
@@ -208,6 +231,9 @@ struct AttnParams {
   const RowInfo* rows;
   float* part_o;    // [n_units][g][d]
   float* part_ml;   // [n_units][g][2]
+  float* ppart_o;   // prefill split-K partials [split tile][part][128 rows][d] (o / l)
+  float* ppart_ml;  // [split tile][part][128 rows][2] (m in log2 units, l)
+  int32_t* pcounters;  // [split tiles] parts finished, cumulative over launches (epoch)
   int32_t* work;      // [0] tile queue, [1] unit queue, [2] CTA done counter, [3] merge queue (self-resetting)
   int64_t chunk_bytes;   // bytes of one (block, kv head) chunk
   int64_t chunk_stride;  // bytes between consecutive (block, kv head) chunks of pool_k / pool_v

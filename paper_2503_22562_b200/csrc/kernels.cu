@@ -318,25 +318,72 @@ __device__ __forceinline__ void mask_tail(uint32_t (&sr)[64], int last) {
 
 struct TileDesc {
   int tbl, o, c, t0, row0, kvh, nkeys, nblk;
+  int j0, j1;         // key steps [j0, j1) of this work item (split-K part; [0, nk) unsplit)
+  int parts, part;    // split-K parts of the q tile and this item's part
+  int stile;          // index of the q tile among split tiles (parts > 1)
 };
 
-// Expand work item t (PrefillSlice records; see internal.h): one 128-row q tile.
+// Expand work item t (PrefillSlice records; see internal.h): one key part of a 128-row q tile.
 __device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
   int i = 0;
   while (i + 1 < p.n_slices && __ldg(&p.slices[i + 1].tbase) <= t) ++i;
   const PrefillSlice sl = p.slices[i];
   const int local = t - sl.tbase;
-  const int qt = sl.nqt - 1 - local / p.Hkv;  // largest key ranges first
+  const int tl = local / sl.parts;            // q tile of the slice (parts of a tile are consecutive)
+  const int qt = sl.nqt - 1 - tl / p.Hkv;     // largest key ranges first
   TileDesc d;
   d.tbl = sl.tbl;
   d.o = sl.o;
   d.c = sl.c;
   d.t0 = qt * p.R;
   d.row0 = sl.row0;
-  d.kvh = local % p.Hkv;
+  d.kvh = tl % p.Hkv;
   d.nkeys = sl.o + min(d.t0 + p.R, sl.c);
   d.nblk = (d.nkeys + p.B - 1) / p.B;
+  const int nk = (d.nkeys + 127) >> 7;
+  d.parts = sl.parts;
+  d.part = local - tl * sl.parts;
+  d.j0 = d.part * nk / sl.parts;
+  d.j1 = (d.part + 1) * nk / sl.parts;
+  d.stile = sl.pbase + tl;
   return d;
+}
+
+// Split-K merge of one q tile (run by the CTA of its last part): for each of the 128 rows
+// (g heads x R chunk rows) m = max_s m_s, w_s = 2^(m_s - m) l_s, o = sum_s w_s o~_s / sum_s w_s
+// in part order (deterministic), LSE = (m + log2 sum w) ln 2.  Threads take (row, 4 dims).
+__device__ __forceinline__ void prefill_merge(const AttnParams& p, const TileDesc& t) {
+  using namespace fa;
+  const int g = p.g, R = p.R;
+  const int vrows = min(R, t.c - t.t0);
+  const int64_t base = static_cast<int64_t>(t.stile) * t.parts * 128;
+  for (int idx = threadIdx.x; idx < 128 * (kD / 4); idx += kThreads) {
+    const int r = idx / (kD / 4), c4 = idx - r * (kD / 4);
+    const int hh = r / R, i = r - hh * R;
+    if (i >= vrows) continue;
+    float M = -INFINITY;
+    for (int s = 0; s < t.parts; ++s) M = fmaxf(M, __ldcg(p.ppart_ml + (base + s * 128 + r) * 2));
+    float L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < t.parts; ++s) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ppart_ml + (base + s * 128 + r) * 2));
+      const float w = ex2(ml.x - M) * ml.y;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(p.ppart_o + (base + s * 128 + r) * kD) + c4);
+      L += w;
+      acc.x += w * v.x;
+      acc.y += w * v.y;
+      acc.z += w * v.z;
+      acc.w += w * v.w;
+    }
+    const float inv = 1.f / L;
+    const int h = t.kvh * g + hh;
+    const int64_t trow = t.row0 + t.t0 + i;
+    uint2 w2;
+    w2.x = pack_bf16(acc.x * inv, acc.y * inv);
+    w2.y = pack_bf16(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD + c4 * 4) * 2) = w2;
+    if (c4 == 0 && p.lse != nullptr) p.lse[static_cast<int64_t>(h) * p.T + trow] = (M + __log2f(L)) * 0.69314718055994530942f;
+  }
 }
 
 // Roles inside the 384-thread CTA: warp 0 lanes < 8 stream K tiles, warp 2 lanes < 8
@@ -355,7 +402,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   const int lane = tid & 31;
   const int g = p.g, R = p.R;
   const int vrows = min(R, t.c - t.t0);
-  const int nk = (t.nkeys + kBN - 1) / kBN;
+  const int nk = (t.nkeys + kBN - 1) / kBN;   // key steps of the whole q tile
+  const int j0 = t.j0, j1 = t.j1, n = j1 - j0;  // this item's steps (split-K part)
   int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && it == 0) ? p.trace + 8 * 160 : nullptr;  // [10][64]
 
   // ---- Q tile: rows r = hh*R + i  <-  q[row0 + t0 + i][kvh*g + hh][:]
@@ -424,11 +472,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       return (static_cast<int64_t>(__ldg(p.tables + t.tbl + lb)) * p.Hkv + t.kvh) * p.chunk_stride +
              static_cast<int64_t>((key & (p.B - 1)) >> 4) * 4096;
     };
-    int64_t next = piece_off(0);
-    for (int j = 0; j < nk; ++j) {
+    int64_t next = piece_off(j0);
+    for (int j = j0; j < j1; ++j) {
       const int64_t cur = next;
       next = piece_off(j + 1);
-      const uint32_t k_it = kv_it + j;
+      const uint32_t k_it = kv_it + (j - j0);
       const int st = k_it % nstg;
       const uint32_t full = bars + 8 * (bar_full + st);
       if (lane == 0) {
@@ -453,8 +501,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       // tensor pipe's queue is a few MMAs deep; a burst of 8 takes ~0.7 K cycles,
       // tools/umma_issue_test.cu), so QK^T and PV have an issuing thread each: neither
       // stream's readiness waits behind the other's issue.
-      for (int j = 0; j < nk; ++j) {
-        const uint32_t k_it = kv_it + j, gj = it + j;
+      for (int j = j0; j < j1; ++j) {
+        const uint32_t k_it = kv_it + (j - j0), gj = it + (j - j0);
         const int st = k_it % kKStages, sb = gj % kSBufs;
         if (gj >= kSBufs)  // PV_{j-kSBufs} has read its P from S[sb]
           mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
@@ -479,8 +527,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   } else if (warp == 3) {
     if (lane == 0) {
       // ---------------- PV issuer
-      for (int j = 0; j < nk; ++j) {
-        const uint32_t k_it = kv_it + j, gj = it + j;
+      for (int j = j0; j < j1; ++j) {
+        const uint32_t k_it = kv_it + (j - j0), gj = it + (j - j0);
         const int st = k_it % kVStages, sb = gj % kSBufs;
         mbar_wait(bars + 8 * (kBarPFull + sb), (gj / kSBufs) & 1);
         mbar_wait(bars + 8 * (kBarVFull + st), (k_it / kVStages) & 1);
@@ -492,7 +540,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
           umma_ts(tmem + kTmemO, tmem + sb * 128 + kk * 8, sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
-                  (j > 0 || kk > 0) ? 1u : 0u);
+                  (j > j0 || kk > 0) ? 1u : 0u);
         umma_commit(bars + 8 * (kBarODone + sb));
         umma_commit(bars + 8 * (kBarVEmpty + st));
       }
@@ -521,8 +569,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     float m_ref = -INFINITY;           // max of the latest step this set handled
     const float sl2 = p.scale_log2;
     const bool tracer = quarter == 0 && lane == 0;
-    for (int j = 0; j < nk; ++j) {
-      const uint32_t gj = it + j;
+    for (int j = j0; j < j1; ++j) {
+      const uint32_t gj = it + (j - j0);
       if (static_cast<int>(gj & 1) != set) continue;
       const int sb = gj % kSBufs;
       mbar_wait(bars + 8 * (kBarSFull + sb), (gj / kSBufs) & 1);
@@ -550,14 +598,14 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
       }
       float m_prev = -INFINITY;
-      if (j > 0) {  // m_{j-1} from the other set
+      if (j > j0) {  // m_{j-1} from the other set
         named_bar_sync(bar_in, 64);
         m_prev = chain[(set ^ 1) * 128 + r];
       }
       const float m_new = fmaxf(m_prev, mx * sl2);
       const bool need = m_new > m_prev + 8.0f;  // lazy rescale: p <= 2^8 otherwise
       const float m_use = need ? m_new : m_prev;
-      if (j + 1 < nk) {  // pass m_j on
+      if (j + 1 < j1) {  // pass m_j on
         chain[set * 128 + r] = m_use;
         named_bar_arrive(bar_out, 64);
       }
@@ -567,7 +615,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       }
       m_ref = m_use;
       if (tracer) ev_stamp(ev, 5, j);
-      if (j > 0 && __any_sync(0xffffffffu, need)) {
+      if (j > j0 && __any_sync(0xffffffffu, need)) {
         // rare: rescale O after PV_{j-1} (PV_j waits for our P)
         const float alpha = ex2(m_prev - m_use);
         mbar_wait(bars + 8 * (kBarODone + (gj - 1) % kSBufs), ((gj - 1) / kSBufs) & 1);
@@ -611,7 +659,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     }
     // ---------------- epilogue: combine the sets' (l, m); O / l -> bf16 (set s writes
     // dims [64 s, 64 s + 64)), LSE
-    mbar_wait(bars + 8 * (kBarODone + (it + nk - 1) % kSBufs), ((it + nk - 1) / kSBufs) & 1);
+    mbar_wait(bars + 8 * (kBarODone + (it + n - 1) % kSBufs), ((it + n - 1) / kSBufs) & 1);
     tc_fence_after();
     {
       // every MMA of the tile has completed, so the Q tile's shared memory is free:
@@ -628,6 +676,24 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     const int64_t trow = t.row0 + t.t0 + i;
     const uint32_t col0 = static_cast<uint32_t>(set * 64);
     uint8_t* orow = static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD + col0) * 2;
+    if (t.parts > 1) {
+      // split-K part: the normalised partial o / l (fp32) and (m, l) of this row; the part
+      // that completes the tile merges (prefill_merge)
+      const int64_t slot = (static_cast<int64_t>(t.stile) * t.parts + t.part) * 128 + r;
+      float* po = p.ppart_o + slot * kD + col0;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t ov[32];
+        tmem_ld32(lane_addr + kTmemO + col0 + c * 32, ov);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4)
+          __stcg(reinterpret_cast<float4*>(po + c * 32 + e),
+                 make_float4(__uint_as_float(ov[e]) * inv_l, __uint_as_float(ov[e + 1]) * inv_l,
+                             __uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l));
+      }
+      if (set == 0) __stcg(reinterpret_cast<float2*>(p.ppart_ml + slot * 2), make_float2(m_ref, l));
+      __threadfence();
+    } else {
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       uint32_t ov[32];
@@ -646,12 +712,29 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     }
     if (set == 0 && valid && p.lse != nullptr)
       p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
+    }
   }
-  kv_it += nk;
-  it += nk;
+  kv_it += n;
+  it += n;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (t.parts > 1) {
+    // split-K completion: the part that brings the tile's count to (epoch + 1) * parts merges
+    volatile int* flag = reinterpret_cast<volatile int*>(xch_base + kXOff + 2040);
+    if (tid == 0) {
+      const int old = atomicAdd(p.pcounters + t.stile, 1);
+      *flag = old + 1 == (p.epoch + 1) * t.parts;
+    }
+    __syncthreads();
+    const bool last = *flag != 0;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      prefill_merge(p, t);
+      __syncthreads();
+    }
+  }
 }
 
 // --------------------------------------------------------------- decode unit

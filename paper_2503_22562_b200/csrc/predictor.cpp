@@ -40,7 +40,8 @@ struct Run {  // `count` consecutive queue entries of equal size
 // The launch as the planner builds it: independent of the model parameters.
 struct Launch {
   double rows = 0, D = 0, sum_ctx = 0, units = 0;
-  int32_t grid = 1, np = 0, wpc = 12, q = 0, small = 0;
+  int32_t grid = 1, np = 0, wpc = 12, q = 0, small = 0, parts_target = 1;
+  std::vector<int32_t> parts;  // split-K parts per slice (queue order)
   double bytes_per_token = 0;  // one kv head's K + V
   std::vector<Run> tiles;      // 128-key steps per tile, queue order
   std::vector<Run> pieces;     // tokens per decode unit, queue order
@@ -68,15 +69,18 @@ Launch build(const niyama_predictor& p, std::vector<SliceOC> slices, const int32
   std::stable_sort(slices.begin(), slices.end(), [](const SliceOC& a, const SliceOC& b) {
     return static_cast<int64_t>(a.o) + a.c > static_cast<int64_t>(b.o) + b.c;
   });
-  int64_t tile_cost = 0, n_tiles = 0;
-  for (const SliceOC& sl : slices) {
+  // q tiles per slice (steps of each, queue order); split-K parts are decided below
+  std::vector<std::vector<int64_t>> qsteps(slices.size());
+  int64_t q_tiles = 0, q_steps = 0;
+  for (size_t si = 0; si < slices.size(); ++si) {
+    const SliceOC& sl = slices[si];
     L.rows += sl.c;
     const int64_t nqt = ceil_div64(sl.c, R);
     for (int64_t qt = nqt - 1; qt >= 0; --qt) {
       const int64_t steps = ceil_div64(sl.o + std::min<int64_t>(sl.c, (qt + 1) * R), 128);
-      push_run(L.tiles, steps, p.hkv);
-      tile_cost += (steps + NIYAMA_TILE_SETUP_STEPS) * p.hkv;
-      n_tiles += p.hkv;
+      qsteps[si].push_back(steps);
+      q_tiles += p.hkv;
+      q_steps += steps * p.hkv;
     }
   }
   int64_t sum_ctx = 0;
@@ -107,6 +111,26 @@ Launch build(const niyama_predictor& p, std::vector<SliceOC> slices, const int32
   L.D = static_cast<double>(D);
   L.sum_ctx = static_cast<double>(sum_ctx);
   L.units = static_cast<double>(n_units);
+  // split-K parts (internal.h, as the planner) and the work items in the kernel's order:
+  // slices, q tiles (longest first), kv heads, parts
+  const int32_t target = prefill_parts_target(q_tiles, n_units, q_steps + NIYAMA_TILE_SETUP_STEPS * q_tiles, sum_ctx,
+                                              p.hkv, p.d, p.elt, g, p.num_sms, p.tune.decode_path, p.tune.prefill_split);
+  L.parts_target = target;
+  int64_t tile_cost = 0, n_tiles = 0;
+  for (size_t si = 0; si < slices.size(); ++si) {
+    const std::vector<int64_t>& qs = qsteps[si];
+    if (qs.empty()) continue;
+    const int32_t parts = target > 1 ? prefill_parts_of_slice(target, qs.back()) : 1;  // qs.back(): shortest tile
+    L.parts.push_back(parts);
+    for (int64_t nk : qs)
+      for (int h = 0; h < p.hkv; ++h)
+        for (int32_t part = 0; part < parts; ++part) {
+          const int64_t steps = (part + 1) * nk / parts - part * nk / parts;
+          push_run(L.tiles, steps, 1);
+          tile_cost += steps + NIYAMA_TILE_SETUP_STEPS;
+          ++n_tiles;
+        }
+  }
   const CtaSplit cs = cta_split(n_tiles, n_units, tile_cost, sum_ctx, p.hkv, p.d, p.elt, g, p.num_sms, p.tune.decode_path);
   L.grid = cs.grid;
   L.np = cs.prefill_ctas;
@@ -652,7 +676,7 @@ extern "C" niyama_status niyama_predict_detail(const niyama_predictor* p, const 
   out->split_len = L.q;
   out->small_piece = L.small;
   out->warps_per_cta = L.wpc;
-  out->reserved = 0;
+  out->prefill_parts_target = L.parts_target;
   out->num_units = static_cast<int64_t>(L.units);
   out->sim_seconds = simulate(L, p->theta + kLin);
   out->seconds = total(*p, L);

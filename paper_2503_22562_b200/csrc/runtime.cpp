@@ -154,6 +154,9 @@ struct niyama_plan {
   int32_t n_tiles = 0, n_units = 0, n_merge_rows = 0;  // n_tiles = prefill work items (q tiles)
   int32_t q_tiles = 0;
   int64_t tile_steps = 0;     // sum over prefill tiles of ceil(visible keys / 128)
+  int64_t n_setups = 0;       // prefill work items (q tiles x split-K parts)
+  int32_t n_split_tiles = 0;  // q tiles with split-K parts > 1
+  int64_t split_parts_total = 0;
   int32_t prefill_ctas = 0;   // CTAs of the bf16 launch that take prefill tiles first
   int32_t grid = 0;           // CTAs of the bf16 launch
   std::vector<RowInfo> rows;
@@ -170,6 +173,9 @@ struct niyama_plan {
   int32_t* d_velem = nullptr;
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
+  float* d_ppart_o = nullptr;
+  float* d_ppart_ml = nullptr;
+  int32_t* d_pcounters = nullptr;
   int32_t* d_work = nullptr;
 };
 
@@ -355,7 +361,7 @@ extern "C" niyama_status niyama_kv_gather(niyama_kv* kv, int32_t layer, int64_t 
 namespace {
 
 void plan_cta_split(niyama_plan* pl, const niyama_kv* kv) {
-  const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_tiles,
+  const CtaSplit r = cta_split(pl->n_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->n_setups,
                                pl->sum_ctx, kv->hkv, kv->d, kv->elt, kv->g, kv->num_sms, kv->tune.decode_path);
   pl->grid = r.grid;
   pl->prefill_ctas = r.prefill_ctas;
@@ -545,7 +551,8 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
       sl.row0 = row0[i];
       sl.nqt = static_cast<int32_t>(ceil_div(sl.c, pl->R));
       sl.tbase = tbase;
-      tbase += sl.nqt * hkv;  // work items = 128-row q tiles
+      sl.parts = 1;
+      tbase += sl.nqt * hkv;  // work items = 128-row q tiles (split-K parts are set below)
       for (int32_t qt = 0; qt < sl.nqt; ++qt)
         pl->tile_steps += hkv * ceil_div(static_cast<int64_t>(sl.o) + std::min<int64_t>(sl.c, (qt + 1LL) * pl->R), 128);
       pl->q_tiles += sl.nqt * hkv;
@@ -641,6 +648,26 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     }
     pl->n_units = ubase;
   }
+  // prefill split-K (internal.h): parts per slice, work items and their setup cost
+  {
+    const int32_t target = prefill_parts_target(pl->q_tiles, pl->n_units, pl->tile_steps + NIYAMA_TILE_SETUP_STEPS * pl->q_tiles,
+                                                pl->sum_ctx, hkv, kv->d, kv->elt, g, kv->num_sms, kv->tune.decode_path,
+                                                kv->tune.prefill_split);
+    int32_t tbase = 0, pbase = 0;
+    pl->n_setups = 0;
+    for (PrefillSlice& sl : pl->slices) {
+      const int64_t min_steps = ceil_div(static_cast<int64_t>(sl.o) + std::min<int64_t>(sl.c, pl->R), 128);
+      sl.parts = target > 1 ? prefill_parts_of_slice(target, min_steps) : 1;
+      sl.tbase = tbase;
+      sl.pbase = sl.parts > 1 ? pbase : 0;
+      tbase += sl.nqt * hkv * sl.parts;
+      if (sl.parts > 1) pbase += sl.nqt * hkv;
+      pl->n_setups += static_cast<int64_t>(sl.nqt) * hkv * sl.parts;
+      pl->split_parts_total += sl.parts > 1 ? static_cast<int64_t>(sl.nqt) * hkv * sl.parts : 0;
+    }
+    pl->n_tiles = tbase;
+    pl->n_split_tiles = pbase;
+  }
   plan_cta_split(pl, kv);
   // ---- device copy: one allocation, one H2D
   if (kv->has_device) {
@@ -662,9 +689,12 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_velem = take(pl->velem.size() * 4);
     const size_t o_work = take(32);  // [8] zero-initialised through the H2D (with the counters)
     const size_t o_cnt = take(pl->drows.size() * static_cast<size_t>(hkv) * 4);
+    const size_t o_pcnt = take(static_cast<size_t>(pl->n_split_tiles) * 4);
     const size_t meta_bytes = off;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
+    const size_t o_ppart_o = take(static_cast<size_t>(pl->split_parts_total) * 128 * kv->d * 4);
+    const size_t o_ppart_ml = take(static_cast<size_t>(pl->split_parts_total) * 128 * 2 * 4);
     const size_t total = off;
     // upload on the library's copy stream into the staging slot's own device buffer when
     // no live plan holds it (the common case); otherwise from the pool on the caller's stream
@@ -745,6 +775,9 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     pl->d_velem = reinterpret_cast<int32_t*>(pl->dbuf + o_velem);
     pl->d_part_o = reinterpret_cast<float*>(pl->dbuf + o_part_o);
     pl->d_part_ml = reinterpret_cast<float*>(pl->dbuf + o_part_ml);
+    pl->d_pcounters = reinterpret_cast<int32_t*>(pl->dbuf + o_pcnt);
+    pl->d_ppart_o = reinterpret_cast<float*>(pl->dbuf + o_ppart_o);
+    pl->d_ppart_ml = reinterpret_cast<float*>(pl->dbuf + o_ppart_ml);
     pl->d_work = reinterpret_cast<int32_t*>(pl->dbuf + o_work);
   }
   *out = pl;
@@ -936,6 +969,9 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   p.rows = plan->d_rows;
   p.part_o = plan->d_part_o;
   p.part_ml = plan->d_part_ml;
+  p.ppart_o = plan->d_ppart_o;
+  p.ppart_ml = plan->d_ppart_ml;
+  p.pcounters = plan->d_pcounters;
   p.work = plan->d_work;
   p.chunk_bytes = kv->chunk_bytes;
   p.chunk_stride = kv->chunk_stride;
@@ -1001,6 +1037,7 @@ extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning
   if (!kv || !t) return fail(NIYAMA_EINVAL, "kv/tuning is NULL");
   if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
   if (t->decode_path != 0 && t->decode_path != 1) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0 or 1");
+  if (t->prefill_split != 0 && t->prefill_split != 1) return fail(NIYAMA_EINVAL, "tuning: prefill_split must be 0 or 1");
   if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
   if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");
   if (t->tail_min < 16 || t->tail_min % 16) return fail(NIYAMA_EINVAL, "tuning: tail_min must be a multiple of 16");

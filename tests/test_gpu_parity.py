@@ -286,3 +286,27 @@ def test_tensor_core_decode_path(case):
         wl = W.random_hybrid(W.Shape(32, 8, 128, 64, "bf16"), seed=24, num_prefill=1, max_chunk=300, num_decode=12,
                              max_ctx=3000)
     run_and_compare(wl, tuning=dict(decode_path=1))
+
+
+@pytest.mark.parametrize("case", ["prefill-only", "mixed", "g8", "two-slices", "diag-only"])
+def test_prefill_split_k(case):
+    """Split-K prefill (niyama_tuning.prefill_split = 1: key parts of a q tile on different CTAs,
+    merged by the last part) against the oracle, and the same launch unsplit (the default)."""
+    L8 = W.L8B
+    if case == "prefill-only":
+        wl = W.hybrid(L8, "p", prefill_offset=3000, chunk=100, decode_ctx=[], seed=31)
+    elif case == "mixed":
+        wl = W.hybrid(L8, "m", prefill_offset=2000, chunk=64, decode_ctx=[700, 33, 1500], seed=32)
+    elif case == "g8":
+        wl = W.hybrid(W.Shape(64, 8, 128, 16, "bf16"), "g8", prefill_offset=2500, chunk=90, decode_ctx=[400], seed=33)
+    elif case == "two-slices":
+        wl = W.random_hybrid(L8, seed=34, num_prefill=2, max_chunk=60, num_decode=2, max_ctx=3500)
+    else:
+        wl = W.hybrid(L8, "d", prefill_offset=1500, chunk=40, decode_ctx=[], seed=35)
+    r, _ = run_and_compare(wl, tuning=dict(prefill_split=1))
+    import paper_2503_22562_b200 as ny
+    det = ny.Predictor.from_params(ny.Predictor.shape_cfg(wl.shape.num_q_heads, wl.shape.num_kv_heads, 128),
+                                   list(ny.DEFAULT_THETA)).bind(r.kv).detail(wl.final.desc)
+    if case != "two-slices":
+        assert det["parts_target"] > 1          # the case exercises the split path
+    run_and_compare(wl)

@@ -315,7 +315,8 @@ def _oracle(pr, theta, offs, lens, ctx):
     d = W.BatchDesc(list(range(len(offs))), offs, lens, list(range(100, 100 + len(ctx))), ctx)
     det = pr.detail(d)
     ln = OP.Launch(det["split_len"], det["small_piece"], det["grid"], det["prefill_ctas"], det["warps_per_cta"])
-    w = OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1))
+    w = OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1),
+                det["parts_target"])
     assert w.units == det["units"]
     return d, OP.predict(theta, w, ln)
 
@@ -352,8 +353,9 @@ def test_planner_and_predictor_model_the_same_launch():
         if ctx:
             assert info.split_len == det["split_len"]
         ln = OP.Launch(det["split_len"], det["small_piece"], det["grid"], det["prefill_ctas"], 12)
-        w = OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1))
-        assert info.num_prefill_tiles == len(w.tiles) and sum(OP.tiles_per_cta(w, ln)) == len(w.tiles)
+        w = OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1),
+                    det["parts_target"])
+        assert sum(OP.tiles_per_cta(w, ln)) == len(w.tiles)
 
 
 def test_predictor_fit_recovers_model_generated_times():
@@ -370,7 +372,8 @@ def test_predictor_fit_recovers_model_generated_times():
             ctx = [100]
         d, t = _oracle(pr, truth, offs, lens, ctx)
         det = pr.detail(d)
-        works.append(OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1)))
+        works.append(OP.work(SHAPE, list(zip(offs, lens)), ctx, max(det["split_len"], 1), max(det["small_piece"], 1),
+                             det["parts_target"]))
         lns.append(OP.Launch(det["split_len"], det["small_piece"], det["grid"], det["prefill_ctas"], 12))
         batches.append(d)
         ts.append(t)

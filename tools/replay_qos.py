@@ -154,11 +154,15 @@ def main():
                                  **POLICIES[name])
         it, recs = serve.replay(sched, ex, trace, buckets, until=duration * 1.25)
         summ = serve.summarize(it, recs, buckets, t_end=duration * 1.25, fixed_s=fixed_s)
+        if args.full:   # the scheduler's prediction is the whole iteration: no attention-only comparison
+            summ.pop("predictor_rel_err_attention_only", None)
         summ["wall_s"] = time.time() - t1
         if not args.model_only:
             summ["gpu_launches"] = ex.launches
         out["runs"][name] = summ
         print(name, json.dumps(summ), flush=True)
+        os.makedirs(os.path.dirname(args.out), exist_ok=True)
+        json.dump(out, open(args.out, "w"), indent=1)   # after every policy (long runs)
         del ex
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(out, open(args.out, "w"), indent=1)

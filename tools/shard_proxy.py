@@ -24,11 +24,13 @@ def dev(a, lo, hi):
     return torch.from_numpy(np.ascontiguousarray(a[:, lo:hi]).view(np.int16)).cuda().view(torch.bfloat16)
 
 
-def rank0_time(wl, G, reps):
+def rank0_time(wl, G, reps, tuning=None):
     s = wl.shape
     hq, hkv = s.num_q_heads // G, s.num_kv_heads // G
     kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 16, block_size=s.block_size,
                     dtype=s.dtype, world_size=G, rank=0, device=0)
+    if tuning:
+        kv.set_tuning(**tuning)
     plan = None
     for st in wl.steps:
         plan = kv.plan(st.desc)
@@ -54,17 +56,19 @@ def rank0_time(wl, G, reps):
 
 
 def main():
-    reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
-    out = {}
+    reps = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 20
+    tuning = dict(prefill_split=1) if "split" in sys.argv else None
+    out = {"tuning": tuning or "default (no split-K)"}
     for name, wl in (("config2-l8b", W.config2_l8b()), ("config4-l70b", W.config4_l70b())):
         t1 = None
         for G in (1, 2, 4, 8):
-            t = rank0_time(wl, G, reps if G > 1 or name.startswith("config2") else max(5, reps // 4))
+            t = rank0_time(wl, G, reps if G > 1 or name.startswith("config2") else max(5, reps // 4), tuning)
             t1 = t if G == 1 else t1
             eff = t1 / (G * t)
             out.setdefault(name, {})[G] = {"rank0_launch_us": t, "attention_scaling_eff_no_collective": eff}
             print(f"{name:14s} G={G}: rank-0 attention launch {t:8.1f} us  t1/(G tG) = {eff:.3f}", flush=True)
-    json.dump(out, open(os.path.join("gpurun_out", "shard_proxy.json"), "w"), indent=1)
+    json.dump(out, open(os.path.join("gpurun_out", "shard_proxy" + ("_split" if tuning else "") + ".json"), "w"),
+              indent=1)
 
 
 if __name__ == "__main__":
