@@ -495,15 +495,16 @@ def main():
     attn_avg_ms = sum(attn_ms) / len(attn_ms)
     ag_avg_ms = sum(ag_ms) / len(ag_ms)
     attn_q = [float(x) for x in np.percentile(np.array(attn_ms) * 1e3, [10, 50, 90])]
-    per_rank = {"attention_us": [attn_avg_ms * 1e3], "allgather_us": [ag_avg_ms * 1e3], "step_us": [ms / args.steps * 1e3]}
+    attn_med_ms = attn_q[1] * 1e-3   # the roofline's launch time: median (robust to a throttled launch)
+    per_rank = {"attention_us": [attn_med_ms * 1e3], "allgather_us": [ag_avg_ms * 1e3], "step_us": [ms / args.steps * 1e3]}
     if dist:
-        t = torch.tensor([ms, attn_avg_ms, ag_avg_ms], device=dev)
+        t = torch.tensor([ms, attn_med_ms, ag_avg_ms], device=dev)
         allr = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(allr, t)
         per_rank = {"attention_us": [float(x[1]) * 1e3 for x in allr], "allgather_us": [float(x[2]) * 1e3 for x in allr],
                     "step_us": [float(x[0]) / args.steps * 1e3 for x in allr]}
         ms = max(float(x[0]) for x in allr)
-        attn_avg_ms = max(float(x[1]) for x in allr)
+        attn_med_ms = max(float(x[1]) for x in allr)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the
     # timed region.  Two buffer sets: the H2D of step i+1 (copy stream) and the
@@ -580,7 +581,7 @@ def main():
 
     B_kv, F = algorithmic(wl, hq, hkv)
     hbm_peak, tf_peak, peak_src = peaks()
-    attn_s = attn_avg_ms * 1e-3
+    attn_s = attn_med_ms * 1e-3
     achieved = B_kv / attn_s / 1e9
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -608,13 +609,14 @@ def main():
                                        "ncu --set full capture (profiles/ncu_traffic.json), not measured in this run",
                      "kernel": "hybrid_attn_bf16_kernel" + (" (incl. the KV append)" if fused else ""),
                      "algorithmic_bytes_per_launch": B_kv,
-                     "launch_us": attn_avg_ms * 1e3, "peak_source": peak_src,
+                     "launch_us": attn_med_ms * 1e3, "launch_stat": "median over the event-bracketed launches (rank max)",
+                     "peak_source": peak_src,
                      "tensor_frac": F / attn_s / (tf_peak * 1e12),
                      "t_roof_us": max(F / (tf_peak * 1e12), B_kv / (hbm_peak * 1e9)) * 1e6},
         "attn_tokens_per_s": T / attn_s,
-        "step_breakdown_us": {"append": 1e3 * sum(append_ms) / len(append_ms), "attention": attn_avg_ms * 1e3,
+        "step_breakdown_us": {"append": 1e3 * sum(append_ms) / len(append_ms), "attention": attn_med_ms * 1e3,
                               "allgather": ag_avg_ms * 1e3,
-                              "other": ms / args.steps * 1e3 - attn_avg_ms * 1e3 - 1e3 * sum(append_ms) / len(append_ms),
+                              "other": ms / args.steps * 1e3 - attn_med_ms * 1e3 - 1e3 * sum(append_ms) / len(append_ms),
                               "host_issue": host_issue_us},
         "attention_launch_us": {"p10": attn_q[0], "median": attn_q[1], "p90": attn_q[2], "mean": attn_avg_ms * 1e3,
                                 "samples": len(attn_ms)},
@@ -624,13 +626,13 @@ def main():
                 "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
         "gpu_launches": (1 if fused else 2) * args.steps,
         "timing_note": (f"attention/append/all-gather launch times from events on every {EV_EVERY}nd timed step; "
-                        "the roofline uses their mean (rank max); the append "
+                        "the roofline uses their median (rank max; the mean is in attention_launch_us); the append "
                         "interval includes the wait for the plan's upload (library copy stream), so 'other' = step "
                         "- append - attention can be negative"),
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
-        "a8": {"predicted_attention_us": pred.predict(batch) * 1e6, "measured_attention_us": attn_avg_ms * 1e3,
-               "rel_err": pred.predict(batch) / (attn_avg_ms * 1e-3) - 1.0,
+        "a8": {"predicted_attention_us": pred.predict(batch) * 1e6, "measured_attention_us": attn_med_ms * 1e3,
+               "rel_err": pred.predict(batch) * 1e3 / attn_med_ms - 1.0,
                "note": "the event model fitted on flushed single launches (profiles/predictor_fit.json) vs the "
                        "mean launch inside the bench step (not flushed: inputs larger than L2)"},
     }
