@@ -310,3 +310,64 @@ def test_prefill_split_k(case):
     if case != "two-slices":
         assert det["parts_target"] > 1          # the case exercises the split path
     run_and_compare(wl)
+
+
+def _kvq(seed, n, shape):
+    g = W.rng(seed)
+    return (W.draw_values(g, (n, shape.num_kv_heads, shape.head_dim), "bf16"),
+            W.draw_values(g, (n, shape.num_kv_heads, shape.head_dim), "bf16"),
+            W.draw_values(g, (n, shape.num_q_heads, shape.head_dim), "bf16"))
+
+
+def test_chunked_prefill_equals_full_prefill():
+    """P:118 (chunked prefills): a 700-token prompt prefilled as chunks 256 + 256 + 188 over three
+    iterations gives, row by row, the output of one 700-token prefill — bitwise (every row runs
+    the same key steps in the same order whatever tile holds it) — and both match the oracle."""
+    import paper_2503_22562_b200 as ny
+    s = W.L8B
+    k, v, q = _kvq(41, 700, s)
+
+    def run(chunks):
+        kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, 64, dtype="bf16", device=0)
+        outs, off = [], 0
+        for c in chunks:
+            p = kv.plan(W.BatchDesc([0], [off], [c]))
+            kv.append(p, 0, to_dev(k[off:off + c], "bf16"), to_dev(v[off:off + c], "bf16"))
+            o = torch.empty((s.num_q_heads, c, s.head_dim), dtype=torch.bfloat16, device="cuda")
+            lse = torch.empty((s.num_q_heads, c), dtype=torch.float32, device="cuda")
+            kv.attention(p, 0, to_dev(q[off:off + c], "bf16"), o, lse)
+            torch.cuda.synchronize()
+            outs.append((o, lse))
+            off += c
+        return torch.cat([o for o, _ in outs], dim=1), torch.cat([l for _, l in outs], dim=1)
+    of, lf = run([700])
+    oc, lc = run([256, 256, 188])
+    assert torch.equal(of.view(torch.int16), oc.view(torch.int16)) and torch.equal(lf, lc)
+    wl = W.Workload("full", s, [W.Step(W.BatchDesc([0], [0], [700]), k, v, q)], 64)
+    _, _, O, L = oracle_for(wl)
+    assert_close(to_host_f64(of, "bf16"), O, lf.cpu().numpy().astype(np.float64), L)
+
+
+def test_decode_row_equals_prefill_row():
+    """A decode row at ctx L with query q equals the prefill row at position L-1 with the same q
+    and keys (two different code paths: split-KV mma.sync decode vs tcgen05 prefill tiles), within
+    the bf16 bar; ctx 1000 and 4096 (split rows, merged in-launch)."""
+    import paper_2503_22562_b200 as ny
+    s = W.L8B
+    for L in (1000, 4096):
+        k, v, q = _kvq(42 + L, L, s)
+        kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, 2 * (L // 16 + 2), dtype="bf16", device=0)
+        p = kv.plan(W.BatchDesc([1, 2], [0, 0], [L - 1, L - 1]))
+        kk = np.concatenate([k[:L - 1], k[:L - 1]])
+        vv = np.concatenate([v[:L - 1], v[:L - 1]])
+        kv.append(p, 0, to_dev(kk, "bf16"), to_dev(vv, "bf16"))
+        p2 = kv.plan(W.BatchDesc([1], [L - 1], [1], decode_seq=[2], decode_ctx=[L]))  # row 0 prefill, row 1 decode
+        kv.append(p2, 0, to_dev(np.concatenate([k[L - 1:], k[L - 1:]]), "bf16"),
+                  to_dev(np.concatenate([v[L - 1:], v[L - 1:]]), "bf16"))
+        o = torch.empty((s.num_q_heads, 2, s.head_dim), dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty((s.num_q_heads, 2), dtype=torch.float32, device="cuda")
+        kv.attention(p2, 0, to_dev(np.concatenate([q[L - 1:], q[L - 1:]]), "bf16"), o, lse)
+        torch.cuda.synchronize()
+        a = o[:, 0].float().cpu().numpy().astype(np.float64)
+        b = o[:, 1].float().cpu().numpy().astype(np.float64)
+        assert_close(b, a, lse[:, 1].cpu().numpy().astype(np.float64), lse[:, 0].cpu().numpy().astype(np.float64))
