@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--fused-append", action="store_true",
                     help="a3-a6 in one launch (niyama_append_attention) instead of niyama_kv_append + "
                          "niyama_hybrid_attention (measured slower on config 2: 113 vs 100 + 10 us)")
+    ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
+                    help="a7 head all-gather: nccl = niyama_allgather_heads after the launch (N > 1 only); fused = "
+                         "niyama_attention_gather, the all-gather inside the attention launch (NVLink stores into "
+                         "an NCCL symmetric window + flag barrier; run at every N, at N = 1 through the GPU's own "
+                         "window mapping)")
     return ap.parse_args()
 
 
@@ -373,11 +378,14 @@ def main():
     fused = args.fused_append
     kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
                     dtype=s.dtype, world_size=world, rank=rank, device=local)
+    gather_fused = args.gather == "fused"
     if world > 1:
         uid = ny.get_unique_id() if rank == 0 else bytes(128)
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
         kv.comm_init(obj[0])
+    elif gather_fused:
+        kv.comm_init(ny.get_unique_id())
 
     def dev_bf16(a, lo, hi):
         return torch.from_numpy(np.ascontiguousarray(a[:, lo:hi]).view(np.int16)).to(dev).view(torch.bfloat16)
@@ -399,6 +407,8 @@ def main():
     o = o_full[q0:q0 + hq]
     lse = lse_full[q0:q0 + hq]
     stream = torch.cuda.current_stream()
+    window = kv.gather_window(T) if gather_fused else None
+    last_win = {}
 
     # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
     fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
@@ -443,7 +453,14 @@ def main():
         plan = kv.plan(batch, stream)                   # a2
         if evs is not None:
             evs[0].record(stream)
-        if fused:   # a3-a6 in ONE launch (niyama_append_attention)
+        if gather_fused:   # a4-a7 (a3-a7 with --fused-append) in ONE launch (niyama_attention_gather)
+            if not fused:
+                kv.append(plan, 0, k_new, v_new, stream)
+            if evs is not None:
+                evs[1].record(stream)
+            last_win["o"] = kv.attention_gather(plan, 0, q, window, k_new if fused else None,
+                                                v_new if fused else None, 0.0, stream)[0]
+        elif fused:   # a3-a6 in ONE launch (niyama_append_attention)
             if evs is not None:
                 evs[1].record(stream)
             kv.append_attention(plan, 0, k_new, v_new, q, o, lse, 0.0, stream)
@@ -454,7 +471,7 @@ def main():
             kv.attention(plan, 0, q, o, lse, 0.0, stream)   # a4-a6
         if evs is not None:
             evs[2].record(stream)
-        if world > 1:
+        if world > 1 and not gather_fused:
             kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
         if evs is not None:
             evs[3].record(stream)
@@ -538,13 +555,20 @@ def main():
         stream.wait_event(ev_out[b_])
         a1_step()
         plan = kv.plan(batch, stream)
-        if fused:
+        if gather_fused:
+            if not fused:
+                kv.append(plan, 0, d_k[b_], d_v[b_], stream)
+            wo, wl_ = kv.attention_gather(plan, 0, d_q[b_], window, d_k[b_] if fused else None,
+                                          d_v[b_] if fused else None, 0.0, stream)
+            e_of[b_].copy_(wo)     # the consumer reads the window before the next call (its contract)
+            e_lf[b_].copy_(wl_)
+        elif fused:
             kv.append_attention(plan, 0, d_k[b_], d_v[b_], d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0,
                                 stream)
         else:
             kv.append(plan, 0, d_k[b_], d_v[b_], stream)
             kv.attention(plan, 0, d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0, stream)
-        if world > 1:
+        if world > 1 and not gather_fused:
             kv.allgather_heads(plan, e_of[b_], e_lf[b_], stream)
         pred.predict(batch)
         plan.rollback()
@@ -574,7 +598,7 @@ def main():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
-    ok = bool(torch.equal(h_o[(args.steps - 1) & 1], o_full.cpu()))
+    ok = bool(torch.equal(h_o[(args.steps - 1) & 1], (last_win["o"] if gather_fused else o_full).cpu()))
     clocks.stop()
     h2d = (h_q.numel() + h_k.numel() + h_v.numel()) * 2
     d2h = h_o[0].numel() * 2
@@ -602,12 +626,15 @@ def main():
                    "l2": f"inputs larger than L2 ({B_kv / 1e6:.0f} MB KV read per step per GPU vs 126 MB L2)",
                    "step": ("a1 slack+chunk, a2 plan, a3-a6 ONE launch (append inside the attention)" if fused else
                             "a1 slack+chunk, a2 plan, a3 append, a4-a6 fused attention") +
-                           (", a7 NCCL all-gather" if world > 1 else "") + ", a8 predict; 1 layer"},
+                           (", a7 all-gather INSIDE the attention launch (symmetric-window stores + flag barrier)"
+                            if gather_fused else ", a7 NCCL all-gather" if world > 1 else "") +
+                           ", a8 predict; 1 layer"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "traffic_source": "stored: dram__bytes_read.sum + dram__bytes_write.sum of this launch from one "
                                        "ncu --set full capture (profiles/ncu_traffic.json), not measured in this run",
-                     "kernel": "hybrid_attn_bf16_kernel" + (" (incl. the KV append)" if fused else ""),
+                     "kernel": "hybrid_attn_bf16_kernel" + (" (incl. the KV append)" if fused else "") +
+                               (" (incl. the head all-gather)" if gather_fused else ""),
                      "algorithmic_bytes_per_launch": B_kv,
                      "launch_us": attn_med_ms * 1e3, "launch_stat": "median over the event-bracketed launches (rank max)",
                      "peak_source": peak_src,

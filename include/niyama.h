@@ -22,6 +22,7 @@
  *   a4-a6 niyama_hybrid_attention                        (ONE fused launch)
  *   a3-a6 niyama_append_attention                        (append + attention, ONE launch)
  *   a7 niyama_comm_init + niyama_allgather_heads         (NCCL over NVLink)
+ *   §8(f)2 niyama_gather_create + niyama_attention_gather (all-gather fused into the launch)
  *   a8 niyama_predictor_fit + niyama_predict_iter_time   (host, fp64)
  *   §8(f)1 niyama_sched_*: QoS scheduler core            (host)
  *
@@ -272,6 +273,45 @@ niyama_status niyama_comm_init(niyama_kv* kv, const void* nccl_unique_id);
 niyama_status niyama_get_unique_id(void* out128); /* ncclGetUniqueId, for rank 0 */
 niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan* plan, void* o_full, float* lse_full,
                                      niyama_stream stream);
+
+/* §8(f)2 — the head all-gather fused into the attention launch (
+ * the exchange is a7's, P:319 TP -> head sharding, §8e).  Instead of a separate
+ * collective after the kernel, every O row (and LSE value) the launch produces is
+ * stored straight into the output window of EVERY rank (NVLink load/store through
+ * NCCL symmetric memory: ncclMemAlloc + ncclCommWindowRegister, peer addresses from
+ * the window's LSA mapping), and the launch's last CTA runs a flag barrier with the
+ * other ranks' launches, so when the kernel completes on rank r its window holds all
+ * G ranks' heads.  bf16 pools only.
+ *
+ * niyama_gather_create (COLLECTIVE over kv's communicator: every rank calls it, after
+ * niyama_comm_init, with the same max_rows) allocates one window holding two output
+ * buffers of o_full [Hq][max_rows][d] bf16 + lse_full [Hq][max_rows] f32 (Hq = all
+ * ranks' heads) and the barrier flags.  EUNSUPPORTED if the NCCL build or the system
+ * gives no symmetric memory (then use niyama_allgather_heads); EINVAL before
+ * comm_init, on an f32 pool or max_rows <= 0.  niyama_gather_destroy is collective too
+ * (stream-ordered: call it after the last launch's stream work completed).
+ *
+ * niyama_attention_gather = niyama_append_attention (k_new, v_new may be NULL: no
+ * append) whose outputs go to the window: on return *o_full / *lse_full (DEVICE, this
+ * rank's mapping) point at the buffer the launch fills, head-major [Hq][T][d] / [Hq][T]
+ * exactly as niyama_allgather_heads leaves them (rank r's heads at r*(Hq/G)).  The two
+ * buffers alternate per call, so a buffer is rewritten only by the call after next;
+ * a rank must finish reading the outputs of call n (stream-ordered work is enough)
+ * before it issues call n + 1, and every rank must issue the same sequence of calls
+ * (the barrier matches them by count; a rank that never arrives makes the others trap
+ * after ~30 s instead of hanging).  plan->T <= max_rows (else EINVAL). */
+typedef struct niyama_gather niyama_gather;
+niyama_status niyama_gather_create(niyama_kv* kv, int32_t max_rows, niyama_gather** out);
+niyama_status niyama_gather_destroy(niyama_gather* g);
+niyama_status niyama_attention_gather(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
+                                      const void* v_new, const void* q, niyama_gather* g, float softmax_scale,
+                                      void** o_full, float** lse_full, niyama_stream stream);
+/* Test support for the same protocol without NVLink peers: n library instances of ONE
+ * process on ONE device, kvs[r] = rank r of world n (bf16, same shape), get n windows in
+ * ordinary device memory (cudaMalloc) cross-linked as each other's peers; the ranks'
+ * niyama_attention_gather launches must then run CONCURRENTLY (one stream per rank) — a
+ * launch's last CTA waits for the others'.  Destroy each with niyama_gather_destroy. */
+niyama_status niyama_debug_gather_group(niyama_kv* const* kvs, int32_t n, int32_t max_rows, niyama_gather** outs);
 
 /* a8 — iteration-time predictor (P:205 ④ "A lightweight predictor is then used
  * to estimate the latency of the batch"; reading R16).  The paper's

@@ -139,6 +139,10 @@ def _load():
         "niyama_comm_init": ([vp, vp], st),
         "niyama_get_unique_id": ([vp], st),
         "niyama_allgather_heads": ([vp, vp, vp, vp, vp], st),
+        "niyama_gather_create": ([vp, i32, C.POINTER(vp)], st),
+        "niyama_gather_destroy": ([vp], st),
+        "niyama_debug_gather_group": ([C.POINTER(vp), i32, i32, C.POINTER(vp)], st),
+        "niyama_attention_gather": ([vp, vp, i32, vp, vp, vp, vp, C.c_float, C.POINTER(vp), C.POINTER(vp), vp], st),
         "niyama_predictor_fit": ([C.POINTER(KVConfig), C.POINTER(SampleC), i32, C.POINTER(vp)], st),
         "niyama_predictor_fit_batches": ([C.POINTER(KVConfig), C.POINTER(BatchDescC), C.POINTER(C.c_double), i32,
                                           C.POINTER(FitOptionsC), C.POINTER(vp)], st),
@@ -358,11 +362,39 @@ class KVCache:
     def allgather_heads(self, plan: Plan, o_full, lse_full=None, stream=None):
         _check(lib.niyama_allgather_heads(self.handle, plan.handle, _ptr(o_full), _ptr(lse_full), _stream(stream)))
 
+    def gather_window(self, max_rows: int) -> "GatherWindow":
+        """§8(f)2: the symmetric output window of the fused all-gather (collective: every rank)."""
+        h = C.c_void_p()
+        _check(lib.niyama_gather_create(self.handle, int(max_rows), C.byref(h)))
+        w = GatherWindow(self, h.value)
+        if not hasattr(self, "_windows"):
+            import weakref
+            self._windows = weakref.WeakSet()
+        self._windows.add(w)
+        return w
+
+    def attention_gather(self, plan: Plan, layer: int, q, window: "GatherWindow", k_new=None, v_new=None,
+                         scale: float = 0.0, stream=None):
+        """Append (optional) + attention + head all-gather in ONE launch (niyama_attention_gather).
+        Returns torch views (o_full [Hq_all][T][d] bf16, lse_full [Hq_all][T] f32) of the window
+        buffer the launch fills; valid until the call after next."""
+        o = C.c_void_p()
+        lse = C.c_void_p()
+        _check(lib.niyama_attention_gather(self.handle, plan.handle, layer, _ptr(k_new), _ptr(v_new), _ptr(q),
+                                           window.handle, float(scale), C.byref(o), C.byref(lse), _stream(stream)))
+        T = plan.info().num_rows
+        hq = self.cfg.num_q_heads   # global head count (every rank's heads are in the window)
+        return (_device_view(o.value, (hq, T, self.cfg.head_dim), "<V2", self.cfg.device),
+                _device_view(lse.value, (hq, T), "<f4", self.cfg.device))
+
     def close(self):
         if getattr(self, "handle", None):
-            # a plan's buffers come from this cache's memory pool: destroy live plans first
+            # a plan's buffers come from this cache's memory pool: destroy live plans first;
+            # gather windows use the communicator the cache owns
             for plan in list(getattr(self, "_plans", ())):
                 plan.close()
+            for w in list(getattr(self, "_windows", ())):
+                w.close()
             lib.niyama_kv_destroy(self.handle)
             self.handle = None
 
@@ -371,6 +403,55 @@ class KVCache:
             self.close()
         except Exception:
             pass
+
+
+class GatherWindow:
+    """niyama_gather: NCCL symmetric window holding the fused all-gather's outputs."""
+
+    def __init__(self, kv: KVCache, handle: int):
+        self.kv = kv
+        self.handle = handle
+
+    def close(self):
+        if self.handle:
+            h, self.handle = self.handle, None
+            _check(lib.niyama_gather_destroy(h))
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def debug_gather_group(kvs, max_rows: int):
+    """niyama_debug_gather_group: windows of n one-device ranks (kvs[r] = rank r of world n)
+    cross-linked as peers (tests of the multi-rank protocol on one GPU)."""
+    n = len(kvs)
+    hs = (C.c_void_p * n)(*[kv.handle for kv in kvs])
+    outs = (C.c_void_p * n)()
+    _check(lib.niyama_debug_gather_group(hs, n, int(max_rows), outs))
+    ws = [GatherWindow(kv, outs[r]) for r, kv in enumerate(kvs)]
+    for kv, w in zip(kvs, ws):
+        if not hasattr(kv, "_windows"):
+            import weakref
+            kv._windows = weakref.WeakSet()
+        kv._windows.add(w)
+    return ws
+
+
+class _CudaArray:
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _device_view(ptr, shape, typestr, device):
+    """A torch tensor aliasing library-owned device memory (no copy)."""
+    import torch
+    if typestr == "<V2":  # bf16: viewed through int16 (no bf16 typestr in the interface)
+        return torch.as_tensor(_CudaArray(ptr, shape, "<i2"), device=f"cuda:{device}").view(torch.bfloat16)
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=f"cuda:{device}")
 
 
 def get_unique_id() -> bytes:

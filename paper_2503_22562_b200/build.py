@@ -2,8 +2,9 @@
 
     python paper_2503_22562_b200/build.py [--force]     (or __graft_entry__.build())
 
-kernels.cu is compiled by nvcc with -gencode arch=compute_100a,code=sm_100a
--lineinfo; runtime.cpp by the host compiler; the shared library links the
+kernels.cu (and gather.cu, the NCCL device-API unit) are compiled by nvcc with
+-gencode arch=compute_100a,code=sm_100a -lineinfo; runtime.cpp, sched.cpp and
+predictor.cpp by the host compiler; the shared library links the
 static CUDA runtime and the NCCL that torch loads (site-packages/nvidia/nccl,
 2.28.x) so a process never holds two NCCLs.
 """
@@ -55,15 +56,20 @@ def build(force: bool = False) -> str:
     s_obj = os.path.join(BUILD, "sched.o")
     p_src = os.path.join(CSRC, "predictor.cpp")
     p_obj = os.path.join(BUILD, "predictor.o")
+    g_src = os.path.join(CSRC, "gather.cu")
+    g_obj = os.path.join(BUILD, "gather.o")
     common = ["-O3", "-std=c++17", "-I", INCLUDE, "-I", CSRC]
     if force or _stale(k_obj, [k_src] + headers):
         _run([NVCC, *ARCH, *common, "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC", "-c", k_src, "-o", k_obj])
+    if force or _stale(g_obj, [g_src] + headers):
+        _run([NVCC, *ARCH, *common, "-I", nccl_inc, "-Xcompiler", "-fPIC", "-c", g_src, "-o", g_obj])
     for src, obj in ((r_src, r_obj), (s_src, s_obj), (p_src, p_obj)):
         if force or _stale(obj, [src] + headers):
             _run([os.environ.get("CXX", "g++"), *common, "-I", os.path.join(CUDA, "include"), "-I", nccl_inc, "-fPIC",
                   "-Wall", "-Wextra", "-Wno-unused-parameter", "-c", src, "-o", obj])
-    if force or _stale(LIB, [k_obj, r_obj, s_obj, p_obj]):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, k_obj, r_obj, s_obj, p_obj, "-lpthread", "-L", nccl_lib,
+    if force or _stale(LIB, [k_obj, g_obj, r_obj, s_obj, p_obj]):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB, k_obj, g_obj, r_obj, s_obj, p_obj, "-lpthread",
+              "-L", nccl_lib,
               "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "--no-undefined"])
     return LIB
 

@@ -9,10 +9,14 @@
 
 #include "niyama.h"
 
+struct ncclWindow_vidmem;  // nccl.h: typedef ncclWindow_vidmem* ncclWindow_t
+
 namespace niyama {
 
 // Sets niyama_last_error() for this thread and returns s (host translation units).
 niyama_status set_error(niyama_status s, const char* msg);
+
+constexpr int kMaxGatherRanks = 8;  // §8(f)2: the ranks of one NVLink node
 
 // ---- shared by the planner (runtime.cpp) and the predictor (predictor.cpp, a8), which
 // models the same launch: one definition of every launch-shaping rule.
@@ -252,6 +256,16 @@ struct AttnParams {
   // (append_total > 0 pieces, claimed through work[4], completion counted in work[5])
   AppendParams ap;
   int32_t append_total;
+  // §8(f)2 fused all-gather: n > 0 stores every O / LSE value at (address + delta[r]) for
+  // each rank r (delta = rank r's window mapping - this rank's window base), then the
+  // last CTA publishes `epoch` into flags[rank] of every rank and waits for all n flags.
+  struct Gather {
+    int32_t n;          // ranks (0 = plain stores to o / lse)
+    int32_t rank;
+    uint32_t epoch;     // launches of this gather object, this one included (monotonic)
+    uint32_t* flags;    // this rank's flag array [n] (window mapping)
+    int64_t delta[kMaxGatherRanks];
+  } gx;
 };
 
 
@@ -263,6 +277,9 @@ cudaError_t launch_gather(const uint8_t* pool_k, const uint8_t* pool_v, const in
 cudaError_t configure_attention_bf16();  // per-device smem opt-in (current device)
 cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s);
 cudaError_t launch_attention_generic_f32(const AttnParams& p, cudaStream_t s);
+// §8(f)2 (gather.cu, the one unit built against nccl_device.h): this process's address of
+// every rank's copy of a symmetric window (offset 0), via the window's LSA mapping; blocking.
+cudaError_t gather_resolve_peers(ncclWindow_vidmem* win, int world, uint64_t* host_out);
 int attention_bf16_smem_bytes();
 
 }  // namespace niyama

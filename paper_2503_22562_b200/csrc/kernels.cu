@@ -299,6 +299,55 @@ constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 0);  // both operands K-major
 }  // namespace fa
 
+// ------------------------------------------------------- output stores (§8(f)2)
+// Every O / LSE value of the launch goes through put_out.  Plain launch (gx.n == 0): one
+// store.  Fused all-gather: the same value at the same window offset on every rank (peer
+// mappings through NVLink; the own rank through its window mapping too), so the kernel's
+// epilogues ARE the all-gather.
+template <typename V>
+__device__ __forceinline__ void put_out(const AttnParams& p, void* dst, const V& v) {
+  if (p.gx.n == 0) {
+    *reinterpret_cast<V*>(dst) = v;
+    return;
+  }
+#pragma unroll 1
+  for (int r = 0; r < p.gx.n; ++r) *reinterpret_cast<V*>(static_cast<uint8_t*>(dst) + p.gx.delta[r]) = v;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* ptr) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* ptr, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(ptr), "r"(v) : "memory");
+}
+
+// The launch's last CTA: publish this launch's epoch to every rank's flag slot `rank`, then
+// wait until every rank published it here.  Ordering (PTX memory model, causality is
+// transitive): each CTA's output stores -> its fence.acq_rel.gpu + done count (observed by
+// this CTA at gpu scope) -> this fence.acq_rel.sys + st.release.sys flag -> the peer's
+// ld.acquire.sys.  A system-scope fence in every CTA instead measured +4 us per launch
+// (config 2 at world 1: 100.4 vs 96.3 us).  Monotonic epochs, no reset.
+// ~30 s without a peer = trap (a rank that never launches), never a silent hang.
+__device__ __forceinline__ void gather_barrier(const AttnParams& p) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int r = 0; r < p.gx.n; ++r)
+    st_release_sys_u32(reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(p.gx.flags + p.gx.rank) + p.gx.delta[r]),
+                       p.gx.epoch);
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int r = 0; r < p.gx.n; ++r) {
+    while (static_cast<int32_t>(ld_acquire_sys_u32(p.gx.flags + r) - p.gx.epoch) < 0) {
+      __nanosleep(64);
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 30ull * 1000000000ull) __trap();
+    }
+  }
+}
+
 // -------------------------------------------------------------- prefill tile
 // Debug event log (niyama_debug_trace): CTA 0's first item, key tiles < 64, clock64 per role.
 __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
@@ -381,8 +430,8 @@ __device__ __forceinline__ void prefill_merge(const AttnParams& p, const TileDes
     uint2 w2;
     w2.x = pack_bf16(acc.x * inv, acc.y * inv);
     w2.y = pack_bf16(acc.z * inv, acc.w * inv);
-    *reinterpret_cast<uint2*>(static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD + c4 * 4) * 2) = w2;
-    if (c4 == 0 && p.lse != nullptr) p.lse[static_cast<int64_t>(h) * p.T + trow] = (M + __log2f(L)) * 0.69314718055994530942f;
+    put_out(p, static_cast<uint8_t*>(p.o) + ((static_cast<int64_t>(h) * p.T + trow) * kD + c4 * 4) * 2, w2);
+    if (c4 == 0 && p.lse != nullptr) put_out(p, p.lse + static_cast<int64_t>(h) * p.T + trow, (M + __log2f(L)) * 0.69314718055994530942f);
   }
 }
 
@@ -706,12 +755,12 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
           w.y = pack_bf16(__uint_as_float(ov[e + 2]) * inv_l, __uint_as_float(ov[e + 3]) * inv_l);
           w.z = pack_bf16(__uint_as_float(ov[e + 4]) * inv_l, __uint_as_float(ov[e + 5]) * inv_l);
           w.w = pack_bf16(__uint_as_float(ov[e + 6]) * inv_l, __uint_as_float(ov[e + 7]) * inv_l);
-          *reinterpret_cast<uint4*>(orow + (c * 32 + e) * 2) = w;
+          put_out(p, orow + (c * 32 + e) * 2, w);
         }
       }
     }
     if (set == 0 && valid && p.lse != nullptr)
-      p.lse[static_cast<int64_t>(h) * p.T + trow] = (m_ref + __log2f(l)) * 0.69314718055994530942f;
+      put_out(p, p.lse + static_cast<int64_t>(h) * p.T + trow, (m_ref + __log2f(l)) * 0.69314718055994530942f);
     }
   }
   kv_it += n;
@@ -1118,13 +1167,13 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         const uint32_t lo = movmatrix_trans(pack_bf16(o[md][0] * invA, o[md][1] * invB));
         const uint32_t hi = movmatrix_trans(pack_bf16(o[md][2] * invA, o[md][3] * invB));
         if (gid < g) {
-          *reinterpret_cast<uint32_t*>(orow + 16 * md + 2 * tig) = lo;
-          *reinterpret_cast<uint32_t*>(orow + 16 * md + 8 + 2 * tig) = hi;
+          put_out(p, orow + 16 * md + 2 * tig, lo);
+          put_out(p, orow + 16 * md + 8 + 2 * tig, hi);
         }
       }
       if (gid == 0 && p.lse != nullptr) {
-        if (hA < g) p.lse[static_cast<int64_t>(u.kvh * g + hA) * p.T + u.row] = (m + __log2f(l)) * 0.69314718055994530942f;
-        if (hB < g) p.lse[static_cast<int64_t>(u.kvh * g + hB) * p.T + u.row] = (mB + __log2f(lB)) * 0.69314718055994530942f;
+        if (hA < g) put_out(p, p.lse + static_cast<int64_t>(u.kvh * g + hA) * p.T + u.row, (m + __log2f(l)) * 0.69314718055994530942f);
+        if (hB < g) put_out(p, p.lse + static_cast<int64_t>(u.kvh * g + hB) * p.T + u.row, (mB + __log2f(lB)) * 0.69314718055994530942f);
       }
     } else {
       float* poA = p.part_o + (static_cast<int64_t>(u.id) * g + hA) * kD;
@@ -1222,9 +1271,9 @@ __device__ __forceinline__ void merge_tail(const AttnParams& p) {
       uint2 w2;
       w2.x = pack_bf16(acc.x * inv, acc.y * inv);
       w2.y = pack_bf16(acc.z * inv, acc.w * inv);
-      *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
+      put_out(p, orow + lane * 4, w2);
       if (lane == 0 && p.lse != nullptr)
-        p.lse[static_cast<int64_t>(h) * p.T + rec.row] = (M + __log2f(L)) * 0.69314718055994530942f;
+        put_out(p, p.lse + static_cast<int64_t>(h) * p.T + rec.row, (M + __log2f(L)) * 0.69314718055994530942f);
       continue;
     }
     float M = -INFINITY;
@@ -1266,9 +1315,9 @@ __device__ __forceinline__ void merge_tail(const AttnParams& p) {
     uint2 w2;
     w2.x = pack_bf16(acc.x * inv, acc.y * inv);
     w2.y = pack_bf16(acc.z * inv, acc.w * inv);
-    *reinterpret_cast<uint2*>(orow + lane * 4) = w2;
+    put_out(p, orow + lane * 4, w2);
     if (lane == 0 && p.lse != nullptr)
-      p.lse[static_cast<int64_t>(h) * p.T + rec.row] = (M + __log2f(L)) * 0.69314718055994530942f;
+      put_out(p, p.lse + static_cast<int64_t>(h) * p.T + rec.row, (M + __log2f(L)) * 0.69314718055994530942f);
   }
 }
 
@@ -1610,9 +1659,9 @@ __device__ __forceinline__ void decode_cta_v2(const AttnParams& p, uint32_t sbas
           if (h < g) {
             __nv_bfloat16* orow = static_cast<__nv_bfloat16*>(p.o) +
                                   (static_cast<int64_t>(d.kvh * g + h) * p.T + d.row) * kD;
-            orow[r] = __float2bfloat16_rn(__uint_as_float(ov[h]) / lh[h]);
+            put_out(p, orow + r, __float2bfloat16_rn(__uint_as_float(ov[h]) / lh[h]));
             if (r == 0 && p.lse != nullptr)
-              p.lse[static_cast<int64_t>(d.kvh * g + h) * p.T + d.row] = (mh[h] + __log2f(lh[h])) * 0.69314718055994530942f;
+              put_out(p, p.lse + static_cast<int64_t>(d.kvh * g + h) * p.T + d.row, (mh[h] + __log2f(lh[h])) * 0.69314718055994530942f);
           }
         }
       } else {
@@ -1765,7 +1814,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
   }
-  if (tid == 0) {
+  if (tid == 0) {  // (the __syncthreads above ordered every thread's output stores before this fence)
     __threadfence();
     const int done = atomicAdd(p.work + 2, 1);
     if (done == static_cast<int>(gridDim.x) - 1) {  // last CTA: reset the queues for the next launch
@@ -1776,6 +1825,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
       p.work[4] = 0;
       p.work[5] = 0;
       __threadfence();
+      if (p.gx.n > 0) gather_barrier(p);
     }
   }
 }

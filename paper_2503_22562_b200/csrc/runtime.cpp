@@ -906,7 +906,8 @@ int64_t append_pieces(const AppendParams& p) {
 }
 
 niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q, void* o, float* lse,
-                             float softmax_scale, niyama_stream stream, const AppendParams* ap);
+                             float softmax_scale, niyama_stream stream, const AppendParams* ap,
+                             const AttnParams::Gather* gx = nullptr);
 }  // namespace
 
 extern "C" niyama_status niyama_kv_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* k_new,
@@ -952,7 +953,8 @@ extern "C" niyama_status niyama_hybrid_attention(niyama_kv* kv, const niyama_pla
 
 namespace {
 niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t layer, const void* q, void* o, float* lse,
-                             float softmax_scale, niyama_stream stream, const AppendParams* ap) {
+                             float softmax_scale, niyama_stream stream, const AppendParams* ap,
+                             const AttnParams::Gather* gx) {
   if (!q || !o) return fail(NIYAMA_EINVAL, "q/o is NULL");
   if ((reinterpret_cast<uintptr_t>(q) | reinterpret_cast<uintptr_t>(o)) & 15)
     return fail(NIYAMA_EINVAL, "q/o must be 16-byte aligned");
@@ -1005,6 +1007,7 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
     p.ap = *ap;
     p.append_total = static_cast<int32_t>(append_pieces(*ap));
   }
+  if (gx) p.gx = *gx;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   DeviceGuard dg(kv->cfg.device);
   NY_CUDA(dg.err);
@@ -1096,6 +1099,190 @@ extern "C" niyama_status niyama_allgather_heads(niyama_kv* kv, const niyama_plan
   r = ncclGroupEnd();
   if (first == ncclSuccess) first = r;
   if (first != ncclSuccess) return fail(NIYAMA_ENCCL, std::string("all-gather: ") + ncclGetErrorString(first));
+  return NIYAMA_OK;
+}
+
+// ================================================ §8(f)2 fused all-gather window
+// One NCCL symmetric window per gather object: [buffer 0 | buffer 1 | flags], each buffer
+// o_full [Hq_all][max_rows][d] bf16 then lse_full [Hq_all][max_rows] f32, 4 KB aligned.
+struct niyama_gather {
+  niyama_kv* kv = nullptr;
+  uint8_t* base = nullptr;
+  size_t bytes = 0, o_bytes = 0, buf_bytes = 0, flags_off = 0;
+  ncclWindow_t win = nullptr;
+  int32_t max_rows = 0;
+  uint32_t epoch = 0;
+  bool nccl_owned = true;  // false: niyama_debug_gather_group (cudaMalloc, one process)
+  AttnParams::Gather gx{};
+};
+
+namespace {
+size_t align4k(size_t x) { return (x + 4095) & ~static_cast<size_t>(4095); }
+
+void gather_release(niyama_gather* g) {
+  if (g->win) ncclCommWindowDeregister(g->kv->comm, g->win);
+  if (g->base) {
+    if (g->nccl_owned)
+      ncclMemFree(g->base);
+    else
+      cudaFree(g->base);
+  }
+  delete g;
+}
+
+niyama_gather* gather_layout(niyama_kv* kv, int32_t max_rows) {
+  auto* g = new niyama_gather;
+  g->kv = kv;
+  g->max_rows = max_rows;
+  const size_t rows_all = static_cast<size_t>(kv->hq) * kv->cfg.world_size * max_rows;
+  g->o_bytes = align4k(rows_all * kv->d * 2);
+  g->buf_bytes = g->o_bytes + align4k(rows_all * sizeof(float));
+  g->flags_off = 2 * g->buf_bytes;
+  g->bytes = g->flags_off + 4096;
+  return g;
+}
+
+niyama_status gather_check(niyama_kv* kv, int32_t max_rows) {
+  if (!kv->has_device) return fail(NIYAMA_EUNSUPPORTED, "no device");
+  if (kv->cfg.dtype != NIYAMA_BF16) return fail(NIYAMA_EINVAL, "the fused all-gather needs a bf16 pool");
+  if (max_rows <= 0) return fail(NIYAMA_EINVAL, "max_rows must be > 0");
+  if (kv->cfg.world_size > kMaxGatherRanks) return fail(NIYAMA_EUNSUPPORTED, "more ranks than one NVLink node (8)");
+  return NIYAMA_OK;
+}
+}  // namespace
+
+extern "C" niyama_status niyama_gather_create(niyama_kv* kv, int32_t max_rows, niyama_gather** out) {
+  if (!kv || !out) return fail(NIYAMA_EINVAL, "kv/out is NULL");
+  *out = nullptr;
+  if (!kv->comm) return fail(NIYAMA_EINVAL, "niyama_comm_init was not called");
+  niyama_status st = gather_check(kv, max_rows);
+  if (st != NIYAMA_OK) return st;
+  const int world = kv->cfg.world_size;
+  DeviceGuard dg(kv->cfg.device);
+  NY_CUDA(dg.err);
+  niyama_gather* g = gather_layout(kv, max_rows);
+  void* base = nullptr;
+  ncclResult_t r = ncclMemAlloc(&base, g->bytes);
+  if (r != ncclSuccess) {
+    delete g;
+    return fail(NIYAMA_EUNSUPPORTED, std::string("ncclMemAlloc: ") + ncclGetErrorString(r));
+  }
+  g->base = static_cast<uint8_t*>(base);
+  // zeroed (flags at epoch 0) and complete before this rank joins the collective
+  // registration, so no peer's first launch can meet an uninitialised flag
+  cudaError_t ce = cudaMemset(g->base, 0, g->bytes);
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    gather_release(g);
+    return fail(NIYAMA_ECUDA, std::string("window init: ") + cudaGetErrorString(ce));
+  }
+  r = ncclCommWindowRegister(kv->comm, g->base, g->bytes, &g->win, NCCL_WIN_COLL_SYMMETRIC);
+  if (r != ncclSuccess || !g->win) {
+    g->win = nullptr;
+    gather_release(g);
+    return fail(NIYAMA_EUNSUPPORTED, std::string("ncclCommWindowRegister: ") + ncclGetErrorString(r));
+  }
+  uint64_t peers[kMaxGatherRanks] = {};
+  ce = gather_resolve_peers(g->win, world, peers);
+  if (ce != cudaSuccess) {
+    gather_release(g);
+    return fail(NIYAMA_ECUDA, std::string("window peer mapping: ") + cudaGetErrorString(ce));
+  }
+  for (int i = 0; i < world; ++i) {
+    if (peers[i] == 0) {
+      gather_release(g);
+      return fail(NIYAMA_EUNSUPPORTED, "the window has no load/store mapping of rank " + std::to_string(i));
+    }
+    g->gx.delta[i] = static_cast<int64_t>(peers[i] - reinterpret_cast<uint64_t>(g->base));
+  }
+  g->gx.n = world;
+  g->gx.rank = kv->cfg.rank;
+  g->gx.flags = reinterpret_cast<uint32_t*>(g->base + g->flags_off);
+  *out = g;
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_debug_gather_group(niyama_kv* const* kvs, int32_t n, int32_t max_rows,
+                                                   niyama_gather** outs) {
+  if (!kvs || !outs || n < 1 || n > kMaxGatherRanks) return fail(NIYAMA_EINVAL, "kvs/outs NULL or n out of [1, 8]");
+  for (int32_t r = 0; r < n; ++r) {
+    outs[r] = nullptr;
+    if (!kvs[r]) return fail(NIYAMA_EINVAL, "kvs[r] is NULL");
+    niyama_status st = gather_check(kvs[r], max_rows);
+    if (st != NIYAMA_OK) return st;
+    if (kvs[r]->cfg.world_size != n || kvs[r]->cfg.rank != r || kvs[r]->cfg.device != kvs[0]->cfg.device ||
+        kvs[r]->hq != kvs[0]->hq || kvs[r]->d != kvs[0]->d)
+      return fail(NIYAMA_EINVAL, "kvs[r] must be rank r of world n, one device, one shape");
+  }
+  DeviceGuard dg(kvs[0]->cfg.device);
+  NY_CUDA(dg.err);
+  niyama_gather* gs[kMaxGatherRanks] = {};
+  cudaError_t ce = cudaSuccess;
+  for (int32_t r = 0; r < n && ce == cudaSuccess; ++r) {
+    gs[r] = gather_layout(kvs[r], max_rows);
+    gs[r]->nccl_owned = false;
+    void* base = nullptr;
+    ce = cudaMalloc(&base, gs[r]->bytes);
+    gs[r]->base = static_cast<uint8_t*>(base);
+    if (ce == cudaSuccess) ce = cudaMemset(base, 0, gs[r]->bytes);
+  }
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    for (int32_t r = 0; r < n; ++r)
+      if (gs[r]) gather_release(gs[r]);
+    return fail(NIYAMA_ECUDA, std::string("debug gather group: ") + cudaGetErrorString(ce));
+  }
+  for (int32_t r = 0; r < n; ++r) {
+    for (int32_t i = 0; i < n; ++i)
+      gs[r]->gx.delta[i] = reinterpret_cast<intptr_t>(gs[i]->base) - reinterpret_cast<intptr_t>(gs[r]->base);
+    gs[r]->gx.n = n;
+    gs[r]->gx.rank = r;
+    gs[r]->gx.flags = reinterpret_cast<uint32_t*>(gs[r]->base + gs[r]->flags_off);
+    outs[r] = gs[r];
+  }
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_gather_destroy(niyama_gather* g) {
+  if (!g) return NIYAMA_OK;
+  DeviceGuard dg(g->kv->cfg.device);
+  NY_CUDA(dg.err);
+  const cudaError_t ce = cudaDeviceSynchronize();
+  gather_release(g);
+  if (ce != cudaSuccess) return fail(NIYAMA_ECUDA, std::string("gather destroy: ") + cudaGetErrorString(ce));
+  return NIYAMA_OK;
+}
+
+extern "C" niyama_status niyama_attention_gather(niyama_kv* kv, const niyama_plan* plan, int32_t layer,
+                                                 const void* k_new, const void* v_new, const void* q,
+                                                 niyama_gather* g, float softmax_scale, void** o_full,
+                                                 float** lse_full, niyama_stream stream) {
+  niyama_status st = check_launch(kv, plan, layer);
+  if (st != NIYAMA_OK) return st;
+  if (!g || !o_full || !lse_full) return fail(NIYAMA_EINVAL, "gather/o_full/lse_full is NULL");
+  if (g->kv != kv) return fail(NIYAMA_EINVAL, "the gather window belongs to another niyama_kv");
+  if (plan->T > g->max_rows) return fail(NIYAMA_EINVAL, "plan rows exceed the window's max_rows");
+  if ((k_new == nullptr) != (v_new == nullptr)) return fail(NIYAMA_EINVAL, "k_new and v_new: both or neither");
+  AppendParams ap{};
+  if (k_new) {
+    st = fill_append(kv, plan, layer, k_new, v_new, ap);
+    if (st != NIYAMA_OK) return st;
+    if (append_pieces(ap) >= (int64_t(1) << 31)) return fail(NIYAMA_EINVAL, "append: too many pieces");
+  }
+  const uint32_t epoch = g->epoch + 1;
+  uint8_t* buf = g->base + (epoch & 1) * g->buf_bytes;
+  const int64_t T = plan->T;
+  uint8_t* o = buf + static_cast<int64_t>(kv->cfg.rank) * kv->hq * T * kv->d * 2;
+  float* lse = reinterpret_cast<float*>(buf + g->o_bytes) + static_cast<int64_t>(kv->cfg.rank) * kv->hq * T;
+  if (T > 0) {
+    AttnParams::Gather gx = g->gx;
+    gx.epoch = epoch;
+    st = attention_impl(kv, plan, layer, q, o, lse, softmax_scale, stream, k_new ? &ap : nullptr, &gx);
+    if (st != NIYAMA_OK) return st;
+    g->epoch = epoch;
+  }
+  *o_full = buf;
+  *lse_full = reinterpret_cast<float*>(buf + g->o_bytes);
   return NIYAMA_OK;
 }
 

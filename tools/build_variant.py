@@ -26,8 +26,9 @@ def main():
     nccl_inc, nccl_lib = B.nccl_dirs()
     subprocess.run([B.NVCC, *B.ARCH, "-O3", "-std=c++17", "-I", B.INCLUDE, "-I", B.CSRC, "-lineinfo", *defs,
                     "-Xcompiler", "-fPIC", "-c", os.path.join(B.CSRC, "kernels.cu"), "-o", k_obj], check=True)
-    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, k_obj,
-                    os.path.join(B.BUILD, "runtime.o"), "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker",
+    objs = [os.path.join(B.BUILD, f"{n}.o") for n in ("gather", "runtime", "sched", "predictor")]
+    subprocess.run([B.NVCC, *B.ARCH, "-shared", "-cudart", "static", "-o", lib, k_obj, *objs, "-lpthread",
+                    "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker",
                     f"-rpath,{nccl_lib}", "-Xlinker", "--no-undefined"], check=True)
     print(lib)
 
