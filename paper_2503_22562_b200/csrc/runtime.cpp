@@ -1154,9 +1154,9 @@ niyama_status gather_check(niyama_kv* kv, int32_t max_rows) {
 extern "C" niyama_status niyama_gather_create(niyama_kv* kv, int32_t max_rows, niyama_gather** out) {
   if (!kv || !out) return fail(NIYAMA_EINVAL, "kv/out is NULL");
   *out = nullptr;
-  if (!kv->comm) return fail(NIYAMA_EINVAL, "niyama_comm_init was not called");
   niyama_status st = gather_check(kv, max_rows);
   if (st != NIYAMA_OK) return st;
+  if (!kv->comm) return fail(NIYAMA_EINVAL, "niyama_comm_init was not called");
   const int world = kv->cfg.world_size;
   DeviceGuard dg(kv->cfg.device);
   NY_CUDA(dg.err);

@@ -494,3 +494,23 @@ def test_iteration_predictor_closed_form_and_committed_fit():
     err = np.abs([p2.predict(desc(r)) / r["seconds"] - 1 for r in held])
     assert float(err.max()) == pytest.approx(fj["errors"]["analytic"]["heldout"]["max"], rel=1e-9)
     assert float(err.max()) <= 0.05 and len(held) >= 30
+
+
+def test_gather_window_host_validation():
+    """§8(f)2 entry points validate before touching a device: no device -> EUNSUPPORTED;
+    the one-process group checks rank/world/shape consistency (EINVAL)."""
+    import paper_2503_22562_b200 as ny
+    kv = ny.KVCache(1, 8, 2, 128, 16, dtype="bf16", device=None)
+    with pytest.raises(ny.NiyamaError) as e:
+        kv.gather_window(16)
+    assert e.value.status == 7
+    ranks = [ny.KVCache(1, 8, 2, 128, 16, dtype="bf16", world_size=2, rank=r, device=None) for r in range(2)]
+    with pytest.raises(ny.NiyamaError) as e:
+        ny.debug_gather_group(ranks, 16)
+    assert e.value.status == 7
+    with pytest.raises(ny.NiyamaError) as e:
+        ny.debug_gather_group(ranks[::-1], 16)     # kvs[r] must be rank r (checked after the device check)
+    assert e.value.status in (1, 7)
+    with pytest.raises(ny.NiyamaError) as e:
+        ny.debug_gather_group([], 16)
+    assert e.value.status == 1
