@@ -211,6 +211,9 @@ constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 #ifndef NIYAMA_V_STAGES
 #define NIYAMA_V_STAGES 2
 #endif
+#ifndef NIYAMA_DIAG_HALF_KV
+#define NIYAMA_DIAG_HALF_KV 0
+#endif
 constexpr int kKStages = NIYAMA_K_STAGES;  // K tile ring depth
 constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
 #ifndef NIYAMA_Q_TMEM
@@ -221,7 +224,17 @@ constexpr int kVStages = NIYAMA_V_STAGES;  // V^T tile ring depth
 // PV(j) to complete, putting two MMA-burst latencies (~0.7 K cycles each) and a softmax
 // into every two steps (L70B prefill-only 556 -> 440 us with three).
 constexpr bool kQTmem = NIYAMA_Q_TMEM != 0;
-constexpr int kSBufs = kQTmem ? 2 : 3;     // S (then P) TMEM buffers: columns [128 b, 128 b + 128)
+// P in TMEM columns of its own (default): S [2][128 cols] | P [2][64 cols of bf16 pairs] | O.
+// An S buffer is free for QK_{j+2} as soon as the softmax of step j has LOADED it, not when
+// PV_j has consumed P (the S-buffer cycle QK -> softmax -> PV -> QK was the prefill step's
+// critical loop: ~5 K cycles per 3 steps, tools/trace.py).  0 = P over the consumed S
+// columns with three S buffers (QK_{j+3} waits for PV_j).
+#ifndef NIYAMA_P_SEPARATE
+#define NIYAMA_P_SEPARATE 1
+#endif
+constexpr bool kPSep = NIYAMA_P_SEPARATE != 0;
+static_assert(!(kPSep && kQTmem), "Q in TMEM needs the P-over-S layout");
+constexpr int kSBufs = (kQTmem || kPSep) ? 2 : 3;  // S TMEM buffers: columns [128 b, 128 b + 128)
 // Q staging tile (SS only) | K stages | V^T stages | end-of-tile exchange (2 KB; the Q
 // tile's space when Q is staged in shared memory)
 constexpr int kQOff = 0;
@@ -264,8 +277,9 @@ constexpr int kBarVFull = kBarKEmpty + kKStages;   // [kVStages]
 constexpr int kBarVEmpty = kBarVFull + kVStages;   // [kVStages]
 constexpr int kBarSFull = kBarVEmpty + kVStages;   // [kSBufs] QK^T committed into S[b]
 constexpr int kBarPFull = kBarSFull + kSBufs;      // [kSBufs] softmax wrote P over S[b] (128 arrivals)
-constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from S[b] committed (S[b] free, O includes it)
-constexpr int kBarDec = kBarODone + kSBufs;        // [kDecSlots] decode ring stages
+constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from P[b] committed (P[b] free, O includes it)
+constexpr int kBarSFree = kBarODone + kSBufs;      // [kSBufs] kPSep: softmax loaded S[b] (128 arrivals)
+constexpr int kBarDec = kBarSFree + kSBufs;        // [kDecSlots] decode ring stages
 constexpr int kB2Full = kBarDec + kDecSlots;  // [kD2Stages] K/V step landed (tx)
 constexpr int kB2Empty = kB2Full + kD2Stages;  // [kD2Stages] PV of the step done (commit)
 constexpr int kB2SFull = kB2Empty + kD2Stages;  // [2] QK^T committed into S^T[b]
@@ -293,7 +307,9 @@ static_assert(kD2ML + 256 <= kDescBytes, "decode-v2 scratch must fit");
 constexpr int kSmemBytes = 1024 /*align slack*/ + kDataBytes + kBarBytes + kMiscBytes + kDescBytes;
 static_assert(kSmemBytes <= 232448, "exceeds 227 KB of dynamic shared memory");
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kTmemO = 128 * kSBufs;  // O accumulator: 128 columns after the S buffers
+constexpr uint32_t kTmemP = 128 * kSBufs;  // kPSep: P[b] at kTmemP + 64 b
+constexpr uint32_t kTmemO = kPSep ? kTmemP + 128 : 128 * kSBufs;  // O accumulator: 128 columns
+static_assert(kTmemO + 128 <= kTmemCols, "TMEM columns");
 constexpr uint32_t kTmemQ = kTmemO + 128;   // Q (kQTmem): 64 columns of bf16 pairs
 constexpr uint32_t kIdescQK = idesc_bf16_f32(128, kBN, 0, 0);
 constexpr uint32_t kIdescPV = idesc_bf16_f32(128, kD, 0, 0);  // both operands K-major
@@ -502,7 +518,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     // Lane u < 8 owns piece u of every step: K = block u of the step (two 128-byte
     // panels of B rows, at B = 16), V^T = the 16-key sub-block u.  Its block-table
     // lookup for step j+1 is issued before step j's copies, so the lookups of a
-    // step run in parallel and off the critical path; lane 0 arms the barrier.
+    // step run in parallel and off the critical path (a deeper lookahead measured no
+    // change); lane 0 arms the barrier.
     const bool isK = warp == 0;
     const uint8_t* pool = isK ? p.pool_k : p.pool_v;
     const uint32_t ring = sbase + (isK ? kKOff : kVOff);
@@ -531,11 +548,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       if (lane == 0) {
         mbar_wait(bars + 8 * (bar_empty + st), ((k_it / nstg) & 1) ^ 1);
         ev_stamp(ev, isK ? 0 : 1, j);
-        mbar_expect_tx(full, kTile);
+        mbar_expect_tx(full, NIYAMA_DIAG_HALF_KV ? kTile / 2 : kTile);
       }
       __syncwarp();
       const uint32_t dst0 = ring + st * kTile;
-      if (lane < npc) {
+      if (lane < (NIYAMA_DIAG_HALF_KV ? npc / 2 : npc)) {  // (diagnostic: half the bytes, wrong results)
         if (isK) {  // one copy per block: B rows x 256 B, contiguous in pool and tile
           bulk_g2s(dst0 + lane * static_cast<uint32_t>(p.chunk_bytes), pool + cur, static_cast<uint32_t>(p.chunk_bytes),
                    full);
@@ -553,8 +570,8 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       for (int j = j0; j < j1; ++j) {
         const uint32_t k_it = kv_it + (j - j0), gj = it + (j - j0);
         const int st = k_it % kKStages, sb = gj % kSBufs;
-        if (gj >= kSBufs)  // PV_{j-kSBufs} has read its P from S[sb]
-          mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
+        if (gj >= kSBufs)  // S[sb] free: loaded by softmax_{j-2} (kPSep) / PV_{j-3} read its P
+          mbar_wait(bars + 8 * ((kPSep ? kBarSFree : kBarODone) + sb), ((gj - kSBufs) / kSBufs) & 1);
         mbar_wait(bars + 8 * (kBarKFull + st), (k_it / kKStages) & 1);
         tc_fence_after();
         ev_stamp(ev, 2, j);
@@ -588,7 +605,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         // [S[sb] + 8 kk, +8) (TS form), B = the V^T sub-block kk (SW32 K-major)
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk)
-          umma_ts(tmem + kTmemO, tmem + sb * 128 + kk * 8, sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
+          umma_ts(tmem + kTmemO, tmem + (kPSep ? kTmemP + sb * 64 : sb * 128) + kk * 8, sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
                   (j > j0 || kk > 0) ? 1u : 0u);
         umma_commit(bars + 8 * (kBarODone + sb));
         umma_commit(bars + 8 * (kBarVEmpty + st));
@@ -627,6 +644,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       if (tracer) ev_stamp(ev, 4, j);
 #if NIYAMA_DIAG_SKIP_SOFTMAX  // timing diagnostic only: P = S bits, no softmax work (wrong results)
       tc_fence_before();
+      if (kPSep) mbar_arrive(bars + 8 * (kBarSFree + sb));
       mbar_arrive(bars + 8 * (kBarPFull + sb));
       continue;
 #endif
@@ -686,6 +704,10 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       for (int hf = 0; hf < 2; ++hf) {
         uint32_t sr[64];
         tmem_ld64(lane_addr + sb * 128 + hf * 64, sr);
+        if (kPSep && hf == 1) {  // S[sb] fully loaded: QK_{j+2} may overwrite it
+          tc_fence_before();
+          mbar_arrive(bars + 8 * (kBarSFree + sb));
+        }
         if (diag) mask_tail(sr, pos - (kbase + hf * 64));
         // p = 2^(s*scale*log2e - m): one FFMA + one MUFU.EX2 each; P (bf16 pairs, even key
         // in the low half) overwrites the consumed columns [32 hf, 32 hf + 32) of S[sb]
@@ -697,7 +719,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
           if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
           pk[c] = pack_bf16(e0, e1);
         }
-        tmem_st32(lane_addr + sb * 128 + hf * 32, pk);
+        if (kPSep && hf == 0 && gj >= kSBufs) {  // P[sb] free: PV_{j-2} done
+          mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
+          tc_fence_after();
+        }
+        tmem_st32(lane_addr + (kPSep ? kTmemP + sb * 64 : sb * 128) + hf * 32, pk);
       }
       l += sum0 + sum1;
       if (tracer) ev_stamp(ev, 8, j);
@@ -1700,6 +1726,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     for (int b = 0; b < kNumBars; ++b) {
       uint32_t cnt = 1;
       if (b >= kBarPFull && b < kBarPFull + kSBufs) cnt = 128;
+      if (b >= kBarSFree && b < kBarSFree + kSBufs) cnt = 128;
       if ((b >= kB2SFree && b < kB2PFull + 2) || (b >= kB2OFree && b < kB2MLFree + 2)) cnt = 128;
       if (b >= kB2DFree && b < kB2DFree + 4) cnt = 4;  // producer, MMA (after the last QK^T), softmax, epilogue
       mbar_init(bars + 8 * b, cnt);

@@ -83,6 +83,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "l70b":
         run(W.config4_l70b())
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "l70b-prefill":
+        run(W.hybrid(W.L70B, "l70b-prefill-c2048-o6144", prefill_offset=6144, chunk=2048, decode_ctx=[], seed=4))
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "gap":
         gap(W.config2_l8b())
         gap(W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2))
