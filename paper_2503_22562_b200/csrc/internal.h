@@ -76,7 +76,7 @@ inline CtaSplit cta_split(int64_t n_tiles, int64_t n_units, int64_t tile_cost, i
   }
   const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
   const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt *
-                    (g > 4 && decode_path == 0 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
+                    (g > 4 && decode_path != 1 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
   int64_t np = static_cast<int64_t>(std::ceil(r.grid * wp / (wp + wd)));
   // a tile-count floor keeps short-tile prefill off the tail (at most 4 tiles per prefill
   // CTA), itself capped at half the grid: with many long tiles (config 4: 1,024) it would
@@ -100,7 +100,7 @@ inline int32_t prefill_parts_target(int64_t q_tiles, int64_t n_units, int64_t ti
   if (n_units > 0) {
     const double wp = static_cast<double>(tile_cost) * NIYAMA_STEP_BYTES;
     const double wd = static_cast<double>(sum_ctx) * hkv * d * 2.0 * elt *
-                      (g > 4 && decode_path == 0 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
+                      (g > 4 && decode_path != 1 ? NIYAMA_WIDE_GROUP_DECODE_WEIGHT : 1.0);
     target = std::ceil(num_sms * wp / (wp + wd));
   }
   return static_cast<int32_t>(std::max<int64_t>(1, std::min<int64_t>(16, static_cast<int64_t>(target) / q_tiles)));
@@ -116,7 +116,9 @@ inline int32_t rows_per_tile(int g) { return 128 / (g > 0 ? g : 1); }
 inline int decode_warps(int g) { return g <= 4 ? 12 : 8; }
 // Decode streams per CTA as the predictor models them: one pipeline (tensor-core path) or
 // one per decode warp (mma.sync path).
-inline int decode_streams(int g, int decode_path) { return decode_path == 1 ? 1 : decode_warps(g); }
+inline int decode_streams(int g, int decode_path) {
+  return decode_path == 1 ? 1 : decode_path == 2 ? 8 : decode_warps(g);
+}
 
 struct KvModel {
   int hq, hkv, d, elt, num_sms;

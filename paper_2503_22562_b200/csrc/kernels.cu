@@ -23,6 +23,7 @@
 
 #include <cfloat>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -211,6 +212,18 @@ constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 #ifndef NIYAMA_V_STAGES
 #define NIYAMA_V_STAGES 2
 #endif
+// Per-step event stamps (prefill roles, decode stages; tools/trace.py, tools/dec_trace.py):
+// diagnostic builds only (tools/build_variant.py TAG -DNIYAMA_DIAG_STEPS=1).  The per-CTA
+// phase timeline of niyama_debug_trace stays in every build.
+#ifndef NIYAMA_DIAG_STEPS
+#define NIYAMA_DIAG_STEPS 0
+#endif
+#ifndef NIYAMA_DIAG_HANG
+#define NIYAMA_DIAG_HANG 0
+#endif
+#ifndef NIYAMA_DIAG_TILES
+#define NIYAMA_DIAG_TILES 0
+#endif
 #ifndef NIYAMA_DIAG_HALF_KV
 #define NIYAMA_DIAG_HALF_KV 0
 #endif
@@ -280,7 +293,8 @@ constexpr int kBarPFull = kBarSFull + kSBufs;      // [kSBufs] softmax wrote P o
 constexpr int kBarODone = kBarPFull + kSBufs;      // [kSBufs] PV from P[b] committed (P[b] free, O includes it)
 constexpr int kBarSFree = kBarODone + kSBufs;      // [kSBufs] kPSep: softmax loaded S[b] (128 arrivals)
 constexpr int kBarDec = kBarSFree + kSBufs;        // [kDecSlots] decode ring stages
-constexpr int kB2Full = kBarDec + kDecSlots;  // [kD2Stages] K/V step landed (tx)
+constexpr int kBarDecEmpty = kBarDec + kDecSlots;  // [kDecSlots] decode_path 2: consumer done with the stage
+constexpr int kB2Full = kBarDecEmpty + kDecSlots;  // [kD2Stages] K/V step landed (tx)
 constexpr int kB2Empty = kB2Full + kD2Stages;  // [kD2Stages] PV of the step done (commit)
 constexpr int kB2SFull = kB2Empty + kD2Stages;  // [2] QK^T committed into S^T[b]
 constexpr int kB2SFree = kB2SFull + 2;          // [2] softmax loaded S^T[b] (128)
@@ -367,7 +381,7 @@ __device__ __forceinline__ void gather_barrier(const AttnParams& p) {
 // -------------------------------------------------------------- prefill tile
 // Debug event log (niyama_debug_trace): CTA 0's first item, key tiles < 64, clock64 per role.
 __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
-  if (ev != nullptr && j < 64) {
+  if (NIYAMA_DIAG_STEPS && ev != nullptr && j < 64) {
     int64_t c;
     asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
     ev[role * 64 + j] = c;
@@ -469,7 +483,11 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   const int vrows = min(R, t.c - t.t0);
   const int nk = (t.nkeys + kBN - 1) / kBN;   // key steps of the whole q tile
   const int j0 = t.j0, j1 = t.j1, n = j1 - j0;  // this item's steps (split-K part)
+#if NIYAMA_DIAG_TILES  // per-tile stamps instead (main loop): [claim | Q ready | tile end][tile]
+  int64_t* ev = nullptr;
+#else
   int64_t* ev = (p.trace != nullptr && blockIdx.x == 0 && it == 0) ? p.trace + 8 * 160 : nullptr;  // [10][64]
+#endif
 
   // ---- Q tile: rows r = hh*R + i  <-  q[row0 + t0 + i][kvh*g + hh][:]
   if (kQTmem) {  // TMEM lane r, columns [kTmemQ, +64): dims (2c, 2c+1) in column c
@@ -498,20 +516,41 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     __syncthreads();
     tc_fence_after();
   } else {
+    // All of a thread's pieces are loaded before any is stored, so the ~6 loads per
+    // thread are in flight together (one memory latency per tile instead of six: the
+    // serial version took ~10 K cycles per tile, tools/tile_trace.py).
     const uint8_t* q = static_cast<const uint8_t*>(p.q);
-    for (int idx = tid; idx < 128 * 16; idx += kThreads) {
+    constexpr int kQPer = (128 * 16 + kThreads - 1) / kThreads;
+    uint4 qv[kQPer];
+#pragma unroll
+    for (int k = 0; k < kQPer; ++k) {
+      const int idx = tid + k * kThreads;
       const int r = idx >> 4, j = idx & 15;
       const int hh = r / R, i = r - hh * R;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (i < vrows) {
+      qv[k] = make_uint4(0, 0, 0, 0);
+      if (idx < 128 * 16 && i < vrows) {
         const int64_t row = t.row0 + t.t0 + i;
-        v = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
+        qv[k] = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
       }
-      st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), v.x, v.y, v.z, v.w);
+    }
+#pragma unroll
+    for (int k = 0; k < kQPer; ++k) {
+      const int idx = tid + k * kThreads;
+      if (idx >= 128 * 16) break;
+      const int r = idx >> 4, j = idx & 15;
+      st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), qv[k].x, qv[k].y,
+                   qv[k].z, qv[k].w);
     }
     fence_proxy_async_smem();
     __syncthreads();
   }
+#if NIYAMA_DIAG_TILES
+  if (p.trace != nullptr && blockIdx.x == 0 && tid == 0 && p.trace[8 * 160 + 3 * 64] < 64) {
+    int64_t c;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+    p.trace[8 * 160 + 64 + p.trace[8 * 160 + 3 * 64]] = c;
+  }
+#endif
 
   if (warp == 0 || warp == 2) {
     // ---------------- producers: 128-key K tiles (warp 0), V^T tiles (warp 2).
@@ -944,6 +983,7 @@ struct DecodeLoader {
         UnitDesc end{};
         end.id = -1;  // end of stream
         desc_store(descs, k, end);
+        __threadfence_block();  // descriptor before count (decode_path 2: read by another warp)
         count_store(n_desc, ++nd);
         return;
       }
@@ -956,6 +996,7 @@ struct DecodeLoader {
       nst = (cur.k1 - cur.k0 + 15) >> 4;
       nxt_step = 0;
       desc_store(descs, k, cur);
+      __threadfence_block();
       count_store(n_desc, ++nd);
     }
     const uint32_t slot = issued % kDecStages;
@@ -1008,7 +1049,103 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* ptr) {
 
 // Compute side: every lane of the warp.  Split rows write an fp32 partial
 // (m, l, o~) at index `unit id` (fire and forget); unsplit rows write O / LSE.
+// Descriptor k of a consumer warp's ring is published by its producer warp: wait for the
+// count, then order the descriptor loads after it.
+__device__ __forceinline__ void wait_desc(uint32_t n_desc, int k) {
+#ifndef NIYAMA_NO_WATCHDOG
+  uint32_t polls = 0;
+#endif
+  while (count_load(n_desc) <= k) {
+    __nanosleep(32);  // a tight shared-memory spin starves the producer warp on this SMSP
+#ifndef NIYAMA_NO_WATCHDOG
+    if (++polls == (NIYAMA_DIAG_HANG ? (1u << 20) : (1u << 28))) {
+      if (NIYAMA_DIAG_HANG && (threadIdx.x & 31) == 0)
+        printf("consumer cta %d warp %d: waits for desc %d, count %d\n", blockIdx.x, threadIdx.x >> 5, k,
+               count_load(n_desc));
+      __trap();
+    }
+#endif
+  }
+  __threadfence_block();
+}
+
+// decode_path 2: producer warp (lane 0) of consumer warps c0 and c0 + 1.  It runs both
+// consumers' DecodeLoader streams (claims, records, table prefetch, descriptor publishing,
+// one 8 KB bulk copy per stage) and refills a consumer's slot as soon as its empty barrier
+// shows the consumer is done with it — taking the loader's ~30 % of the per-stage cycle off
+// the compute warps (ncu round 2: the lane-0 loader was the largest block of decode stall
+// samples at g = 8, where warps 8-11 had no decode work at all).
 template <int kDecWarpsT, int kDecStages>
+__device__ __forceinline__ void decode_producer(const AttnParams& p, uint32_t sbase, uint32_t bars, uint32_t descs_base,
+                                                uint32_t n_desc_base, int c0) {
+  using namespace fa;
+  DecodeLoader<kDecStages> ld[2];
+  const int dec_first = p.n_tiles > 0 ? p.prefill_ctas : 0;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c = c0 + i;
+    ld[i].s = ld[i].nst = 0;
+    ld[i].nxt_step = 0;
+    ld[i].nxt_id = 0;
+    ld[i].id_base = (static_cast<int>(gridDim.x) - dec_first) * kDecWarpsT;
+    ld[i].reserved = static_cast<int>(blockIdx.x) >= dec_first
+                         ? (static_cast<int>(blockIdx.x) - dec_first) * kDecWarpsT + c
+                         : -1;
+    ld[i].done = false;
+    ld[i].issued = 0;
+    ld[i].phys = 0;
+    ld[i].warm = false;
+    ld[i].ph1 = ld[i].ph2 = 0;
+    ld[i].nd = 0;
+  }
+  auto ring = [&](int i) { return sbase + (c0 + i) * kDecStages * kDecStage; };
+  auto fbar = [&](int i) { return bars + 8 * (kBarDec + (c0 + i) * kDecStages); };
+  auto ebar = [&](int i) { return bars + 8 * (kBarDecEmpty + (c0 + i) * kDecStages); };
+  auto descs = [&](int i) { return descs_base + (c0 + i) * 4 * 32; };
+  auto ndesc = [&](int i) { return n_desc_base + (c0 + i) * 16; };
+  for (int k = 0; k < kDecStages; ++k)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) ld[i].issue_next(p, ring(i), fbar(i), descs(i), ndesc(i));
+  ld[0].warm = ld[1].warm = true;
+#ifndef NIYAMA_NO_WATCHDOG
+  uint32_t idle = 0;
+#endif
+  while (!(ld[0].done && ld[1].done)) {
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (ld[i].done) continue;
+      const uint32_t slot = ld[i].issued % kDecStages;
+      const uint32_t use = ld[i].issued / kDecStages;  // >= 1 here: the initial fill covered use 0
+      if (mbar_test(ebar(i) + 8 * slot, (use - 1) & 1)) {
+        ld[i].issue_next(p, ring(i), fbar(i), descs(i), ndesc(i));
+        any = true;
+      }
+    }
+    if (!any) __nanosleep(20);  // yield the SMSP to the consumer warps while their slots are busy
+#ifndef NIYAMA_NO_WATCHDOG
+    if (any) {
+      idle = 0;
+    } else if (++idle == (NIYAMA_DIAG_HANG ? (1u << 20) : (1u << 28))) {
+#if NIYAMA_DIAG_HANG
+      for (int i = 0; i < 2; ++i) {
+        uint64_t st;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(st) : "r"(ebar(i) + 8 * (ld[i].issued % kDecStages)));
+        printf("producer cta %d c %d: issued %u done %d s %d nst %d nxt_id %d nd %d ebar %llx\n", blockIdx.x, c0 + i,
+               ld[i].issued, ld[i].done, ld[i].s, ld[i].nst, ld[i].nxt_id, ld[i].nd, (unsigned long long)st);
+      }
+#endif
+      __trap();
+    }
+#endif
+  }
+}
+
+// kProd (decode_path 2): this warp only computes; a producer warp (decode_producer) claims its
+// units, publishes their descriptors and issues its stage copies, and the warp hands each
+// consumed stage back through the slot's empty barrier.  Otherwise lane 0 is the warp's own
+// loader (DecodeLoader), interleaved with the compute.
+template <int kDecWarpsT, int kDecStages, bool kProd = false>
 __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t sbase, uint32_t bars,
                                                  uint32_t descs, uint32_t n_desc) {
   using namespace fa;
@@ -1042,18 +1179,20 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
   ld.warm = false;
   ld.ph1 = ld.ph2 = 0;
   ld.nd = 0;
-  if (lane == 0) {
+  if (!kProd && lane == 0) {
     count_store(n_desc, 0);
     for (int k = 0; k < kDecStages; ++k) ld.issue_next(p, ring, bar0, descs, n_desc);
   }
   ld.warm = true;
   __syncwarp();
+  const uint32_t ebar0 = bars + 8 * (kBarDecEmpty + warp * kDecStages);  // kProd: slot empty barriers
 
   uint32_t qn0[8], qn2[8];
   bool qn_valid = false;
   int pending = -1;  // completion counter of the last split unit, not yet published
   for (int ck = 0;; ++ck) {
     __syncwarp();
+    if (kProd) wait_desc(n_desc, ck);
     const UnitDesc u = desc_load(descs, ck);
     if (u.id < 0) break;
     const int nst = (u.k1 - u.k0 + 15) >> 4;
@@ -1079,8 +1218,10 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
       const uint32_t ph = (dec_iter / kDecStages) & 1;
       const uint32_t stg = ring + slot * kDecStage;
       // diagnostics (p.trace, decode-only launches): warp 0 of CTA 0, first 64 stages
-      int64_t* dev = (p.trace != nullptr && p.n_tiles == 0 && blockIdx.x == 0 && warp == 0 && lane == 0 &&
-                      dec_iter < 64) ? p.trace + 8 * 160 : nullptr;
+      // (compiled in only with NIYAMA_DIAG_STEPS: the per-stage checks and stores cost ~5 % of
+      // the decode loop's stall samples, ncu round 2)
+      int64_t* dev = (NIYAMA_DIAG_STEPS && p.trace != nullptr && p.n_tiles == 0 && blockIdx.x == 0 && warp == 0 &&
+                      lane == 0 && dec_iter < 64) ? p.trace + 8 * 160 : nullptr;
       auto dstamp = [&](int role) {
         if (dev != nullptr) dev[role * 64 + dec_iter] = static_cast<int64_t>(clock64());
       };
@@ -1154,20 +1295,26 @@ __device__ __forceinline__ void decode_warp_loop(const AttnParams& p, uint32_t s
         publish_split(p, pending, lane);
         pending = -1;
       }
-      if (p.trace != nullptr && dec_iter == 0 && warp == 0 && lane == 0) {  // diagnostics: first stage done
+      if (NIYAMA_DIAG_STEPS && p.trace != nullptr && dec_iter == 0 && warp == 0 && lane == 0) {  // diagnostics: first stage done
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[8 * blockIdx.x + 7] = static_cast<int64_t>(t);
       }
       __syncwarp();
       dstamp(4);
-      if (lane == 0) ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
+      if (lane == 0) {
+        if (kProd)
+          mbar_arrive(ebar0 + 8 * slot);  // hand the slot back to the producer
+        else
+          ld.issue_next(p, ring, bar0, descs, n_desc);  // refill this slot
+      }
       dstamp(5);
       ++dec_iter;
       // prefetch the next unit's Q fragments once its descriptor is published
       if (!qn_valid && s + 2 >= nst) {
         __syncwarp();
         if (count_load(n_desc) > ck + 1) {
+          if (kProd) __threadfence_block();  // the descriptor was written before the count
           const UnitDesc nu = desc_load(descs, ck + 1);
           if (nu.id >= 0) {
             load_q_frags(p, nu, gid, tig, qn0, qn2);
@@ -1371,7 +1518,7 @@ __device__ __forceinline__ void decode_cta_v2(const AttnParams& p, uint32_t sbas
   // diagnostics (p.trace): CTA 0, steps < 64: clock64 per role (0 copies issued, 1 QK issued,
   // 2 S ready (softmax), 3 P written, 4 PV issued, 5 stage full seen by the MMA, 6 stage empty
   // seen by the producer)
-  int64_t* tr2 = (p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * 160 : nullptr;
+  int64_t* tr2 = (NIYAMA_DIAG_STEPS && p.trace != nullptr && blockIdx.x == 0) ? p.trace + 8 * 160 : nullptr;
   auto stamp = [&](int role, uint32_t j) {
     if (tr2 != nullptr && j < 64) tr2[role * 64 + j] = static_cast<int64_t>(clock64());
   };
@@ -1789,12 +1936,29 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   int n_done_items = 0;
   uint32_t kv_it = 0, it = 0;
   while (any_items) {
+#if NIYAMA_DIAG_TILES  // CTA 0: clock64 at the claim, after the Q load and at the tile end; count at [3][0]
+    int64_t* tev = (p.trace != nullptr && blockIdx.x == 0 && tid == 0 && n_done_items < 64) ? p.trace + 8 * 160 : nullptr;
+    if (tev) {
+      int64_t c;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+      tev[n_done_items] = c;
+      tev[3 * 64] = n_done_items;
+    }
+#endif
     if (tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
     __syncthreads();
     const int item = *item_slot;
     __syncthreads();
     if (item >= p.n_tiles) break;
     prefill_tile(p, tile_desc(p, item), sbase, bars, tmem, reinterpret_cast<float*>(misc + kMiscBytes), smem, kv_it, it);
+#if NIYAMA_DIAG_TILES
+    if (tev) {
+      int64_t c;
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+      tev[2 * 64 + n_done_items] = c;
+      tev[4 * 64 + n_done_items] = item;
+    }
+#endif
     ++n_done_items;
   }
   uint64_t t_prefill = 0;
@@ -1812,6 +1976,19 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
     decode_cta_v2(p, sbase, bars, tmem, smem_u32(misc + kMiscBytes));
     tc_fence_before();
     __syncthreads();
+    if (p.n_merge_rows > 0) merge_tail(p);
+  } else if (p.n_units > 0 && p.dec_mode == 2) {
+    // producer/consumer decode: warps 0-7 compute (3-stage rings), warps 8-11 load for two each
+    const uint32_t descs0 = smem_u32(misc + kMiscBytes), n_desc0 = smem_u32(misc + 64);
+    if (warp < 8) {
+      if ((tid & 31) == 0) count_store(n_desc0 + 16 * warp, 0);
+      __syncthreads();
+      decode_warp_loop<8, 3, true>(p, sbase, bars, descs0 + warp * 4 * 32, n_desc0 + 16 * warp);
+    } else {
+      __syncthreads();  // the consumers' descriptor counts are zeroed
+      if ((tid & 31) == 0) decode_producer<8, 3>(p, sbase, bars, descs0, n_desc0, 2 * (warp - 8));
+      __syncwarp();
+    }
     if (p.n_merge_rows > 0) merge_tail(p);
   } else if (p.n_units > 0 && warp < p.dec_warps) {  // the other warps only serve the prefill softmax
     UnitDesc* descs = reinterpret_cast<UnitDesc*>(misc + kMiscBytes) + 4 * warp;

@@ -980,7 +980,7 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   p.kv_adjacent = kv->v_offset == kv->chunk_bytes ? 1 : 0;
   // g <= 4: 12 decode warps x 2-stage rings; g = 8 (twice the MMA work per byte): 8 x 3
   // (measured: config 2 102.6 -> 99.4 us with 12; config 4 1180 -> 1218 us with 12)
-  p.dec_warps = kv->g <= 4 ? 12 : 8;
+  p.dec_warps = decode_streams(kv->g, kv->tune.decode_path);
   p.dec_mode = kv->tune.decode_path;
   p.T = plan->T;
   p.Hq = kv->hq;
@@ -1039,7 +1039,7 @@ extern "C" niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning
 extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t) {
   if (!kv || !t) return fail(NIYAMA_EINVAL, "kv/tuning is NULL");
   if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
-  if (t->decode_path != 0 && t->decode_path != 1) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0 or 1");
+  if (t->decode_path < 0 || t->decode_path > 2) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0, 1 or 2");
   if (t->prefill_split != 0 && t->prefill_split != 1) return fail(NIYAMA_EINVAL, "tuning: prefill_split must be 0 or 1");
   if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
   if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");

@@ -288,6 +288,35 @@ def test_tensor_core_decode_path(case):
     run_and_compare(wl, tuning=dict(decode_path=1))
 
 
+@pytest.mark.parametrize("case", ["ragged", "g8", "long-split", "blocks64", "config4-sampled"])
+def test_producer_consumer_decode_path(case):
+    """niyama_tuning.decode_path = 2 (warps 8-11 load for the 8 compute warps) against the
+    oracle, and bitwise equal to decode_path 0 (same units, same per-unit arithmetic)."""
+    if case == "ragged":
+        wl = W.random_hybrid(W.L8B, seed=21, num_prefill=2, max_chunk=300, num_decode=20, max_ctx=3000)
+    elif case == "g8":
+        wl = W.random_hybrid(W.Shape(64, 8, 128, 16, "bf16"), seed=22, num_prefill=1, max_chunk=200, num_decode=9,
+                             max_ctx=2500)
+    elif case == "long-split":
+        wl = W.hybrid(W.L8B, "long", prefill_offset=0, chunk=0, decode_ctx=[8192, 17, 4095, 1], seed=23)
+    elif case == "blocks64":
+        wl = W.random_hybrid(W.Shape(32, 8, 128, 64, "bf16"), seed=24, num_prefill=1, max_chunk=300, num_decode=12,
+                             max_ctx=3000)
+    else:
+        wl = W.config4_l70b()
+    rows = None
+    if case == "config4-sampled":
+        T = wl.final.desc.num_rows
+        rows = list(range(T - 128, T, 9)) + [0, 1000, 2047]
+    r2, _ = run_and_compare(wl, rows=rows, tuning=dict(decode_path=2))
+    o2, l2 = r2.attention()
+    r0 = Run(wl)
+    o0, l0 = r0.attention()
+    torch.cuda.synchronize()
+    assert torch.equal(o2.view(torch.int16), o0.view(torch.int16))
+    assert torch.equal(l2, l0)
+
+
 @pytest.mark.parametrize("case", ["prefill-only", "mixed", "g8", "two-slices", "diag-only"])
 def test_prefill_split_k(case):
     """Split-K prefill (niyama_tuning.prefill_split = 1: key parts of a q tile on different CTAs,

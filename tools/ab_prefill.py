@@ -18,7 +18,8 @@ def main():
                W.config4_l70b(),
                W.hybrid(W.L8B, "l8b-prefill-c2048-o2048", prefill_offset=2048, chunk=2048, decode_ctx=[], seed=4),
                W.hybrid(W.L8B, "l8b-prefill-c512-o1536", prefill_offset=1536, chunk=512, decode_ctx=[], seed=2),
-               W.config2_l8b()):
+               W.config2_l8b(),
+               W.hybrid(W.L8B, "decode-only-64", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2)):
         time_it(wl, reps=30)
 
 

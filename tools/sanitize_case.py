@@ -17,13 +17,15 @@ CASES = {
     "g8": lambda: W.random_hybrid(W.Shape(16, 2, 128, 16, "bf16"), seed=8, num_prefill=1, max_chunk=100,
                                   num_decode=5, max_ctx=2500),
     "config2": lambda: W.config2_l8b(),
+    "dec": lambda: W.hybrid(W.L8B, "dec", prefill_offset=0, chunk=0, decode_ctx=[300, 17, 1000, 45], seed=7),
 }
 
 if __name__ == "__main__":
     name = sys.argv[1]
-    fused = len(sys.argv) > 2 and sys.argv[2] == "fused"
+    fused = "fused" in sys.argv[2:]
+    tuning = dict(decode_path=2) if "path2" in sys.argv[2:] else None
     wl = CASES[name]()
-    r = Run(wl, fused=fused)
+    r = Run(wl, fused=fused, tuning=tuning)
     o, lse = r.attention()
     o2, _ = r.attention()      # second launch of the same plan (epoch counters, self-reset queues)
     torch.cuda.synchronize()
