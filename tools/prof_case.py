@@ -20,6 +20,8 @@ elif case == "decode":
     wl = W.hybrid(W.L8B, "decode-only", prefill_offset=0, chunk=0, decode_ctx=W.l8b_decode_ctx(), seed=2)
 elif case == "l70b":
     wl = W.config4_l70b()
+elif case == "l70bp":
+    wl = W.hybrid(W.L70B, "l70b-prefill-c2048-o6144", prefill_offset=6144, chunk=2048, decode_ctx=[], seed=4)
 else:
     wl = W.config2_l8b()
 kv, plan, q, o, lse = setup(wl)
