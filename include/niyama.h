@@ -244,9 +244,13 @@ niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
  *   prefill_split     1 = split-K of prefill q tiles when they are fewer than their CTAs (key
  *                     parts on different CTAs, merged by the last part; parity-tested, measured
  *                     slower: DESIGN.md 6.1), 0 = never split (default)
- *   decode_path       bf16 decode units: 0 = per-warp mma.sync streams (default), 1 = one
- *                     tensor-core (tcgen05) pipeline per CTA over 128-token steps (same
- *                     results within bf16 rounding; measured slower: DESIGN.md 6.1)
+ *   decode_path       bf16 decode units: 0 = auto (default: 2 when g > 4, else 3), 1 = one
+ *                     tensor-core (tcgen05) pipeline per CTA over 128-token steps (measured
+ *                     slower: DESIGN.md 6.1), 2 = producer warps: warps 8-11 claim units and
+ *                     issue the stage copies of two compute warps each (warps 0-7), 3 = every
+ *                     decode warp is its own loader (12 warps at g <= 4, 8 at g = 8).  All
+ *                     paths give the same results within bf16 rounding; 0, 2 and 3 are bitwise
+ *                     identical (same units, same per-unit arithmetic)
  * A changed tuning applies to plans created afterwards (split, CTA split) and to
  * launches issued afterwards (grid cap). */
 typedef struct {

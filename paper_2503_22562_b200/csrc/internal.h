@@ -116,6 +116,7 @@ inline int32_t rows_per_tile(int g) { return 128 / (g > 0 ? g : 1); }
 inline int decode_warps(int g) { return g <= 4 ? 12 : 8; }
 // Decode streams per CTA as the predictor models them: one pipeline (tensor-core path) or
 // one per decode warp (mma.sync path).
+// (decode_path 0 = auto resolves to 2 at g = 8, which also runs 8 compute warps)
 inline int decode_streams(int g, int decode_path) {
   return decode_path == 1 ? 1 : decode_path == 2 ? 8 : decode_warps(g);
 }

@@ -981,7 +981,13 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   // g <= 4: 12 decode warps x 2-stage rings; g = 8 (twice the MMA work per byte): 8 x 3
   // (measured: config 2 102.6 -> 99.4 us with 12; config 4 1180 -> 1218 us with 12)
   p.dec_warps = decode_streams(kv->g, kv->tune.decode_path);
-  p.dec_mode = kv->tune.decode_path;
+  // decode_path 0 = auto: producer warps at g = 8 (the 4 warps a 3-stage ring layout leaves
+  // idle; config 4 870 -> 850 us), per-warp loaders at g <= 4 (12 compute warps measured
+  // faster: config 2 96.3 vs 98.4 us with 8 + 4); kernel modes 0 per-warp, 1 tcgen05, 2 producer
+  {
+    const int dp = kv->tune.decode_path;
+    p.dec_mode = dp == 1 ? 1 : (dp == 2 || (dp == 0 && kv->g > 4)) ? 2 : 0;
+  }
   p.T = plan->T;
   p.Hq = kv->hq;
   p.Hkv = kv->hkv;
@@ -1039,7 +1045,7 @@ extern "C" niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning
 extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t) {
   if (!kv || !t) return fail(NIYAMA_EINVAL, "kv/tuning is NULL");
   if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
-  if (t->decode_path < 0 || t->decode_path > 2) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0, 1 or 2");
+  if (t->decode_path < 0 || t->decode_path > 3) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0-3");
   if (t->prefill_split != 0 && t->prefill_split != 1) return fail(NIYAMA_EINVAL, "tuning: prefill_split must be 0 or 1");
   if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
   if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");

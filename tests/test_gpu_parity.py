@@ -291,7 +291,8 @@ def test_tensor_core_decode_path(case):
 @pytest.mark.parametrize("case", ["ragged", "g8", "long-split", "blocks64", "config4-sampled"])
 def test_producer_consumer_decode_path(case):
     """niyama_tuning.decode_path = 2 (warps 8-11 load for the 8 compute warps) against the
-    oracle, and bitwise equal to decode_path 0 (same units, same per-unit arithmetic)."""
+    oracle, and bitwise equal to decode_path 3 (every warp its own loader) and to the default
+    (auto) path: same units, same per-unit arithmetic."""
     if case == "ragged":
         wl = W.random_hybrid(W.L8B, seed=21, num_prefill=2, max_chunk=300, num_decode=20, max_ctx=3000)
     elif case == "g8":
@@ -310,11 +311,12 @@ def test_producer_consumer_decode_path(case):
         rows = list(range(T - 128, T, 9)) + [0, 1000, 2047]
     r2, _ = run_and_compare(wl, rows=rows, tuning=dict(decode_path=2))
     o2, l2 = r2.attention()
-    r0 = Run(wl)
-    o0, l0 = r0.attention()
-    torch.cuda.synchronize()
-    assert torch.equal(o2.view(torch.int16), o0.view(torch.int16))
-    assert torch.equal(l2, l0)
+    for tuning in (dict(decode_path=3), None):
+        r0 = Run(wl, tuning=tuning)
+        o0, l0 = r0.attention()
+        torch.cuda.synchronize()
+        assert torch.equal(o2.view(torch.int16), o0.view(torch.int16))
+        assert torch.equal(l2, l0)
 
 
 @pytest.mark.parametrize("case", ["prefill-only", "mixed", "g8", "two-slices", "diag-only"])
