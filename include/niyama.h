@@ -251,6 +251,11 @@ niyama_status niyama_debug_trace(niyama_kv* kv, int64_t* device_buf);
  *                     decode warp is its own loader (12 warps at g <= 4, 8 at g = 8).  All
  *                     paths give the same results within bf16 rounding; 0, 2 and 3 are bitwise
  *                     identical (same units, same per-unit arithmetic)
+ *   prefill_pairs     0 = auto (default: pairs when g > 4), 1 = prefill q tiles run in CTA
+ *                     pairs (clusters of 2): the two q tiles (qt, qt - 1) of a kv head share
+ *                     every K/V step, each CTA issuing half of the step's bulk copies multicast
+ *                     into both (half the TMA issue and L2 reads per SM; bitwise identical
+ *                     results); 2 = one q tile per CTA.  Ignored with prefill_split
  * A changed tuning applies to plans created afterwards (split, CTA split) and to
  * launches issued afterwards (grid cap). */
 typedef struct {
@@ -262,6 +267,7 @@ typedef struct {
   int32_t plan_copy_stream;
   int32_t decode_path;
   int32_t prefill_split;
+  int32_t prefill_pairs;
 } niyama_tuning;
 niyama_status niyama_kv_get_tuning(const niyama_kv* kv, niyama_tuning* out);
 niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning* t); /* EINVAL on out-of-range fields */

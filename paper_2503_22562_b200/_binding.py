@@ -56,7 +56,7 @@ class PlanInfo(C.Structure):
 class Tuning(C.Structure):
     _fields_ = [("prefill_ctas", C.c_int32), ("split_len", C.c_int32), ("tail_div", C.c_int32),
                 ("tail_min", C.c_int32), ("grid_cap", C.c_int32), ("plan_copy_stream", C.c_int32),
-                ("decode_path", C.c_int32), ("prefill_split", C.c_int32)]
+                ("decode_path", C.c_int32), ("prefill_split", C.c_int32), ("prefill_pairs", C.c_int32)]
 
 
 class SampleC(C.Structure):

@@ -32,6 +32,7 @@ inline niyama_tuning default_tuning() {
   t.tail_min = NIYAMA_TAIL_MIN;
   t.grid_cap = 0;
   t.plan_copy_stream = 1;
+  t.prefill_pairs = 0;
   return t;
 }
 
@@ -269,6 +270,12 @@ struct AttnParams {
     uint32_t* flags;    // this rank's flag array [n] (window mapping)
     int64_t delta[kMaxGatherRanks];
   } gx;
+  // Prefill CTA pairs (niyama_tuning.prefill_pairs): clusters of 2 CTAs take the two q tiles
+  // (qt, qt - 1) of one kv head together; each CTA issues half of every K/V step's copies,
+  // multicast into both CTAs' shared memory.  n_pair_items = sum over slices of
+  // ceil(nqt / 2) * Hkv.  0 = one q tile per CTA.
+  int32_t pairs;
+  int32_t n_pair_items;
 };
 
 

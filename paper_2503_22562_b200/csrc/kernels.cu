@@ -221,6 +221,9 @@ constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 #ifndef NIYAMA_DIAG_HANG
 #define NIYAMA_DIAG_HANG 0
 #endif
+#ifndef NIYAMA_ONE_SLOAD
+#define NIYAMA_ONE_SLOAD 0
+#endif
 #ifndef NIYAMA_DIAG_TILES
 #define NIYAMA_DIAG_TILES 0
 #endif
@@ -428,6 +431,38 @@ __device__ __forceinline__ TileDesc tile_desc(const AttnParams& p, int t) {
   return d;
 }
 
+// Prefill CTA pairs (p.pairs): item t = (slice, q-tile pair, kv head); CTA `rank` of the
+// cluster takes q tile nqt-1 - 2*pair - rank.  Both run the pair's key steps (those of the
+// longer tile, rank 0's); a missing partner tile (odd nqt) is a tile with no valid rows.
+__device__ __forceinline__ TileDesc tile_desc_pair(const AttnParams& p, int t, int rank) {
+  int i = 0, base = 0;
+  for (;; ++i) {
+    const int npi = (p.slices[i].nqt + 1) / 2 * p.Hkv;
+    if (i + 1 >= p.n_slices || t < base + npi) break;
+    base += npi;
+  }
+  const PrefillSlice sl = p.slices[i];
+  const int local = t - base;
+  const int qp = local / p.Hkv;
+  const int qt_a = sl.nqt - 1 - 2 * qp;  // rank 0's (longer) tile
+  const int qt = qt_a - rank;
+  TileDesc d;
+  d.tbl = sl.tbl;
+  d.o = sl.o;
+  d.row0 = sl.row0;
+  d.kvh = local - qp * p.Hkv;
+  d.t0 = (qt >= 0 ? qt : qt_a) * p.R;
+  d.c = qt >= 0 ? sl.c : d.t0;  // no partner tile: no valid rows (c - t0 = 0)
+  d.nkeys = sl.o + min(qt_a * p.R + p.R, sl.c);
+  d.nblk = (d.nkeys + p.B - 1) / p.B;
+  d.parts = 1;
+  d.part = 0;
+  d.j0 = 0;
+  d.j1 = (d.nkeys + 127) >> 7;
+  d.stile = 0;
+  return d;
+}
+
 // Split-K merge of one q tile (run by the CTA of its last part): for each of the 128 rows
 // (g heads x R chunk rows) m = max_s m_s, w_s = 2^(m_s - m) l_s, o = sum_s w_s o~_s / sum_s w_s
 // in part order (deterministic), LSE = (m + log2 sum w) ln 2.  Threads take (row, 4 dims).
@@ -480,6 +515,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
   const int warp = tid >> 5;
   const int lane = tid & 31;
   const int g = p.g, R = p.R;
+  const uint32_t rank = p.pairs ? cluster_ctarank() : 0u;
   const int vrows = min(R, t.c - t.t0);
   const int nk = (t.nkeys + kBN - 1) / kBN;   // key steps of the whole q tile
   const int j0 = t.j0, j1 = t.j1, n = j1 - j0;  // this item's steps (split-K part)
@@ -591,13 +627,16 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       }
       __syncwarp();
       const uint32_t dst0 = ring + st * kTile;
-      if (lane < (NIYAMA_DIAG_HALF_KV ? npc / 2 : npc)) {  // (diagnostic: half the bytes, wrong results)
-        if (isK) {  // one copy per block: B rows x 256 B, contiguous in pool and tile
-          bulk_g2s(dst0 + lane * static_cast<uint32_t>(p.chunk_bytes), pool + cur, static_cast<uint32_t>(p.chunk_bytes),
-                   full);
-        } else {
-          bulk_g2s(dst0 + lane * 4096, pool + cur, 4096, full);
-        }
+      // CTA pairs: this CTA issues the pieces it owns (odd/even lanes; a single K piece: rank 0)
+      // multicast into both CTAs of the cluster, whose full barriers each expect the whole step
+      const bool own = !p.pairs || (npc >= 2 ? (lane & 1) == static_cast<int>(rank) : rank == 0);
+      if (lane < (NIYAMA_DIAG_HALF_KV ? npc / 2 : npc) && own) {  // (diagnostic: half the bytes, wrong results)
+        const uint32_t bytes = isK ? static_cast<uint32_t>(p.chunk_bytes) : 4096u;
+        const uint32_t dst = dst0 + lane * bytes;  // K: one copy per block (B rows x 256 B); V^T: sub-block
+        if (p.pairs)
+          bulk_g2s_mc(dst, pool + cur, bytes, full, 0x3);
+        else
+          bulk_g2s(dst, pool + cur, bytes, full);
       }
     }
   } else if (warp == 1) {
@@ -625,7 +664,10 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
                      kIdescQK, kk > 0);
         }
         umma_commit(bars + 8 * (kBarSFull + sb));
-        umma_commit(bars + 8 * (kBarKEmpty + st));
+        if (p.pairs)  // the stage is free only when both CTAs' QK^T have read it
+          umma_commit_mc(bars + 8 * (kBarKEmpty + st), 0x3);
+        else
+          umma_commit(bars + 8 * (kBarKEmpty + st));
         ev_stamp(ev, 9, j);
       }
     }
@@ -647,7 +689,10 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
           umma_ts(tmem + kTmemO, tmem + (kPSep ? kTmemP + sb * 64 : sb * 128) + kk * 8, sw32_desc(va + kk * 4096, 16, 256), kIdescPV,
                   (j > j0 || kk > 0) ? 1u : 0u);
         umma_commit(bars + 8 * (kBarODone + sb));
-        umma_commit(bars + 8 * (kBarVEmpty + st));
+        if (p.pairs)
+          umma_commit_mc(bars + 8 * (kBarVEmpty + st), 0x3);
+        else
+          umma_commit(bars + 8 * (kBarVEmpty + st));
       }
     }
   } else if (warp >= 4) {
@@ -689,6 +734,29 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
 #endif
       const int kbase = j * kBN;
       const bool diag = kbase + kBN - 1 > pos;
+#if NIYAMA_ONE_SLOAD
+      // S is loaded from TMEM once (128 registers) and P packed in place over the consumed
+      // values; S[sb] is released to QK_{j+2} right after the load
+      uint32_t sr[128];
+      tmem_ld128(lane_addr + sb * 128, sr);
+      if (kPSep) {
+        tc_fence_before();
+        mbar_arrive(bars + 8 * (kBarSFree + sb));
+      }
+      if (diag) {
+        mask_tail(*reinterpret_cast<uint32_t(*)[64]>(sr), pos - kbase);
+        mask_tail(*reinterpret_cast<uint32_t(*)[64]>(sr + 64), pos - (kbase + 64));
+      }
+      float mx;
+      {
+        float m8[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = __uint_as_float(sr[k]);
+#pragma unroll
+        for (int e = 8; e < 128; ++e) m8[e & 7] = fmaxf(m8[e & 7], __uint_as_float(sr[e]));
+        mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      }
+#else
       float mx = -INFINITY;
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
@@ -703,6 +771,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
       }
+#endif
       float m_prev = -INFINITY;
       if (j > j0) {  // m_{j-1} from the other set
         named_bar_sync(bar_in, 64);
@@ -722,8 +791,16 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       m_ref = m_use;
       if (tracer) ev_stamp(ev, 5, j);
       if (j > j0 && __any_sync(0xffffffffu, need)) {
-        // rare: rescale O after PV_{j-1} (PV_j waits for our P)
+        // rare: rescale O after PV_{j-1} (PV_j waits for our P).  A parity wait is only
+        // unambiguous while the barrier is at most one phase behind the awaited one: this
+        // set knows PV_{j-4} is done (its P-free wait at step j-2) but not PV_{j-3}, which
+        // shares PV_{j-1}'s barrier when there are 2 S buffers.  So first wait for PV_{j-2}
+        // (its barrier's previous phase, PV_{j-4}, is known complete; completion of PV_{j-2}
+        // implies PV_{j-3}), then for PV_{j-1}.  (Waiting for PV_{j-1} alone returned early
+        // whenever PV_{j-3} was still running: O rescaled under a running PV, an
+        // intermittent wrong row found by tools/gather_stress.py.)
         const float alpha = ex2(m_prev - m_use);
+        if (gj >= 2) mbar_wait(bars + 8 * (kBarODone + (gj - 2) % kSBufs), ((gj - 2) / kSBufs) & 1);
         mbar_wait(bars + 8 * (kBarODone + (gj - 1) % kSBufs), ((gj - 1) / kSBufs) & 1);
         tc_fence_after();
 #pragma unroll 1
@@ -739,6 +816,21 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       if (tracer) ev_stamp(ev, 7, j);
       const float nm = -m_use;
       float sum0 = 0.f, sum1 = 0.f;
+#if NIYAMA_ONE_SLOAD
+#pragma unroll
+      for (int c = 0; c < 64; ++c) {  // P pair c overwrites sr[c] (its S values were sr[2c], sr[2c+1], c <= 2c)
+        const float e0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, nm));
+        const float e1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, nm));
+        if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
+        sr[c] = pack_bf16(e0, e1);
+      }
+      if (kPSep && gj >= kSBufs) {  // P[sb] free: PV_{j-2} done
+        mbar_wait(bars + 8 * (kBarODone + sb), ((gj - kSBufs) / kSBufs) & 1);
+        tc_fence_after();
+      }
+      tmem_st32(lane_addr + (kPSep ? kTmemP + sb * 64 : sb * 128), *reinterpret_cast<uint32_t(*)[32]>(sr));
+      tmem_st32(lane_addr + (kPSep ? kTmemP + sb * 64 : sb * 128) + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+#else
 #pragma unroll 1
       for (int hf = 0; hf < 2; ++hf) {
         uint32_t sr[64];
@@ -764,6 +856,7 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         }
         tmem_st32(lane_addr + (kPSep ? kTmemP + sb * 64 : sb * 128) + hf * 32, pk);
       }
+#endif
       l += sum0 + sum1;
       if (tracer) ev_stamp(ev, 8, j);
       tmem_wait_st();
@@ -781,6 +874,10 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
       float2* xq = reinterpret_cast<float2*>(smem_gen + kXOff);
       xq[set * 128 + r] = make_float2(l, m_set);
       named_bar_sync(9 + quarter, 64);
+      // the set that handled step j1-2 may have passed its ODone wait early (same
+      // two-phases-behind ambiguity as above); the set of the last step waited for PV_{j1-1}
+      // unambiguously, and O is read only after this barrier with it
+      tc_fence_after();
       const float2 other = xq[(set ^ 1) * 128 + r];
       m_ref = fmaxf(m_set, other.y);  // the max of the last step (the chain never decreases)
       l = l * ex2(m_set - m_ref) + other.x * ex2(other.y - m_ref);
@@ -1876,6 +1973,9 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
       if (b >= kBarSFree && b < kBarSFree + kSBufs) cnt = 128;
       if ((b >= kB2SFree && b < kB2PFull + 2) || (b >= kB2OFree && b < kB2MLFree + 2)) cnt = 128;
       if (b >= kB2DFree && b < kB2DFree + 4) cnt = 4;  // producer, MMA (after the last QK^T), softmax, epilogue
+      // CTA pairs: a K/V stage is free once both CTAs' MMAs have read it (multicast commits)
+      if (p.pairs && ((b >= kBarKEmpty && b < kBarKEmpty + kKStages) || (b >= kBarVEmpty && b < kBarVEmpty + kVStages)))
+        cnt = 2;
       mbar_init(bars + 8 * b, cnt);
     }
     fence_mbar_init();
@@ -1890,6 +1990,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (p.pairs) cluster_sync_all();  // both CTAs' barriers exist before any multicast copy or commit
   const uint32_t tmem = need_tmem ? *tmem_slot : 0u;
   // Launched with programmatic stream serialization: everything above touched only
   // on-chip state; every global access below comes after the preceding grid (the
@@ -1945,6 +2046,19 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
       tev[3 * 64] = n_done_items;
     }
 #endif
+    if (p.pairs) {
+      // the cluster's rank-0 CTA claims a q-tile pair; its partner reads the claim through DSMEM
+      const uint32_t rank = cluster_ctarank();
+      if (rank == 0 && tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
+      cluster_sync_all();
+      const int item = rank == 0 ? *item_slot : ld_shared_cluster_s32(mapa_shared(smem_u32(const_cast<int*>(item_slot)), 0));
+      __syncthreads();
+      if (item >= p.n_pair_items) break;
+      prefill_tile(p, tile_desc_pair(p, item, static_cast<int>(rank)), sbase, bars, tmem,
+                   reinterpret_cast<float*>(misc + kMiscBytes), smem, kv_it, it);
+      ++n_done_items;
+      continue;
+    }
     if (tid == 0) *item_slot = atomicAdd(p.work + 0, 1);
     __syncthreads();
     const int item = *item_slot;
@@ -1967,6 +2081,7 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   // bulk copies of the prefill were consumed before the last item barrier.
   fence_proxy_async_smem();
   __syncthreads();
+  if (p.pairs) cluster_sync_all();  // no partner copy or commit targets this CTA from here on
   if (dec_v2) {
     // tensor-core decode pipeline; its shared memory starts zeroed (padding rows of the
     // Q^T / P^T tiles, and V^T columns of partial steps must be finite: they meet P = 0)
@@ -2048,11 +2163,18 @@ cudaError_t launch_attention_bf16(const AttnParams& p, int grid, cudaStream_t s)
   cfg.blockDim = dim3(fa::kThreads);
   cfg.dynamicSmemBytes = fa::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (p.pairs) {  // prefill CTA pairs: clusters of 2 consecutive CTAs
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 2;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.numAttrs = 2;
+  }
   return cudaLaunchKernelEx(&cfg, hybrid_attn_bf16_kernel, p);
 }
 

@@ -1019,8 +1019,18 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
   NY_CUDA(dg.err);
   NY_CUDA(wait_plan(plan, stream));
   if (kv->cfg.dtype == NIYAMA_BF16) {  // shapes checked at niyama_kv_create
-    const int grid = kv->tune.grid_cap > 0 ? std::min(kv->tune.grid_cap, plan->grid) : plan->grid;
+    int grid = kv->tune.grid_cap > 0 ? std::min(kv->tune.grid_cap, plan->grid) : plan->grid;
     p.prefill_ctas = std::min(plan->prefill_ctas, grid);
+    const bool pairs = kv->tune.prefill_pairs == 1 || (kv->tune.prefill_pairs == 0 && kv->g > 4);
+    if (pairs && plan->n_tiles > 0 && plan->n_split_tiles == 0) {
+      // CTA pairs: clusters of 2 (even grid, even prefill CTA count), one item per q-tile pair
+      // (auto at g = 8: config 4 866 -> 849 us; neutral at g = 4, tools/ab_pairs.py)
+      p.pairs = 1;
+      p.n_pair_items = 0;
+      for (const PrefillSlice& sl : plan->slices) p.n_pair_items += (sl.nqt + 1) / 2 * kv->hkv;
+      grid = std::min(grid + (grid & 1), kv->num_sms & ~1);
+      p.prefill_ctas = std::min(grid, std::max(2, p.prefill_ctas + (p.prefill_ctas & 1)));
+    }
     NY_CUDA(launch_attention_bf16(p, grid, s));
     ++plan->launches;
   } else {
@@ -1047,6 +1057,7 @@ extern "C" niyama_status niyama_kv_set_tuning(niyama_kv* kv, const niyama_tuning
   if (t->prefill_ctas < 0 || t->grid_cap < 0) return fail(NIYAMA_EINVAL, "tuning: prefill_ctas/grid_cap < 0");
   if (t->decode_path < 0 || t->decode_path > 3) return fail(NIYAMA_EINVAL, "tuning: decode_path must be 0-3");
   if (t->prefill_split != 0 && t->prefill_split != 1) return fail(NIYAMA_EINVAL, "tuning: prefill_split must be 0 or 1");
+  if (t->prefill_pairs < 0 || t->prefill_pairs > 2) return fail(NIYAMA_EINVAL, "tuning: prefill_pairs must be 0-2");
   if (t->split_len != 0 && (t->split_len < 16 || t->split_len % 16)) return fail(NIYAMA_EINVAL, "tuning: split_len");
   if (t->tail_div < 1 || t->tail_div > 16) return fail(NIYAMA_EINVAL, "tuning: tail_div outside [1, 16]");
   if (t->tail_min < 16 || t->tail_min % 16) return fail(NIYAMA_EINVAL, "tuning: tail_min must be a multiple of 16");

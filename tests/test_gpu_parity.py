@@ -319,6 +319,40 @@ def test_producer_consumer_decode_path(case):
         assert torch.equal(l2, l0)
 
 
+@pytest.mark.parametrize("case", ["ragged", "odd-tiles", "g8", "blocks64", "blocks128", "config4-sampled"])
+def test_prefill_cta_pairs(case):
+    """niyama_tuning.prefill_pairs = 1 (clusters of 2 CTAs share every K/V step of two q
+    tiles, each issuing half the copies multicast into both) against the oracle, and bitwise
+    equal to one q tile per CTA (the partner's extra key step, if any, is fully masked)."""
+    L8 = W.L8B
+    if case == "ragged":
+        wl = W.random_hybrid(L8, seed=71, num_prefill=2, max_chunk=300, num_decode=12, max_ctx=3000)
+    elif case == "odd-tiles":   # nqt = 3 and 1: a partner without a tile
+        wl = W.hybrid(L8, "odd", prefill_offset=700, chunk=80, decode_ctx=[900, 33], seed=72)
+    elif case == "g8":
+        wl = W.random_hybrid(W.Shape(64, 8, 128, 16, "bf16"), seed=73, num_prefill=1, max_chunk=200, num_decode=9,
+                             max_ctx=2500)
+    elif case == "blocks64":
+        wl = W.random_hybrid(W.Shape(32, 8, 128, 64, "bf16"), seed=74, num_prefill=2, max_chunk=300, num_decode=6,
+                             max_ctx=3000)
+    elif case == "blocks128":
+        wl = W.random_hybrid(W.Shape(32, 8, 128, 128, "bf16"), seed=75, num_prefill=1, max_chunk=400, num_decode=4,
+                             max_ctx=3000)
+    else:
+        wl = W.config4_l70b()
+    rows = None
+    if case == "config4-sampled":
+        T = wl.final.desc.num_rows
+        rows = list(range(0, 2048, 97)) + [2047, T - 1]
+    r2, _ = run_and_compare(wl, rows=rows, tuning=dict(prefill_pairs=1))
+    o2, l2 = r2.attention()
+    r0 = Run(wl, tuning=dict(prefill_pairs=2))
+    o0, l0 = r0.attention()
+    torch.cuda.synchronize()
+    assert torch.equal(o2.view(torch.int16), o0.view(torch.int16))
+    assert torch.equal(l2, l0)
+
+
 @pytest.mark.parametrize("case", ["prefill-only", "mixed", "g8", "two-slices", "diag-only"])
 def test_prefill_split_k(case):
     """Split-K prefill (niyama_tuning.prefill_split = 1: key parts of a q tile on different CTAs,
@@ -402,3 +436,28 @@ def test_decode_row_equals_prefill_row():
         a = o[:, 0].float().cpu().numpy().astype(np.float64)
         b = o[:, 1].float().cpu().numpy().astype(np.float64)
         assert_close(b, a, lse[:, 1].cpu().numpy().astype(np.float64), lse[:, 0].cpu().numpy().astype(np.float64))
+
+
+@pytest.mark.parametrize("scale", [2.0, 4.0])
+def test_repeated_launches_bitwise_peaky(scale):
+    """Peaky queries make the prefill softmax's lazy O rescale frequent; 24 launches of the same
+    plan must agree bitwise.  (Pins the rescale's wait for PV_{j-1}: a parity wait two phases
+    behind returned early and rescaled O under a running PV — an intermittent wrong row,
+    tools/gather_stress.py.)"""
+    wl = W.random_hybrid(W.L8B, seed=81, num_prefill=2, max_chunk=300, num_decode=12, max_ctx=2500)
+    r = Run(wl)
+    qd = to_dev(wl.final.q, "bf16") * scale
+    T = wl.final.desc.num_rows
+    s = wl.shape
+    ref = None
+    for _ in range(24):
+        o = torch.empty((s.num_q_heads, T, s.head_dim), dtype=torch.bfloat16, device="cuda")
+        lse = torch.empty((s.num_q_heads, T), dtype=torch.float32, device="cuda")
+        r.kv.attention(r.plan, 0, qd, o, lse)
+        if ref is None:
+            torch.cuda.synchronize()
+            ref = (o, lse)
+            continue
+        torch.cuda.synchronize()
+        assert torch.equal(o.view(torch.int16), ref[0].view(torch.int16))
+        assert torch.equal(lse, ref[1])

@@ -24,6 +24,8 @@ if __name__ == "__main__":
     name = sys.argv[1]
     fused = "fused" in sys.argv[2:]
     tuning = dict(decode_path=2) if "path2" in sys.argv[2:] else None
+    if "pairs" in sys.argv[2:]:
+        tuning = dict(prefill_pairs=1)
     wl = CASES[name]()
     r = Run(wl, fused=fused, tuning=tuning)
     o, lse = r.attention()
