@@ -365,11 +365,17 @@ niyama_status niyama_debug_gather_group(niyama_kv* const* kvs, int32_t n, int32_
 #define NIYAMA_PRED_SMS 148
 #define NIYAMA_TAIL_DIV 4
 #define NIYAMA_TAIL_MIN 256
-#define NIYAMA_STEP_BYTES 160e3
+/* CTA split: one 128-key prefill step weighs as much CTA time as this many bytes of decode
+ * KV (recalibrated late in round 2 on the faster kernel, tools/cap_sweep.py: the best fixed
+ * prefill-CTA counts of 15 L8B shapes imply 95-125 KB; round 1 used 160 KB, which gave
+ * config 2 60 prefill CTAs where 48 measured 2 % faster and c1024/o1024/D64 10 % slower
+ * than its best). */
+#define NIYAMA_STEP_BYTES 115e3
 /* CTA split: decode KV bytes weigh this much more when g = Hq/Hkv > 4 (the launch then
- * streams decode with 8 warps per CTA instead of 12, so a CTA moves fewer bytes per
- * unit time; config 4 measured 1,073 us at the unweighted split, 926 us at 80 CTAs). */
-#define NIYAMA_WIDE_GROUP_DECODE_WEIGHT 1.8
+ * streams decode with 8 compute warps per CTA instead of 12, so a CTA moves fewer bytes per
+ * unit time; config 4: 858 us at the rule's 82-84 CTAs, 861 at 80, 866 at 88, 963 at 72,
+ * tools/cap_sweep_l70b.py). */
+#define NIYAMA_WIDE_GROUP_DECODE_WEIGHT 1.25
 #define NIYAMA_TILE_SETUP_STEPS 2
 #define NIYAMA_NUM_PARAMS 16
 

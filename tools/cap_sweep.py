@@ -15,8 +15,9 @@ from sweep_predictor import Rig  # noqa: E402
 SHAPES = [  # (chunk, offset, D)
     (512, 1536, 64), (2048, 4096, 16), (1024, 1024, 64), (256, 1280, 256), (2048, 2048, 128),
     (512, 1536, 0), (2048, 0, 0), (256, 0, 16), (1024, 3072, 16),
+    (256, 1536, 16), (512, 1536, 16), (256, 1536, 64), (1024, 1024, 16), (512, 3584, 128), (2048, 2048, 32),
 ]
-CAPS = [0, 8, 16, 24, 32, 48, 64, 96, 128, 148]
+CAPS = [0, 8, 16, 24, 32, 40, 48, 56, 64, 80, 96, 112, 128, 148]
 
 
 def main():
