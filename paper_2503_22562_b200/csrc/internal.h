@@ -221,6 +221,8 @@ struct AppendParams {
   const int32_t* vgrp;
   const int32_t* velem;
   int32_t n_grp, n_elem;
+  const uint8_t* pf_base;  // plan metadata to prefetch into L2 (pf_bytes, multiple of 16; 0 = none)
+  uint32_t pf_bytes;
 };
 
 struct AttnParams {

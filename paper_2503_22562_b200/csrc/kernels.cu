@@ -122,8 +122,19 @@ __device__ __forceinline__ void append_piece(const AppendParams& p, const int id
   }
 }
 
+// Diagnostic A/B: the append kernel prefetches the plan's metadata into L2 (default off).
+#ifndef NIYAMA_PLAN_PREFETCH
+#define NIYAMA_PLAN_PREFETCH 0
+#endif
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendParams p) {
   grid_dep_launch();  // the attention launch that follows may start its prologue
+#if NIYAMA_PLAN_PREFETCH
+  if (blockIdx.x == 0 && p.pf_bytes > 0) {  // plan metadata into L2 for the attention launch
+    const uint32_t chunk = 16384;
+    for (uint32_t o = threadIdx.x * chunk; o < p.pf_bytes; o += blockDim.x * chunk)
+      bulk_prefetch_l2(p.pf_base + o, min(chunk, p.pf_bytes - o));
+  }
+#endif
   const int total = append_total(p);
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x)
     append_piece(p, idx);

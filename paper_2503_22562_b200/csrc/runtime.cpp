@@ -139,6 +139,7 @@ struct niyama_plan {
   cudaStream_t stream = nullptr;
   cudaEvent_t ready = nullptr;  // this plan's own event, recorded right after its upload (either path)
   int32_t slot = -1;            // staging slot whose device buffer holds the plan (-1: pool)
+  size_t meta_bytes = 0;        // uploaded part of dbuf (tables, queues, counters): the append prefetches it
   int32_t T = 0, prefill_rows = 0, D = 0, split_len = 0, R = 0;
   int64_t sum_ctx = 0;
   std::vector<int32_t> slot_map;
@@ -691,6 +692,7 @@ extern "C" niyama_status niyama_plan_create(niyama_kv* kv, const niyama_batch_de
     const size_t o_cnt = take(pl->drows.size() * static_cast<size_t>(hkv) * 4);
     const size_t o_pcnt = take(static_cast<size_t>(pl->n_split_tiles) * 4);
     const size_t meta_bytes = off;
+    pl->meta_bytes = meta_bytes;
     const size_t o_part_o = take(static_cast<size_t>(pl->n_units) * g * kv->d * 4);
     const size_t o_part_ml = take(static_cast<size_t>(pl->n_units) * g * 2 * 4);
     const size_t o_ppart_o = take(static_cast<size_t>(pl->split_parts_total) * 128 * kv->d * 4);
@@ -895,6 +897,10 @@ niyama_status fill_append(niyama_kv* kv, const niyama_plan* plan, int32_t layer,
   p.velem = plan->d_velem;
   p.n_grp = static_cast<int32_t>(plan->vgrp.size());
   p.n_elem = static_cast<int32_t>(plan->velem.size());
+  // the plan's freshly uploaded metadata (block tables, unit queue, ...) into L2 while the
+  // append runs, so the attention launch that follows does not start on cold plan data
+  p.pf_base = plan->dbuf;
+  p.pf_bytes = static_cast<uint32_t>(std::min<size_t>(plan->meta_bytes, size_t(64) << 20) & ~size_t(15));
   return NIYAMA_OK;
 }
 
