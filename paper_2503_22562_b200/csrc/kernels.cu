@@ -1977,8 +1977,12 @@ __global__ void __launch_bounds__(fa::kThreads, 1) hybrid_attn_bf16_kernel(const
   uint64_t t_entry = 0;
   if (p.trace != nullptr && tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_entry));
 
-  if (tid == 0) {
-    for (int b = 0; b < kNumBars; ++b) {
+  // one barrier per thread (a serial loop of ~90 inits by one thread sat in every launch's
+  // prologue); the fence by each initialising thread, then the CTA barrier below
+  static_assert(kNumBars <= kThreads, "one mbarrier per initialising thread");
+  if (tid < kNumBars) {
+    {
+      const int b = tid;
       uint32_t cnt = 1;
       if (b >= kBarPFull && b < kBarPFull + kSBufs) cnt = 128;
       if (b >= kBarSFree && b < kBarSFree + kSBufs) cnt = 128;
