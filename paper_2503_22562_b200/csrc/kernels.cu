@@ -402,6 +402,24 @@ __device__ __forceinline__ void ev_stamp(int64_t* ev, int role, int j) {
   }
 }
 
+// 2^x on the FMA/ALU pipes (FA4-style): x = n + f with n = rint(x) (magic-number add),
+// f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (relative error < 1e-3, below bf16's
+// 2^-8 rounding of P); n added to the exponent bits.  x < -125 (incl. masked -inf) -> 0.
+#ifndef NIYAMA_POLY_EXP
+#define NIYAMA_POLY_EXP 0
+#endif
+__device__ __forceinline__ float ex2_poly(float x) {
+  const float xc = fmaxf(x, -125.f);
+  const float t = xc + 12582912.f;       // 1.5 * 2^23: rint(xc) in the low mantissa bits
+  const float n = t - 12582912.f;
+  const float f = xc - n;
+  float pl = fmaf(0.0555041087f, f, 0.2402265070f);
+  pl = fmaf(pl, f, 0.6931471806f);
+  pl = fmaf(pl, f, 1.0f);
+  const float r = __int_as_float(__float_as_int(pl) + (__float_as_int(t) << 23));
+  return x < -125.f ? 0.f : r;
+}
+
 // Causal mask of one 64-column slice of a score row: columns e > last become -inf.
 __device__ __forceinline__ void mask_tail(uint32_t (&sr)[64], int last) {
 #pragma unroll
@@ -856,8 +874,15 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
         uint32_t pk[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          const float e0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, nm));
-          const float e1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, nm));
+          float e0, e1;
+          if (NIYAMA_POLY_EXP > 0 && c % (NIYAMA_POLY_EXP > 0 ? NIYAMA_POLY_EXP : 1) == 0) {
+            // every NIYAMA_POLY_EXP-th pair on the FMA pipe instead of MUFU (FA4's trick)
+            e0 = ex2_poly(fmaf(__uint_as_float(sr[2 * c]), sl2, nm));
+            e1 = ex2_poly(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, nm));
+          } else {
+            e0 = ex2(fmaf(__uint_as_float(sr[2 * c]), sl2, nm));
+            e1 = ex2(fmaf(__uint_as_float(sr[2 * c + 1]), sl2, nm));
+          }
           if (c & 1) sum1 += e0 + e1; else sum0 += e0 + e1;
           pk[c] = pack_bf16(e0, e1);
         }
