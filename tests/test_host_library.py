@@ -260,11 +260,16 @@ def test_tuning_roundtrip_validation_and_effect():
     t = kv.tuning()
     assert (t.prefill_ctas, t.split_len, t.tail_div, t.tail_min, t.grid_cap, t.plan_copy_stream) == \
         (0, 0, 4, 256, 0, 1)
-    for bad in ({"split_len": 24}, {"tail_div": 0}, {"tail_min": 8}, {"prefill_ctas": -1}, {"plan_copy_stream": 2}):
+    assert (t.decode_path, t.prefill_split, t.prefill_pairs) == (0, 0, 0)   # auto / off / auto
+    for bad in ({"split_len": 24}, {"tail_div": 0}, {"tail_min": 8}, {"prefill_ctas": -1}, {"plan_copy_stream": 2},
+                {"decode_path": 4}, {"decode_path": -1}, {"prefill_split": 2}, {"prefill_pairs": 3}):
         with pytest.raises(ny.NiyamaError) as e:
             kv.set_tuning(**bad)
         assert e.value.status == NB.EINVAL
     assert kv.tuning().split_len == 0          # a rejected call changes nothing
+    for ok in ({"decode_path": 3}, {"decode_path": 2}, {"prefill_pairs": 1}, {"prefill_pairs": 2}):
+        kv.set_tuning(**ok)
+        assert all(getattr(kv.tuning(), k) == v for k, v in ok.items())
     ctx = W.l8b_decode_ctx()
     wl = W.hybrid(W.L8B, "tune", prefill_offset=1536, chunk=512, decode_ctx=ctx, seed=0)
     kv = host_kv(W.L8B, wl.num_blocks)
