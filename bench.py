@@ -411,7 +411,8 @@ def main():
     last_win = {}
 
     # a8 predictor: fitted parameters from the config-3 sweep if committed, else roofline-shaped defaults
-    fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json")
+    fit_path = os.path.join(ROOT, "profiles", "predictor_fit.json" if args.config == "l8b" else
+                            f"predictor_fit_{args.config}.json")
     cfg = ny.Predictor.shape_cfg(s.num_q_heads, s.num_kv_heads, s.head_dim, s.dtype, world)
     theta = list(ny.DEFAULT_THETA)   # the config-3 fit of round 2 (profiles/predictor_fit.json)
     if os.path.exists(fit_path):

@@ -523,3 +523,27 @@ def test_gather_window_host_validation():
     with pytest.raises(ny.NiyamaError) as e:
         ny.debug_gather_group([], 16)
     assert e.value.status == 1
+
+
+def test_committed_l70b_fit_reproduces():
+    """profiles/predictor_fit_l70b.json (config-4 head shapes, Hq 64 / Hkv 8, the launch at g = 8
+    with CTA pairs and producer-warp decode): the recorded predictions reproduce through the C ABI
+    and the held-out errors are the file's own (measured: p50 1.2 %, p95 5.5 %, max 7.1 %)."""
+    fj = json.load(open(os.path.join(ROOT, "profiles", "predictor_fit_l70b.json")))
+    sw = json.load(open(os.path.join(ROOT, fj["sweep"])))
+    assert sw["config"] == "l70b"
+    pr = ny.Predictor.from_params(ny.Predictor.shape_cfg(64, 8, 128, "bf16"), fj["theta"])
+    byk = {(p["kind"], p["seed"], p["chunk"], p["D"]): p for p in fj["points"]}
+    held = []
+    for r in sw["points"]:
+        c = r["chunk"]
+        d = W.BatchDesc([0] if c else [], [r["offset"]] if c else [], [c] if c else [], list(range(1, r["D"] + 1)),
+                        list(r["ctx"]))
+        rec = byk[(r["kind"], r["seed"], r["chunk"], r["D"])]
+        assert pr.predict(d) == pytest.approx(rec["predicted"], rel=1e-12)
+        if r["kind"] == "offgrid" or (r["kind"] == "grid" and r["seed"] == 2):
+            held.append(pr.predict(d) / r["seconds"] - 1)
+    held = np.abs(held)
+    assert len(held) == fj["fit"]["heldout_points"] == 60
+    assert float(held.max()) == pytest.approx(fj["heldout_rel_err"]["max"], rel=1e-9)
+    assert float(np.percentile(held, 95)) <= 0.06 and float(held.max()) <= 0.08

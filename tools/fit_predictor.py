@@ -50,7 +50,7 @@ def main():
     sw = json.load(open(args.sweep))
     pts = sw["points"]
     train, held = split(pts)
-    cfg = ny.Predictor.shape_cfg(32, 8, 128, "bf16")
+    cfg = ny.Predictor.shape_cfg(64 if sw.get("config") == "l70b" else 32, 8, 128, "bf16")
     t0 = time.time()
     pr = ny.Predictor.fit_batches(cfg, [desc(r) for r in train], [r["seconds"] for r in train],
                                   subsample=args.subsample, max_evals=args.max_evals)
