@@ -4,20 +4,22 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl niyama|reference] [--config l8b|l70b]
 
 A STEP is one pass of the whole hot path over one
-batch, for one layer: a1 min slack + max feasible chunk (host), a2 plan (host
-bookkeeping + one H2D), a3 KV append (kernel), a4-a6 the fused hybrid
-attention launch (kernel), a7 head all-gather (NCCL, N>1), a8 predictor eval
-(host).  The same batch is replayed every step (sequences are truncated back
-after planning, host-only).  Default workload = BASELINE config 2:
-Llama-3-8B attention shapes (32 q / 8 kv heads, d 128, bf16, block 16), a
-512-token prefill chunk at offset 1536 plus 64 decodes with ctx ~ U{1..4096}
-(PCG64 seed 0, sum ctx 133,674).  value = tokens of the batch (T = 576) per
-second of device time, max over ranks (strong scaling: heads are sharded over
-N GPUs, the batch is fixed).
+batch, i.e. one serving iteration: a1 min slack + max feasible chunk (host), a2
+plan (host bookkeeping + one H2D, ONCE per iteration: the plan serves every
+layer), then for each of the model's L attention layers (32 for Llama-3-8B,
+--layers to change) a3 KV append (kernel) and a4-a6 the fused hybrid attention
+launch (kernel) over that layer's own paged KV (+ a7 head all-gather, NCCL,
+N>1), and a8 predictor eval (host).  The same batch is replayed every step
+(sequences are truncated back after planning, host-only).  Default workload =
+BASELINE config 2: Llama-3-8B attention shapes (32 q / 8 kv heads, d 128, bf16,
+block 16), a 512-token prefill chunk at offset 1536 plus 64 decodes with ctx ~
+U{1..4096} (PCG64 seed 0, sum ctx 133,674).  value = layer-tokens (T = 576 rows
+x L layers) per second of device time, max over ranks (strong scaling: heads
+are sharded over N GPUs, the batch is fixed).
 
 Timing: CUDA events on the launching stream, W untimed warm-up steps, a
 barrier + synchronize on both sides of exactly K timed steps.  L2: inputs
-larger than L2 (556 MB of KV read per step vs 126 MB of L2).  The
+larger than L2 (556 MB of KV read per layer, every layer its own, vs 126 MB).  The
 `roofline` object uses the attention launch's own per-launch event times.
 """
 from __future__ import annotations
@@ -45,6 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="niyama", choices=["niyama", "reference"])
     ap.add_argument("--config", default="l8b", choices=["l8b", "l70b"])
+    ap.add_argument("--layers", type=int, default=0,
+                    help="attention layers per step (0 = the model's: 32 for Llama-3-8B, 80 for Llama-3-70B); one "
+                         "plan serves all layers of the iteration (SURVEY 8(a) a2), each layer has its own KV")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--settle-s", type=float, default=1.0, help="untimed GPU work before warm-up (clock settle)")
     ap.add_argument("--host-only", action="store_true",
@@ -376,7 +381,11 @@ def main():
     hq, hkv = s.num_q_heads // world, s.num_kv_heads // world
     q0, k0 = rank * hq, rank * hkv
     fused = args.fused_append
-    kv = ny.KVCache(1, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
+    # the model's layer count (Llama-3-8B 32, Llama-3-70B 80), capped so the per-rank KV of all
+    # layers fits in ~120 GB of HBM (config 4 at N = 1: 4.3 GB per layer -> 27 layers)
+    per_layer = (wl.num_blocks + 64) * hkv * s.block_size * s.head_dim * 2 * s.elt_bytes
+    L = args.layers if args.layers > 0 else min(32 if args.config == "l8b" else 80, max(1, int(120e9 // per_layer)))
+    kv = ny.KVCache(L, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
                     dtype=s.dtype, world_size=world, rank=rank, device=local)
     gather_fused = args.gather == "fused"
     if world > 1:
@@ -390,10 +399,12 @@ def main():
     def dev_bf16(a, lo, hi):
         return torch.from_numpy(np.ascontiguousarray(a[:, lo:hi]).view(np.int16)).to(dev).view(torch.bfloat16)
 
-    # prefix fill (untimed): sequences pre-filled by the library's own append
+    # prefix fill (untimed): sequences pre-filled by the library's own append, every layer
     for st in wl.steps[:-1]:
         p = kv.plan(st.desc)
-        kv.append(p, 0, dev_bf16(st.k, k0, k0 + hkv), dev_bf16(st.v, k0, k0 + hkv))
+        kd, vd = dev_bf16(st.k, k0, k0 + hkv), dev_bf16(st.v, k0, k0 + hkv)
+        for layer in range(L):
+            kv.append(p, layer, kd, vd)
         torch.cuda.synchronize()
         p.close()
     fin = wl.final
@@ -446,36 +457,38 @@ def main():
     # launch overlap of append -> attention, so they bracket every EV_EVERY-th timed
     # step only; the attention roofline uses the mean over those launches.
     EV_EVERY = 2
-    ev = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) if i % EV_EVERY == 0 else None
-          for i in range(args.steps)]
+    ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)] if i % EV_EVERY == 0
+          else None for i in range(args.steps)]
 
     def step(evs=None):
         a1_step()                                       # a1 (host)
-        plan = kv.plan(batch, stream)                   # a2
-        if evs is not None:
-            evs[0].record(stream)
-        if gather_fused:   # a4-a7 (a3-a7 with --fused-append) in ONE launch (niyama_attention_gather)
-            if not fused:
-                kv.append(plan, 0, k_new, v_new, stream)
-            if evs is not None:
-                evs[1].record(stream)
-            last_win["o"] = kv.attention_gather(plan, 0, q, window, k_new if fused else None,
-                                                v_new if fused else None, 0.0, stream)[0]
-        elif fused:   # a3-a6 in ONE launch (niyama_append_attention)
-            if evs is not None:
-                evs[1].record(stream)
-            kv.append_attention(plan, 0, k_new, v_new, q, o, lse, 0.0, stream)
-        else:
-            kv.append(plan, 0, k_new, v_new, stream)        # a3
-            if evs is not None:
-                evs[1].record(stream)
-            kv.attention(plan, 0, q, o, lse, 0.0, stream)   # a4-a6
-        if evs is not None:
-            evs[2].record(stream)
-        if world > 1 and not gather_fused:
-            kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
-        if evs is not None:
-            evs[3].record(stream)
+        plan = kv.plan(batch, stream)                   # a2: once per iteration, all layers
+        for layer in range(L):
+            ev_ = evs[layer] if evs is not None else None   # events bracket every layer's launches
+            if ev_ is not None:
+                ev_[0].record(stream)
+            if gather_fused:   # a4-a7 (a3-a7 with --fused-append) in ONE launch (niyama_attention_gather)
+                if not fused:
+                    kv.append(plan, layer, k_new, v_new, stream)
+                if ev_ is not None:
+                    ev_[1].record(stream)
+                last_win["o"] = kv.attention_gather(plan, layer, q, window, k_new if fused else None,
+                                                    v_new if fused else None, 0.0, stream)[0]
+            elif fused:   # a3-a6 in ONE launch (niyama_append_attention)
+                if ev_ is not None:
+                    ev_[1].record(stream)
+                kv.append_attention(plan, layer, k_new, v_new, q, o, lse, 0.0, stream)
+            else:
+                kv.append(plan, layer, k_new, v_new, stream)        # a3
+                if ev_ is not None:
+                    ev_[1].record(stream)
+                kv.attention(plan, layer, q, o, lse, 0.0, stream)   # a4-a6
+            if ev_ is not None:
+                ev_[2].record(stream)
+            if world > 1 and not gather_fused:
+                kv.allgather_heads(plan, o_full, lse_full, stream)   # a7
+            if ev_ is not None:
+                ev_[3].record(stream)
         pred.predict(batch)                             # a8
         plan.rollback()                                 # replay the same batch next step (host only)
         plan.close()
@@ -507,9 +520,9 @@ def main():
     if dist:
         dist.barrier()
     ms = e0.elapsed_time(e1)
-    attn_ms = [e[1].elapsed_time(e[2]) for e in ev if e is not None]
-    append_ms = [e[0].elapsed_time(e[1]) for e in ev if e is not None]
-    ag_ms = [e[2].elapsed_time(e[3]) for e in ev if e is not None]
+    attn_ms = [e[1].elapsed_time(e[2]) for es in ev if es is not None for e in es]
+    append_ms = [e[0].elapsed_time(e[1]) for es in ev if es is not None for e in es]
+    ag_ms = [e[2].elapsed_time(e[3]) for es in ev if es is not None for e in es]
     attn_avg_ms = sum(attn_ms) / len(attn_ms)
     ag_avg_ms = sum(ag_ms) / len(ag_ms)
     attn_q = [float(x) for x in np.percentile(np.array(attn_ms) * 1e3, [10, 50, 90])]
@@ -544,41 +557,45 @@ def main():
         for e_ in (ev_used[b_], ev_out[b_]):
             e_.record(stream)
 
+    ctr = [0]   # layers issued so far: buffer set = ctr & 1
+
     def e2e_step(i):
-        b_ = i & 1
-        with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_used[b_])
-            d_q[b_].copy_(h_q, non_blocking=True)
-            d_k[b_].copy_(h_k, non_blocking=True)
-            d_v[b_].copy_(h_v, non_blocking=True)
-            ev_in[b_].record(s_in)
-        stream.wait_event(ev_in[b_])
-        stream.wait_event(ev_out[b_])
         a1_step()
         plan = kv.plan(batch, stream)
-        if gather_fused:
-            if not fused:
-                kv.append(plan, 0, d_k[b_], d_v[b_], stream)
-            wo, wl_ = kv.attention_gather(plan, 0, d_q[b_], window, d_k[b_] if fused else None,
-                                          d_v[b_] if fused else None, 0.0, stream)
-            e_of[b_].copy_(wo)     # the consumer reads the window before the next call (its contract)
-            e_lf[b_].copy_(wl_)
-        elif fused:
-            kv.append_attention(plan, 0, d_k[b_], d_v[b_], d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0,
-                                stream)
-        else:
-            kv.append(plan, 0, d_k[b_], d_v[b_], stream)
-            kv.attention(plan, 0, d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0, stream)
-        if world > 1 and not gather_fused:
-            kv.allgather_heads(plan, e_of[b_], e_lf[b_], stream)
+        for layer in range(L):   # each layer's Q/K/V arrive from the host, its O goes back
+            b_ = ctr[0] & 1
+            ctr[0] += 1
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_used[b_])
+                d_q[b_].copy_(h_q, non_blocking=True)
+                d_k[b_].copy_(h_k, non_blocking=True)
+                d_v[b_].copy_(h_v, non_blocking=True)
+                ev_in[b_].record(s_in)
+            stream.wait_event(ev_in[b_])
+            stream.wait_event(ev_out[b_])
+            if gather_fused:
+                if not fused:
+                    kv.append(plan, layer, d_k[b_], d_v[b_], stream)
+                wo, wl_ = kv.attention_gather(plan, layer, d_q[b_], window, d_k[b_] if fused else None,
+                                              d_v[b_] if fused else None, 0.0, stream)
+                e_of[b_].copy_(wo)     # the consumer reads the window before the next call (its contract)
+                e_lf[b_].copy_(wl_)
+            elif fused:
+                kv.append_attention(plan, layer, d_k[b_], d_v[b_], d_q[b_], e_of[b_][q0:q0 + hq],
+                                    e_lf[b_][q0:q0 + hq], 0.0, stream)
+            else:
+                kv.append(plan, layer, d_k[b_], d_v[b_], stream)
+                kv.attention(plan, layer, d_q[b_], e_of[b_][q0:q0 + hq], e_lf[b_][q0:q0 + hq], 0.0, stream)
+            if world > 1 and not gather_fused:
+                kv.allgather_heads(plan, e_of[b_], e_lf[b_], stream)
+            ev_used[b_].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_used[b_])
+                h_o[b_].copy_(e_of[b_], non_blocking=True)
+                ev_out[b_].record(s_out)
         pred.predict(batch)
         plan.rollback()
         plan.close()
-        ev_used[b_].record(stream)
-        with torch.cuda.stream(s_out):
-            s_out.wait_event(ev_used[b_])
-            h_o[b_].copy_(e_of[b_], non_blocking=True)
-            ev_out[b_].record(s_out)
 
     for i in range(args.warmup):
         e2e_step(i)
@@ -599,10 +616,10 @@ def main():
         t = torch.tensor([e2e_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t[0])
-    ok = bool(torch.equal(h_o[(args.steps - 1) & 1], (last_win["o"] if gather_fused else o_full).cpu()))
+    ok = bool(torch.equal(h_o[(ctr[0] - 1) & 1], (last_win["o"] if gather_fused else o_full).cpu()))
     clocks.stop()
-    h2d = (h_q.numel() + h_k.numel() + h_v.numel()) * 2
-    d2h = h_o[0].numel() * 2
+    h2d = (h_q.numel() + h_k.numel() + h_v.numel()) * 2 * L
+    d2h = h_o[0].numel() * 2 * L
 
     B_kv, F = algorithmic(wl, hq, hkv)
     hbm_peak, tf_peak, peak_src = peaks()
@@ -613,7 +630,7 @@ def main():
     if os.path.exists(prof):
         pj = json.load(open(prof))
         traffic = pj.get(f"{args.config}-g{world}", {}).get("dram_bytes_per_launch")
-    value = T * args.steps / (ms * 1e-3)
+    value = T * L * args.steps / (ms * 1e-3)   # layer-tokens: each of the L layers attends the T rows
     out = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -624,12 +641,15 @@ def main():
                    "chunk_offset": desc.prefill_offset[0] if desc.num_prefill else 0,
                    "num_decode": desc.num_decode, "sum_ctx": int(sum(desc.decode_ctx)), "T": T,
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
-                   "l2": f"inputs larger than L2 ({B_kv / 1e6:.0f} MB KV read per step per GPU vs 126 MB L2)",
-                   "step": ("a1 slack+chunk, a2 plan, a3-a6 ONE launch (append inside the attention)" if fused else
-                            "a1 slack+chunk, a2 plan, a3 append, a4-a6 fused attention") +
+                   "layers": L,
+                   "l2": f"inputs larger than L2 ({B_kv / 1e6:.0f} MB KV read per layer per GPU vs 126 MB L2; "
+                         f"every layer has its own KV)",
+                   "step": (f"one iteration: a1 slack+chunk, a2 plan (once), then per layer x{L}: " +
+                            ("a3-a6 ONE launch (append inside the attention)" if fused else
+                             "a3 append, a4-a6 fused attention")) +
                            (", a7 all-gather INSIDE the attention launch (symmetric-window stores + flag barrier)"
                             if gather_fused else ", a7 NCCL all-gather" if world > 1 else "") +
-                           ", a8 predict; 1 layer"},
+                           "; a8 predict; value = T x layers / step time"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "traffic_source": "stored: dram__bytes_read.sum + dram__bytes_write.sum of this launch from one "
@@ -644,19 +664,23 @@ def main():
         "attn_tokens_per_s": T / attn_s,
         "step_breakdown_us": {"append": 1e3 * sum(append_ms) / len(append_ms), "attention": attn_med_ms * 1e3,
                               "allgather": ag_avg_ms * 1e3,
-                              "other": ms / args.steps * 1e3 - attn_med_ms * 1e3 - 1e3 * sum(append_ms) / len(append_ms),
-                              "host_issue": host_issue_us},
+                              "other_per_layer": ms / args.steps / L * 1e3 - attn_med_ms * 1e3
+                                                 - 1e3 * sum(append_ms) / len(append_ms),
+                              "step": ms / args.steps * 1e3, "per_layer": ms / args.steps / L * 1e3,
+                              "host_issue": host_issue_us,
+                              "note": "append/attention/allgather: every layer's launches of the event-bracketed steps"},
         "attention_launch_us": {"p10": attn_q[0], "median": attn_q[1], "p90": attn_q[2], "mean": attn_avg_ms * 1e3,
                                 "samples": len(attn_ms)},
         "per_rank": per_rank,
-        "e2e": {"value": T * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": T * L * args.steps / (e2e_ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "output_matches_device_run": ok,
-                "pipeline": "2 buffer sets; H2D(i+1) and D2H(i-1) on copy streams overlap step i"},
-        "gpu_launches": (1 if fused else 2) * args.steps,
-        "timing_note": (f"attention/append/all-gather launch times from events on every {EV_EVERY}nd timed step; "
-                        "the roofline uses their median (rank max; the mean is in attention_launch_us); the append "
-                        "interval includes the wait for the plan's upload (library copy stream), so 'other' = step "
-                        "- append - attention can be negative"),
+                "pipeline": "per layer: its Q/K/V H2D and O D2H on copy streams, 2 buffer sets, overlapping the "
+                            "neighbouring layers' kernels"},
+        "gpu_launches": (1 if fused else 2) * L * args.steps,
+        "timing_note": (f"attention/append/all-gather launch times from events around every layer's launches on "
+                        f"every {EV_EVERY}nd timed step (those steps lose the append -> attention programmatic "
+                        "overlap); the roofline uses their median (rank max; mean, p10, p90 in attention_launch_us); "
+                        "the append interval of layer 0 includes the wait for the plan's upload"),
         "clocks": clocks.summary(t_settle, t_wall1),
         "a1": a1,
         "a8": {"predicted_attention_us": pred.predict(batch) * 1e6, "measured_attention_us": attn_med_ms * 1e3,
