@@ -18,10 +18,10 @@ BF16, F32 = 0, 1
 DEVICE_NONE = -1
 NUM_PARAMS = 16
 # the config-3 fit of round 2 (L8B shapes, profiles/predictor_fit.json; tools/fit_predictor.py)
-DEFAULT_THETA = (1.944968362477925e-05, 7.958268227385193e-10, 0.0, 0.0, 1.6329528254560657e-09, 1.0,
-                 9.20142626540479e-07, 2.144757276602644e-08, 1.493309233263597e-07, 7.939176120262634,
-                 999999999999.999, 1.0000000000000007e-09, 7437295825259.413,
-                 0.2052998067519462, 84206186074.78609, 0.0010000000000000002)
+DEFAULT_THETA = (1.8615542699363073e-05, 4.3100249351440104e-11, 0.0, 0.0, 1.823173461287965e-09, 1.0,
+                 9.032153394238483e-07, 3.309503023249454e-08, 1.6819914137084094e-07, 7.7212032074647,
+                 43416718287.28031, 2.1810731598188094e-08, 7443378861402.669,
+                 0.22390466300385214, 84583517506.78802, 0.0010000000000000002)
 PARAM_NAMES = ["c0 (s)", "per row c+D (s)", "per decode (s)", "per ctx token (s)", "per unit (s)", "kappa (T_sim)",
                "tau0 (s/step)", "tau_p (s/step)", "tau_d (s/step)", "sigma (steps/tile)", "r_w (B/s per warp)",
                "u0 (s/unit)", "BW (B/s)", "gamma", "r_cta (B/s)", "sigma0 (steps/CTA)"]

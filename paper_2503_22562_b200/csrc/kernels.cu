@@ -232,6 +232,12 @@ constexpr int kTile = 2 * kPanel;   // 128 rows x 256 B = 32 KB (one region)
 #ifndef NIYAMA_DIAG_HANG
 #define NIYAMA_DIAG_HANG 0
 #endif
+// The K/V producers start an item's copies while the other warps load its Q tile
+// (measured: config 2 99.4-99.9 -> 96.3 us, L70B prefill-only 426 -> 420 us,
+// profiles/r02s3/ab_earlykv.txt); 0 restores the CTA-wide Q barrier.
+#ifndef NIYAMA_EARLY_KV
+#define NIYAMA_EARLY_KV 1
+#endif
 #ifndef NIYAMA_ONE_SLOAD
 #define NIYAMA_ONE_SLOAD 0
 #endif
@@ -584,30 +590,41 @@ __device__ __forceinline__ void prefill_tile(const AttnParams& p, const TileDesc
     // All of a thread's pieces are loaded before any is stored, so the ~6 loads per
     // thread are in flight together (one memory latency per tile instead of six: the
     // serial version took ~10 K cycles per tile, tools/tile_trace.py).
+    // NIYAMA_EARLY_KV: the K/V producer warps (0, 2) skip the Q load and start the item's
+    // bulk copies at once, so the ring fill overlaps the Q load; the other 10 warps load Q
+    // and meet at a named barrier (the QK issuer is one of them).
     const uint8_t* q = static_cast<const uint8_t*>(p.q);
-    constexpr int kQPer = (128 * 16 + kThreads - 1) / kThreads;
-    uint4 qv[kQPer];
+    constexpr int kLoaders = NIYAMA_EARLY_KV ? kThreads - 64 : kThreads;
+    const bool loader = !NIYAMA_EARLY_KV || (warp != 0 && warp != 2);
+    const int lidx = NIYAMA_EARLY_KV ? (warp == 1 ? lane : (warp - 2) * 32 + lane) : tid;
+    if (loader) {
+      constexpr int kQPer = (128 * 16 + kLoaders - 1) / kLoaders;
+      uint4 qv[kQPer];
 #pragma unroll
-    for (int k = 0; k < kQPer; ++k) {
-      const int idx = tid + k * kThreads;
-      const int r = idx >> 4, j = idx & 15;
-      const int hh = r / R, i = r - hh * R;
-      qv[k] = make_uint4(0, 0, 0, 0);
-      if (idx < 128 * 16 && i < vrows) {
-        const int64_t row = t.row0 + t.t0 + i;
-        qv[k] = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
+      for (int k = 0; k < kQPer; ++k) {
+        const int idx = lidx + k * kLoaders;
+        const int r = idx >> 4, j = idx & 15;
+        const int hh = r / R, i = r - hh * R;
+        qv[k] = make_uint4(0, 0, 0, 0);
+        if (idx < 128 * 16 && i < vrows) {
+          const int64_t row = t.row0 + t.t0 + i;
+          qv[k] = __ldg(reinterpret_cast<const uint4*>(q + ((row * p.Hq + t.kvh * g + hh) * kD) * 2 + j * 16));
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < kQPer; ++k) {
-      const int idx = tid + k * kThreads;
-      if (idx >= 128 * 16) break;
-      const int r = idx >> 4, j = idx & 15;
-      st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), qv[k].x, qv[k].y,
-                   qv[k].z, qv[k].w);
+      for (int k = 0; k < kQPer; ++k) {
+        const int idx = lidx + k * kLoaders;
+        if (idx >= 128 * 16) break;
+        const int r = idx >> 4, j = idx & 15;
+        st_shared_v4(sbase + kQOff + (j >> 3) * kPanel + r * 128 + (((j & 7) ^ (r & 7)) << 4), qv[k].x, qv[k].y,
+                     qv[k].z, qv[k].w);
+      }
+      fence_proxy_async_smem();
+      if (NIYAMA_EARLY_KV)
+        named_bar_sync(13, kLoaders);
+      else
+        __syncthreads();
     }
-    fence_proxy_async_smem();
-    __syncthreads();
   }
 #if NIYAMA_DIAG_TILES
   if (p.trace != nullptr && blockIdx.x == 0 && tid == 0 && p.trace[8 * 160 + 3 * 64] < 64) {
