@@ -1028,13 +1028,17 @@ niyama_status attention_impl(niyama_kv* kv, const niyama_plan* plan, int32_t lay
     int grid = kv->tune.grid_cap > 0 ? std::min(kv->tune.grid_cap, plan->grid) : plan->grid;
     p.prefill_ctas = std::min(plan->prefill_ctas, grid);
     const bool pairs = kv->tune.prefill_pairs == 1 || (kv->tune.prefill_pairs == 0 && kv->g > 4);
-    if (pairs && plan->n_tiles > 0 && plan->n_split_tiles == 0) {
+    // an odd grid grows by one CTA (never past the SM count or a grid_cap) or shrinks by one:
+    // the queues hand work to whichever CTAs run, so the CTA count changes no result
+    const int cap = kv->tune.grid_cap > 0 ? std::min(kv->tune.grid_cap, kv->num_sms) : kv->num_sms;
+    const int even_grid = (grid & 1) && grid + 1 <= cap ? grid + 1 : grid & ~1;
+    if (pairs && plan->n_tiles > 0 && plan->n_split_tiles == 0 && even_grid >= 2) {
       // CTA pairs: clusters of 2 (even grid, even prefill CTA count), one item per q-tile pair
       // (auto at g = 8: config 4 866 -> 849 us; neutral at g = 4, tools/ab_pairs.py)
       p.pairs = 1;
       p.n_pair_items = 0;
       for (const PrefillSlice& sl : plan->slices) p.n_pair_items += (sl.nqt + 1) / 2 * kv->hkv;
-      grid = std::min(grid + (grid & 1), kv->num_sms & ~1);
+      grid = even_grid;
       p.prefill_ctas = std::min(grid, std::max(2, p.prefill_ctas + (p.prefill_ctas & 1)));
     }
     NY_CUDA(launch_attention_bf16(p, grid, s));

@@ -353,6 +353,21 @@ def test_prefill_cta_pairs(case):
     assert torch.equal(l2, l0)
 
 
+@pytest.mark.parametrize("cap", [1, 5, 6])
+def test_prefill_cta_pairs_small_grids(cap):
+    """CTA pairs under a grid cap: an odd cap (5) runs 4 or 6 CTAs in pairs, a cap of 1 keeps one
+    tile per CTA; results bitwise equal to the unpaired launch and within the oracle's bounds."""
+    wl = W.random_hybrid(W.Shape(64, 8, 128, 16, "bf16"), seed=76, num_prefill=2, max_chunk=150, num_decode=5,
+                         max_ctx=1500)
+    r2, _ = run_and_compare(wl, tuning=dict(prefill_pairs=1, grid_cap=cap))
+    o2, l2 = r2.attention()
+    r0 = Run(wl, tuning=dict(prefill_pairs=2))
+    o0, l0 = r0.attention()
+    torch.cuda.synchronize()
+    assert torch.equal(o2.view(torch.int16), o0.view(torch.int16))
+    assert torch.equal(l2, l0)
+
+
 @pytest.mark.parametrize("case", ["prefill-only", "mixed", "g8", "two-slices", "diag-only"])
 def test_prefill_split_k(case):
     """Split-K prefill (niyama_tuning.prefill_split = 1: key parts of a q tile on different CTAs,
