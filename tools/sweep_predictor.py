@@ -157,6 +157,12 @@ def sweep(args):
         chunk = 0 if u < 0.08 else int(g.integers(1, 2049))
         D = 0 if 0.08 <= u < 0.16 else int(g.integers(1, args.max_decode + 1))
         run("random", 1000 + i, chunk, D)
+    g = np.random.default_rng(789)
+    for i in range(args.train_small):
+        # extra training points in the regime the scheduler mostly runs (decode-only or a
+        # chunk <= 512 with <= 64 decodes; config-5 replays), where the fit is weakest
+        chunk = 0 if g.random() < 0.3 else int(g.integers(1, 513))
+        run("random", 5000 + i, chunk, int(g.integers(1, min(64, args.max_decode) + 1)))
     return rows, time.time() - t0
 
 
@@ -168,6 +174,8 @@ def main():
     ap.add_argument("--offgrid", type=int, default=40)
     ap.add_argument("--train-random", type=int, default=120)
     ap.add_argument("--max-decode", type=int, default=256)
+    ap.add_argument("--train-small", type=int, default=0,
+                    help="extra training points with chunk <= 512 (30 %% decode-only) and <= 64 decodes")
     ap.add_argument("--trace-every", type=int, default=3, help="per-CTA timeline of every k-th point (0 = none)")
     ap.add_argument("--raw", default=os.path.join(ROOT, "profiles", "r02", "predictor_sweep_l8b.json"))
     args = ap.parse_args()
