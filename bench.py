@@ -456,7 +456,7 @@ def main():
     # Per-launch events cost device time (~1-2 us each) and break the programmatic
     # launch overlap of append -> attention, so they bracket every EV_EVERY-th timed
     # step only; the attention roofline uses the mean over those launches.
-    EV_EVERY = 2
+    EV_EVERY = 4
     ev = [[tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(L)] if i % EV_EVERY == 0
           else None for i in range(args.steps)]
 
@@ -678,7 +678,7 @@ def main():
                             "neighbouring layers' kernels"},
         "gpu_launches": (1 if fused else 2) * L * args.steps,
         "timing_note": (f"attention/append/all-gather launch times from events around every layer's launches on "
-                        f"every {EV_EVERY}nd timed step (those steps lose the append -> attention programmatic "
+                        f"every {EV_EVERY}th timed step (those steps lose the append -> attention programmatic "
                         "overlap); the roofline uses their median (rank max; mean, p10, p90 in attention_launch_us); "
                         "the append interval of layer 0 includes the wait for the plan's upload"),
         "clocks": clocks.summary(t_settle, t_wall1),

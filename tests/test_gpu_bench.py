@@ -35,7 +35,7 @@ def test_bench_line_contract():
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0.05 < r["frac"] < 1.2
     assert r["algorithmic_bytes_per_launch"] == 555917312       # config 2: 135,722 tokens x 4,096 B
     assert d["gpu_launches"] == 2 * 2 * 4                         # append + attention per layer per step
-    assert d["attention_launch_us"]["samples"] == 2 * 2           # every 2nd step, every layer
+    assert d["attention_launch_us"]["samples"] == 1 * 2           # every 4th step (step 0 of 4), every layer
 
 
 def test_bench_reference_arm_line():
