@@ -133,7 +133,7 @@ class GpuExecutor:
 
 
 def replay(sched: Scheduler, executor, trace: Sequence, buckets: Sequence[QoSBucket], until: float = math.inf,
-           max_iters: int = 10_000_000):
+           max_iters: int = 10_000_000, record: Optional[list] = None):
     """The serving loop (SPEC's event loop): admit arrivals up to `now`, build the
     batch, execute it, advance `now`, complete it.  Returns (iterations, requests)."""
     reqs = sorted(trace, key=lambda r: (r.t_arrival, r.id))
@@ -160,6 +160,8 @@ def replay(sched: Scheduler, executor, trace: Sequence, buckets: Sequence[QoSBuc
                 break
             now = max(now, reqs[i].t_arrival)
             continue
+        if record is not None:  # the batch descriptors (predictor calibration on the engine's own iterations)
+            record.append(batch.desc())
         dt = executor.run(batch)
         iters.append(IterRecord(now, dt, batch.predicted, sum(n for _, _, n in batch.slices), len(batch.decodes),
                                 len(batch.slices), batch.budget, batch.infeasible, len(batch.relegated),

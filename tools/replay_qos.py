@@ -82,6 +82,10 @@ def main():
     ap.add_argument("--full", action="store_true",
                     help="full Llama-3-8B iterations: cuBLAS linear layers around every layer's append + attention, "
                          "scheduled with the full-iteration predictor (profiles/iteration_fit.json's sweep)")
+    ap.add_argument("--calibrate", action="store_true",
+                    help="after the runs, refit the attention predictor on the measured attention launches of the "
+                         "first policy's replay (the engine's own profile, as Vidur profiling feeds the paper's "
+                         "predictor) and replay every policy again with it (same trace)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "replay_config5.json"))
     args = ap.parse_args()
     shape = W.L8B
@@ -136,7 +140,10 @@ def main():
         import torch  # noqa: F401
         blocks = 60000
         gpu = dict(blocks=blocks)
-    for name in args.policies.split(","):
+    cal = {"theta": None}
+    recorded = []
+
+    def run_policy(name, tag, theta):
         t1 = time.time()
         sched = make_sched(pred, name, layers_s, fixed_s, tdec)
         if args.model_only:
@@ -148,22 +155,44 @@ def main():
                 from sweep_iteration import LinearLayers
                 linear = LinearLayers(max_t=2048 + 2048)
             ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048, linear=linear)
-            pred_b = make_pred(ex.kv)
+            pred_b = make_pred(ex.kv) if theta is None else ny.Predictor.from_params(cfg, theta).bind(ex.kv)
             sched = ny.Scheduler(pred_b, max_chunk=2048, layers=layers_s, fixed_s=fixed_s, decode_token_s=tdec,
                                  history_min_samples=30, kv_token_budget=int(gpu["blocks"] * 16 * 0.9),
                                  **POLICIES[name])
-        it, recs = serve.replay(sched, ex, trace, buckets, until=duration * 1.25)
+        rec = [] if (args.calibrate and theta is None and not recorded and not args.model_only) else None
+        it, recs = serve.replay(sched, ex, trace, buckets, until=duration * 1.25, record=rec)
+        if rec is not None:
+            recorded.append((rec, [x.attention_s / args.layers for x in it]))
         summ = serve.summarize(it, recs, buckets, t_end=duration * 1.25, fixed_s=fixed_s)
         if args.full:   # the scheduler's prediction is the whole iteration: no attention-only comparison
             summ.pop("predictor_rel_err_attention_only", None)
         summ["wall_s"] = time.time() - t1
         if not args.model_only:
             summ["gpu_launches"] = ex.launches
-        out["runs"][name] = summ
-        print(name, json.dumps(summ), flush=True)
+        out["runs"][tag] = summ
+        print(tag, json.dumps(summ), flush=True)
         os.makedirs(os.path.dirname(args.out), exist_ok=True)
         json.dump(out, open(args.out, "w"), indent=1)   # after every policy (long runs)
         del ex
+
+    for name in args.policies.split(","):
+        run_policy(name, name, None)
+    if args.calibrate and recorded:
+        descs, secs = recorded[0]
+        keep = [i for i, x in enumerate(secs) if x == x and x > 0]
+        step = max(1, len(keep) // 3000)
+        keep = keep[::step]
+        t1 = time.time()
+        p_cal = ny.Predictor.fit_batches(cfg, [descs[i] for i in keep], [secs[i] for i in keep],
+                                         start=list(ny.DEFAULT_THETA))
+        cal["theta"] = [float(x) for x in p_cal.params()]
+        err = np.abs([p_cal.predict(descs[i]) / secs[i] - 1.0 for i in keep])
+        out["calibration"] = {"iterations": len(keep), "fit_s": time.time() - t1, "theta": cal["theta"],
+                              "in_sample_rel_err": {"p50": float(np.median(err)), "p95": float(np.percentile(err, 95)),
+                                                    "max": float(err.max())}}
+        print("calibration", json.dumps(out["calibration"]["in_sample_rel_err"]), flush=True)
+        for name in args.policies.split(","):
+            run_policy(name, name + "@calibrated", cal["theta"])
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(out, open(args.out, "w"), indent=1)
 
