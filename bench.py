@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--fused-append", action="store_true",
                     help="a3-a6 in one launch (niyama_append_attention) instead of niyama_kv_append + "
                          "niyama_hybrid_attention (measured slower on config 2: 113 vs 100 + 10 us)")
+    ap.add_argument("--tuning", default="",
+                    help="diagnostics: niyama_tuning fields for the timed KVCache, e.g. prefill_ctas=88,split_len=256 "
+                         "(include/niyama.h; default = the planner's own choices)")
     ap.add_argument("--gather", default="nccl", choices=["nccl", "fused"],
                     help="a7 head all-gather: nccl = niyama_allgather_heads after the launch (N > 1 only); fused = "
                          "niyama_attention_gather, the all-gather inside the attention launch (NVLink stores into "
@@ -387,6 +390,8 @@ def main():
     L = args.layers if args.layers > 0 else min(32 if args.config == "l8b" else 80, max(1, int(120e9 // per_layer)))
     kv = ny.KVCache(L, s.num_q_heads, s.num_kv_heads, s.head_dim, wl.num_blocks + 64, block_size=s.block_size,
                     dtype=s.dtype, world_size=world, rank=rank, device=local)
+    if args.tuning:
+        kv.set_tuning(**{k: int(v) for k, v in (x.split("=") for x in args.tuning.split(","))})
     gather_fused = args.gather == "fused"
     if world > 1:
         uid = ny.get_unique_id() if rank == 0 else bytes(128)
@@ -649,7 +654,8 @@ def main():
                              "a3 append, a4-a6 fused attention")) +
                            (", a7 all-gather INSIDE the attention launch (symmetric-window stores + flag barrier)"
                             if gather_fused else ", a7 NCCL all-gather" if world > 1 else "") +
-                           "; a8 predict; value = T x layers / step time"},
+                           "; a8 predict; value = T x layers / step time",
+                   **({"tuning": args.tuning} if args.tuning else {})},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
                      "traffic_source": "stored: dram__bytes_read.sum + dram__bytes_write.sum of this launch from one "
