@@ -1,10 +1,10 @@
 # Config-4 prefill-CTA count under the bench's own sustained (power-capped) conditions:
-# 27-layer steps, alternating settings, two passes.   bash tools/ab_l70b_ctas.sh OUT n1 n2 ...  (0 = planner default)
+# 27-layer steps, alternating settings, two passes.   bash tools/ab_l70b_ctas.sh OUT n1 n2 ...  (0 = planner default; key=val = any tuning field)
 set -u
 out=$1; shift
 for rep in 1 2; do
   for n in "$@"; do
-    if [ "$n" = 0 ]; then tun=""; else tun="--tuning prefill_ctas=$n"; fi
+    case "$n" in 0) tun="";; *=*) tun="--tuning $n";; *) tun="--tuning prefill_ctas=$n";; esac
     timeout 600 python bench.py --config l70b --no-cpu-baseline --steps 120 --warmup 10 $tun 2>/dev/null | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
