@@ -75,9 +75,13 @@ class GpuExecutor:
     """n_layers x (append + attention) of the batch on cuda:device, timed with CUDA events."""
 
     def __init__(self, shape, n_layers: int, num_blocks: int, max_rows: int = 2048 + 512, device: int = 0,
-                 seed: int = 0, linear=None):
+                 seed: int = 0, linear=None, head_start_us: float = 0.0):
         """linear: optional callable object with pre(h) -> (q, k, v) and post(h, o, T) -> h (a model's
-        linear layers, e.g. cuBLAS GEMMs) run around every layer's append + attention."""
+        linear layers, e.g. cuBLAS GEMMs) run around every layer's append + attention.
+        head_start_us > 0: the stream spins that long (torch.cuda._sleep, before the timed region)
+        so the host enqueues the whole iteration before the GPU starts it; otherwise a batch whose
+        kernels are shorter than the binding's per-launch host cost is timed with the host's
+        launch gaps inside (tools/replay_outliers.py)."""
         import torch
         self.torch = torch
         self.n_layers = n_layers
@@ -101,6 +105,7 @@ class GpuExecutor:
         self.last_attention_s = 0.0
         self.launches = 0
         self.linear = linear
+        self.head_start_cycles = int(head_start_us * 2000.0)   # ~2 GHz SM clock
 
     def run(self, batch) -> float:
         T = sum(n for _, _, n in batch.slices) + len(batch.decodes)
@@ -110,6 +115,9 @@ class GpuExecutor:
         q, k, v = self.q[:T], self.k[:T], self.v[:T]
         o = self.obuf[:self.hq * T * self.d].view(self.hq, T, self.d)
         h = self.linear.x[:T] if self.linear is not None else None
+        if self.head_start_cycles > 0:
+            with self.torch.cuda.stream(self.stream):
+                self.torch.cuda._sleep(self.head_start_cycles)
         self.e0.record(self.stream)
         for layer in range(self.n_layers):
             if self.linear is not None:

@@ -86,6 +86,9 @@ def main():
                     help="after the runs, refit the attention predictor on the measured attention launches of the "
                          "first policy's replay (the engine's own profile, as Vidur profiling feeds the paper's "
                          "predictor) and replay every policy again with it (same trace)")
+    ap.add_argument("--head-start-us", type=float, default=0.0,
+                    help="GpuExecutor head start: the host enqueues each iteration before the GPU starts it, so the "
+                         "replica clock and the attention times hold no host launch gaps (serve.py)")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "replay_config5.json"))
     args = ap.parse_args()
     shape = W.L8B
@@ -113,7 +116,7 @@ def main():
     s = t_ref / 0.050
     buckets = buckets_scaled(s)
     tdec = t_ref                                        # R25: a decode iteration ~ the reference iteration
-    out = {"layers": args.layers, "engine": "full iteration (cuBLAS linear layers + attention)" if args.full
+    out = {"layers": args.layers, "head_start_us": args.head_start_us, "engine": "full iteration (cuBLAS linear layers + attention)" if args.full
            else "attention-only (append + attention per layer)", "scale": s, "strict_tbt_s": 0.050 * s, "ttft_s": 6.0 * s,
            "ttlt_s": [600.0 * s, 1800.0 * s], "fixed_s_per_iteration": fixed_s, "reference_iteration_s": t_ref}
     t0 = time.time()
@@ -154,7 +157,8 @@ def main():
                 sys.path.insert(0, os.path.join(ROOT, "tools"))
                 from sweep_iteration import LinearLayers
                 linear = LinearLayers(max_t=2048 + 2048)
-            ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048, linear=linear)
+            ex = serve.GpuExecutor(shape, args.layers, gpu["blocks"], max_rows=2048 + 2048, linear=linear,
+                                   head_start_us=args.head_start_us)
             pred_b = make_pred(ex.kv) if theta is None else ny.Predictor.from_params(cfg, theta).bind(ex.kv)
             sched = ny.Scheduler(pred_b, max_chunk=2048, layers=layers_s, fixed_s=fixed_s, decode_token_s=tdec,
                                  history_min_samples=30, kv_token_budget=int(gpu["blocks"] * 16 * 0.9),
